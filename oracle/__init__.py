@@ -1,0 +1,155 @@
+"""ctypes binding of the CPU oracle (oracle/uellm_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  Never imported by paper_2409_14961_b200/.
+
+parity pins: see oracle/uellm_oracle.c header and DESIGN.md "Oracle and its pins".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "uellm_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_CONTRACT", 3: "ERR_CONFIG", 4: "ERR_OVERFLOW"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {STATUS.get(status, status)}")
+        self.status = status
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C11 + pthreads, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-pthread", "-Wall", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class OrcConfig(C.Structure):
+    _fields_ = [("mode", C.c_uint32), ("window", C.c_uint32), ("max_batch", C.c_uint32),
+                ("split_on_slo_change", C.c_uint32), ("kv_bytes_per_elem", C.c_uint32),
+                ("n_layers", C.c_uint32), ("hidden", C.c_uint32), ("pad0", C.c_uint32),
+                ("kv_cap_bytes", C.c_uint64),
+                ("t_batch_us", C.c_uint32), ("t_iter_us", C.c_uint32), ("t_tok_us", C.c_uint32),
+                ("t_prefill_us", C.c_uint32), ("lambda_us", C.c_uint64),
+                ("w1", C.c_double), ("w2", C.c_double), ("l1", C.c_double), ("l2", C.c_double),
+                ("threshold", C.c_double), ("eps", C.c_double),
+                ("eq2_additive", C.c_uint32), ("pad1", C.c_uint32)]
+
+
+BATCH_STAT_DTYPE = np.dtype([
+    ("start", "<u4"), ("size", "<u4"), ("max_in", "<u4"), ("max_out", "<u4"),
+    ("gen_tokens", "<u8"), ("pad_in", "<u8"), ("pad_out", "<u8"), ("kv_bytes", "<u8"),
+    ("est_us", "<u8"), ("completion_us", "<u8"),
+    ("viol_alone", "<u4"), ("viol_seq", "<u4"), ("over_cap", "<u4"), ("window", "<u4")])
+
+
+class OrcTotals(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("n", "batches", "gen_tokens", "pad_in", "pad_out",
+                                          "kv_bytes_max", "dp_cost", "viol_alone", "viol_seq",
+                                          "over_cap", "makespan_us")] + \
+               [("mean_latency_s", C.c_double), ("throughput_tok_s", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+        f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+        _lib.orc_slo_us.argtypes = [C.c_float, C.POINTER(C.c_uint32)]
+        _lib.orc_kv_bytes.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                      C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]
+        _lib.orc_schedule.argtypes = [C.c_uint64, u32p, u32p, f32p, C.POINTER(OrcConfig),
+                                      u32p, u32p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                      C.c_int]
+        _lib.orc_stats.argtypes = [C.c_uint64, u32p, u32p, f32p, C.POINTER(OrcConfig),
+                                   u32p, u32p, C.c_uint64, C.c_void_p, C.POINTER(OrcTotals)]
+        for f in ("orc_sizeof_config", "orc_sizeof_batch_stat", "orc_sizeof_totals"):
+            getattr(_lib, f).restype = C.c_uint64
+        assert _lib.orc_sizeof_config() == C.sizeof(OrcConfig)
+        assert _lib.orc_sizeof_batch_stat() == BATCH_STAT_DTYPE.itemsize
+        assert _lib.orc_sizeof_totals() == C.sizeof(OrcTotals)
+    return _lib
+
+
+def to_config(cfg) -> OrcConfig:
+    c = OrcConfig()
+    for name, _ in OrcConfig._fields_:
+        if name.startswith("pad"):
+            continue
+        setattr(c, name, getattr(cfg, name))
+    return c
+
+
+def slo_us(x: float) -> int:
+    v = C.c_uint32()
+    st = lib().orc_slo_us(C.c_float(x), C.byref(v))
+    if st:
+        raise OracleError(st, "slo_us")
+    return v.value
+
+
+def kv_bytes(kvpe, b, l, h, s, n) -> int:
+    v = C.c_uint64()
+    st = lib().orc_kv_bytes(kvpe, b, l, h, s, n, C.byref(v))
+    if st:
+        raise OracleError(st, "kv_bytes")
+    return v.value
+
+
+def _arrays(inp, out, slo):
+    return (np.ascontiguousarray(inp, np.uint32), np.ascontiguousarray(out, np.uint32),
+            np.ascontiguousarray(slo, np.float32))
+
+
+def schedule(inp, out, slo, cfg, nthreads: int = 1):
+    """-> (order u32[n], offsets u32[m+1], m, dp_cost)."""
+    inp, out, slo = _arrays(inp, out, slo)
+    n = inp.shape[0]
+    order = np.zeros(max(n, 1), np.uint32)
+    offsets = np.zeros(n + 1, np.uint32)
+    m = C.c_uint64()
+    cost = C.c_uint64()
+    c = to_config(cfg)
+    st = lib().orc_schedule(n, inp, out, slo, C.byref(c), order, offsets, C.byref(m),
+                            C.byref(cost), nthreads)
+    if st:
+        raise OracleError(st, "schedule")
+    return order[:n], offsets[: m.value + 1], m.value, cost.value
+
+
+def stats(inp, out, slo, cfg, order, offsets):
+    """-> (per_batch structured array, totals dict)."""
+    inp, out, slo = _arrays(inp, out, slo)
+    n = inp.shape[0]
+    order = np.ascontiguousarray(order, np.uint32)
+    offsets = np.ascontiguousarray(offsets, np.uint32)
+    m = offsets.shape[0] - 1
+    pb = np.zeros(max(m, 1), BATCH_STAT_DTYPE)
+    tot = OrcTotals()
+    c = to_config(cfg)
+    if n == 0:
+        order = np.zeros(1, np.uint32)
+        inp = out = np.zeros(1, np.uint32)
+        slo = np.zeros(1, np.float32)
+    st = lib().orc_stats(n, inp, out, slo, C.byref(c), order, offsets, m,
+                         pb.ctypes.data_as(C.c_void_p), C.byref(tot))
+    if st:
+        raise OracleError(st, "stats")
+    return pb[:m], tot.as_dict()

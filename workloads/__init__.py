@@ -1,0 +1,227 @@
+"""Seeded synthetic query streams and scheduler configurations (c1-c5).
+
+This module is shared INPUT plumbing: both the CPU oracle (oracle/) and the CUDA path
+(paper_2409_14961_b200/) are fed from it, so it deliberately contains none of the
+method's arithmetic -- no SLO conversion, no sort, no cost model, no KV formula.  It
+only draws numbers and states configuration constants.
+
+Distributions are proposals (the paper publishes none):
+  * SLO: "ranging from 1 second to 350 seconds"; class-valued variants for c2-c4.
+  * input length: lognormal (Alpaca-like prompts, P:195 names Alpaca as the workload).
+  * predicted output length: lognormal (c2) or Pareto long tail up to 4096 (c3-c5),
+    quantised to the profiler's length buckets ("categorize the output lengths").
+Recipe and readings: DESIGN.md section "Input recipe".
+
+Queries are returned as three numpy arrays (caller SoA):
+  input_len u32, pred_out_len u32, slo_s f32 (seconds).
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass
+
+import numpy as np
+
+# Segmentation modes (the numeric values of the C-ABI enum and of the oracle's enum).
+MODE_SEG_DP = 0
+MODE_SLO_ODBS = 1
+MODE_FIFO = 2
+MODE_SORT_ONLY = 3
+
+# KV reserve of LLaMA-2-7B (fp16 weights 2 * 6,738,415,616 B) on one 180 GB B200:
+# T of P:366 ("memory reserved for KV Cache"), in bytes.  With 4 B/elem, 32 layers,
+# hidden 4096 this is 317,617 tokens of KV.
+KV_RESERVE_LLAMA2_7B_180GB = 180_000_000_000 - 2 * 6_738_415_616
+
+
+@dataclass
+class SchedConfig:
+    """Scheduler configuration; field names and meaning follow include/uellm.h."""
+    mode: int = MODE_SEG_DP
+    window: int = 0                 # queries per scheduling window, 0 = all
+    max_batch: int = 256            # W
+    split_on_slo_change: int = 0
+    kv_bytes_per_elem: int = 4      # the "4" of P:60
+    n_layers: int = 32              # LLaMA-2-7B
+    hidden: int = 4096
+    kv_cap_bytes: int = 0           # 0 = no cap
+    t_batch_us: int = 1000          # service-time model (R7)
+    t_iter_us: int = 2000
+    t_tok_us: int = 40
+    t_prefill_us: int = 10
+    lambda_us: int = 0              # penalty per violating query (R8/R14)
+    w1: float = 1.0                 # Alg. 1 weights / overheads / threshold
+    w2: float = 1.0
+    l1: float = 1.0
+    l2: float = 1.0
+    threshold: float = 1000.0
+    eps: float = 1e-9
+    eq2_additive: int = 0
+
+    def replace(self, **kw) -> "SchedConfig":
+        return dataclasses.replace(self, **kw)
+
+
+def _rng(seed: int, stream: int = 0) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(key=[seed & (2**64 - 1), stream]))
+
+
+def _lognormal_int(rng, median, sigma, lo, hi, n):
+    x = rng.lognormal(mean=np.log(median), sigma=sigma, size=n)
+    return np.clip(np.rint(x), lo, hi).astype(np.uint32)
+
+
+def _bucket_up(x, width, hi):
+    x = ((x.astype(np.int64) + width - 1) // width) * width
+    return np.clip(x, width, hi).astype(np.uint32)
+
+
+def _pareto_out(rng, n, alpha=1.2, xm=32, hi=4096, width=16):
+    x = xm * (1.0 + rng.pareto(alpha, size=n))
+    x = np.minimum(np.ceil(x), hi)
+    return _bucket_up(x.astype(np.int64), width, hi)
+
+
+SLO_CLASSES_8 = np.geomspace(1.0, 350.0, 8).astype(np.float32)
+SLO_CLASSES_3 = np.array([2.0, 30.0, 350.0], dtype=np.float32)
+
+
+def gen_uniform_slo(n, seed, lo=1.0, hi=350.0):
+    """The paper's own protocol: per-request SLO uniform in [1 s, 350 s]."""
+    rng = _rng(seed, 7)
+    return rng.uniform(lo, hi, size=n).astype(np.float32)
+
+
+def c1(seed: int, lam: int = 0):
+    """16 queries, 1 SLO class (0.3 s), outputs 8-128, cap = 4 queries' KV (BJ configs[0])."""
+    rng = _rng(seed, 1)
+    n = 16
+    inp = rng.integers(1, 65, size=n).astype(np.uint32)
+    out = rng.integers(8, 129, size=n).astype(np.uint32)
+    slo = np.full(n, 0.3, dtype=np.float32)
+    # 4 queries of the largest possible length (64 + 128 tokens) at 4*32*4096 B/token
+    cap = 4 * 192 * 524_288
+    cfg = SchedConfig(window=0, max_batch=16, kv_cap_bytes=cap, lambda_us=lam)
+    return inp, out, slo, cfg
+
+
+def c2(seed: int, lam: int = 10**9, split: int = 0, n: int = 10_000):
+    """10^4 queries, 3 SLO classes, Alpaca-like lengths, W = 64 (BJ configs[1])."""
+    rng = _rng(seed, 2)
+    inp = _lognormal_int(rng, 24, 0.6, 1, 512, n)
+    out = _bucket_up(_lognormal_int(rng, 64, 0.9, 1, 1024, n), 32, 1024)
+    slo = SLO_CLASSES_3[rng.integers(0, 3, size=n)]
+    cfg = SchedConfig(window=0, max_batch=64, kv_cap_bytes=KV_RESERVE_LLAMA2_7B_180GB,
+                      lambda_us=lam, split_on_slo_change=split)
+    return inp, out, slo, cfg
+
+
+def long_tail(n: int, seed: int, stream: int = 3):
+    """c3/c4 query shape: 8 log-spaced SLO classes in [1, 350] s, lognormal inputs
+    (median 128, sigma 1, <= 4096), Pareto(1.2) x 32 outputs (<= 4096, 16-token buckets)."""
+    rng = _rng(seed, stream)
+    inp = _lognormal_int(rng, 128, 1.0, 1, 4096, n)
+    out = _pareto_out(rng, n)
+    slo = SLO_CLASSES_8[rng.integers(0, 8, size=n)]
+    return inp, out, slo
+
+
+def c3(seed: int, lam: int = 10**9, split: int = 0, n: int = 1_000_000):
+    """10^6 queries, 8 SLO classes, long-tail outputs <= 4096, LLaMA-2-7B KV cap (configs[2])."""
+    inp, out, slo = long_tail(n, seed)
+    cfg = SchedConfig(window=0, max_batch=256, kv_cap_bytes=KV_RESERVE_LLAMA2_7B_180GB,
+                      lambda_us=lam, split_on_slo_change=split)
+    return inp, out, slo, cfg
+
+
+def c4(seed: int, lam: int = 10**9, n: int = 100_000_000, window: int = 1_000_000):
+    """10^8 queries streamed in 10^6-query windows (BJ configs[3]); shape as c3."""
+    inp, out, slo = long_tail(n, seed)
+    cfg = SchedConfig(window=window, max_batch=256, kv_cap_bytes=KV_RESERVE_LLAMA2_7B_180GB,
+                      lambda_us=lam)
+    return inp, out, slo, cfg
+
+
+C5_KV_CAP_BYTES = 16_384 * 524_288   # 16,384 tokens of LLaMA-2-7B KV
+
+
+def c5(seed: int, n: int = 10_000_000, window: int = 1_000_000, lam: int = 10**9):
+    """Adversarial mix (BJ configs[4]), four equal contiguous segments:
+      (i)   identical keys: slo 30 s, input 128, output 256;
+      (ii)  all-violating: slo 1 ms (< t_batch + t_iter), c3-shaped lengths;
+      (iii) 1% of queries alone exceed the KV cap (in + out in (16384, 32768]);
+      (iv)  anti-sorted: strictly ascending distinct SLOs with descending outputs."""
+    rng = _rng(seed, 5)
+    q = n // 4
+    sizes = [q, q, q, n - 3 * q]
+    ins, outs, slos = [], [], []
+    # (i)
+    ins.append(np.full(sizes[0], 128, np.uint32))
+    outs.append(np.full(sizes[0], 256, np.uint32))
+    slos.append(np.full(sizes[0], 30.0, np.float32))
+    # (ii)
+    a, b, _ = long_tail(sizes[1], seed, stream=51)
+    ins.append(a); outs.append(b); slos.append(np.full(sizes[1], 1e-3, np.float32))
+    # (iii)
+    a, b, c = long_tail(sizes[2], seed, stream=52)
+    big = rng.random(sizes[2]) < 0.01
+    nb = int(big.sum())
+    tot = rng.integers(16_385, 32_769, size=nb)
+    bi = np.maximum(1, (tot * rng.random(nb)).astype(np.int64))
+    bi = np.minimum(bi, tot - 1)
+    a = a.copy(); b = b.copy()
+    a[big] = bi.astype(np.uint32)
+    b[big] = (tot - bi).astype(np.uint32)
+    ins.append(a); outs.append(b); slos.append(c)
+    # (iv)
+    m = sizes[3]
+    ins.append(_lognormal_int(rng, 128, 1.0, 1, 4096, m))
+    outs.append(np.linspace(4096, 1, m).astype(np.uint32))
+    slos.append(np.linspace(1.0, 350.0, m, dtype=np.float64).astype(np.float32))
+    inp = np.concatenate(ins); out = np.concatenate(outs); slo = np.concatenate(slos)
+    cfg = SchedConfig(window=window, max_batch=256, kv_cap_bytes=C5_KV_CAP_BYTES, lambda_us=lam)
+    return inp, out, slo, cfg
+
+
+def random_small(seed: int, n: int, pattern: str = "rand"):
+    """Tiny brute-force-checkable instances with a random configuration.
+    pattern: rand | ties | bucket | identical | descending | classes."""
+    rng = _rng(seed, 9)
+    if pattern == "identical":
+        inp = np.full(n, int(rng.integers(1, 50)), np.uint32)
+        out = np.full(n, int(rng.integers(1, 50)), np.uint32)
+        slo = np.full(n, np.float32(rng.uniform(0.001, 0.5)), np.float32)
+    else:
+        inp = rng.integers(1, 40, size=n).astype(np.uint32)
+        out = rng.integers(1, 40, size=n).astype(np.uint32)
+        if pattern == "ties":
+            inp = rng.integers(1, 4, size=n).astype(np.uint32) * 8
+            out = rng.integers(1, 4, size=n).astype(np.uint32) * 8
+        if pattern == "bucket":
+            out = (rng.integers(1, 5, size=n) * 16).astype(np.uint32)
+        if pattern == "descending":
+            out = np.sort(out)[::-1].copy()
+        slo = rng.uniform(0.0005, 0.05, size=n).astype(np.float32)
+        if pattern in ("ties", "classes", "bucket"):
+            cls = np.array([0.002, 0.01, 0.03], dtype=np.float32)
+            slo = cls[rng.integers(0, 3, size=n)]
+        if pattern == "descending":
+            slo = np.sort(slo)
+    cap = int(rng.choice([0, 300, 1200, 5000, 30000]))
+    cfg = SchedConfig(
+        window=0,
+        max_batch=int(rng.integers(1, n + 2)),
+        split_on_slo_change=int(rng.integers(0, 2)),
+        kv_bytes_per_elem=int(rng.choice([1, 2, 4])),
+        n_layers=int(rng.integers(1, 4)),
+        hidden=int(rng.integers(1, 4)),
+        t_batch_us=int(rng.integers(0, 3000)),
+        t_iter_us=int(rng.integers(0, 300)),
+        t_tok_us=int(rng.integers(0, 50)),
+        t_prefill_us=int(rng.integers(0, 20)),
+        lambda_us=int(rng.choice([0, 1, 1000, 10**6, 10**9])),
+    )
+    cfg.kv_cap_bytes = cap
+    if cfg.t_batch_us == 0 and cfg.t_iter_us == 0 and rng.random() < 0.5:
+        cfg.t_batch_us = 1
+    return inp, out, slo, cfg
