@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the UELLM batch-scheduler hot path on B200 (BASELINE.json metric:
+"queries scheduled/sec (device-timed, max over ranks) and HBM GB/s vs roofline").
+
+One step = one pass of the whole hot path over one batch of synthetic queries resident in HBM:
+uellm_profile_load (validate + SLO->us + key pack) -> uellm_schedule_batches (radix sort,
+SEG-DP, traceback, offsets) -> uellm_batch_stats (per-batch stats + totals), plus, at N > 1,
+the allgather of per-rank totals (a9).  Workload at N = 1: BJ configs[3] (10^8 queries in
+10^6-query windows, c4).  Weak scaling: every rank schedules its own 10^8-query stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl uellm|reference] [--config c4]
+
+--impl reference times the CPU oracle (oracle/, as it stands) on the host cores, on a bounded
+sample of the same workload.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "queries scheduled/sec (device-timed, max over ranks)"
+UNIT = "queries/s"
+# per-candidate-evaluation lane-ops of the SEG-DP inner loop: the SASS of
+# one candidate round (loads, max updates, est, feasibility, D1 test, compaction) issues this
+# many instructions per live candidate; used to express the DP's work in lane-ops.
+DP_OPS_PER_EVAL = 64
+SMS = 148
+LANES_PER_SM = 128
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("sm_max_mhz", 1965.0), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+def workload(name: str, rank: int, n_override: int | None):
+    import workloads as W
+    if name == "c4":
+        n = n_override or 100_000_000
+        inp, out, slo, cfg = W.c4(seed=rank, n=n)
+        return "c4: 1e8 queries, 1e6-query windows, 8 SLO classes, long-tail outputs <=4096, " \
+               "LLaMA-2-7B KV cap, W=256, lambda=1e9 us", inp, out, slo, cfg
+    if name == "c3":
+        inp, out, slo, cfg = W.c3(seed=rank, n=n_override or 1_000_000)
+        return "c3: 1e6 queries, one window", inp, out, slo, cfg
+    if name == "c5":
+        inp, out, slo, cfg = W.c5(seed=rank, n=n_override or 10_000_000)
+        return "c5: 1e7 adversarial queries, 1e6-query windows", inp, out, slo, cfg
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows if len(r) >= 9 for k in range(4)
+                          if r[5 + k].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def compulsory_bytes(n: int, m: int) -> int:
+    # 12 B/query read (in, out, slo), 4 B/query order, 4 B per offset,
+    # 80 B per-batch record, totals
+    return 12 * n + 4 * n + 4 * (m + 1) + 80 * m + 112
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    k = d.get("kernels", {}).get(kernel)
+    return k.get("dram_bytes_per_launch") if k else None
+
+
+def cpu_baseline(inp, out, slo, cfg, windows: int):
+    """The oracle as it stands on the host cores, on a bounded sample (first `windows` windows)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    nq = min(len(inp), windows * cfg.window)
+    t = time.perf_counter()
+    o = oracle.schedule(inp[:nq], out[:nq], slo[:nq], cfg, nthreads=cores)
+    oracle.stats(inp[:nq], out[:nq], slo[:nq], cfg, o[0], o[1])
+    dt = time.perf_counter() - t
+    return {"value": nq / dt, "unit": UNIT, "cores": min(cores, windows), "kind": "oracle",
+            "sample": f"first {windows} windows ({nq} queries) of the same workload, schedule + stats, "
+                      f"{min(cores, windows)} threads (one window per thread), {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    desc, inp, out, slo, cfg = workload(args.config, 0, args.n)
+    cores = os.cpu_count() or 1
+    wl = cfg.window or len(inp)
+    nwin = max(1, min(cores, len(inp) // wl))
+    nq = nwin * wl
+    import oracle
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        o = oracle.schedule(inp[:nq], out[:nq], slo[:nq], cfg, nthreads=cores)
+        oracle.stats(inp[:nq], out[:nq], slo[:nq], cfg, o[0], o[1])
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.mean(times))
+    value = nq / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": desc, "sample_queries": nq, "windows": nwin},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, nwin), "kind": "oracle",
+                             "sample": f"{nwin} windows x {wl} queries per step, one window per thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="uellm", choices=["uellm", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--n", type=int, default=None, help="override query count (testing only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    desc, inp, out, slo, cfg = workload(args.config, rank, args.n)
+    n = len(inp)
+    d_in = torch.from_numpy(inp.view(np.int32)).to(dev)
+    d_out = torch.from_numpy(out.view(np.int32)).to(dev)
+    d_slo = torch.from_numpy(slo).to(dev)
+    stream = torch.cuda.Stream(device=dev)
+    g = GpuScheduler(n, cfg, device=dev)
+    K, Wm = args.steps, args.warmup
+    nst = len(U.STAGES)
+    # per-step stage events (caller-owned; recorded by the library on `stream`)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst)] for _ in range(K)]
+    ld = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for row in ev:
+            for e in row:
+                e.record(stream)          # materialise the cudaEvent_t handles
+    gather_buf = torch.zeros(world * 16, dtype=torch.int64, device=dev)
+
+    def step(k=None):
+        if k is not None:
+            ld[k][0].record(stream)
+        g.load(d_in, d_out, d_slo, stream)
+        if k is not None:
+            ld[k][1].record(stream)
+            U.set_stage_events(g.profile, ev[k])
+        g.schedule(stream)
+        g.stats(stream)
+        if world > 1:   # a9: one NCCL allgather of the per-rank totals
+            with torch.cuda.stream(stream):
+                mine = g.totals.view(torch.int64)[:13].clone()
+                mine = torch.cat([mine, torch.zeros(3, dtype=torch.int64, device=dev)])
+                dist.all_gather_into_tensor(gather_buf, mine)
+
+    for _ in range(Wm):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(K):
+        step(k)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_total = t0.elapsed_time(t1)
+    ms_step = ms_total / K
+    t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step_max = float(t.item())
+    # per-stage device times (mean over steps)
+    st_ms = {}
+    for a, b, name in [(0, 1, "sort"), (1, 2, "decode"), (2, 3, "dp_local"), (3, 4, "dp_fix"),
+                       (4, 5, "dp_cascade"), (5, 6, "traceback"), (6, 7, "compact"), (8, 9, "stats")]:
+        st_ms[name] = float(np.mean([ev[k][a].elapsed_time(ev[k][b]) for k in range(K)]))
+    st_ms["load"] = float(np.mean([ld[k][0].elapsed_time(ld[k][1]) for k in range(K)]))
+    diag = g.diagnostics(stream)
+    res = g.results()
+    m = res["m"]
+    hbm_gbs, sm_max, peak_src = peaks()
+    value = world * n / (ms_step_max / 1e3)
+
+    # dominant kernel roofline
+    dom = max(st_ms, key=st_ms.get)
+    if dom in ("dp_local", "dp_fix", "dp_cascade"):
+        evals = diag["dp_candidate_evals"]
+        dp_ms = st_ms["dp_local"] + st_ms["dp_fix"] + st_ms["dp_cascade"]
+        achieved = evals * DP_OPS_PER_EVAL / (dp_ms / 1e3) / 1e12
+        peak = SMS * LANES_PER_SM * sm_max * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "k_dp_local+k_dp_fix+k_dp_cascade", "achieved": achieved,
+                "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak,
+                "traffic": ncu_traffic("k_dp_local"),
+                "work": f"{evals} candidate evaluations x {DP_OPS_PER_EVAL} lane-ops "
+                        f"({evals / n:.1f} per query)",
+                "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32/FP32 lanes x {sm_max:.0f} MHz (guide unit counts)"}
+    else:
+        # HBM-bound stages: algorithmic bytes per launch of the stage
+        alg = {"sort": 24 * n * diag["sort_passes"], "decode": 24 * n, "stats": 12 * n + 80 * m,
+               "load": 24 * n, "traceback": 2 * n, "compact": n // 8 + 4 * m}.get(dom, 0)
+        achieved = alg / (st_ms[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
+                "frac": achieved / hbm_gbs, "traffic": ncu_traffic(dom)}
+    comp = compulsory_bytes(n, m)
+    step_hbm = {"compulsory_bytes": comp, "achieved_gbs": comp / (ms_step_max / 1e3) / 1e9,
+                "peak_gbs": hbm_gbs, "frac": comp / (ms_step_max / 1e3) / 1e9 / hbm_gbs,
+                "peak_source": peak_src}
+
+    # e2e: the C-ABI with HOST buffers (pinned), H2D/D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        p_in = torch.from_numpy(inp.view(np.int32)).pin_memory()
+        p_out = torch.from_numpy(out.view(np.int32)).pin_memory()
+        p_slo = torch.from_numpy(slo).pin_memory()
+        h_order = torch.empty(n, dtype=torch.int32).pin_memory()
+        h_offs = torch.empty(n + 1, dtype=torch.int32).pin_memory()
+        h_nb = torch.zeros(1, dtype=torch.int64).pin_memory()
+        h_tot = torch.zeros(U.TOTALS_BYTES, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            p = U.profile_load(n, p_in, p_out, p_slo, g.cfg, g.ws, g.ws_bytes, stream)
+            U.schedule_batches(p, g.cfg, h_order, h_offs, h_nb, stream)
+            U.batch_stats(p, g.cfg, h_offs, h_nb, None, h_tot, stream)
+            if world > 1:
+                with torch.cuda.stream(stream):
+                    mine = torch.from_numpy(h_tot.numpy()[:104].view(np.int64).copy()).to(dev)
+                    mine = torch.cat([mine, torch.zeros(3, dtype=torch.int64, device=dev)])
+                    dist.all_gather_into_tensor(gather_buf, mine)
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([e0.elapsed_time(e1) / K], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        mh = int(h_nb.item())
+        e2e = {"value": world * n / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 4 * n + 4 * (mh + 1) + 8 + U.TOTALS_BYTES,
+               "ms_per_step": float(te.item())}
+        assert mh == m, "host-buffer path disagrees with the device path"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        cpu = cpu_baseline(inp, out, slo, cfg, windows=min(cores, max(1, n // (cfg.window or n))))
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm,
+            "ms_per_step": ms_step_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic (workloads.c4 seeded generator, rank = seed)",
+            "config": {"workload": desc, "queries_per_rank": n, "window": cfg.window,
+                       "max_batch": cfg.max_batch, "lambda_us": cfg.lambda_us,
+                       "l2": "inputs 1.2 GB/rank >> 126 MB L2; no flush needed",
+                       "parallelism": f"{world} rank(s), windows independent, one allgather of totals"},
+            "roofline": roof, "step_hbm_roofline": step_hbm, "stage_ms": st_ms,
+            "gpu_launches": int(diag["sched_launches"] + diag["stats_launches"] + 1),
+            "diagnostics": diag, "batches": m, "dp_cost": res["totals"]["dp_cost"],
+            "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,241 @@
+/*
+ * include/uellm.h -- C ABI of the B200-native UELLM batch scheduler (libuellm.so).
+ *
+ * UELLM (arXiv 2409.14961) Sec. 4.2: the batch scheduler receives "a list of requests after
+ * profiling" and outputs "a list of batch" (Alg. 1).  This library
+ * computes that step as a data-parallel GPU path on sm_100a:
+ *
+ *   uellm_profile_load      validate the profiled queries (input length, predicted output
+ *                           length, SLO), convert SLO to integer microseconds, pack sort keys
+ *   uellm_schedule_batches  sort by (SLO, predicted length) and segment the
+ *                           sorted stream into batches (SEG-DP / Alg. 1 / FIFO / sort-only)
+ *   uellm_batch_stats       per-batch padding, generated tokens (b x O), KV-cache peak
+ *                           bytes (4*b*l*h*(s+n)), estimated latency and SLO violations
+ *
+ * Citations: P:NNN = /root/reference/PAPER.md line; S:NNN = SPEC.md line; Rk = reading k in
+ * DESIGN.md.  The C ABI is plain: no exceptions, no C++ or torch types, no global state, no
+ * allocation.  All device work is stream-ordered on `stream` (a cudaStream_t passed as void*,
+ * NULL = legacy default stream).
+ *
+ * Pointers: each pointer argument is marked [host], [device] or [host|device].  [host|device]
+ * pointers are classified with cudaPointerGetAttributes: device/managed memory is used in
+ * place; host memory (pinned or pageable) is staged through the workspace with
+ * cudaMemcpyAsync on `stream`, and a call with a host OUTPUT synchronises `stream` before it
+ * returns.  Ownership: the caller owns every buffer; the library never frees or retains them.
+ *
+ * Errors: every call returns a uellm_status.  Outputs are written only when the call returns
+ * UELLM_OK.  Argument, configuration and launch errors are detected synchronously.
+ * uellm_profile_load is the only call that always synchronises (it reads a 64-byte validation
+ * record back from the device); schedule/stats with device outputs never synchronise.
+ */
+#ifndef UELLM_H_
+#define UELLM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UELLM_ABI_VERSION 1u
+
+typedef int32_t uellm_status;
+enum {
+    UELLM_OK = 0,
+    UELLM_ERR_ARG = 1,          /* NULL / misaligned pointer, workspace too small, n >= 2^32 - 1   */
+    UELLM_ERR_CONTRACT = 2,     /* a query violates its invariants: input_len == 0,
+                                   pred_out_len == 0, SLO not finite / <= 0, or slo_us outside
+                                   [1, 2^32-1] ("contract error", S:98 typed rejection)     */
+    UELLM_ERR_CONFIG = 3,       /* config invariant violated                       */
+    UELLM_ERR_OVERFLOW = 4,     /* a KV-byte or cost bound could overflow 64 bits          */
+    UELLM_ERR_CUDA = 5,         /* a CUDA runtime call or kernel launch failed                     */
+    UELLM_ERR_UNSUPPORTED = 6   /* valid, but outside this build's limits (e.g. max_batch > 4096)  */
+};
+
+/* Segmentation of the sorted stream (uellm_config.mode). */
+enum {
+    UELLM_MODE_SEG_DP = 0,      /* exact min over contiguous segmentations of the (SLO, length)-
+                                   sorted window of sum_batches est_us + lambda * violations, under
+                                   b <= max_batch and the KV cap (R7, R8, R14) */
+    UELLM_MODE_SLO_ODBS = 1,    /* Alg. 1 literal (readings R1-R5); SLO-DBS = w1 = 0,
+                                   ODBS = w2 = 0                                            */
+    UELLM_MODE_FIFO = 2,        /* default batching baseline: arrival order, chunks of W    */
+    UELLM_MODE_SORT_ONLY = 3    /* sorted order, every query its own batch                          */
+};
+
+/* Profiled queries, caller SoA (input_len >= 1, predicted output length >= 1,
+ * slo > 0 seconds).  Element k is the query with arrival index k. */
+typedef struct {
+    uint64_t n;                     /* number of queries, < 2^32 - 1                         */
+    const uint32_t *input_len;      /* [host|device] n x Input_i (tokens)             */
+    const uint32_t *pred_out_len;   /* [host|device] n x predicted Output_i (tokens)  */
+    const float *slo_s;             /* [host|device] n x SLO_i in seconds            */
+} uellm_queries;
+
+/* Scheduler configuration.  Same meaning in every mode unless noted. */
+typedef struct {
+    uint32_t mode;                  /* UELLM_MODE_*                                                */
+    uint32_t window;                /* queries per scheduling window (consecutive arrival chunks,
+                                       R15); 0 = one window of all n.  No batch crosses a window. */
+    uint32_t max_batch;             /* W >= 1, maximum batch size; <= 4096 in this build          */
+    uint32_t split_on_slo_change;   /* 0|1: 1 = batches never mix SLO values (R15)                 */
+    uint32_t kv_bytes_per_elem;     /* the "4" of 4*b*l*h*(s+n) (R13)                        */
+    uint32_t n_layers;              /* l                                                    */
+    uint32_t hidden;                /* h                                                    */
+    uint32_t dp_tile;               /* SEG-DP tile length in queries, 0 = automatic; otherwise
+                                       rounded up to a multiple of max_batch and >= 2*max_batch.
+                                       A tuning knob: results are identical for every value.       */
+    uint64_t kv_cap_bytes;          /* per-batch KV reserve T of P:366 (R6); 0 = no cap.  A batch
+                                       of b >= 2 queries is admissible iff
+                                       kv_bytes_per_elem*b*l*h*(s+O) <= kv_cap_bytes; a single
+                                       query is always admissible (R10).                           */
+    uint32_t t_batch_us;            /* service-time model est_us = t_batch + t_iter*O            */
+    uint32_t t_iter_us;             /*      + t_tok*b*O + t_prefill*b*s   (R7; b batch size,       */
+    uint32_t t_tok_us;              /*      s max input, O max predicted output)            */
+    uint32_t t_prefill_us;
+    uint64_t lambda_us;             /* SEG-DP penalty per query whose slo_us < est_us of its own
+                                       batch (R8, R14)                                             */
+    double w1, w2;                  /* Alg. 1 weights; w1, w2 >= 0, w1 + w2 > 0        */
+    double l1, l2;                  /* Alg. 1 overheads L1, L2, >= 0                 */
+    double threshold;               /* Alg. 1 Threshold, > 0                               */
+    double eps;                     /* Alg. 1 line 20 dynamic-cap guard (R5), > 0                   */
+    uint32_t eq2_additive;          /* 0|1: Alg. 1 T_o with Eq. 2's '+' instead of '-' (R2)        */
+    uint32_t reserved;              /* must be 0                                                    */
+} uellm_config;
+
+/* One batch (UELLM_MODE_*: batch t = order[batch_offsets[t] .. batch_offsets[t+1])). 80 bytes. */
+typedef struct {
+    uint32_t start;                 /* first scheduled position of the batch                       */
+    uint32_t size;                  /* b                                                            */
+    uint32_t max_in;                /* s = max Input_i, the padded input length             */
+    uint32_t max_out;               /* O = max predicted Output_i                           */
+    uint64_t gen_tokens;            /* b x O                                                */
+    uint64_t pad_in;                /* sum (s - Input_i): input padding tokens       */
+    uint64_t pad_out;               /* sum (O - Output_i): redundant generated tokens               */
+    uint64_t kv_bytes;              /* kv_bytes_per_elem * b * l * h * (s + O)               */
+    uint64_t est_us;                /* estimated service time (R7)                                  */
+    uint64_t completion_us;         /* inclusive prefix of est_us over the window's batches
+                                       (sequential execution, all queries present at t=0)  */
+    uint32_t viol_alone;            /* members with slo_us < est_us                                 */
+    uint32_t viol_seq;              /* members with slo_us < completion_us                          */
+    uint32_t over_cap;              /* 1 if kv_cap_bytes != 0 and kv_bytes > kv_cap_bytes          */
+    uint32_t window;                /* window index                                                 */
+} uellm_batch_stat;
+
+/* Totals over all batches. */
+typedef struct {
+    uint64_t n, batches, gen_tokens, pad_in, pad_out;
+    uint64_t kv_bytes_max;
+    uint64_t dp_cost;               /* sum_batches (est_us + lambda_us * viol_alone): the SEG-DP
+                                       objective of this schedule                                  */
+    uint64_t viol_alone, viol_seq, over_cap;
+    uint64_t makespan_us;           /* sum of est_us                                        */
+    double mean_latency_s;          /* sum over queries of completion_us(batch) / n * 1e-6          */
+    double throughput_tok_s;        /* gen_tokens / (makespan_us * 1e-6)                            */
+} uellm_totals;
+
+/* Diagnostics of the last uellm_schedule_batches call on a profile (SEG-DP internals). */
+typedef struct {
+    uint64_t tiles;                 /* SEG-DP tiles                                                 */
+    uint64_t tile_len;              /* tile length (queries)                                        */
+    uint64_t fixups_unconverged;    /* tiles whose parallel fix-up did not converge in the tile     */
+    uint64_t cascade_reruns;        /* sequential fix-up re-runs performed by the cascade           */
+    uint64_t fixup_positions;       /* positions re-evaluated by fix-ups (parallel + cascade)      */
+    uint64_t trace_unmerged;        /* traceback tiles whose walk did not coalesce in the tile      */
+    uint64_t trace_rewalks;         /* full tile re-walks performed by the traceback cascade        */
+    uint64_t sort_passes;           /* radix passes actually run (constant digits are skipped)      */
+    uint64_t dp_cost;               /* SEG-DP: sum over windows of the optimal cost C[w1]; else 0   */
+    uint64_t dp_candidate_evals;    /* SEG-DP: breakpoint candidates evaluated (all passes)         */
+    uint64_t sched_launches;        /* kernels launched by the last uellm_schedule_batches          */
+    uint64_t stats_launches;        /* kernels launched by the last uellm_batch_stats               */
+} uellm_diagnostics;
+
+/* Optional per-stage timing.  Stage boundaries at which uellm_schedule_batches /
+ * uellm_batch_stats record caller-supplied CUDA events on their stream: */
+enum {
+    UELLM_STAGE_SCHED_BEGIN = 0,    /* schedule entered                                  */
+    UELLM_STAGE_SORT_END = 1,       /* radix sort done (a2/a3)                           */
+    UELLM_STAGE_DECODE_END = 2,     /* scheduled-order records written (a4)              */
+    UELLM_STAGE_DP_LOCAL_END = 3,   /* SEG-DP local tiles done (a6)                      */
+    UELLM_STAGE_DP_FIX_END = 4,     /* SEG-DP fix-ups done                               */
+    UELLM_STAGE_DP_CASCADE_END = 5, /* SEG-DP cascade done                               */
+    UELLM_STAGE_TRACE_END = 6,      /* traceback / segmentation marks done (a7)          */
+    UELLM_STAGE_SCHED_END = 7,      /* batch_offsets written                             */
+    UELLM_STAGE_STATS_BEGIN = 8,
+    UELLM_STAGE_STATS_END = 9,      /* per-batch stats + totals done (a8)                */
+    UELLM_STAGE_COUNT = 10
+};
+
+/* Opaque POD view of a loaded profile: pointers into the workspace plus host-side metadata.
+ * Valid while the workspace it was loaded into is alive and not reused by another load. */
+typedef struct {
+    uint64_t opaque[40];
+} uellm_profile;
+
+/* ABI version (UELLM_ABI_VERSION) and struct sizes, for bindings to check their layouts. [host] */
+uint32_t uellm_abi_version(void);
+uint64_t uellm_sizeof(int which);   /* 0 config, 1 batch_stat, 2 totals, 3 profile, 4 diagnostics */
+
+/* Human-readable name of a status code.  [host]  Never NULL; static storage. */
+const char *uellm_status_string(uellm_status s);
+
+/* Device workspace bytes needed to load and schedule n queries with cfg (a pure function of
+ * n, cfg->window, cfg->max_batch, cfg->dp_tile).  [host]  Returns 0 if cfg is NULL. */
+size_t uellm_workspace_bytes(uint64_t n, const uellm_config *cfg);
+
+/* Validate and load n profiled queries (Sec. 4.1 output).
+ *   q          [host] query SoA; its arrays are [host|device].  Device arrays are used in place
+ *              and must stay unchanged until the last schedule/stats call on the profile.
+ *   cfg        [host] configuration; checked here (UELLM_ERR_CONFIG).
+ *   ws         [device] workspace of ws_bytes >= uellm_workspace_bytes(n, cfg), 256-B aligned.
+ *   out        [host] receives the profile view.
+ * Computes slo_us = rint(double(slo_s) * 1e6) (half-even, R12), rejects invalid queries with
+ * UELLM_ERR_CONTRACT, and returns UELLM_ERR_OVERFLOW when
+ * window * (E + lambda*W) >= 2^63 with E = t_batch + t_iter*max_out +
+ * (t_tok*max_out + t_prefill*max_in)*W, or when kv_bytes_per_elem*l*h*W*(max_in+max_out)
+ * does not fit 64 bits.  Synchronises `stream` once (64-byte validation record). */
+uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg, void *ws,
+                                size_t ws_bytes, void *stream, uellm_profile *out);
+
+/* Sort and segment the loaded queries (Alg. 1 stages 1-3; SEG-DP, R14).
+ *   p              [host] profile from uellm_profile_load (same cfg).
+ *   order          [host|device] n x u32: caller index of the query at scheduled position k.
+ *                  Windows ascending; inside a window (slo_us, pred_out_len, index) ascending
+ *                  (R11, R9) except UELLM_MODE_FIFO (arrival order).
+ *   batch_offsets  [host|device] capacity n+1 x u32: batch t is positions
+ *                  [batch_offsets[t], batch_offsets[t+1]); batch_offsets[0] = 0,
+ *                  batch_offsets[num_batches] = n.  Batches in scan order.
+ *   num_batches    [host|device] 1 x u64.
+ * SEG-DP ties: the smallest minimising breakpoint at every position (R9).  The device-side
+ * results of the call also remain in the workspace for uellm_batch_stats. */
+uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *cfg,
+                                    uint32_t *order, uint32_t *batch_offsets,
+                                    uint64_t *num_batches, void *stream);
+
+/* Per-batch statistics of the schedule produced by the
+ * last uellm_schedule_batches call on p.
+ *   batch_offsets, num_batches  [host|device] that call's outputs.  Device pointers may hold
+ *                  a caller-modified segmentation of the same order.  Host pointers are accepted
+ *                  only when that schedule call also returned its results to host memory; the
+ *                  library then reads the workspace copy it staged them through.
+ *   per_batch      [device] capacity num_batches x uellm_batch_stat, or NULL.
+ *   totals         [host|device] 1 x uellm_totals.
+ * Integer statistics are exact; mean_latency_s and throughput_tok_s are doubles computed from
+ * exact 128-bit / 64-bit integer sums. */
+uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg,
+                               const uint32_t *batch_offsets, const uint64_t *num_batches,
+                               uellm_batch_stat *per_batch, uellm_totals *totals, void *stream);
+
+/* Attach (n <= UELLM_STAGE_COUNT) caller-owned cudaEvent_t handles (void*, created with timing
+ * enabled; NULL entries are skipped) to the profile; subsequent schedule/stats calls record
+ * event k at stage boundary k on their stream.  n = 0 detaches.  [host] */
+uellm_status uellm_set_stage_events(uellm_profile *p, void *const *events, uint32_t n);
+
+/* Diagnostics of the last schedule call on p.  [host] out; synchronises `stream`. */
+uellm_status uellm_get_diagnostics(const uellm_profile *p, uellm_diagnostics *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UELLM_H_ */

@@ -1,0 +1,436 @@
+// abi.cu -- the C ABI of include/uellm.h: argument/config validation, workspace carving and
+// stream-ordered orchestration of the kernels (host code only; no allocation, no globals).
+#include <cstring>
+
+#include "internal.cuh"
+
+using namespace uellm;
+
+namespace uellm {
+
+uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_tile)
+{
+    uint64_t T;
+    if (dp_tile) {
+        T = align_up(dp_tile, W);
+    } else {
+        const uint64_t target_tiles = 148ull * 24;   // ~24 resident DP warps per SM
+        T = ceil_div(n ? n : 1, target_tiles);
+        T = T < 16ull * W ? 16ull * W : T;
+        T = align_up(T, W);
+    }
+    if (T < 2ull * W) T = 2ull * W;
+    if (T > window) T = align_up(window, W);   // one tile per window
+    return T;
+}
+
+WsLayout make_layout(uint64_t n, const uellm_config &cfg)
+{
+    WsLayout L;
+    std::memset(&L, 0, sizeof L);
+    L.n = n;
+    L.window = cfg.window ? (cfg.window < n ? cfg.window : n) : n;
+    if (L.window == 0) L.window = 1;
+    L.nwin = n ? ceil_div(n, L.window) : 0;
+    L.W = cfg.max_batch ? cfg.max_batch : 1;
+    L.tile_len = choose_tile_len(n, L.window, (uint32_t)L.W, cfg.dp_tile);
+    L.tpw = ceil_div(L.window, L.tile_len);
+    L.ntiles = L.tpw * L.nwin;
+    L.sort_tpw = ceil_div(L.window, kSortTile);
+    L.sort_tiles = L.sort_tpw * L.nwin;
+    L.nwords = (n + 1 + 31) / 32;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
+    const uint64_t N = n ? n : 1;
+    L.stage_in = take(4 * N); L.stage_out = take(4 * N); L.stage_slo = take(4 * N);
+    L.keys0 = take(8 * N); L.keys1 = take(8 * N); L.keys2 = take(8 * N);
+    L.vals0 = take(4 * N); L.vals1 = take(4 * N); L.vals2 = take(4 * N);
+    L.rin = take(4 * N); L.rout = take(4 * N); L.rslo = take(4 * N);
+    L.order = take(4 * N); L.offsets = take(4 * (N + 1));
+    L.argx = take(2 * N);
+    L.tiles = take(sizeof(TileRec) * (L.ntiles ? L.ntiles : 1));
+    L.bitmap = take(4 * L.nwords); L.wscan = take(4 * L.nwords);
+    const uint64_t nblk = ceil_div(L.nwords, kScanBlock) + ceil_div(N, kScanBlock) + 2;
+    L.blocksum = take(4 * nblk);
+    L.blockagg = take(8 * nblk);
+    L.hist = take(4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));
+    L.meta = take(sizeof(LoadMeta)); L.diag = take(sizeof(Diag)); L.acc = take(sizeof(StatAcc));
+    L.nb = take(8); L.totals = take(sizeof(uellm_totals));
+    L.wincost = take(8 * (L.nwin ? L.nwin : 1));
+    L.total = off;
+    return L;
+}
+
+}  // namespace uellm
+
+namespace {
+
+template <class T>
+T *at(uint8_t *ws, uint64_t off) { return reinterpret_cast<T *>(ws + off); }
+
+bool is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+uellm_status check_config(const uellm_config *c)
+{
+    if (c->mode > UELLM_MODE_SORT_ONLY) return UELLM_ERR_CONFIG;
+    if (c->max_batch < 1) return UELLM_ERR_CONFIG;
+    if (c->split_on_slo_change > 1 || c->eq2_additive > 1 || c->reserved != 0) return UELLM_ERR_CONFIG;
+    if (c->mode == UELLM_MODE_SLO_ODBS) {
+        if (!(c->w1 >= 0.0) || !(c->w2 >= 0.0) || !(c->w1 + c->w2 > 0.0)) return UELLM_ERR_CONFIG;
+        if (!(c->threshold > 0.0) || !(c->eps > 0.0) || !(c->l1 >= 0.0) || !(c->l2 >= 0.0)) return UELLM_ERR_CONFIG;
+    }
+    if (c->kv_cap_bytes != 0 && (c->kv_bytes_per_elem == 0 || c->n_layers == 0 || c->hidden == 0))
+        return UELLM_ERR_CONFIG;
+    if (c->max_batch > kMaxBatchLimit) return UELLM_ERR_UNSUPPORTED;
+    return UELLM_OK;
+}
+
+inline const ProfileView *view_of(const uellm_profile *p) { return reinterpret_cast<const ProfileView *>(p); }
+
+uint64_t layout_key(const uellm_config *c)
+{
+    return ((uint64_t)c->window << 32) ^ ((uint64_t)c->max_batch << 8) ^ ((uint64_t)c->dp_tile * 0x9E3779B97F4A7C15ull);
+}
+
+inline void rec(const ProfileView &v, int k, cudaStream_t st)
+{
+    if ((uint64_t)k < v.n_events && v.events[k]) cudaEventRecord((cudaEvent_t)v.events[k], st);
+}
+
+#define CU(x)                                   \
+    do {                                        \
+        if ((x) != cudaSuccess) {               \
+            cudaGetLastError();                 \
+            return UELLM_ERR_CUDA;              \
+        }                                       \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+uint32_t uellm_abi_version(void) { return UELLM_ABI_VERSION; }
+
+uint64_t uellm_sizeof(int which)
+{
+    switch (which) {
+    case 0: return sizeof(uellm_config);
+    case 1: return sizeof(uellm_batch_stat);
+    case 2: return sizeof(uellm_totals);
+    case 3: return sizeof(uellm_profile);
+    case 4: return sizeof(uellm_diagnostics);
+    default: return 0;
+    }
+}
+
+const char *uellm_status_string(uellm_status s)
+{
+    switch (s) {
+    case UELLM_OK: return "UELLM_OK";
+    case UELLM_ERR_ARG: return "UELLM_ERR_ARG";
+    case UELLM_ERR_CONTRACT: return "UELLM_ERR_CONTRACT";
+    case UELLM_ERR_CONFIG: return "UELLM_ERR_CONFIG";
+    case UELLM_ERR_OVERFLOW: return "UELLM_ERR_OVERFLOW";
+    case UELLM_ERR_CUDA: return "UELLM_ERR_CUDA";
+    case UELLM_ERR_UNSUPPORTED: return "UELLM_ERR_UNSUPPORTED";
+    default: return "UELLM_ERR_UNKNOWN";
+    }
+}
+
+size_t uellm_workspace_bytes(uint64_t n, const uellm_config *cfg)
+{
+    if (!cfg) return 0;
+    return (size_t)make_layout(n, *cfg).total;
+}
+
+uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg, void *ws, size_t ws_bytes,
+                                void *stream, uellm_profile *out)
+{
+    if (!q || !cfg || !out) return UELLM_ERR_ARG;
+    const uint64_t n = q->n;
+    if (n >= 0xffffffffull) return UELLM_ERR_ARG;
+    if (n > 0 && (!q->input_len || !q->pred_out_len || !q->slo_s)) return UELLM_ERR_ARG;
+    uellm_status s = check_config(cfg);
+    if (s != UELLM_OK) return s;
+    const WsLayout L = make_layout(n, *cfg);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255) || ws_bytes < L.total) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = (uint8_t *)ws;
+
+    ProfileView v;
+    std::memset(&v, 0, sizeof v);
+    v.magic = kProfileMagic;
+    v.n = n; v.window = L.window; v.nwin = L.nwin; v.ws = w; v.ws_bytes = ws_bytes;
+    v.W = cfg->max_batch;
+    v.cfg_hash = layout_key(cfg);
+    v.diag_off = L.diag;
+    v.wincost_off = L.wincost;
+    if (n == 0) {
+        std::memcpy(out, &v, sizeof v);
+        return UELLM_OK;
+    }
+    const uint32_t *din = q->input_len, *dout = q->pred_out_len;
+    const float *dslo = q->slo_s;
+    if (!is_device_ptr(din)) {
+        CU(cudaMemcpyAsync(at<uint32_t>(w, L.stage_in), din, 4 * n, cudaMemcpyHostToDevice, st));
+        din = at<uint32_t>(w, L.stage_in);
+    }
+    if (!is_device_ptr(dout)) {
+        CU(cudaMemcpyAsync(at<uint32_t>(w, L.stage_out), dout, 4 * n, cudaMemcpyHostToDevice, st));
+        dout = at<uint32_t>(w, L.stage_out);
+    }
+    if (!is_device_ptr(dslo)) {
+        CU(cudaMemcpyAsync(at<float>(w, L.stage_slo), dslo, 4 * n, cudaMemcpyHostToDevice, st));
+        dslo = at<float>(w, L.stage_slo);
+    }
+    LoadMeta *meta = at<LoadMeta>(w, L.meta);
+    CU(cudaMemsetAsync(meta, 0, sizeof(LoadMeta), st));
+    CU(cudaMemsetAsync(&meta->key_and, 0xff, sizeof(unsigned long long), st));
+    CU(launch_load(din, dout, dslo, n, at<unsigned long long>(w, L.keys0), at<uint32_t>(w, L.vals0), meta, st));
+    LoadMeta hm;
+    CU(cudaMemcpyAsync(&hm, meta, sizeof hm, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (hm.bad) return UELLM_ERR_CONTRACT;
+    // overflow bounds (checked once, with the true maxima)
+    typedef unsigned __int128 u128;
+    const u128 W = cfg->max_batch;
+    const u128 E = (u128)cfg->t_batch_us + (u128)cfg->t_iter_us * hm.max_out +
+                   ((u128)cfg->t_tok_us * hm.max_out + (u128)cfg->t_prefill_us * hm.max_in) * W;
+    const u128 bound = (u128)L.window * (E + (u128)cfg->lambda_us * W);
+    if (bound >= ((u128)1 << 63)) return UELLM_ERR_OVERFLOW;
+    const u128 kv = (u128)cfg->kv_bytes_per_elem * cfg->n_layers * cfg->hidden * W * ((u128)hm.max_in + hm.max_out);
+    if (kv >= ((u128)1 << 64)) return UELLM_ERR_OVERFLOW;
+    v.d_in = din; v.d_out = dout;
+    v.max_in = hm.max_in; v.max_out = hm.max_out; v.max_slo = hm.max_slo;
+    v.key_or = hm.key_or; v.key_and = hm.key_and;
+    std::memcpy(out, &v, sizeof v);
+    return UELLM_OK;
+}
+
+uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *cfg, uint32_t *order,
+                                    uint32_t *batch_offsets, uint64_t *num_batches, void *stream)
+{
+    if (!p || !cfg || !num_batches) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
+    uellm_status s = check_config(cfg);
+    if (s != UELLM_OK) return s;
+    const uint64_t n = v.n;
+    if (n > 0 && (!order || !batch_offsets)) return UELLM_ERR_ARG;
+    if (!batch_offsets) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = v.ws;
+    const WsLayout L = make_layout(n, *cfg);
+    if (L.total > v.ws_bytes) return UELLM_ERR_ARG;
+    const bool dev_order = n == 0 || is_device_ptr(order);
+    const bool dev_offs = is_device_ptr(batch_offsets);
+    const bool dev_nb = is_device_ptr(num_batches);
+    uint32_t *d_order = dev_order ? order : at<uint32_t>(w, L.order);
+    uint32_t *d_offs = dev_offs ? batch_offsets : at<uint32_t>(w, L.offsets);
+    unsigned long long *d_nb = dev_nb ? (unsigned long long *)num_batches : at<unsigned long long>(w, L.nb);
+    Diag *diag = at<Diag>(w, L.diag);
+    {
+        Diag hd;
+        std::memset(&hd, 0, sizeof hd);
+        hd.tiles = cfg->mode == UELLM_MODE_SEG_DP ? L.ntiles : 0;
+        hd.tile_len = L.tile_len;
+        CU(cudaMemcpyAsync(diag, &hd, sizeof hd, cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(at<unsigned long long>(w, L.wincost), 0, 8 * (L.nwin ? L.nwin : 1), st));
+    }
+    rec(v, UELLM_STAGE_SCHED_BEGIN, st);
+    int launches = 0;
+    if (n == 0) {
+        const uint32_t zero32 = 0;
+        const uint64_t zero64 = 0;
+        if (dev_offs) { CU(cudaMemcpyAsync(batch_offsets, &zero32, 4, cudaMemcpyHostToDevice, st)); }
+        else batch_offsets[0] = 0;
+        if (dev_nb) { CU(cudaMemcpyAsync(num_batches, &zero64, 8, cudaMemcpyHostToDevice, st)); }
+        else *num_batches = 0;
+        if (!dev_offs || !dev_nb) CU(cudaStreamSynchronize(st));
+        return UELLM_OK;
+    }
+    // a3: sort (every mode except FIFO)
+    const unsigned long long *keys = at<unsigned long long>(w, L.keys0);
+    const uint32_t *vals = at<uint32_t>(w, L.vals0);
+    int passes = 0;
+    if (cfg->mode != UELLM_MODE_FIFO) {
+        const unsigned long long vary = v.key_or ^ v.key_and;
+        uint32_t mask = 0;
+        for (int d = 0; d < 8; ++d) if ((vary >> (8 * d)) & 0xffull) mask |= 1u << d;
+        CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
+                              at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
+                              at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st));
+        launches += 3 * passes;
+    }
+    rec(v, UELLM_STAGE_SORT_END, st);
+    uint32_t *rin = at<uint32_t>(w, L.rin), *rout = at<uint32_t>(w, L.rout), *rslo = at<uint32_t>(w, L.rslo);
+    CU(launch_decode(keys, vals, v.d_in, n, rin, rout, rslo, d_order, st));
+    launches += 1;
+    rec(v, UELLM_STAGE_DECODE_END, st);
+    {
+        unsigned long long sp = (unsigned long long)passes;
+        CU(cudaMemcpyAsync(&diag->sort_passes, &sp, 8, cudaMemcpyHostToDevice, st));
+    }
+    // a6/a7: segmentation -> boundary bitmap
+    uint32_t *bm = at<uint32_t>(w, L.bitmap);
+    CU(cudaMemsetAsync(bm, 0, 4 * L.nwords, st));
+    const unsigned long long unit =
+        (unsigned long long)cfg->kv_bytes_per_elem * cfg->n_layers * cfg->hidden;
+    const unsigned long long cap_tok = cfg->kv_cap_bytes ? cfg->kv_cap_bytes / unit : ~0ull;
+    if (cfg->mode == UELLM_MODE_SEG_DP) {
+        DPParams P;
+        std::memset(&P, 0, sizeof P);
+        P.rin = rin; P.rout = rout; P.rslo = rslo;
+        P.Cx = at<long long>(w, L.keys1); P.CFx = at<long long>(w, L.keys2);
+        P.argx = at<uint16_t>(w, L.argx);
+        P.tiles = at<TileRec>(w, L.tiles);
+        P.diag = diag;
+        P.wincost = at<unsigned long long>(w, L.wincost);
+        P.n = (uint32_t)n; P.window = (uint32_t)L.window; P.nwin = (uint32_t)L.nwin;
+        P.tile_len = (uint32_t)L.tile_len; P.tpw = (uint32_t)L.tpw; P.W = cfg->max_batch;
+        P.cap_slots = (uint32_t)align_up(cfg->max_batch + 1, 32);
+        P.split = cfg->split_on_slo_change;
+        P.cap_tok = cap_tok;
+        P.t_batch = cfg->t_batch_us; P.t_iter = cfg->t_iter_us; P.t_tok = cfg->t_tok_us;
+        P.t_pre = cfg->t_prefill_us; P.lambda = cfg->lambda_us;
+        void *ev[3] = {nullptr, nullptr, nullptr};
+        for (int k = 0; k < 3; ++k)
+            if ((uint64_t)(UELLM_STAGE_DP_LOCAL_END + k) < v.n_events) ev[k] = v.events[UELLM_STAGE_DP_LOCAL_END + k];
+        int dl = 0;
+        CU(run_segdp(P, L.ntiles, st, ev, &dl));
+        launches += dl;
+        CU(run_traceback(P, bm, L.ntiles, st));
+        launches += 3;
+    } else if (cfg->mode == UELLM_MODE_SLO_ODBS) {
+        Alg1Params A;
+        std::memset(&A, 0, sizeof A);
+        A.rin = rin; A.rout = rout; A.rslo = rslo;
+        A.n = (uint32_t)n; A.window = (uint32_t)L.window; A.nwin = (uint32_t)L.nwin; A.W = cfg->max_batch;
+        A.split = cfg->split_on_slo_change; A.cap_tok = cap_tok;
+        A.w1 = cfg->w1; A.w2 = cfg->w2; A.l1 = cfg->l1; A.l2 = cfg->l2; A.threshold = cfg->threshold;
+        A.eps = cfg->eps; A.eq2_additive = cfg->eq2_additive;
+        rec(v, UELLM_STAGE_DP_LOCAL_END, st); rec(v, UELLM_STAGE_DP_FIX_END, st); rec(v, UELLM_STAGE_DP_CASCADE_END, st);
+        CU(launch_alg1(A, bm, st));
+        launches += 1;
+    } else {
+        rec(v, UELLM_STAGE_DP_LOCAL_END, st); rec(v, UELLM_STAGE_DP_FIX_END, st); rec(v, UELLM_STAGE_DP_CASCADE_END, st);
+        CU(launch_mark_fifo(bm, n, L.window, cfg->max_batch, cfg->mode == UELLM_MODE_SORT_ONLY, st));
+        launches += 1;
+    }
+    rec(v, UELLM_STAGE_TRACE_END, st);
+    // a7: compaction -> batch_offsets, num_batches (also kept in the workspace for stats)
+    CU(run_compact(bm, n, at<uint32_t>(w, L.wscan), at<uint32_t>(w, L.blocksum), d_offs, d_nb, st));
+    launches += 3;
+    rec(v, UELLM_STAGE_SCHED_END, st);
+    {
+        unsigned long long lc = (unsigned long long)launches;
+        CU(cudaMemcpyAsync(&diag->sched_launches, &lc, 8, cudaMemcpyHostToDevice, st));
+    }
+    if (!dev_order || !dev_offs || !dev_nb) {
+        uint64_t m = 0;
+        CU(cudaMemcpyAsync(&m, d_nb, 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (!dev_nb) *num_batches = m;
+        if (!dev_offs) CU(cudaMemcpyAsync(batch_offsets, d_offs, 4 * (m + 1), cudaMemcpyDeviceToHost, st));
+        if (!dev_order) CU(cudaMemcpyAsync(order, d_order, 4 * n, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    CU(cudaGetLastError());
+    return UELLM_OK;
+}
+
+uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg, const uint32_t *batch_offsets,
+                               const uint64_t *num_batches, uellm_batch_stat *per_batch, uellm_totals *totals,
+                               void *stream)
+{
+    if (!p || !cfg || !totals || !batch_offsets || !num_batches) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
+    uellm_status s = check_config(cfg);
+    if (s != UELLM_OK) return s;
+    if (per_batch && !is_device_ptr(per_batch)) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = v.ws;
+    const uint64_t n = v.n;
+    const WsLayout L = make_layout(n, *cfg);
+    const bool dev_tot = is_device_ptr(totals);
+    const uint32_t *d_offs = is_device_ptr(batch_offsets) ? batch_offsets : at<uint32_t>(w, L.offsets);
+    const unsigned long long *d_nb = is_device_ptr(num_batches) ? (const unsigned long long *)num_batches
+                                                                : at<unsigned long long>(w, L.nb);
+    if (n == 0) d_nb = at<unsigned long long>(w, L.nb);
+    if (n == 0) CU(cudaMemsetAsync(at<unsigned long long>(w, L.nb), 0, 8, st));
+    uellm_totals *d_tot = dev_tot ? totals : at<uellm_totals>(w, L.totals);
+    StatsParams S;
+    std::memset(&S, 0, sizeof S);
+    S.rin = at<uint32_t>(w, L.rin); S.rout = at<uint32_t>(w, L.rout); S.rslo = at<uint32_t>(w, L.rslo);
+    S.offsets = d_offs; S.num_batches = d_nb; S.n_cap = n; S.window = (uint32_t)L.window; S.nwin = (uint32_t)L.nwin;
+    S.est = at<unsigned long long>(w, L.keys1); S.compl_ = at<unsigned long long>(w, L.keys2);
+    S.blocksum_u32 = at<uint32_t>(w, L.blocksum); S.blockagg = at<unsigned long long>(w, L.blockagg);
+    S.per_batch = per_batch; S.acc = at<StatAcc>(w, L.acc); S.totals = d_tot; S.n = n;
+    S.kv_unit = (unsigned long long)cfg->kv_bytes_per_elem * cfg->n_layers * cfg->hidden;
+    S.kv_cap = cfg->kv_cap_bytes;
+    S.t_batch = cfg->t_batch_us; S.t_iter = cfg->t_iter_us; S.t_tok = cfg->t_tok_us; S.t_pre = cfg->t_prefill_us;
+    S.lambda = cfg->lambda_us;
+    rec(v, UELLM_STAGE_STATS_BEGIN, st);
+    CU(run_stats(S, st));
+    rec(v, UELLM_STAGE_STATS_END, st);
+    {
+        unsigned long long lc = n ? 6ull : 1ull;
+        CU(cudaMemcpyAsync(&at<Diag>(w, L.diag)->stats_launches, &lc, 8, cudaMemcpyHostToDevice, st));
+    }
+    if (!dev_tot) {
+        CU(cudaMemcpyAsync(totals, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    return UELLM_OK;
+}
+
+uellm_status uellm_set_stage_events(uellm_profile *p, void *const *events, uint32_t n)
+{
+    if (!p || n > UELLM_STAGE_COUNT || (n && !events)) return UELLM_ERR_ARG;
+    ProfileView &v = *reinterpret_cast<ProfileView *>(p);
+    if (v.magic != kProfileMagic) return UELLM_ERR_ARG;
+    for (uint32_t k = 0; k < UELLM_STAGE_COUNT; ++k) v.events[k] = k < n ? events[k] : nullptr;
+    v.n_events = n;
+    return UELLM_OK;
+}
+
+uellm_status uellm_get_diagnostics(const uellm_profile *p, uellm_diagnostics *out, void *stream)
+{
+    if (!p || !out) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    Diag hd;
+    CU(cudaMemcpyAsync(&hd, v.ws + v.diag_off, sizeof hd, cudaMemcpyDeviceToHost, st));
+    uint64_t nwin = v.nwin;
+    uint64_t cost = 0;
+    if (nwin) {
+        uint64_t *wc = new uint64_t[nwin];
+        if (cudaMemcpyAsync(wc, v.ws + v.wincost_off, 8 * nwin, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            delete[] wc;
+            cudaGetLastError();
+            return UELLM_ERR_CUDA;
+        }
+        for (uint64_t i = 0; i < nwin; ++i) cost += wc[i];
+        delete[] wc;
+    } else {
+        CU(cudaStreamSynchronize(st));
+    }
+    out->tiles = hd.tiles; out->tile_len = hd.tile_len; out->fixups_unconverged = hd.fixups_unconverged;
+    out->cascade_reruns = hd.cascade_reruns; out->fixup_positions = hd.fixup_positions;
+    out->trace_unmerged = hd.trace_unmerged; out->trace_rewalks = hd.trace_rewalks;
+    out->sort_passes = hd.sort_passes; out->dp_cost = cost;
+    out->dp_candidate_evals = hd.dp_evals; out->sched_launches = hd.sched_launches;
+    out->stats_launches = hd.stats_launches;
+    return UELLM_OK;
+}
+
+}  // extern "C"

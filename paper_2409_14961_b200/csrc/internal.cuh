@@ -1,0 +1,167 @@
+// internal.cuh -- shared declarations of the libuellm CUDA path (sm_100a).
+// Product code only: nothing here is shared with oracle/ (the CPU oracle has its own types).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/uellm.h"
+
+namespace uellm {
+
+constexpr uint32_t kMaxBatchLimit = 4096;      // W limit of this build (UELLM_ERR_UNSUPPORTED)
+constexpr uint32_t kSortTile = 4096;           // keys per radix-sort CTA (256 threads x 16)
+constexpr uint32_t kSortThreads = 256;
+constexpr uint32_t kSortItems = kSortTile / kSortThreads;
+constexpr uint32_t kDpWarpsPerCta = 8;
+constexpr uint32_t kScanBlock = 1024;          // elements per CTA in the scan kernels
+constexpr uint64_t kProfileMagic = 0x55454c4c4d763031ull;  // "UELLMv01"
+
+static inline __host__ __device__ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+static inline __host__ __device__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// --------------------------------------------------------------------------------------
+// Device-side validation record written by the load kernel (read back once, 64 bytes).
+struct LoadMeta {
+    uint32_t bad;            // bit 0 input_len == 0, bit 1 out == 0, bit 2 SLO invalid
+    uint32_t max_in, max_out, max_slo;
+    unsigned long long key_or, key_and;
+    uint32_t pad[8];
+};
+static_assert(sizeof(LoadMeta) == 64, "LoadMeta is 64 bytes");
+
+// Per-tile state of the SEG-DP and the traceback (one record per tile).
+struct TileRec {
+    uint32_t s, e;           // the tile decides boundaries (s, e]
+    uint32_t conv;           // fix-up converged (tile 0 of a window: 1)
+    uint32_t conv_pos;       // boundary at which the fix-up converged
+    uint32_t fix_end;        // last boundary whose arg the fix-up wrote
+    uint32_t valid;          // tile exists
+    int64_t delta;           // C_fix - C_local on the converged region
+    int64_t off_local;       // true C = Cx + off_local for boundaries > conv_pos   (cascade)
+    int64_t off_fix;         // true C = CFx + off_fix for boundaries <= fix_end       (cascade)
+    uint32_t exitA, exitB;   // traceback: exit of the walk from e / from the true entry
+    uint32_t merged, pad;
+};
+
+struct Diag {                // device counters, see uellm_diagnostics
+    unsigned long long tiles, tile_len, fixups_unconverged, cascade_reruns, fixup_positions,
+        trace_unmerged, trace_rewalks, sort_passes, dp_evals, sched_launches, stats_launches;
+};
+
+// Exact 128-bit accumulator of sum(b * completion_us) for mean_latency_s.
+struct StatAcc {
+    unsigned long long gen, pad_in, pad_out, kv_max, dp_cost, viol_alone, viol_seq, over_cap,
+        makespan, lat_lo, lat_hi, batches;
+};
+
+// --------------------------------------------------------------------------------------
+// Workspace layout (byte offsets from the workspace base, 256-B aligned).
+struct WsLayout {
+    uint64_t n, nwin, window, W, tile_len, tpw, ntiles, sort_tpw, sort_tiles, nwords;
+    uint64_t stage_in, stage_out, stage_slo;      // host-input staging
+    uint64_t keys0, keys1, keys2;                 // packed keys (kept) + sort ping-pong;
+    uint64_t vals0, vals1, vals2;                 // keys1/keys2 re-used as Cx/CFx, est/completion
+    uint64_t rin, rout, rslo;                     // scheduled-order records
+    uint64_t order, offsets;                      // internal copies of the schedule
+    uint64_t argx;                                // u16 per position
+    uint64_t tiles;                               // TileRec[ntiles]
+    uint64_t bitmap, wscan, blocksum, blockagg;   // boundary bitmap + scan scratch
+    uint64_t hist;                                // u32[sort_tiles * 256]
+    uint64_t meta, diag, acc, nb, totals, wincost;
+    uint64_t total;
+};
+
+// Host-side POD view stored inside uellm_profile (<= 320 bytes).
+struct ProfileView {
+    uint64_t magic;
+    uint64_t n, window, nwin;
+    uint8_t *ws;
+    uint64_t ws_bytes;
+    const uint32_t *d_in, *d_out;                 // caller device arrays or staging copies
+    uint32_t max_in, max_out, max_slo, W;
+    unsigned long long key_or, key_and;
+    uint64_t cfg_hash;
+    uint64_t diag_off, wincost_off;               // workspace offsets read by get_diagnostics
+    uint64_t n_events;
+    void *events[UELLM_STAGE_COUNT];              // caller cudaEvent_t handles (stage timing)
+    uint64_t pad[11];
+};
+static_assert(sizeof(ProfileView) <= sizeof(uellm_profile), "ProfileView fits uellm_profile");
+
+WsLayout make_layout(uint64_t n, const uellm_config &cfg);
+uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_tile);
+
+// --------------------------------------------------------------------------------------
+// Kernel launchers (each returns cudaGetLastError()).
+cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
+                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, cudaStream_t st);
+
+// Segmented (per-window) stable LSD radix sort of (key, val) over the digits of
+// `digit_mask` (bit d set = digit d of 8 bits varies).  *keys_io / *vals_io is the (read-only)
+// input; passes alternate between buffers A and B and on return *keys_io / *vals_io point at
+// the sorted result (the input itself when no digit varies).  *passes = passes run.
+cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
+                               unsigned long long *keys_a, uint32_t *vals_a,
+                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
+                               uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
+                               int *passes, cudaStream_t st);
+
+// Decode sorted keys into records: slo = key >> 32, out = key & 0xffffffff, idx = val.
+cudaError_t launch_decode(const unsigned long long *keys, const uint32_t *vals, const uint32_t *in,
+                          uint64_t n, uint32_t *rin, uint32_t *rout, uint32_t *rslo,
+                          uint32_t *order, cudaStream_t st);
+
+struct DPParams {
+    const uint32_t *rin, *rout, *rslo;
+    long long *Cx, *CFx;
+    uint16_t *argx;
+    TileRec *tiles;
+    Diag *diag;
+    unsigned long long *wincost;
+    uint32_t n, window, nwin, tile_len, tpw, W, cap_slots, split;
+    unsigned long long cap_tok;                  // ~0ull = no cap
+    unsigned long long t_batch, t_iter, t_tok, t_pre, lambda;
+};
+// ev[0..2]: events recorded after the local, fix-up and cascade kernels (NULL = none).
+cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void *const ev[3], int *launches);
+
+// Traceback of SEG-DP args into the boundary bitmap.
+cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, cudaStream_t st);
+
+// Bitmaps of the other modes.
+cudaError_t launch_mark_fifo(uint32_t *bitmap, uint64_t n, uint64_t window, uint32_t W, int sort_only,
+                             cudaStream_t st);
+struct Alg1Params {
+    const uint32_t *rin, *rout, *rslo;
+    uint32_t n, window, nwin, W, split;
+    unsigned long long cap_tok;
+    double w1, w2, l1, l2, threshold, eps;
+    uint32_t eq2_additive;
+};
+cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, cudaStream_t st);
+
+// Compaction of the boundary bitmap (n+1 bits) into batch_offsets, num_batches.
+cudaError_t run_compact(const uint32_t *bitmap, uint64_t n, uint32_t *wscan, uint32_t *blocksum,
+                        uint32_t *offsets, unsigned long long *num_batches, cudaStream_t st);
+
+struct StatsParams {
+    const uint32_t *rin, *rout, *rslo;
+    const uint32_t *offsets;
+    const unsigned long long *num_batches;
+    uint64_t n_cap;                             // capacity bound of batches (n)
+    uint32_t window, nwin;
+    unsigned long long *est, *compl_;
+    uint32_t *blocksum_u32;                     // scratch
+    unsigned long long *blockagg;               // scratch
+    uellm_batch_stat *per_batch;
+    StatAcc *acc;
+    uellm_totals *totals;
+    uint64_t n;
+    unsigned long long kv_unit;                 // kv_bytes_per_elem * l * h
+    unsigned long long kv_cap;                  // 0 = none
+    unsigned long long t_batch, t_iter, t_tok, t_pre, lambda;
+};
+cudaError_t run_stats(const StatsParams &S, cudaStream_t st);
+
+}  // namespace uellm

@@ -1,0 +1,186 @@
+// k_sort.cu -- a3: stable LSD radix sort of (key, arrival index), segmented by scheduling
+// window (P:228 / P:256 "sort by SLO in ascending order", with the predicted length as
+// secondary key, R11).  8-bit digits; digits constant over all keys are skipped.
+//
+// Per pass (reduce-then-scan):
+//   k_sort_up    per 4096-key tile (tiles never cross a window): digit histogram, warp-
+//                aggregated with match.any (skewed class-valued SLO digits would otherwise
+//                serialise on a few shared-memory bins).
+//   k_sort_scan  per window: exclusive offsets of (tile, digit) in window-major order.
+//   k_sort_down  per tile: stable rank of every key (match.any peers + per-warp running
+//                counts), then scatter.  Stability: tile order, warp order, iteration order,
+//                lane order all follow input order.
+#include "internal.cuh"
+
+namespace uellm {
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void tile_range(uint64_t t, uint64_t n, uint64_t window, uint64_t tpw,
+                                           uint64_t &start, uint64_t &end)
+{
+    uint64_t w = t / tpw, k = t % tpw;
+    uint64_t w0 = w * window, wend = min(w0 + window, n);
+    start = w0 + k * kSortTile;
+    end = min(start + kSortTile, wend);
+    if (start > end) start = end;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_up(const unsigned long long *__restrict__ kin,
+                                                          uint32_t *__restrict__ hist, uint64_t n,
+                                                          uint64_t window, uint64_t tpw, int shift)
+{
+    __shared__ uint32_t h[256];
+    const int tid = threadIdx.x;
+    h[tid] = 0;
+    __syncthreads();
+    uint64_t start, end;
+    tile_range(blockIdx.x, n, window, tpw, start, end);
+#pragma unroll 4
+    for (uint32_t i = 0; i < kSortItems; ++i) {
+        uint64_t p = start + (uint64_t)i * kSortThreads + tid;
+        bool valid = p < end;
+        uint32_t act = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            uint32_t d = (uint32_t)(kin[p] >> shift) & 0xffu;
+            uint32_t peers = __match_any_sync(act, d);
+            if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
+}
+
+__global__ void __launch_bounds__(256) k_sort_scan(uint32_t *__restrict__ hist, uint64_t n,
+                                                   uint64_t window, uint64_t tpw)
+{
+    __shared__ uint32_t s[256];
+    const uint64_t w = blockIdx.x;
+    const int d = threadIdx.x;
+    const uint64_t w0 = w * window;
+    const uint64_t L = min(window, n - w0);
+    const uint64_t ntl = ceil_div(L, kSortTile);
+    uint32_t run = 0;
+    for (uint64_t k = 0; k < ntl; ++k) {
+        uint32_t *c = hist + (w * tpw + k) * 256 + d;
+        uint32_t v = *c;
+        *c = run;
+        run += v;
+    }
+    s[d] = run;
+    __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {   // Hillis-Steele inclusive scan over digits
+        uint32_t v = d >= off ? s[d - off] : 0;
+        __syncthreads();
+        s[d] += v;
+        __syncthreads();
+    }
+    const uint32_t base = (uint32_t)w0 + s[d] - run;
+    for (uint64_t k = 0; k < ntl; ++k) hist[(w * tpw + k) * 256 + d] += base;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_down(const unsigned long long *__restrict__ kin,
+                                                            const uint32_t *__restrict__ vin,
+                                                            unsigned long long *__restrict__ kout,
+                                                            uint32_t *__restrict__ vout,
+                                                            const uint32_t *__restrict__ hist,
+                                                            uint64_t n, uint64_t window, uint64_t tpw,
+                                                            int shift)
+{
+    constexpr int kWarps = kSortThreads / 32;
+    constexpr int kPerWarpIters = kSortTile / kWarps / 32;     // 16
+    __shared__ uint32_t whist[kWarps][256];
+    __shared__ uint32_t tbase[256];
+    uint64_t start, end;
+    tile_range(blockIdx.x, n, window, tpw, start, end);
+    if (start >= end) return;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < kWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
+    tbase[tid] = hist[(uint64_t)blockIdx.x * 256 + tid];
+    __syncthreads();
+
+    unsigned long long kr[kPerWarpIters];
+    uint32_t vr[kPerWarpIters], rank[kPerWarpIters];
+    const uint64_t base = start + (uint64_t)warp * (kPerWarpIters * 32);
+#pragma unroll
+    for (int r = 0; r < kPerWarpIters; ++r) {
+        uint64_t p = base + r * 32 + lane;
+        bool valid = p < end;
+        kr[r] = valid ? kin[p] : 0ull;
+        vr[r] = valid ? vin[p] : 0u;
+    }
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < kPerWarpIters; ++r) {
+        uint64_t p = base + r * 32 + lane;
+        bool valid = p < end;
+        uint32_t act = __ballot_sync(0xffffffffu, valid);
+        uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
+        uint32_t peers = 0;
+        if (valid) {
+            peers = __match_any_sync(act, d);
+            rank[r] = whist[warp][d] + __popc(peers & lt);
+        }
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) whist[warp][d] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {   // exclusive scan over warps, per digit
+        uint32_t run = 0;
+#pragma unroll
+        for (int wv = 0; wv < kWarps; ++wv) {
+            uint32_t c = whist[wv][tid];
+            whist[wv][tid] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kPerWarpIters; ++r) {
+        uint64_t p = base + r * 32 + lane;
+        if (p < end) {
+            uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
+            uint32_t pos = tbase[d] + whist[warp][d] + rank[r];
+            kout[pos] = kr[r];
+            vout[pos] = vr[r];
+        }
+    }
+}
+
+cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
+                               unsigned long long *keys_a, uint32_t *vals_a,
+                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
+                               uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
+                               int *passes, cudaStream_t st)
+{
+    *passes = 0;
+    if (n == 0) return cudaSuccess;
+    const uint64_t tpw = ceil_div(window, kSortTile);
+    const uint64_t tiles = tpw * nwin;
+    const unsigned long long *kin = *keys_io;
+    const uint32_t *vin = *vals_io;
+    for (int d = 0; d < 8; ++d) {
+        if (!(digit_mask >> d & 1u)) continue;
+        unsigned long long *kout = (*passes & 1) ? keys_b : keys_a;
+        uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
+        k_sort_up<<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
+        k_sort_scan<<<(unsigned)nwin, 256, 0, st>>>(hist, n, window, tpw);
+        k_sort_down<<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw, 8 * d);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        kin = kout;
+        vin = vout;
+        ++*passes;
+    }
+    *keys_io = kin;
+    *vals_io = vin;
+    return cudaSuccess;
+}
+
+}  // namespace uellm

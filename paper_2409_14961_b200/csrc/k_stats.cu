@@ -1,0 +1,274 @@
+// k_stats.cu -- a8: per-batch statistics of a schedule.
+//   size b, s = max input (padded length), O = max predicted output, b x O generated
+//   tokens, input / output padding, KV peak bytes 4*b*l*h*(s+O), est_us (R7),
+//   completion_us = inclusive prefix of est_us over each window's batches,
+//   viol_alone = #{slo_us < est_us}, viol_seq = #{slo_us < completion_us}, over_cap.
+// Totals are exact integer sums (sum b*completion in 128 bits); the two reported doubles are
+// formed once at the end.
+//
+//   k_stats_est    warp per batch: b, s, O -> est_us
+//   k_seg_scan_*   segmented inclusive scan of est_us by window (chunk scan, chunk carries,
+//                  carry-in), giving completion_us
+//   k_stats_final  warp per batch: all fields, per-batch record, block-aggregated totals
+//   k_totals       one thread: uellm_totals
+#include "internal.cuh"
+
+namespace uellm {
+
+__device__ __forceinline__ uint32_t warp_max(uint32_t v)
+{
+    return __reduce_max_sync(0xffffffffu, v);
+}
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v)
+{
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+struct BatchCore {
+    uint32_t a, z, b, s, O;
+    unsigned long long sin, sout, est;
+};
+
+__device__ __forceinline__ BatchCore batch_core(const StatsParams &S, uint64_t t)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    BatchCore c;
+    c.a = S.offsets[t];
+    c.z = S.offsets[t + 1];
+    c.b = c.z - c.a;
+    uint32_t s = 0, O = 0;
+    unsigned long long si = 0, so = 0;
+    for (uint32_t k = c.a + lane; k < c.z; k += 32) {
+        const uint32_t vi = __ldg(S.rin + k), vo = __ldg(S.rout + k);
+        s = max(s, vi); O = max(O, vo);
+        si += vi; so += vo;
+    }
+    c.s = warp_max(s);
+    c.O = warp_max(O);
+    c.sin = warp_sum64(si);
+    c.sout = warp_sum64(so);
+    c.est = S.t_batch + S.t_iter * c.O + S.t_tok * (unsigned long long)c.b * c.O +
+            S.t_pre * (unsigned long long)c.b * c.s;
+    return c;
+}
+
+__global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
+{
+    const uint64_t m = *S.num_batches;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < m; t += nw) {
+        BatchCore c = batch_core(S, t);
+        if ((threadIdx.x & 31) == 0) S.est[t] = c.est;
+    }
+}
+
+// ---- segmented inclusive scan of est by window (head flag = first batch of a window) ----
+__device__ __forceinline__ bool head_flag(const StatsParams &S, uint64_t t)
+{
+    return t == 0 || (S.offsets[t] / S.window) != (S.offsets[t - 1] / S.window);
+}
+
+// block-wide segmented inclusive scan of (v, f); returns inclusive value, aggregate in *agg/*aggf
+__device__ unsigned long long block_seg_scan(unsigned long long v, uint32_t f, unsigned long long *agg,
+                                             uint32_t *aggf)
+{
+    __shared__ unsigned long long sv[kScanBlock / 32];
+    __shared__ uint32_t sf[kScanBlock / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long ov = __shfl_up_sync(0xffffffffu, v, d);
+        uint32_t of = __shfl_up_sync(0xffffffffu, f, d);
+        if (lane >= d) { if (!f) v += ov; f |= of; }
+    }
+    if (lane == 31) { sv[warp] = v; sf[warp] = f; }
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long wv = lane < kScanBlock / 32 ? sv[lane] : 0;
+        uint32_t wf = lane < kScanBlock / 32 ? sf[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            unsigned long long ov = __shfl_up_sync(0xffffffffu, wv, d);
+            uint32_t of = __shfl_up_sync(0xffffffffu, wf, d);
+            if (lane >= d) { if (!wf) wv += ov; wf |= of; }
+        }
+        if (lane < kScanBlock / 32) { sv[lane] = wv; sf[lane] = wf; }
+    }
+    __syncthreads();
+    if (warp > 0 && !f) v += sv[warp - 1];   // f here = "a head in my warp prefix up to me"
+    *agg = sv[kScanBlock / 32 - 1];
+    *aggf = sf[kScanBlock / 32 - 1];
+    __syncthreads();
+    return v;
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_seg_scan_local(StatsParams S)
+{
+    const uint64_t m = *S.num_batches;
+    const uint64_t nchunks = ceil_div(m, kScanBlock);
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint64_t t = c * kScanBlock + threadIdx.x;
+        const bool v = t < m;
+        unsigned long long x = v ? S.est[t] : 0;
+        uint32_t f = v ? head_flag(S, t) : 0;
+        unsigned long long agg;
+        uint32_t aggf;
+        unsigned long long inc = block_seg_scan(x, f, &agg, &aggf);
+        if (v) S.compl_[t] = inc;
+        if (threadIdx.x == 0) { S.blockagg[c] = agg; S.blocksum_u32[c] = aggf; }
+    }
+}
+
+// carry-in of every chunk: segmented exclusive scan of the chunk aggregates (one CTA)
+__global__ void __launch_bounds__(kScanBlock) k_seg_scan_chunks(StatsParams S)
+{
+    const uint64_t m = *S.num_batches;
+    const uint64_t nchunks = ceil_div(m, kScanBlock);
+    const uint64_t per = ceil_div(nchunks, kScanBlock);
+    const uint64_t a = threadIdx.x * per, z = min(a + per, nchunks);
+    unsigned long long v = 0;
+    uint32_t f = 0;
+    for (uint64_t c = a; c < z; ++c) {             // thread-local segmented reduce
+        if (S.blocksum_u32[c]) { v = S.blockagg[c]; f = 1; } else v += S.blockagg[c];
+    }
+    unsigned long long agg;
+    uint32_t aggf;
+    // exclusive = inclusive of the previous thread: shift by one via shared memory
+    unsigned long long inc = block_seg_scan(v, f, &agg, &aggf);
+    __shared__ unsigned long long incs[kScanBlock];
+    incs[threadIdx.x] = inc;
+    __syncthreads();
+    unsigned long long carry = threadIdx.x ? incs[threadIdx.x - 1] : 0;
+    for (uint64_t c = a; c < z; ++c) {
+        const unsigned long long ag = S.blockagg[c];
+        const uint32_t fl = S.blocksum_u32[c];
+        S.blockagg[c] = carry;                     // carry into chunk c
+        carry = fl ? ag : carry + ag;
+    }
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_seg_scan_apply(StatsParams S)
+{
+    __shared__ uint32_t seen_head;
+    const uint64_t m = *S.num_batches;
+    const uint64_t nchunks = ceil_div(m, kScanBlock);
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint64_t t = c * kScanBlock + threadIdx.x;
+        const bool v = t < m;
+        // carry applies to elements before the chunk's first head
+        uint32_t f = v ? head_flag(S, t) : 0;
+        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        if (threadIdx.x == 0) seen_head = 0xffffffffu;
+        __syncthreads();
+        if (bal && (threadIdx.x & 31) == 0) atomicMin(&seen_head, (threadIdx.x & ~31u) + (__ffs(bal) - 1));
+        __syncthreads();
+        if (v && threadIdx.x < seen_head) S.compl_[t] += S.blockagg[c];
+        __syncthreads();
+    }
+}
+
+// ---- all fields + totals ----
+__global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
+{
+    __shared__ unsigned long long red[8][12];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t m = *S.num_batches;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long a_gen = 0, a_pin = 0, a_pout = 0, a_kv = 0, a_obj = 0, a_v1 = 0, a_v2 = 0, a_oc = 0,
+                       a_mk = 0, a_llo = 0, a_lhi = 0, a_nb = 0;
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < m; t += nw) {
+        const BatchCore c = batch_core(S, t);
+        const unsigned long long compl_us = S.compl_[t];
+        uint32_t v1 = 0, v2 = 0;
+        for (uint32_t k = c.a + lane; k < c.z; k += 32) {
+            const unsigned long long su = __ldg(S.rslo + k);
+            v1 += su < c.est;
+            v2 += su < compl_us;
+        }
+        v1 = warp_sum(v1);
+        v2 = warp_sum(v2);
+        const unsigned long long kv = S.kv_unit * (unsigned long long)c.b * ((unsigned long long)c.s + c.O);
+        const uint32_t oc = (S.kv_cap != 0 && kv > S.kv_cap) ? 1u : 0u;
+        const unsigned long long gen = (unsigned long long)c.b * c.O;
+        const unsigned long long pin = (unsigned long long)c.b * c.s - c.sin;
+        const unsigned long long pout = gen - c.sout;
+        if (lane == 0) {
+            if (S.per_batch) {
+                uellm_batch_stat r;
+                r.start = c.a; r.size = c.b; r.max_in = c.s; r.max_out = c.O;
+                r.gen_tokens = gen; r.pad_in = pin; r.pad_out = pout; r.kv_bytes = kv;
+                r.est_us = c.est; r.completion_us = compl_us;
+                r.viol_alone = v1; r.viol_seq = v2; r.over_cap = oc; r.window = c.a / S.window;
+                S.per_batch[t] = r;
+            }
+            a_gen += gen; a_pin += pin; a_pout += pout; a_kv = max(a_kv, kv);
+            a_obj += c.est + S.lambda * v1; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += c.est; a_nb += 1;
+            const unsigned long long lo = (unsigned long long)c.b * compl_us;
+            const unsigned long long hi = __umul64hi((unsigned long long)c.b, compl_us);
+            a_llo += lo; a_lhi += hi + (a_llo < lo ? 1ull : 0ull);
+        }
+    }
+    if (lane == 0) {
+        unsigned long long *r = red[warp];
+        r[0] = a_gen; r[1] = a_pin; r[2] = a_pout; r[3] = a_kv; r[4] = a_obj; r[5] = a_v1;
+        r[6] = a_v2; r[7] = a_oc; r[8] = a_mk; r[9] = a_llo; r[10] = a_lhi; r[11] = a_nb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s[12] = {};
+        const int nwarps = blockDim.x >> 5;
+        for (int w = 0; w < nwarps; ++w) {
+            for (int f = 0; f < 12; ++f) {
+                if (f == 3) s[3] = max(s[3], red[w][3]);
+                else if (f == 9) { unsigned long long lo = red[w][9]; s[9] += lo; if (s[9] < lo) s[10] += 1; }
+                else s[f] += red[w][f];
+            }
+        }
+        StatAcc *A = S.acc;
+        if (s[11] == 0) return;
+        atomicAdd(&A->gen, s[0]); atomicAdd(&A->pad_in, s[1]); atomicAdd(&A->pad_out, s[2]);
+        atomicMax(&A->kv_max, s[3]); atomicAdd(&A->dp_cost, s[4]); atomicAdd(&A->viol_alone, s[5]);
+        atomicAdd(&A->viol_seq, s[6]); atomicAdd(&A->over_cap, s[7]); atomicAdd(&A->makespan, s[8]);
+        const unsigned long long old = atomicAdd(&A->lat_lo, s[9]);
+        atomicAdd(&A->lat_hi, s[10] + (old + s[9] < old ? 1ull : 0ull));
+        atomicAdd(&A->batches, s[11]);
+    }
+}
+
+__global__ void k_totals(StatsParams S)
+{
+    const StatAcc &A = *S.acc;
+    uellm_totals T;
+    T.n = S.n;
+    T.batches = *S.num_batches;
+    T.gen_tokens = A.gen; T.pad_in = A.pad_in; T.pad_out = A.pad_out; T.kv_bytes_max = A.kv_max;
+    T.dp_cost = A.dp_cost; T.viol_alone = A.viol_alone; T.viol_seq = A.viol_seq; T.over_cap = A.over_cap;
+    T.makespan_us = A.makespan;
+    const double lat = (double)A.lat_hi * 18446744073709551616.0 + (double)A.lat_lo;
+    T.mean_latency_s = S.n ? lat / (double)S.n * 1e-6 : 0.0;
+    T.throughput_tok_s = A.makespan ? (double)A.gen / ((double)A.makespan * 1e-6) : 0.0;
+    *S.totals = T;
+}
+
+cudaError_t run_stats(const StatsParams &S, cudaStream_t st)
+{
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(S.acc, 0, sizeof(StatAcc), st))) return e;
+    if (S.n > 0) {
+        const unsigned wblocks = 148 * 8;
+        uint64_t sb = ceil_div(S.n_cap, kScanBlock);
+        const unsigned sblocks = (unsigned)(sb < 296 ? sb : 296);
+        k_stats_est<<<wblocks, 256, 0, st>>>(S);
+        k_seg_scan_local<<<sblocks, kScanBlock, 0, st>>>(S);
+        k_seg_scan_chunks<<<1, kScanBlock, 0, st>>>(S);
+        k_seg_scan_apply<<<sblocks, kScanBlock, 0, st>>>(S);
+        k_stats_final<<<wblocks, 256, 0, st>>>(S);
+    }
+    k_totals<<<1, 1, 0, st>>>(S);
+    return cudaGetLastError();
+}
+
+}  // namespace uellm

@@ -1,0 +1,263 @@
+// k_trace.cu -- a7: traceback of the SEG-DP argmins into a boundary bitmap, compaction of the
+// bitmap into batch_offsets (P:245 / P:286-290: "ready list" of batches in scan order), and the
+// Alg. 1 (SLO-ODBS) segmentation.
+//
+// Bit b of the bitmap = "a batch starts at scheduled position b"; bit n closes the last batch.
+// Traceback: the path from a window end w1 is w1 -> arg[w1] -> ... -> w0.  Tile-parallel:
+//   T1  every tile walks from its own last boundary e (assumed on the path), marks its nodes
+//       and records where the walk leaves the tile (exitA);
+//   T2  every tile re-walks from the true entry candidate (the next tile's exitA) until the
+//       walk meets a marked node (paths coalesce) and clears the nodes that are not on it;
+//   T3  per window, tiles whose entry turned out different are re-walked in full (rare).
+#include "internal.cuh"
+
+namespace uellm {
+
+__device__ __forceinline__ void bm_set(uint32_t *bm, uint32_t b) { atomicOr(bm + (b >> 5), 1u << (b & 31)); }
+__device__ __forceinline__ bool bm_test(uint32_t *bm, uint32_t b) { return (__ldcg(bm + (b >> 5)) >> (b & 31)) & 1u; }
+// clear bits [a, z] (inclusive); no-op if a > z
+__device__ void bm_clear(uint32_t *bm, uint32_t a, uint32_t z)
+{
+    if (a > z) return;
+    const uint32_t wa = a >> 5, wz = z >> 5;
+    for (uint32_t w = wa; w <= wz; ++w) {
+        const uint32_t lo = (w == wa) ? (a & 31) : 0;
+        const uint32_t hi = (w == wz) ? (z & 31) : 31;
+        const uint32_t m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1)) & ~((1u << lo) - 1);
+        atomicAnd(bm + w, ~m);
+    }
+}
+
+__device__ __forceinline__ uint32_t arg_of(const uint16_t *argx, uint32_t j) { return j - (uint32_t)argx[j - 1]; }
+
+__global__ void k_trace_a(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t ntiles, uint32_t *bm)
+{
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const TileRec r = tiles[t];
+    if (!r.valid) return;
+    uint32_t j = r.e, i;
+    bm_set(bm, j);
+    for (;;) {
+        i = arg_of(argx, j);
+        if (i <= r.s) break;
+        bm_set(bm, i);
+        j = i;
+    }
+    tiles[t].exitA = i;
+}
+
+__global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t ntiles, uint64_t tpw,
+                          uint32_t *bm, Diag *diag)
+{
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const TileRec r = tiles[t];
+    if (!r.valid) return;
+    const bool last = ((t + 1) % tpw == 0) || !tiles[t + 1].valid;
+    uint32_t exitB = r.exitA, merged = 1;
+    if (!last) {
+        const uint32_t q = tiles[t + 1].exitA;      // entry into this tile if tile t+1 is right
+        if (q != r.e) {
+            bm_clear(bm, q + 1, r.e);
+            uint32_t j = q;
+            for (;;) {
+                if (bm_test(bm, j)) break;              // met the A-walk: identical below
+                bm_set(bm, j);
+                const uint32_t i = arg_of(argx, j);
+                bm_clear(bm, max(i, r.s) + 1, j - 1);
+                if (i <= r.s) { exitB = i; merged = (i == r.exitA); break; }
+                j = i;
+            }
+            if (!merged) atomicAdd(&diag->trace_unmerged, 1ull);
+        }
+    }
+    tiles[t].exitB = exitB;
+    tiles[t].merged = merged;
+}
+
+__global__ void k_trace_c(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t tpw, uint64_t nwin,
+                          uint64_t window, uint32_t *bm, Diag *diag)
+{
+    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwin) return;
+    const uint64_t t0 = w * tpw;
+    uint32_t K = 0;
+    while (K < tpw && tiles[t0 + K].valid) ++K;
+    if (K == 0) return;
+    bm_set(bm, (uint32_t)(w * window));                 // every window starts a batch
+    uint32_t exit_true = tiles[t0 + K - 1].exitB;
+    for (int k = (int)K - 2; k >= 0; --k) {
+        const TileRec r = tiles[t0 + k];
+        if (exit_true == tiles[t0 + k + 1].exitA) {
+            exit_true = r.exitB;
+            continue;
+        }
+        // the walk into this tile enters elsewhere: re-walk it in full
+        atomicAdd(&diag->trace_rewalks, 1ull);
+        bm_clear(bm, r.s + 1, r.e);
+        uint32_t j = exit_true, i;
+        for (;;) {
+            bm_set(bm, j);
+            i = arg_of(argx, j);
+            if (i <= r.s) break;
+            j = i;
+        }
+        tiles[t0 + k].exitB = i;
+        exit_true = i;
+    }
+}
+
+cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, cudaStream_t st)
+{
+    if (P.n == 0) return cudaSuccess;
+    const unsigned tb = 128;
+    k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
+    k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag);
+    k_trace_c<<<(unsigned)ceil_div(P.nwin, 64), 64, 0, st>>>(P.argx, P.tiles, P.tpw, P.nwin, P.window, bitmap,
+                                                           P.diag);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Alg. 1 SLO-ODBS with readings R1-R6/R10/R12, one thread per window over the
+// sorted records (sequential scan, as printed).  Doubles with explicit round-to-nearest
+// intrinsics (no FMA contraction) so every decision matches the CPU oracle bit for bit.
+__global__ void k_alg1(Alg1Params A, uint32_t *bm)
+{
+    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= A.nwin) return;
+    const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
+    uint64_t bsize = 0, MI = 0;
+    double L_CM = 0.0, O_CM = 0.0, CM = 0.0;
+    for (uint64_t x = w0; x < w1; ++x) {
+        const uint32_t su = A.rslo[x];
+        const double slo = __ddiv_rn((double)su, 1e6);
+        const double len = (double)A.rout[x];
+        const uint32_t inx = A.rin[x];
+        if (A.split && bsize > 0 && su != A.rslo[x - 1]) {
+            bsize = 0; L_CM = 0.0; O_CM = 0.0; CM = 0.0; MI = 0;
+        }
+        const double nb1 = (double)(bsize + 1);
+        const double T_l = __dmul_rn(__dmul_rn(__dadd_rn(slo, L_CM), nb1), A.l1);
+        double T_o = A.eq2_additive ? __dadd_rn(len, O_CM) : __dsub_rn(len, O_CM);
+        T_o = __dmul_rn(__dmul_rn(T_o, nb1), A.l2);
+        const double Total = __dadd_rn(__dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
+        bool admit = (bsize == 0);
+        if (!admit && Total <= A.threshold) {
+            const uint64_t s = max((uint64_t)inx, MI);
+            const uint64_t O = (uint64_t)(len > O_CM ? len : O_CM);
+            admit = (bsize + 1 <= 1) || ((bsize + 1) * (s + O) <= A.cap_tok);
+        }
+        const double cmq = __dadd_rn(__dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
+        if (admit) {
+            if (bsize == 0) bm_set(bm, (uint32_t)x);
+            bsize += 1;
+            if (slo > L_CM) L_CM = slo;
+            if (len > O_CM) O_CM = len;
+            if (cmq > CM) CM = cmq;
+            if (inx > MI) MI = inx;
+        } else {
+            bm_set(bm, (uint32_t)x);
+            bsize = 1; L_CM = slo; O_CM = len; CM = cmq; MI = inx;
+        }
+        const double den = CM > A.eps ? CM : A.eps;
+        const double capd = floor(__ddiv_rn(A.threshold, den));
+        const uint64_t cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
+        if (bsize >= cap) { bsize = 0; L_CM = 0.0; O_CM = 0.0; CM = 0.0; MI = 0; }
+    }
+    if (w == A.nwin - 1) bm_set(bm, A.n);
+}
+
+cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, cudaStream_t st)
+{
+    if (A.n == 0) return cudaSuccess;
+    k_alg1<<<(unsigned)ceil_div(A.nwin, 64), 64, 0, st>>>(A, bitmap);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Compaction: batch_offsets = ascending positions of the set bits; num_batches = count - 1.
+template <int NT>
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t *total)
+{
+    __shared__ uint32_t wsum[NT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = lane < NT / 32 ? wsum[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, d);
+            if (lane >= d) s += y;
+        }
+        if (lane < NT / 32) wsum[lane] = s;
+    }
+    __syncthreads();
+    const uint32_t before = warp ? wsum[warp - 1] : 0;
+    *total = wsum[NT / 32 - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_compact_count(const uint32_t *bm, uint64_t nwords, uint32_t *wscan,
+                                                              uint32_t *blocksum)
+{
+    const uint64_t w = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+    const uint32_t c = w < nwords ? __popc(bm[w]) : 0;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<kScanBlock>(c, &tot);
+    if (w < nwords) wscan[w] = ex;
+    if (threadIdx.x == 0) blocksum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_compact_blocks(uint32_t *blocksum, uint64_t nblocks,
+                                                               unsigned long long *num_batches)
+{
+    const uint64_t per = ceil_div(nblocks, kScanBlock);
+    const uint64_t a = threadIdx.x * per, z = min(a + per, nblocks);
+    uint32_t s = 0;
+    for (uint64_t b = a; b < z; ++b) s += blocksum[b];
+    uint32_t tot;
+    uint32_t run = block_excl_scan<kScanBlock>(s, &tot);
+    for (uint64_t b = a; b < z; ++b) { uint32_t v = blocksum[b]; blocksum[b] = run; run += v; }
+    if (threadIdx.x == 0) *num_batches = (unsigned long long)tot - 1ull;
+}
+
+__global__ void __launch_bounds__(256) k_compact_write(const uint32_t *bm, uint64_t nwords, const uint32_t *wscan,
+                                                       const uint32_t *blocksum, uint32_t *offsets)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += stride) {
+        uint32_t bits = bm[w];
+        if (!bits) continue;
+        uint32_t pos = blocksum[w / kScanBlock] + wscan[w];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            offsets[pos++] = (uint32_t)(w * 32 + b);
+        }
+    }
+}
+
+cudaError_t run_compact(const uint32_t *bitmap, uint64_t n, uint32_t *wscan, uint32_t *blocksum,
+                        uint32_t *offsets, unsigned long long *num_batches, cudaStream_t st)
+{
+    const uint64_t nwords = (n + 1 + 31) / 32;
+    const uint64_t nblocks = ceil_div(nwords, kScanBlock);
+    k_compact_count<<<(unsigned)nblocks, kScanBlock, 0, st>>>(bitmap, nwords, wscan, blocksum);
+    k_compact_blocks<<<1, kScanBlock, 0, st>>>(blocksum, nblocks, num_batches);
+    uint64_t wb = ceil_div(nwords, 256);
+    if (wb > 148ull * 16) wb = 148ull * 16;
+    k_compact_write<<<(unsigned)wb, 256, 0, st>>>(bitmap, nwords, wscan, blocksum, offsets);
+    return cudaGetLastError();
+}
+
+}  // namespace uellm

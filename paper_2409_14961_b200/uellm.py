@@ -1,0 +1,195 @@
+"""Thin ctypes binding of libuellm.so (include/uellm.h).  Argument marshalling only: every
+step of the scheduling path runs in the library's sm_100a kernels.  PyTorch supplies device
+memory (workspace and outputs) and streams; numpy / pinned host arrays may be passed where the
+header allows [host|device] pointers.
+
+There is no fallback: if libuellm.so is missing or fails to load, importing this module
+raises.  Names mirror the C ABI (uellm_profile_load -> profile_load, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libuellm.so")
+
+OK, ERR_ARG, ERR_CONTRACT, ERR_CONFIG, ERR_OVERFLOW, ERR_CUDA, ERR_UNSUPPORTED = range(7)
+MODE_SEG_DP, MODE_SLO_ODBS, MODE_FIFO, MODE_SORT_ONLY = range(4)
+
+
+class UellmError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {status_string(status)}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("mode", C.c_uint32), ("window", C.c_uint32), ("max_batch", C.c_uint32),
+                ("split_on_slo_change", C.c_uint32), ("kv_bytes_per_elem", C.c_uint32),
+                ("n_layers", C.c_uint32), ("hidden", C.c_uint32), ("dp_tile", C.c_uint32),
+                ("kv_cap_bytes", C.c_uint64),
+                ("t_batch_us", C.c_uint32), ("t_iter_us", C.c_uint32), ("t_tok_us", C.c_uint32),
+                ("t_prefill_us", C.c_uint32), ("lambda_us", C.c_uint64),
+                ("w1", C.c_double), ("w2", C.c_double), ("l1", C.c_double), ("l2", C.c_double),
+                ("threshold", C.c_double), ("eps", C.c_double),
+                ("eq2_additive", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class Queries(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("input_len", C.c_void_p), ("pred_out_len", C.c_void_p),
+                ("slo_s", C.c_void_p)]
+
+
+class Totals(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("n", "batches", "gen_tokens", "pad_in", "pad_out",
+                                          "kv_bytes_max", "dp_cost", "viol_alone", "viol_seq",
+                                          "over_cap", "makespan_us")] + \
+               [("mean_latency_s", C.c_double), ("throughput_tok_s", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Profile(C.Structure):
+    _fields_ = [("opaque", C.c_uint64 * 40)]
+
+
+class Diagnostics(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("tiles", "tile_len", "fixups_unconverged", "cascade_reruns",
+                                          "fixup_positions", "trace_unmerged", "trace_rewalks",
+                                          "sort_passes", "dp_cost", "dp_candidate_evals",
+                                          "sched_launches", "stats_launches")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+BATCH_STAT_DTYPE = np.dtype([
+    ("start", "<u4"), ("size", "<u4"), ("max_in", "<u4"), ("max_out", "<u4"),
+    ("gen_tokens", "<u8"), ("pad_in", "<u8"), ("pad_out", "<u8"), ("kv_bytes", "<u8"),
+    ("est_us", "<u8"), ("completion_us", "<u8"),
+    ("viol_alone", "<u4"), ("viol_seq", "<u4"), ("over_cap", "<u4"), ("window", "<u4")])
+TOTALS_BYTES = C.sizeof(Totals)
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"libuellm.so not built ({_LIB_PATH}); run __graft_entry__.build()")
+_lib = C.CDLL(_LIB_PATH)
+_lib.uellm_abi_version.restype = C.c_uint32
+_lib.uellm_sizeof.restype = C.c_uint64
+_lib.uellm_sizeof.argtypes = [C.c_int]
+_lib.uellm_status_string.restype = C.c_char_p
+_lib.uellm_status_string.argtypes = [C.c_int32]
+_lib.uellm_workspace_bytes.restype = C.c_size_t
+_lib.uellm_workspace_bytes.argtypes = [C.c_uint64, C.POINTER(Config)]
+_lib.uellm_profile_load.restype = C.c_int32
+_lib.uellm_profile_load.argtypes = [C.POINTER(Queries), C.POINTER(Config), C.c_void_p, C.c_size_t,
+                                    C.c_void_p, C.POINTER(Profile)]
+_lib.uellm_schedule_batches.restype = C.c_int32
+_lib.uellm_schedule_batches.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
+_lib.uellm_batch_stats.restype = C.c_int32
+_lib.uellm_batch_stats.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+_lib.uellm_set_stage_events.restype = C.c_int32
+_lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
+_lib.uellm_get_diagnostics.restype = C.c_int32
+_lib.uellm_get_diagnostics.argtypes = [C.POINTER(Profile), C.POINTER(Diagnostics), C.c_void_p]
+
+assert _lib.uellm_abi_version() == 1
+assert _lib.uellm_sizeof(0) == C.sizeof(Config)
+assert _lib.uellm_sizeof(1) == BATCH_STAT_DTYPE.itemsize == 80
+assert _lib.uellm_sizeof(2) == C.sizeof(Totals)
+assert _lib.uellm_sizeof(3) == C.sizeof(Profile)
+assert _lib.uellm_sizeof(4) == C.sizeof(Diagnostics)
+
+LIBRARY_PATH = _LIB_PATH
+
+
+def status_string(s: int) -> str:
+    return _lib.uellm_status_string(s).decode()
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise UellmError(st, what)
+
+
+def make_config(cfg) -> Config:
+    """Build the C config from any object with the uellm_config field names (e.g.
+    workloads.SchedConfig)."""
+    c = Config()
+    for name, _ in Config._fields_:
+        if name == "reserved":
+            continue
+        if hasattr(cfg, name):
+            setattr(c, name, getattr(cfg, name))
+    return c
+
+
+def _ptr(x) -> int | None:
+    """Raw address of a torch tensor / numpy array (no copies: marshalling only)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    return int(x)
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def workspace_bytes(n: int, cfg: Config) -> int:
+    return _lib.uellm_workspace_bytes(n, C.byref(cfg))
+
+
+def profile_load(n: int, input_len, pred_out_len, slo_s, cfg: Config, ws, ws_bytes: int,
+                 stream=None) -> Profile:
+    q = Queries(n, _ptr(input_len), _ptr(pred_out_len), _ptr(slo_s))
+    p = Profile()
+    _check(_lib.uellm_profile_load(C.byref(q), C.byref(cfg), _ptr(ws), ws_bytes,
+                                   _stream_handle(stream), C.byref(p)), "uellm_profile_load")
+    return p
+
+
+def schedule_batches(p: Profile, cfg: Config, order, batch_offsets, num_batches, stream=None):
+    _check(_lib.uellm_schedule_batches(C.byref(p), C.byref(cfg), _ptr(order), _ptr(batch_offsets),
+                                       _ptr(num_batches), _stream_handle(stream)),
+           "uellm_schedule_batches")
+
+
+def batch_stats(p: Profile, cfg: Config, batch_offsets, num_batches, per_batch, totals, stream=None):
+    _check(_lib.uellm_batch_stats(C.byref(p), C.byref(cfg), _ptr(batch_offsets), _ptr(num_batches),
+                                  _ptr(per_batch), _ptr(totals), _stream_handle(stream)),
+           "uellm_batch_stats")
+
+
+STAGES = ["sched_begin", "sort_end", "decode_end", "dp_local_end", "dp_fix_end", "dp_cascade_end",
+          "trace_end", "sched_end", "stats_begin", "stats_end"]
+
+
+def set_stage_events(p: Profile, events):
+    """events: sequence of torch.cuda.Event(enable_timing=True) (or raw handles / None)."""
+    arr = (C.c_void_p * max(len(events), 1))(*[None if e is None else
+                                               (e.cuda_event if hasattr(e, "cuda_event") else int(e))
+                                               for e in events])
+    _check(_lib.uellm_set_stage_events(C.byref(p), arr, len(events)), "uellm_set_stage_events")
+
+
+def get_diagnostics(p: Profile, stream=None) -> dict:
+    d = Diagnostics()
+    _check(_lib.uellm_get_diagnostics(C.byref(p), C.byref(d), _stream_handle(stream)),
+           "uellm_get_diagnostics")
+    return d.as_dict()

@@ -1,0 +1,244 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the CPU oracle on the same seeded
+inputs.  Bit-exact: order, batch_offsets, num_batches, dp_cost and every integer statistic;
+mean_latency_s / throughput_tok_s within 1e-6 relative (north_star / SURVEY 8(c))."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ["start", "size", "max_in", "max_out", "gen_tokens", "pad_in", "pad_out", "kv_bytes",
+              "est_us", "completion_us", "viol_alone", "viol_seq", "over_cap", "window"]
+TOT_INT = ["n", "batches", "gen_tokens", "pad_in", "pad_out", "kv_bytes_max", "dp_cost", "viol_alone",
+           "viol_seq", "over_cap", "makespan_us"]
+REL = 1e-6
+
+
+def gpu_run(inp, out, slo, cfg, per_batch=True):
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    dev = torch.device("cuda:0")
+    g = GpuScheduler(len(inp), cfg, device=dev, per_batch=per_batch)
+    g.run(torch.from_numpy(np.ascontiguousarray(inp).view(np.int32)).to(dev),
+          torch.from_numpy(np.ascontiguousarray(out).view(np.int32)).to(dev),
+          torch.from_numpy(np.ascontiguousarray(slo)).to(dev))
+    r = g.results()
+    r["diag"] = g.diagnostics()
+    return r
+
+
+def assert_parity(inp, out, slo, cfg, stats=True, nthreads=8):
+    r = gpu_run(inp, out, slo, cfg, per_batch=stats)
+    o_order, o_offs, o_m, o_cost = oracle.schedule(inp, out, slo, cfg, nthreads=nthreads)
+    assert np.array_equal(r["order"], o_order), "order"
+    assert r["m"] == o_m, ("num_batches", r["m"], o_m)
+    assert np.array_equal(r["offsets"], o_offs), "batch_offsets"
+    if cfg.mode == W.MODE_SEG_DP:
+        assert r["diag"]["dp_cost"] == o_cost, ("dp_cost", r["diag"]["dp_cost"], o_cost)
+    if stats:
+        pb, tot = oracle.stats(inp, out, slo, cfg, o_order, o_offs)
+        for f in INT_FIELDS:
+            assert np.array_equal(r["per_batch"][f], pb[f]), f
+        for f in TOT_INT:
+            assert r["totals"][f] == tot[f], (f, r["totals"][f], tot[f])
+        for f in ("mean_latency_s", "throughput_tok_s"):
+            assert r["totals"][f] == pytest.approx(tot[f], rel=REL, abs=0), f
+        if cfg.mode == W.MODE_SEG_DP:
+            assert r["totals"]["dp_cost"] == o_cost
+    return r
+
+
+# ------------------------------------------------------------------ tiny / brute-force size
+@pytest.mark.parametrize("pattern", ["rand", "ties", "bucket", "identical", "descending", "classes"])
+def test_small_random(pattern):
+    for seed in range(40):
+        n = 1 + seed % 12
+        inp, out, slo, cfg = W.random_small(seed * 13 + 5, n, pattern)
+        assert_parity(inp, out, slo, cfg)
+
+
+@pytest.mark.parametrize("seed", range(0, 60, 3))
+def test_c1(seed):
+    for lam in (0, 10**6):
+        assert_parity(*W.c1(seed, lam))
+
+
+# ------------------------------------------------------------------ configs c2 / c3
+@pytest.mark.parametrize("lam,split", [(0, 0), (10**9, 0), (10**9, 1), (0, 1)])
+def test_c2(lam, split):
+    assert_parity(*W.c2(7, lam=lam, split=split))
+
+
+@pytest.mark.parametrize("lam", [0, 10**9])
+def test_c3(lam):
+    r = assert_parity(*W.c3(3, lam=lam), nthreads=1)
+    assert r["diag"]["tiles"] > 1
+
+
+def test_c3_windows_ragged():
+    inp, out, slo, cfg = W.c3(4, n=333_333)
+    assert_parity(inp, out, slo, cfg.replace(window=50_000))
+
+
+# ------------------------------------------------------------------ tiling / fix-up / cascade
+@pytest.mark.parametrize("W_,tile", [(64, 128), (64, 192), (256, 512), (16, 32)])
+def test_forced_small_tiles(W_, tile):
+    """Tiles of 2-3 W rarely converge, so the fix-up cascade and the traceback re-walks run."""
+    inp, out, slo, cfg = W.c2(11, n=20_000)
+    cfg = cfg.replace(max_batch=W_, dp_tile=tile)
+    r = assert_parity(inp, out, slo, cfg)
+    d = r["diag"]
+    assert d["tiles"] >= 20_000 // (2 * tile)
+    assert d["fixup_positions"] > 0
+
+
+def test_identical_keys_tiles():
+    # c5-i: identical keys never converge off-phase; tiles are W-aligned so they do
+    n = 50_000
+    inp = np.full(n, 128, np.uint32); out = np.full(n, 256, np.uint32); slo = np.full(n, 30.0, np.float32)
+    cfg = W.SchedConfig(max_batch=256, kv_cap_bytes=W.C5_KV_CAP_BYTES, lambda_us=10**9, dp_tile=1024)
+    assert_parity(inp, out, slo, cfg)
+    assert_parity(inp, out, slo, cfg.replace(kv_cap_bytes=0, dp_tile=768))
+
+
+def test_all_violating_and_over_cap():
+    inp, out, slo, cfg = W.c5(2, n=40_000, window=10_000)
+    r = assert_parity(inp, out, slo, cfg)
+    assert r["totals"]["over_cap"] > 0 and r["totals"]["viol_alone"] > 0
+
+
+# ------------------------------------------------------------------ other modes
+def test_modes_fifo_sortonly():
+    inp, out, slo, cfg = W.c2(5, n=5000)
+    assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_FIFO, window=1234))
+    assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_SORT_ONLY))
+
+
+@pytest.mark.parametrize("w1,w2,thr,split", [(1.0, 0.0, 300.0, 0), (0.0, 1.0, 500.0, 0),
+                                             (1.0, 0.01, 800.0, 1), (0.5, 0.5, 60.0, 0)])
+def test_mode_slo_odbs(w1, w2, thr, split):
+    inp, out, slo, cfg = W.c2(9, n=8000, split=split)
+    assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_SLO_ODBS, w1=w1, w2=w2, threshold=thr, window=3000))
+
+
+# ------------------------------------------------------------------ edges and errors
+def test_edges():
+    for n in (1, 2, 3, 31, 32, 33):
+        inp, out, slo, cfg = W.c2(n, n=n)
+        assert_parity(inp, out, slo, cfg)
+    inp, out, slo, cfg = W.c2(1, n=700)
+    assert_parity(inp, out, slo, cfg.replace(max_batch=1))
+    assert_parity(inp, out, slo, cfg.replace(max_batch=4096))
+
+
+def test_empty():
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    g = GpuScheduler(0, W.SchedConfig(), device="cuda:0")
+    z = torch.zeros(0, dtype=torch.int32, device="cuda:0")
+    g.run(z, z, torch.zeros(0, dtype=torch.float32, device="cuda:0"))
+    r = g.results()
+    assert r["m"] == 0 and list(r["offsets"]) == [0]
+    assert r["totals"]["n"] == 0 and r["totals"]["batches"] == 0
+
+
+def test_contract_and_config_errors():
+    from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    inp, out, slo, cfg = W.c2(0, n=100)
+    g = GpuScheduler(100, cfg, device="cuda:0")
+    for bad in ("in", "out", "slo_nan", "slo_neg", "slo_zero_us"):
+        i2, o2, s2 = inp.copy(), out.copy(), slo.copy()
+        if bad == "in": i2[5] = 0
+        if bad == "out": o2[99] = 0
+        if bad == "slo_nan": s2[0] = np.nan
+        if bad == "slo_neg": s2[3] = -1.0
+        if bad == "slo_zero_us": s2[7] = 4e-7
+        with pytest.raises(U.UellmError) as e:
+            g.load(torch.from_numpy(i2.view(np.int32)).cuda(), torch.from_numpy(o2.view(np.int32)).cuda(),
+                   torch.from_numpy(s2).cuda())
+        assert e.value.status == U.ERR_CONTRACT
+    # cost bound overflow
+    g2 = GpuScheduler(100, cfg.replace(lambda_us=2**62), device="cuda:0")
+    with pytest.raises(U.UellmError) as e:
+        g2.load(torch.from_numpy(inp.view(np.int32)).cuda(), torch.from_numpy(out.view(np.int32)).cuda(),
+                torch.from_numpy(slo).cuda())
+    assert e.value.status == U.ERR_OVERFLOW
+
+
+def test_host_buffers_end_to_end():
+    """The C-ABI with HOST buffers (staging inside the library) equals the device path."""
+    from paper_2409_14961_b200.scheduler import schedule_host
+    inp, out, slo, cfg = W.c3(8, n=200_000)
+    cfg = cfg.replace(window=64_000)
+    order, offs, m, tot = schedule_host(inp, out, slo, cfg, device="cuda:0")
+    o_order, o_offs, o_m, o_cost = oracle.schedule(inp, out, slo, cfg, nthreads=8)
+    assert np.array_equal(order, o_order) and np.array_equal(offs, o_offs) and m == o_m
+    assert tot["dp_cost"] == o_cost
+
+
+def test_repeat_schedule_same_profile():
+    """schedule/stats can be re-run on one loaded profile (keys are kept in the workspace)."""
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    inp, out, slo, cfg = W.c2(2, n=6000)
+    g = GpuScheduler(6000, cfg, device="cuda:0")
+    g.run(torch.from_numpy(inp.view(np.int32)).cuda(), torch.from_numpy(out.view(np.int32)).cuda(),
+          torch.from_numpy(slo).cuda())
+    a = g.results()
+    g.schedule(); g.stats()
+    b = g.results()
+    assert np.array_equal(a["offsets"], b["offsets"]) and a["totals"] == b["totals"]
+
+
+# ------------------------------------------------------------------ full sizes (sampled)
+def _window_sample_parity(inp, out, slo, cfg, r, windows):
+    """Windows are independent (O1): the oracle recomputes sampled windows one by one and
+    they must match the GPU's full-size run bit for bit."""
+    wl = cfg.window
+    offs = r["offsets"].astype(np.int64)
+    for w in windows:
+        a, z = w * wl, min(len(inp), (w + 1) * wl)
+        c = cfg.replace(window=0)
+        o_order, o_offs, o_m, o_cost = oracle.schedule(inp[a:z], out[a:z], slo[a:z], c)
+        assert np.array_equal(r["order"][a:z], o_order + a), w
+        sel = offs[(offs >= a) & (offs <= z)]
+        assert np.array_equal(sel, o_offs.astype(np.int64) + a), w
+        pb = r["per_batch"]
+        mine = pb[(pb["start"] >= a) & (pb["start"] < z)]
+        _, o_tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], c, o_order, o_offs)
+        assert int(mine["est_us"].sum()) == o_tot["makespan_us"]
+        assert int((mine["est_us"] + cfg.lambda_us * mine["viol_alone"].astype(np.uint64)).sum()) == o_cost
+
+
+def _global_properties(n, cfg, r):
+    offs = r["offsets"].astype(np.int64)
+    assert offs[0] == 0 and offs[-1] == n and np.all(np.diff(offs) > 0)
+    assert np.all(np.diff(offs) <= cfg.max_batch)
+    wl = cfg.window or n
+    assert set(range(0, n, wl)) <= set(offs.tolist())          # windows start batches
+    pb = r["per_batch"]
+    assert int(pb["size"].sum()) == n
+    if cfg.kv_cap_bytes:
+        assert np.all((pb["kv_bytes"] <= cfg.kv_cap_bytes) | (pb["size"] == 1))
+    assert r["totals"]["dp_cost"] == r["diag"]["dp_cost"]      # stats recompute == DP optimum
+    o = r["order"]
+    assert np.array_equal(np.sort(o), np.arange(n, dtype=np.uint32))
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    """BJ configs[3] at its full size (10^8 queries, 10^6-query windows) in bench.py's launch
+    configuration; three windows re-derived by the oracle, global invariants on all."""
+    inp, out, slo, cfg = W.c4(0)
+    r = gpu_run(inp, out, slo, cfg)
+    _global_properties(len(inp), cfg, r)
+    _window_sample_parity(inp, out, slo, cfg, r, [0, 57, 99])
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled():
+    inp, out, slo, cfg = W.c5(0)
+    r = gpu_run(inp, out, slo, cfg)
+    _global_properties(len(inp), cfg, r)
+    _window_sample_parity(inp, out, slo, cfg, r, [1, 3, 6, 9])

@@ -57,6 +57,7 @@ class SchedConfig:
     threshold: float = 1000.0
     eps: float = 1e-9
     eq2_additive: int = 0
+    dp_tile: int = 0                # GPU SEG-DP tile length (tuning only; 0 = automatic)
 
     def replace(self, **kw) -> "SchedConfig":
         return dataclasses.replace(self, **kw)
