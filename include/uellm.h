@@ -101,7 +101,8 @@ typedef struct {
     double threshold;               /* Alg. 1 Threshold, > 0                               */
     double eps;                     /* Alg. 1 line 20 dynamic-cap guard (R5), > 0                   */
     uint32_t eq2_additive;          /* 0|1: Alg. 1 T_o with Eq. 2's '+' instead of '-' (R2)        */
-    uint32_t reserved;              /* must be 0                                                    */
+    uint32_t flags;                 /* bit 0: force the generic 64-bit SEG-DP kernels (testing; same
+                                       results); other bits must be 0                               */
 } uellm_config;
 
 /* One batch (UELLM_MODE_*: batch t = order[batch_offsets[t] .. batch_offsets[t+1])). 80 bytes. */

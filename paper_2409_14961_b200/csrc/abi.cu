@@ -80,7 +80,7 @@ uellm_status check_config(const uellm_config *c)
 {
     if (c->mode > UELLM_MODE_SORT_ONLY) return UELLM_ERR_CONFIG;
     if (c->max_batch < 1) return UELLM_ERR_CONFIG;
-    if (c->split_on_slo_change > 1 || c->eq2_additive > 1 || c->reserved != 0) return UELLM_ERR_CONFIG;
+    if (c->split_on_slo_change > 1 || c->eq2_additive > 1 || (c->flags & ~1u) != 0) return UELLM_ERR_CONFIG;
     if (c->mode == UELLM_MODE_SLO_ODBS) {
         if (!(c->w1 >= 0.0) || !(c->w2 >= 0.0) || !(c->w1 + c->w2 > 0.0)) return UELLM_ERR_CONFIG;
         if (!(c->threshold > 0.0) || !(c->eps > 0.0) || !(c->l1 >= 0.0) || !(c->l2 >= 0.0)) return UELLM_ERR_CONFIG;
@@ -294,11 +294,17 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         P.wincost = at<unsigned long long>(w, L.wincost);
         P.n = (uint32_t)n; P.window = (uint32_t)L.window; P.nwin = (uint32_t)L.nwin;
         P.tile_len = (uint32_t)L.tile_len; P.tpw = (uint32_t)L.tpw; P.W = cfg->max_batch;
-        P.cap_slots = (uint32_t)align_up(cfg->max_batch + 1, 32);
+        P.cap_slots = (uint32_t)align_up(cfg->max_batch + 33, 32);
         P.split = cfg->split_on_slo_change;
         P.cap_tok = cap_tok;
         P.t_batch = cfg->t_batch_us; P.t_iter = cfg->t_iter_us; P.t_tok = cfg->t_tok_us;
         P.t_pre = cfg->t_prefill_us; P.lambda = cfg->lambda_us;
+        {
+            typedef unsigned __int128 u128;
+            const u128 E = (u128)cfg->t_batch_us + (u128)cfg->t_iter_us * v.max_out +
+                           ((u128)cfg->t_tok_us * v.max_out + (u128)cfg->t_prefill_us * v.max_in) * cfg->max_batch;
+            P.narrow = (v.max_in < 65536u && v.max_out < 65536u && E < ((u128)1 << 32) && !(cfg->flags & 1u)) ? 1u : 0u;
+        }
         void *ev[3] = {nullptr, nullptr, nullptr};
         for (int k = 0; k < 3; ++k)
             if ((uint64_t)(UELLM_STAGE_DP_LOCAL_END + k) < v.n_events) ev[k] = v.events[UELLM_STAGE_DP_LOCAL_END + k];

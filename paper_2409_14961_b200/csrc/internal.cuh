@@ -120,6 +120,7 @@ struct DPParams {
     Diag *diag;
     unsigned long long *wincost;
     uint32_t n, window, nwin, tile_len, tpw, W, cap_slots, split;
+    uint32_t narrow;                             // 32-bit fast path valid (see k_segdp.cu)
     unsigned long long cap_tok;                  // ~0ull = no cap
     unsigned long long t_batch, t_iter, t_tok, t_pre, lambda;
 };

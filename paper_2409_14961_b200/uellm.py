@@ -34,7 +34,7 @@ class Config(C.Structure):
                 ("t_prefill_us", C.c_uint32), ("lambda_us", C.c_uint64),
                 ("w1", C.c_double), ("w2", C.c_double), ("l1", C.c_double), ("l2", C.c_double),
                 ("threshold", C.c_double), ("eps", C.c_double),
-                ("eq2_additive", C.c_uint32), ("reserved", C.c_uint32)]
+                ("eq2_additive", C.c_uint32), ("flags", C.c_uint32)]
 
 
 class Queries(C.Structure):
@@ -121,8 +121,6 @@ def make_config(cfg) -> Config:
     workloads.SchedConfig)."""
     c = Config()
     for name, _ in Config._fields_:
-        if name == "reserved":
-            continue
         if hasattr(cfg, name):
             setattr(c, name, getattr(cfg, name))
     return c

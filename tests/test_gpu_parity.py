@@ -242,3 +242,18 @@ def test_c5_full_size_sampled():
     r = gpu_run(inp, out, slo, cfg)
     _global_properties(len(inp), cfg, r)
     _window_sample_parity(inp, out, slo, cfg, r, [1, 3, 6, 9])
+
+
+@pytest.mark.parametrize("gen", [lambda: W.c2(3, n=20_000), lambda: W.c3(6, n=150_000)])
+def test_generic_64bit_path(gen):
+    """flags bit 0 forces the generic 64-bit SEG-DP kernels: identical results."""
+    inp, out, slo, cfg = gen()
+    assert_parity(inp, out, slo, cfg.replace(flags=1, dp_tile=4 * cfg.max_batch))
+    assert_parity(inp, out, slo, cfg.replace(flags=0, dp_tile=4 * cfg.max_batch))
+
+
+def test_wide_values_take_generic_path():
+    """lengths >= 2^16 disable the 32-bit fast path automatically."""
+    inp, out, slo, cfg = W.c2(4, n=3000)
+    inp = inp.copy(); inp[::97] = 70_000
+    assert_parity(inp, out, slo, cfg.replace(kv_cap_bytes=0, lambda_us=0))

@@ -58,6 +58,7 @@ class SchedConfig:
     eps: float = 1e-9
     eq2_additive: int = 0
     dp_tile: int = 0                # GPU SEG-DP tile length (tuning only; 0 = automatic)
+    flags: int = 0                  # GPU: bit 0 forces the generic 64-bit SEG-DP kernels (testing)
 
     def replace(self, **kw) -> "SchedConfig":
         return dataclasses.replace(self, **kw)
