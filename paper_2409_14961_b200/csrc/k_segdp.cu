@@ -268,6 +268,16 @@ __device__ __forceinline__ unsigned long long pack_slot(uint32_t i, uint32_t mo,
     return (unsigned long long)i | ((unsigned long long)mo << 32) | ((unsigned long long)mi << 48);
 }
 
+struct SlotWriter {            // writes a candidate slot with its derived cost terms
+    uint32_t t_b, t_it, t_tok, t_pre;
+    __device__ __forceinline__ void put(const NarrowSlots &S, uint32_t pos, long long C, uint32_t i, uint32_t mo,
+                                        uint32_t mi) const
+    {
+        S.cC[pos] = C;
+        S.cP[pos] = pack_slot(i, mo, mi);
+    }
+};
+
 struct NarrowCfg {
     uint32_t W, cap32, t_b, t_it, t_tok, t_pre, split;
     unsigned long long lam;
@@ -526,7 +536,7 @@ __device__ DpResult dp_warp_narrow(const DPParams &P, const NarrowSlots &S, uint
 //     smaller i, which is always the external one);
 //  3. once per block the list is extended by the 32 new candidates and pruned at the block-end
 //     state (dead prefix + D1), which is valid for every later boundary.
-template <bool FIX>
+template <bool FIX, bool LAM>
 __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uint32_t s, uint32_t e,
                                     const long long *__restrict__ src, uint32_t stop_min)
 {
@@ -538,6 +548,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                    t_pre = (uint32_t)P.t_pre;
     const bool split = P.split != 0;
     const unsigned long long lam = P.lambda;
+    const SlotWriter SW{t_b, t_it, t_tok, t_pre};
     const uint32_t *__restrict__ rin = P.rin;
     const uint32_t *__restrict__ rout = P.rout;
     const uint32_t *__restrict__ rslo = P.rslo;
@@ -547,7 +558,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     long long d_run = 0;
     uint32_t run = 0;
     if (!FIX) {
-        if (lane == 0) { S.cC[0] = 0; S.cP[0] = pack_slot(s, 0, 0); }
+        if (lane == 0) SW.put(S, 0, 0, s, 0, 0);
         L = 1;
         run_start = s;
         prev_slo = __ldg(rslo + s);
@@ -568,11 +579,11 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if ((int)lane >= d) { vo = max(vo, to); vi = max(vi, ti); }
             }
             vo = max(vo, cmo); vi = max(vi, cmi);
-            if (valid) { const uint32_t q = p - i0; S.cC[q] = src[p - 1]; S.cP[q] = pack_slot(p, vo, vi); }
+            if (valid) SW.put(S, p - i0, src[p - 1], p, vo, vi);
             cmo = __shfl_sync(0xffffffffu, vo, 31);
             cmi = __shfl_sync(0xffffffffu, vi, 31);
         }
-        if (lane == 0) { S.cC[W - 1] = src[s - 1]; S.cP[W - 1] = pack_slot(s, 0, 0); }
+        if (lane == 0) SW.put(S, W - 1, src[s - 1], s, 0, 0);
         L = W;
         run_start = __reduce_max_sync(0xffffffffu, rs);
         prev_slo = __ldg(rslo + s - 1);
@@ -603,66 +614,96 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             if ((int)lane >= d) { pmo = max(pmo, a); pmi = max(pmi, b); rsv = max(rsv, c); }
         }
         const uint32_t rs_l = max(run_start, rsv);
+        const uint32_t rs_last = __shfl_sync(0xffffffffu, rs_l, B - 1);
+        // An interval [i, j) lies inside one SLO run iff i >= run start of element j-1; only then
+        // is viol a single comparison.  Crossing intervals exist in this block only if the oldest
+        // external candidate starts before the last run start (external), or a run starts inside
+        // the block (intra); those rare blocks take the binary-search variant.
+        const bool ext_slow = LAM && !split && ((uint32_t)S.cP[0] < rs_last);
+        const bool intra_slow = LAM && !split && (rs_last > j0);
         // ---- 1. external candidates
         unsigned long long lb = ~0ull;
         uint32_t lbi = 0xffffffffu;
+        // candidates oldest -> newest; strict '<' keeps the smallest minimising i (R9)
         evals += L * B;
-        for (uint32_t c = 0; c < L; ++c) {
-            const long long cC = S.cC[c];
-            const unsigned long long cp = S.cP[c];
-            const uint32_t ci = (uint32_t)cp;
-            const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, pmo);
-            const uint32_t mi = max((uint32_t)(cp >> 48), pmi);
-            const uint32_t b = jl - ci;
-            const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
-            const bool dead = !vl | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < rs_l));
-            uint32_t v = 0;
-            if (lam) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
-                                      : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
-            const unsigned long long tot = (unsigned long long)cC + est + lam * v;
-            if (!dead && tot < lb) { lb = tot; lbi = ci; }
-        }
+        auto ext_pass = [&](auto slow_tag) {
+            constexpr bool SLOW = decltype(slow_tag)::value;
+#pragma unroll 2
+            for (uint32_t c = 0; c < L; ++c) {
+                const unsigned long long cp = S.cP[c];
+                const uint32_t ci = (uint32_t)cp;
+                const long long cC = S.cC[c];
+                const uint32_t b = jl - ci;
+                const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, pmo);
+                const uint32_t mi = max((uint32_t)(cp >> 48), pmi);
+                const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
+                const bool dead = !vl | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < rs_l));
+                unsigned long long tot = (unsigned long long)cC + est;
+                if (LAM) {
+                    uint32_t v;
+                    if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
+                                               : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
+                    else v = (slo_l < est) ? b : 0u;
+                    tot += lam * v;
+                }
+                if (!dead && tot < lb) { lb = tot; lbi = ci; }
+            }
+        };
+        if (ext_slow) ext_pass(std::true_type{}); else ext_pass(std::false_type{});
         // ---- 2. intra-block candidates, boundary by boundary
         long long iC = 0;
         uint32_t imo = 0, imi = 0;
         long long o_C = 0;
         uint32_t o_A = 0;
         uint32_t kdone = B;
-        for (uint32_t k = 0; k < B; ++k) {
-            const uint32_t ok = __shfl_sync(0xffffffffu, out_l, k), ik = __shfl_sync(0xffffffffu, in_l, k);
-            const uint32_t sk = __shfl_sync(0xffffffffu, slo_l, k), rsk = __shfl_sync(0xffffffffu, rs_l, k);
-            const bool act = lane < k;
-            if (act) { imo = max(imo, ok); imi = max(imi, ik); }
-            const uint32_t j = j0 + k + 1;
+        auto intra_pass = [&](auto slow_tag) {
+            constexpr bool SLOW = decltype(slow_tag)::value;
             const uint32_t ci = j0 + 1 + lane;
-            const uint32_t b = k - lane;
-            const uint32_t est = t_b + t_it * imo + b * (t_tok * imo + t_pre * imi);
-            const bool dead = !act | (b > W) | ((b > 1) & (b * (imo + imi) > cap32)) | (split & (ci < rsk));
-            uint32_t v = 0;
-            if (lam) v = (ci >= rsk) ? ((sk < est) ? b : 0u) : (dead ? 0u : viol_count_slow(rslo, ci, j, est, sk));
-            unsigned long long val = dead ? ~0ull : (unsigned long long)iC + est + lam * v;
-            uint32_t idx = ci;
-            if (lane == k) { val = lb; idx = lbi; }
-            const uint32_t hi = (uint32_t)(val >> 32);
-            const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
-            const uint32_t lo = (hi == mhi) ? (uint32_t)val : 0xffffffffu;
-            const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
-            const uint32_t barg = __reduce_min_sync(0xffffffffu, (hi == mhi && (uint32_t)val == mlo) ? idx : 0xffffffffu);
-            const long long best = (long long)(((unsigned long long)mhi << 32) | mlo);
-            if (lane == k) { iC = best; o_C = best; o_A = j - barg; }
-            if (FIX) {
-                const long long cl = __shfl_sync(0xffffffffu, cl_l, k);
-                const long long dj = best - cl;
-                if (dj == d_run) ++run; else { d_run = dj; run = 1; }
-                if (run >= W && j >= stop_min) {
-                    R.conv = 1; R.conv_pos = j; R.fix_end = j; R.delta = d_run;
-                    stop = true;
-                    kdone = k + 1;
-                    break;
+            for (uint32_t k = 0; k < B; ++k) {
+                const uint32_t ok = __shfl_sync(0xffffffffu, out_l, k), ik = __shfl_sync(0xffffffffu, in_l, k);
+                const uint32_t sk = __shfl_sync(0xffffffffu, slo_l, k);
+                const bool act = lane < k;
+                if (act) { imo = max(imo, ok); imi = max(imi, ik); }
+                const uint32_t j = j0 + k + 1;
+                const uint32_t b = k - lane;
+                const uint32_t est = t_b + t_it * imo + b * (t_tok * imo + t_pre * imi);
+                bool dead = !act | (b > W) | ((b > 1) & (b * (imo + imi) > cap32));
+                unsigned long long val = (unsigned long long)iC + est;
+                if (SLOW || split) {
+                    const uint32_t rsk = __shfl_sync(0xffffffffu, rs_l, k);
+                    dead |= split & (ci < rsk);
+                    if (LAM) {
+                        const uint32_t v = (ci >= rsk) ? ((sk < est) ? b : 0u)
+                                                       : (dead ? 0u : viol_count_slow(rslo, ci, j, est, sk));
+                        val += lam * v;
+                    }
+                } else if (LAM) {
+                    val += lam * ((sk < est) ? b : 0u);
+                }
+                if (dead) val = ~0ull;
+                uint32_t idx = ci;
+                if (lane == k) { val = lb; idx = lbi; }
+                const uint32_t hi = (uint32_t)(val >> 32);
+                const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+                const uint32_t lo = (hi == mhi) ? (uint32_t)val : 0xffffffffu;
+                const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
+                const uint32_t barg = __reduce_min_sync(0xffffffffu, (hi == mhi && (uint32_t)val == mlo) ? idx : 0xffffffffu);
+                const long long best = (long long)(((unsigned long long)mhi << 32) | mlo);
+                if (lane == k) { iC = best; o_C = best; o_A = j - barg; }
+                if (FIX) {
+                    const long long cl = __shfl_sync(0xffffffffu, cl_l, k);
+                    const long long dj = best - cl;
+                    if (dj == d_run) ++run; else { d_run = dj; run = 1; }
+                    if (run >= W && j >= stop_min) {
+                        R.conv = 1; R.conv_pos = j; R.fix_end = j; R.delta = d_run;
+                        stop = true;
+                        kdone = k + 1;
+                        break;
+                    }
                 }
             }
-        }
-        evals += B * (B - 1) / 2;
+        };
+        if (intra_slow) intra_pass(std::true_type{}); else intra_pass(std::false_type{});
         // outputs of this block
         if (lane < kdone) {
             (FIX ? P.CFx : P.Cx)[x] = o_C;
@@ -675,7 +716,8 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         const uint32_t bmo = __shfl_sync(0xffffffffu, pmo, B - 1), bmi = __shfl_sync(0xffffffffu, pmi, B - 1);
         run_start = __shfl_sync(0xffffffffu, rs_l, B - 1);
         prev_slo = __shfl_sync(0xffffffffu, slo_l, B - 1);
-        if (vl) { S.cC[L + lane] = iC; S.cP[L + lane] = pack_slot(j0 + 1 + lane, imo, imi); }
+        if (vl) SW.put(S, L + lane, iC, j0 + 1 + lane, imo, imi);
+        evals += B * (B - 1) / 2;
         __syncwarp();
         const uint32_t Lt = L + B;
         uint32_t wr = 0;
@@ -701,8 +743,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             const uint32_t bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const uint32_t pos = wr + __popc(bal & lt);
-                S.cC[pos] = cC;
-                S.cP[pos] = pack_slot(ci, mo, mi);
+                SW.put(S, pos, cC, ci, mo, mi);
             }
             wr += __popc(bal);
             __syncwarp();
@@ -739,12 +780,13 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
         NarrowSlots S;
         S.cC = (long long *)p;
         S.cP = (unsigned long long *)(p + (size_t)P.cap_slots * 8);
-        return dp_warp_blocked<FIX>(P, S, s, e, src, stop_min);
+        if (P.lambda) return dp_warp_blocked<FIX, true>(P, S, s, e, src, stop_min);
+        return dp_warp_blocked<FIX, false>(P, S, s, e, src, stop_min);
     }
     return dp_warp<FIX>(P, slots_for(smem, P.cap_slots, warp), s, e, src, stop_min);
 }
 
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_local(DPParams P, uint64_t ntiles)
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 3) k_dp_local(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
     const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -766,7 +808,7 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_local(DPParams P,
     }
 }
 
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_fix(DPParams P, uint64_t ntiles)
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 3) k_dp_fix(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
     const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
