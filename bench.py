@@ -174,6 +174,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.distributed import GATHER_WORDS, combine_totals
     from paper_2409_14961_b200.scheduler import GpuScheduler
 
     torch.cuda.set_device(local)
@@ -196,7 +197,8 @@ def main():
         for row in ev:
             for e in row:
                 e.record(stream)          # materialise the cudaEvent_t handles
-    gather_buf = torch.zeros(world * 16, dtype=torch.int64, device=dev)
+    gather_buf = torch.zeros(world * GATHER_WORDS, dtype=torch.int64, device=dev)
+    gather_in = torch.zeros(GATHER_WORDS, dtype=torch.int64, device=dev)
 
     def step(k=None):
         if k is not None:
@@ -207,11 +209,10 @@ def main():
             U.set_stage_events(g.profile, ev[k])
         g.schedule(stream)
         g.stats(stream)
-        if world > 1:   # a9: one NCCL allgather of the per-rank totals
+        if world > 1:   # a9: one NCCL allgather of the per-rank totals (device-resident)
             with torch.cuda.stream(stream):
-                mine = g.totals.view(torch.int64)[:13].clone()
-                mine = torch.cat([mine, torch.zeros(3, dtype=torch.int64, device=dev)])
-                dist.all_gather_into_tensor(gather_buf, mine)
+                gather_in[:13].copy_(g.totals.view(torch.int64)[:13])
+                dist.all_gather_into_tensor(gather_buf, gather_in)
 
     for _ in range(Wm):
         step()
@@ -291,9 +292,8 @@ def main():
             U.batch_stats(p, g.cfg, h_offs, h_nb, None, h_tot, stream)
             if world > 1:
                 with torch.cuda.stream(stream):
-                    mine = torch.from_numpy(h_tot.numpy()[:104].view(np.int64).copy()).to(dev)
-                    mine = torch.cat([mine, torch.zeros(3, dtype=torch.int64, device=dev)])
-                    dist.all_gather_into_tensor(gather_buf, mine)
+                    gather_in[:13].copy_(h_tot.view(torch.int64)[:13], non_blocking=True)
+                    dist.all_gather_into_tensor(gather_buf, gather_in)
         e2e_step()
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -331,6 +331,8 @@ def main():
             "roofline": roof, "step_hbm_roofline": step_hbm, "stage_ms": st_ms,
             "gpu_launches": int(diag["sched_launches"] + diag["stats_launches"] + 1),
             "diagnostics": diag, "batches": m, "dp_cost": res["totals"]["dp_cost"],
+            "job_totals": ({k: v for k, v in combine_totals(gather_buf.view(world, GATHER_WORDS)).items()
+                            if k in ("n", "batches", "dp_cost", "viol_alone")} if world > 1 else None),
             "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -8,9 +8,11 @@
 //   arg[j]    = the smallest minimising i                                      (R9)
 //
 // GPU design:
-//  * one warp per tile of T positions (T a multiple of W, tiles never cross windows); lanes
-//    evaluate the live breakpoint candidates of the tile's current position in parallel and
-//    reduce (cost, i) with three redux.sync.min;
+//  * one warp per tile of T positions (T a multiple of W, tiles never cross windows);
+//  * fast path (dp_warp_blocked, 32-bit cost arithmetic): blocks of 32 boundaries, lane =
+//    boundary for the candidates born before the block, lane = candidate for the ones born
+//    inside it (argmin by three redux.sync.min per boundary); generic path (dp_warp, 64-bit):
+//    lane = candidate, one boundary at a time;
 //  * exact dominance pruning D1 against the next live candidate:
 //      i dead once C[i'] - C[i] < (i' - i) * (t_tok*MO(i',j) + t_prefill*MI(i',j)),
 //    plus the monotone deaths (b > W, KV cap, SLO split) which always form a prefix;
@@ -252,12 +254,7 @@ __device__ DpResult dp_warp(const DPParams &P, const WarpSlots &S, uint32_t s, u
 // Fast path ("narrow"): valid when max_in, max_out < 2^16 and
 //   E = t_batch + t_iter*max_out + W*(t_tok*max_out + t_prefill*max_in) < 2^32,
 // so est, S = t_tok*MO + t_prefill*MI, b*S and b*(MI+MO) all fit 32 bits (checked on the host).
-// Same recurrence, same tie rule, same pruning as dp_warp; differences are mechanical:
-//  * two positions (j, j+1) per iteration: every live candidate is loaded once, evaluated for
-//    both, D1-tested and compacted once (at the j+1 state); the candidate born at j is
-//    evaluated for j+1 as a scalar after C[j] is known;
-//  * a slot is 16 bytes: C (i64) and (i | MO << 32 | MI << 48);
-//  * branch-free predicated evaluation; D1 neighbour read from shared memory.
+// A candidate slot is 16 bytes: C (i64) and (i | MO << 32 | MI << 48).
 struct NarrowSlots {
     long long *cC;
     unsigned long long *cP;     // i | mo << 32 | mi << 48
@@ -277,251 +274,6 @@ struct SlotWriter {            // writes a candidate slot with its derived cost 
         S.cP[pos] = pack_slot(i, mo, mi);
     }
 };
-
-struct NarrowCfg {
-    uint32_t W, cap32, t_b, t_it, t_tok, t_pre, split;
-    unsigned long long lam;
-};
-
-// cost of candidate (C, i) for boundary j with maxima (mo, mi); ~0 if infeasible or !valid
-__device__ __forceinline__ unsigned long long narrow_total(const NarrowCfg &K, const uint32_t *__restrict__ rslo,
-                                                          bool valid, long long C, uint32_t i, uint32_t j,
-                                                          uint32_t mo, uint32_t mi, uint32_t rs, uint32_t slo_x)
-{
-    const uint32_t b = j - i;
-    const uint32_t S = K.t_tok * mo + K.t_pre * mi;
-    const uint32_t est = K.t_b + K.t_it * mo + b * S;
-    const bool dead = !valid | (b > K.W) | ((b > 1) & (b * (mo + mi) > K.cap32)) | ((K.split != 0) & (i < rs));
-    unsigned long long tot = (unsigned long long)C + est;
-    if (K.lam && !dead) {
-        uint32_t v;
-        if (i >= rs) v = (slo_x < est) ? b : 0u;
-        else v = viol_count_slow(rslo, i, j, est, slo_x);
-        tot += K.lam * v;
-    }
-    return dead ? ~0ull : tot;
-}
-
-template <bool FIX>
-__device__ DpResult dp_warp_narrow(const DPParams &P, const NarrowSlots &S, uint32_t s, uint32_t e,
-                                   const long long *__restrict__ src, uint32_t stop_min)
-{
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t lt = lane_lt();
-    NarrowCfg K;
-    K.W = P.W; K.cap32 = (uint32_t)min(P.cap_tok, 0xffffffffull);
-    K.t_b = (uint32_t)P.t_batch; K.t_it = (uint32_t)P.t_iter; K.t_tok = (uint32_t)P.t_tok;
-    K.t_pre = (uint32_t)P.t_pre; K.split = P.split; K.lam = P.lambda;
-    const uint32_t *__restrict__ rin = P.rin;
-    const uint32_t *__restrict__ rout = P.rout;
-    const uint32_t *__restrict__ rslo = P.rslo;
-    DpResult R;
-    R.conv = 0; R.conv_pos = e; R.fix_end = e; R.delta = 0; R.positions = 0; R.evals = 0;
-    uint32_t L, run_start, prev_slo;
-    long long Cprev;
-    long long d_run = 0;
-    uint32_t run = 0;
-    if (!FIX) {
-        if (lane == 0) { S.cC[0] = 0; S.cP[0] = pack_slot(s, 0, 0); }
-        L = 1;
-        run_start = s;
-        prev_slo = __ldg(rslo + s);
-        Cprev = 0;
-    } else {
-        const uint32_t W = K.W, i0 = s - W + 1;
-        uint32_t cmo = 0, cmi = 0, rs = i0;
-        for (uint32_t r = 0; r * 32 < W; ++r) {
-            const uint32_t off = r * 32 + lane + 1;
-            const bool valid = off <= W - 1;
-            const uint32_t p = s - off;
-            uint32_t vo = valid ? __ldg(rout + p) : 0, vi = valid ? __ldg(rin + p) : 0;
-            const uint32_t vs = valid ? __ldg(rslo + p) : 0;
-            const uint32_t vsp = (valid && p > i0) ? __ldg(rslo + p - 1) : vs;
-            if (valid && p > i0 && vs != vsp) rs = max(rs, p);
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t to = __shfl_up_sync(0xffffffffu, vo, d), ti = __shfl_up_sync(0xffffffffu, vi, d);
-                if ((int)lane >= d) { vo = max(vo, to); vi = max(vi, ti); }
-            }
-            vo = max(vo, cmo); vi = max(vi, cmi);
-            if (valid) { const uint32_t q = p - i0; S.cC[q] = src[p - 1]; S.cP[q] = pack_slot(p, vo, vi); }
-            cmo = __shfl_sync(0xffffffffu, vo, 31);
-            cmi = __shfl_sync(0xffffffffu, vi, 31);
-        }
-        if (lane == 0) { S.cC[W - 1] = src[s - 1]; S.cP[W - 1] = pack_slot(s, 0, 0); }
-        L = W;
-        run_start = __reduce_max_sync(0xffffffffu, rs);
-        prev_slo = __ldg(rslo + s - 1);
-        Cprev = src[s - 1];
-        d_run = Cprev;
-        run = 1;
-    }
-    __syncwarp();
-
-    uint32_t cbase = s, c_in = 0, c_out = 0, c_slo = 0;
-    long long c_cl = 0, o_C = 0;
-    uint32_t o_A = 0;
-    auto refill = [&](uint32_t base) {
-        const uint32_t p = base + lane;
-        const bool v = p < e;
-        c_in = v ? __ldg(rin + p) : 0;
-        c_out = v ? __ldg(rout + p) : 0;
-        c_slo = v ? __ldg(rslo + p) : 0;
-        if (FIX) c_cl = v ? P.Cx[p] : 0;
-    };
-    auto flush = [&](uint32_t upto) {
-        const uint32_t p = cbase + lane;
-        if (p < upto) {
-            (FIX ? P.CFx : P.Cx)[p] = o_C;
-            P.argx[p] = (uint16_t)o_A;
-        }
-    };
-    refill(cbase);
-
-    uint32_t j = s + 1;          // boundaries j (element x0 = j-1) and j+1 (element x1 = j)
-    uint32_t done = s;           // last boundary computed
-    bool stop = false;
-    while (j <= e && !stop) {
-        const uint32_t x0 = j - 1;
-        if (x0 - cbase >= 32) { flush(x0); cbase = x0; refill(cbase); }
-        const bool two = (j + 1 <= e);
-        const uint32_t l0 = x0 - cbase, l1 = l0 + 1;   // l1 <= 31 since x0 - cbase is even
-        const uint32_t in0 = __shfl_sync(0xffffffffu, c_in, l0), out0 = __shfl_sync(0xffffffffu, c_out, l0);
-        const uint32_t slo0 = __shfl_sync(0xffffffffu, c_slo, l0);
-        const uint32_t in1 = __shfl_sync(0xffffffffu, c_in, l1), out1 = __shfl_sync(0xffffffffu, c_out, l1);
-        const uint32_t slo1 = __shfl_sync(0xffffffffu, c_slo, l1);
-        uint32_t rs0 = run_start;
-        if (slo0 != prev_slo) rs0 = x0;
-        uint32_t rs1 = rs0;
-        if (two && slo1 != slo0) rs1 = x0 + 1;
-        const uint32_t omax = two ? max(out0, out1) : out0, imax = two ? max(in0, in1) : in0;
-        // ---- rounds over the live candidates
-        unsigned long long lb0 = ~0ull, lb1 = ~0ull;
-        uint32_t lbi0 = 0xffffffffu, lbi1 = 0xffffffffu;
-        uint32_t wr = 0;
-        R.evals += (unsigned long long)L * (two ? 2u : 1u);
-        const uint32_t nr = (L + 31) >> 5;
-        const uint32_t jj = two ? j + 1 : j;              // state at which survival is decided
-        const uint32_t rsx = two ? rs1 : rs0;
-        const uint32_t oldest = (uint32_t)S.cP[0];        // smallest live i (broadcast read)
-        // a candidate interval crosses an SLO-run boundary only if it starts before the run
-        const bool slow = (K.lam != 0) && (K.split == 0) && (oldest < rsx);
-        const uint32_t tbm0 = 0, tbm1 = 0;
-        (void)tbm0; (void)tbm1;
-        auto round = [&](auto slow_tag) {
-            constexpr bool SLOW = decltype(slow_tag)::value;
-            for (uint32_t r = 0; r < nr; ++r) {
-                const uint32_t k = r * 32 + lane;
-                const bool valid = k < L;
-                const bool has_next = k + 1 < L;
-                long long cC = 0, nC = 0;
-                unsigned long long cp = 0, np = 0;
-                if (valid) { cC = S.cC[k]; cp = S.cP[k]; }
-                if (has_next) { nC = S.cC[k + 1]; np = S.cP[k + 1]; }
-                const uint32_t ci = (uint32_t)cp;
-                // position j: maxima over [ci, j)
-                const uint32_t mo0 = max((uint32_t)(cp >> 32) & 0xffffu, out0);
-                const uint32_t mi0 = max((uint32_t)(cp >> 48), in0);
-                const uint32_t b0 = j - ci;
-                const uint32_t e0 = K.t_b + K.t_it * mo0 + b0 * (K.t_tok * mo0 + K.t_pre * mi0);
-                const bool dead0 = !valid | (b0 > K.W) | ((b0 > 1) & (b0 * (mo0 + mi0) > K.cap32)) |
-                                   ((K.split != 0) & (ci < rs0));
-                // position j+1: maxima over [ci, j+1)
-                const uint32_t mo1 = max(mo0, out1), mi1 = max(mi0, in1);
-                const uint32_t b1 = b0 + 1;
-                const uint32_t e1 = K.t_b + K.t_it * mo1 + b1 * (K.t_tok * mo1 + K.t_pre * mi1);
-                const bool dead1 = !two | !valid | (b1 > K.W) | (b1 * (mo1 + mi1) > K.cap32) |
-                                   ((K.split != 0) & (ci < rs1));
-                uint32_t v0 = 0, v1 = 0;
-                if (K.lam) {
-                    if (SLOW) {
-                        v0 = dead0 ? 0u : (ci >= rs0 ? ((slo0 < e0) ? b0 : 0u) : viol_count_slow(rslo, ci, j, e0, slo0));
-                        v1 = dead1 ? 0u : (ci >= rs1 ? ((slo1 < e1) ? b1 : 0u) : viol_count_slow(rslo, ci, j + 1, e1, slo1));
-                    } else {
-                        v0 = (slo0 < e0) ? b0 : 0u;
-                        v1 = (slo1 < e1) ? b1 : 0u;
-                    }
-                }
-                const unsigned long long t0 = (unsigned long long)cC + e0 + K.lam * v0;
-                const unsigned long long t1 = (unsigned long long)cC + e1 + K.lam * v1;
-                if (!dead0 && t0 < lb0) { lb0 = t0; lbi0 = ci; }
-                if (!dead1 && t1 < lb1) { lb1 = t1; lbi1 = ci; }
-                // survival at state jj: alive and not dominated by slot k+1 (D1)
-                const bool dead = two ? dead1 : dead0;
-                const uint32_t ni = (uint32_t)np;
-                const uint32_t nmo = max((uint32_t)(np >> 32) & 0xffffu, omax), nmi = max((uint32_t)(np >> 48), imax);
-                const uint32_t nS = K.t_tok * nmo + K.t_pre * nmi;
-                const bool dominated = has_next && (nC - cC < (long long)(unsigned long long)((ni - ci) * nS));
-                const bool keep = !dead && !dominated;
-                __syncwarp();
-                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    const uint32_t pos = wr + __popc(bal & lt);
-                    S.cC[pos] = cC;
-                    S.cP[pos] = pack_slot(ci, two ? mo1 : mo0, two ? mi1 : mi0);
-                }
-                wr += __popc(bal);
-                __syncwarp();
-            }
-        };
-        if (slow) round(std::true_type{}); else round(std::false_type{});
-        (void)jj;
-        L = wr;
-        // ---- argmin for j
-        uint32_t hi = (uint32_t)(lb0 >> 32);
-        uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
-        uint32_t lo = (hi == mhi) ? (uint32_t)lb0 : 0xffffffffu;
-        uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
-        uint32_t barg0 = __reduce_min_sync(0xffffffffu, (hi == mhi && (uint32_t)lb0 == mlo) ? lbi0 : 0xffffffffu);
-        const long long best0 = (long long)(((unsigned long long)mhi << 32) | mlo);
-        long long best1 = 0;
-        uint32_t barg1 = 0;
-        if (two) {
-            hi = (uint32_t)(lb1 >> 32);
-            mhi = __reduce_min_sync(0xffffffffu, hi);
-            lo = (hi == mhi) ? (uint32_t)lb1 : 0xffffffffu;
-            mlo = __reduce_min_sync(0xffffffffu, lo);
-            barg1 = __reduce_min_sync(0xffffffffu, (hi == mhi && (uint32_t)lb1 == mlo) ? lbi1 : 0xffffffffu);
-            best1 = (long long)(((unsigned long long)mhi << 32) | mlo);
-            // candidate born at j (a single query, always admissible) for boundary j+1
-            const unsigned long long tj = narrow_total(K, rslo, true, best0, j, j + 1, out1, in1, rs1, slo1);
-            if (tj < (unsigned long long)best1) { best1 = (long long)tj; barg1 = j; }
-        }
-        if (lane == l0) { o_C = best0; o_A = j - barg0; }
-        if (two && lane == l1) { o_C = best1; o_A = j + 1 - barg1; }
-        // ---- append the candidates born at j (maxima over [j, j+1)) and j+1 (empty)
-        if (two) {
-            if (lane == 0) {
-                S.cC[L] = best0; S.cP[L] = pack_slot(j, out1, in1);
-                S.cC[L + 1] = best1; S.cP[L + 1] = pack_slot(j + 1, 0, 0);
-            }
-            L += 2;
-        }
-        __syncwarp();
-        R.positions += two ? 2 : 1;
-        run_start = two ? rs1 : rs0;
-        prev_slo = two ? slo1 : slo0;
-        Cprev = two ? best1 : best0;
-        done = two ? j + 1 : j;
-        if (FIX) {
-            for (int q = 0; q < (two ? 2 : 1); ++q) {
-                const uint32_t jq = j + q;
-                const long long cl = __shfl_sync(0xffffffffu, c_cl, l0 + q);
-                const long long dj = (q ? best1 : best0) - cl;
-                if (dj == d_run) ++run; else { d_run = dj; run = 1; }
-                if (run >= K.W && jq >= stop_min) {
-                    R.conv = 1; R.conv_pos = jq; R.fix_end = done; R.delta = d_run;
-                    stop = true;
-                    break;
-                }
-            }
-        }
-        j += 2;
-    }
-    (void)Cprev;
-    flush(done);                          // positions [cbase, done)
-    return R;
-}
 
 // -------------------------------------------------------------------------------------
 // Blocked fast path (narrow arithmetic).  Positions are processed in blocks of 32 boundaries

@@ -257,3 +257,24 @@ def test_wide_values_take_generic_path():
     inp, out, slo, cfg = W.c2(4, n=3000)
     inp = inp.copy(); inp[::97] = 70_000
     assert_parity(inp, out, slo, cfg.replace(kv_cap_bytes=0, lambda_us=0))
+
+
+def test_sharded_ranks_equal_single_run():
+    """T5 on one GPU: the window blocks of 4 emulated ranks, scheduled separately, give exactly
+    the single-run batches and (combined via the a9 packing) the single-run totals."""
+    from paper_2409_14961_b200 import distributed as D
+    inp, out, slo, cfg = W.c3(12, n=400_000)
+    cfg = cfg.replace(window=30_000)
+    full = gpu_run(inp, out, slo, cfg)
+    rows, offs_all = [], []
+    for r in range(4):
+        a, z = D.query_range(len(inp), cfg.window, 4, r)
+        part = gpu_run(inp[a:z], out[a:z], slo[a:z], cfg)
+        rows.append(D.pack_totals(part["totals"], "cpu"))
+        offs_all.append(part["offsets"][:-1].astype(np.int64) + a)
+        assert np.array_equal(part["order"].astype(np.int64) + a, full["order"][a:z].astype(np.int64))
+    offs = np.concatenate(offs_all + [np.array([len(inp)])])
+    assert np.array_equal(offs, full["offsets"].astype(np.int64))
+    comb = D.combine_totals(torch.stack(rows))
+    for f in D.TOTAL_FIELDS:
+        assert comb[f] == full["totals"][f], f
