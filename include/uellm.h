@@ -150,6 +150,8 @@ typedef struct {
     uint64_t dp_candidate_evals;    /* SEG-DP: breakpoint candidates evaluated (all passes)         */
     uint64_t sched_launches;        /* kernels launched by the last uellm_schedule_batches          */
     uint64_t stats_launches;        /* kernels launched by the last uellm_batch_stats               */
+    uint64_t sort_key_bits;         /* sort key width: bits(rank) + bits(max_out) when the distinct
+                                       SLO values (<= 1024) were rank-compressed, else 64          */
 } uellm_diagnostics;
 
 /* Optional per-stage timing.  Stage boundaries at which uellm_schedule_batches /

@@ -46,6 +46,8 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.keys0 = take(8 * N); L.keys1 = take(8 * N); L.keys2 = take(8 * N);
     L.vals0 = take(4 * N); L.vals1 = take(4 * N); L.vals2 = take(4 * N);
     L.rin = take(4 * N); L.rout = take(4 * N); L.rslo = take(4 * N);
+    L.keysc = take(4 * N);
+    L.slo_set = take(4 * kSloSetSize); L.slo_rank = take(4 * kSloSetSize); L.slo_table = take(4 * kSloRankMax);
     L.order = take(4 * N); L.offsets = take(4 * (N + 1));
     L.argx = take(2 * N);
     L.tiles = take(sizeof(TileRec) * (L.ntiles ? L.ntiles : 1));
@@ -192,7 +194,9 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     LoadMeta *meta = at<LoadMeta>(w, L.meta);
     CU(cudaMemsetAsync(meta, 0, sizeof(LoadMeta), st));
     CU(cudaMemsetAsync(&meta->key_and, 0xff, sizeof(unsigned long long), st));
-    CU(launch_load(din, dout, dslo, n, at<unsigned long long>(w, L.keys0), at<uint32_t>(w, L.vals0), meta, st));
+    CU(cudaMemsetAsync(at<uint32_t>(w, L.slo_set), 0, 4 * kSloSetSize, st));
+    CU(launch_load(din, dout, dslo, n, at<unsigned long long>(w, L.keys0), at<uint32_t>(w, L.vals0), meta,
+                   at<uint32_t>(w, L.slo_set), st));
     LoadMeta hm;
     CU(cudaMemcpyAsync(&hm, meta, sizeof hm, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -209,6 +213,7 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     v.d_in = din; v.d_out = dout;
     v.max_in = hm.max_in; v.max_out = hm.max_out; v.max_slo = hm.max_slo;
     v.key_or = hm.key_or; v.key_and = hm.key_and;
+    v.slo_distinct = hm.slo_distinct; v.slo_overflow = hm.slo_overflow;
     std::memcpy(out, &v, sizeof v);
     return UELLM_OK;
 }
@@ -255,27 +260,51 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         if (!dev_offs || !dev_nb) CU(cudaStreamSynchronize(st));
         return UELLM_OK;
     }
-    // a3: sort (every mode except FIFO)
-    const unsigned long long *keys = at<unsigned long long>(w, L.keys0);
-    const uint32_t *vals = at<uint32_t>(w, L.vals0);
-    int passes = 0;
-    if (cfg->mode != UELLM_MODE_FIFO) {
-        const unsigned long long vary = v.key_or ^ v.key_and;
-        uint32_t mask = 0;
-        for (int d = 0; d < 8; ++d) if ((vary >> (8 * d)) & 0xffull) mask |= 1u << d;
-        CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
-                              at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                              at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st));
-        launches += 3 * passes;
-    }
-    rec(v, UELLM_STAGE_SORT_END, st);
+    // a3: sort (every mode except FIFO) + a4: records in scheduled order
     uint32_t *rin = at<uint32_t>(w, L.rin), *rout = at<uint32_t>(w, L.rout), *rslo = at<uint32_t>(w, L.rslo);
-    CU(launch_decode(keys, vals, v.d_in, n, rin, rout, rslo, d_order, st));
+    int passes = 0;
+    int ob = 0;
+    while (ob < 32 && (v.max_out >> ob)) ++ob;                 // bits(max_out)
+    int rb = 0;
+    while (v.slo_distinct > 1 && rb < 32 && ((v.slo_distinct - 1) >> rb)) ++rb;   // bits(distinct - 1)
+    const bool compressed = cfg->mode != UELLM_MODE_FIFO && !v.slo_overflow && v.slo_distinct >= 1 &&
+                            v.slo_distinct <= kSloRankMax && rb + ob <= 32;
+    if (compressed) {
+        uint32_t *kc = at<uint32_t>(w, L.keysc);
+        CU(launch_slo_rank(at<unsigned long long>(w, L.keys0), n, at<uint32_t>(w, L.slo_set),
+                           at<uint32_t>(w, L.slo_table), at<uint32_t>(w, L.slo_rank), ob, kc, st));
+        launches += 2;
+        uint32_t mask = 0;
+        for (int d = 0; d < 4; ++d) if (8 * d < rb + ob) mask |= 1u << d;
+        const uint32_t *k32 = kc;
+        const uint32_t *vals = at<uint32_t>(w, L.vals0);
+        CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
+                                (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
+                                at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st));
+        launches += 3 * passes;
+        rec(v, UELLM_STAGE_SORT_END, st);
+        CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
+    } else {
+        const unsigned long long *keys = at<unsigned long long>(w, L.keys0);
+        const uint32_t *vals = at<uint32_t>(w, L.vals0);
+        if (cfg->mode != UELLM_MODE_FIFO) {
+            const unsigned long long vary = v.key_or ^ v.key_and;
+            uint32_t mask = 0;
+            for (int d = 0; d < 8; ++d) if ((vary >> (8 * d)) & 0xffull) mask |= 1u << d;
+            CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
+                                  at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
+                                  at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st));
+            launches += 3 * passes;
+        }
+        rec(v, UELLM_STAGE_SORT_END, st);
+        CU(launch_decode(keys, vals, v.d_in, n, rin, rout, rslo, d_order, st));
+    }
     launches += 1;
     rec(v, UELLM_STAGE_DECODE_END, st);
     {
-        unsigned long long sp = (unsigned long long)passes;
-        CU(cudaMemcpyAsync(&diag->sort_passes, &sp, 8, cudaMemcpyHostToDevice, st));
+        unsigned long long sp[2] = {(unsigned long long)passes, compressed ? (unsigned long long)(rb + ob) : 64ull};
+        CU(cudaMemcpyAsync(&diag->sort_passes, &sp[0], 8, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(&diag->sort_key_bits, &sp[1], 8, cudaMemcpyHostToDevice, st));
     }
     // a6/a7: segmentation -> boundary bitmap
     uint32_t *bm = at<uint32_t>(w, L.bitmap);
@@ -435,7 +464,7 @@ uellm_status uellm_get_diagnostics(const uellm_profile *p, uellm_diagnostics *ou
     out->trace_unmerged = hd.trace_unmerged; out->trace_rewalks = hd.trace_rewalks;
     out->sort_passes = hd.sort_passes; out->dp_cost = cost;
     out->dp_candidate_evals = hd.dp_evals; out->sched_launches = hd.sched_launches;
-    out->stats_launches = hd.stats_launches;
+    out->stats_launches = hd.stats_launches; out->sort_key_bits = hd.sort_key_bits;
     return UELLM_OK;
 }
 

@@ -16,6 +16,9 @@ constexpr uint32_t kSortItems = kSortTile / kSortThreads;
 constexpr uint32_t kDpWarpsPerCta = 8;
 constexpr uint32_t kScanBlock = 1024;          // elements per CTA in the scan kernels
 constexpr uint64_t kProfileMagic = 0x55454c4c4d763031ull;  // "UELLMv01"
+constexpr uint32_t kSloSetSize = 4096;         // global hash set of distinct slo_us values
+constexpr uint32_t kSloSetBits = 12;
+constexpr uint32_t kSloRankMax = 1024;         // rank-compress the sort key up to this many values
 
 static inline __host__ __device__ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 static inline __host__ __device__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
@@ -26,7 +29,8 @@ struct LoadMeta {
     uint32_t bad;            // bit 0 input_len == 0, bit 1 out == 0, bit 2 SLO invalid
     uint32_t max_in, max_out, max_slo;
     unsigned long long key_or, key_and;
-    uint32_t pad[8];
+    uint32_t slo_distinct, slo_overflow;
+    uint32_t pad[6];
 };
 static_assert(sizeof(LoadMeta) == 64, "LoadMeta is 64 bytes");
 
@@ -46,7 +50,7 @@ struct TileRec {
 
 struct Diag {                // device counters, see uellm_diagnostics
     unsigned long long tiles, tile_len, fixups_unconverged, cascade_reruns, fixup_positions,
-        trace_unmerged, trace_rewalks, sort_passes, dp_evals, sched_launches, stats_launches;
+        trace_unmerged, trace_rewalks, sort_passes, dp_evals, sched_launches, stats_launches, sort_key_bits;
 };
 
 // Exact 128-bit accumulator of sum(b * completion_us) for mean_latency_s.
@@ -63,6 +67,8 @@ struct WsLayout {
     uint64_t keys0, keys1, keys2;                 // packed keys (kept) + sort ping-pong;
     uint64_t vals0, vals1, vals2;                 // keys1/keys2 re-used as Cx/CFx, est/completion
     uint64_t rin, rout, rslo;                     // scheduled-order records
+    uint64_t keysc;                               // rank-compressed u32 keys
+    uint64_t slo_set, slo_rank, slo_table;        // distinct-SLO hash set, slot ranks, sorted values
     uint64_t order, offsets;                      // internal copies of the schedule
     uint64_t argx;                                // u16 per position
     uint64_t tiles;                               // TileRec[ntiles]
@@ -85,7 +91,8 @@ struct ProfileView {
     uint64_t diag_off, wincost_off;               // workspace offsets read by get_diagnostics
     uint64_t n_events;
     void *events[UELLM_STAGE_COUNT];              // caller cudaEvent_t handles (stage timing)
-    uint64_t pad[11];
+    uint32_t slo_distinct, slo_overflow;
+    uint64_t pad[10];
 };
 static_assert(sizeof(ProfileView) <= sizeof(uellm_profile), "ProfileView fits uellm_profile");
 
@@ -95,7 +102,17 @@ uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_ti
 // --------------------------------------------------------------------------------------
 // Kernel launchers (each returns cudaGetLastError()).
 cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
-                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, cudaStream_t st);
+                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, uint32_t *slo_set,
+                        cudaStream_t st);
+// Rank table of the distinct SLO values + u32 keys rank << ob | out.
+cudaError_t launch_slo_rank(const unsigned long long *keys, uint64_t n, const uint32_t *slo_set, uint32_t *table,
+                            uint32_t *rank_of_slot, int ob, uint32_t *keys32, cudaStream_t st);
+cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
+                                 uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
+                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st);
+cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const uint32_t *in, uint64_t n,
+                            const uint32_t *table, int ob, uint32_t *rin, uint32_t *rout, uint32_t *rslo,
+                            uint32_t *order, cudaStream_t st);
 
 // Segmented (per-window) stable LSD radix sort of (key, val) over the digits of
 // `digit_mask` (bit d set = digit d of 8 bits varies).  *keys_io / *vals_io is the (read-only)

@@ -1,5 +1,6 @@
 // k_load.cu -- a1/a2: validate profiled queries, SLO seconds -> integer us, key packing;
-// decode of sorted keys into scheduled-order records; boundary marks of FIFO / sort-only.
+// SLO rank compression; decode of sorted keys into scheduled-order records; boundary marks of
+// FIFO / sort-only.
 //
 // a1: reject input_len == 0, pred_out_len == 0, non-finite or <= 0 SLO and
 //     slo_us outside [1, 2^32-1]; slo_us = rint(double(slo_s) * 1e6), half-even
@@ -7,37 +8,73 @@
 // a2: key = slo_us << 32 | pred_out_len, payload = arrival index.  Ascending key order is
 //     (SLO, predicted length) order (P:228 + R11); a stable sort keeps arrival order on ties
 //     (R9).  Digits that are constant across all keys are skipped by the sort (OR/AND masks).
+//     The load also collects the set of distinct slo_us values (per-CTA shared-memory hash set,
+//     merged into a 4096-slot global set); with at most kSloRankMax distinct values the sort key
+//     becomes rank(slo_us) << bits(max_out) | out in 32 bits -- the rank among the distinct
+//     values preserves the key order exactly.
 #include "internal.cuh"
 
 namespace uellm {
 
-__global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in,
-                                              const uint32_t *__restrict__ out,
+__device__ __forceinline__ uint32_t slo_hash(uint32_t v, uint32_t bits) { return (v * 0x9E3779B1u) >> (32 - bits); }
+
+__global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, const uint32_t *__restrict__ out,
                                               const float *__restrict__ slo, uint64_t n,
-                                              unsigned long long *__restrict__ keys,
-                                              uint32_t *__restrict__ vals, LoadMeta *meta)
+                                              unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                                              LoadMeta *meta, uint32_t *__restrict__ slo_set)
 {
+    constexpr uint32_t kCtaSlots = 2048, kCtaBits = 11, kCtaMax = kSloRankMax;
+    __shared__ uint32_t cset[kCtaSlots];
+    __shared__ uint32_t ccount, cover;
+    for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) cset[i] = 0;
+    if (threadIdx.x == 0) { ccount = 0; cover = meta->slo_overflow; }
+    __syncthreads();
     uint32_t bad = 0, mx_in = 0, mx_out = 0, mx_slo = 0;
     unsigned long long kor = 0, kand = ~0ull;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        uint32_t a = __ldg(in + k), o = __ldg(out + k);
-        float sf = __ldg(slo + k);
-        double x = (double)sf;
+    const uint64_t iters = ceil_div(n, stride);
+    for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t k = it * stride + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const bool v = k < n;
         uint32_t su = 0;
-        if (a == 0) bad |= 1u;
-        if (o == 0) bad |= 2u;
-        if (!(x > 0.0) || !isfinite(x)) {
-            bad |= 4u;
-        } else {
-            double r = rint(__dmul_rn(x, 1e6));      // one correctly rounded product, half-even
-            if (r < 1.0 || r > 4294967295.0) bad |= 4u; else su = (uint32_t)r;
+        if (v) {
+            uint32_t a = __ldg(in + k), o = __ldg(out + k);
+            float sf = __ldg(slo + k);
+            double x = (double)sf;
+            if (a == 0) bad |= 1u;
+            if (o == 0) bad |= 2u;
+            if (!(x > 0.0) || !isfinite(x)) {
+                bad |= 4u;
+            } else {
+                double r = rint(__dmul_rn(x, 1e6));      // one correctly rounded product, half-even
+                if (r < 1.0 || r > 4294967295.0) bad |= 4u; else su = (uint32_t)r;
+            }
+            unsigned long long key = ((unsigned long long)su << 32) | o;
+            keys[k] = key;
+            vals[k] = (uint32_t)k;
+            mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
+            kor |= key; kand &= key;
         }
-        unsigned long long key = ((unsigned long long)su << 32) | o;
-        keys[k] = key;
-        vals[k] = (uint32_t)k;
-        mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
-        kor |= key; kand &= key;
+        // distinct-SLO collection (warp-deduplicated; stops once the CTA saw > kCtaMax values)
+        const uint32_t cv = __shfl_sync(0xffffffffu, *(volatile uint32_t *)&cover, 0);
+        if (!cv) {
+            const uint32_t act = __ballot_sync(0xffffffffu, v && su != 0);
+            if (v && su != 0) {
+                const uint32_t peers = __match_any_sync(act, su);
+                if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+                    uint32_t h = slo_hash(su, kCtaBits);
+                    for (uint32_t probe = 0; probe < kCtaSlots; ++probe) {
+                        const uint32_t old = atomicCAS(&cset[h], 0u, su);
+                        if (old == 0u) {
+                            if (atomicAdd(&ccount, 1u) + 1 > kCtaMax) cover = 1;
+                            break;
+                        }
+                        if (old == su) break;
+                        h = (h + 1) & (kCtaSlots - 1);
+                    }
+                }
+            }
+        }
     }
     // warp reductions, one atomic per warp
     for (int d = 16; d; d >>= 1) {
@@ -56,16 +93,91 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in,
         atomicOr(&meta->key_or, kor);
         atomicAnd(&meta->key_and, kand);
     }
+    __syncthreads();
+    // merge the CTA's distinct SLO values into the global set
+    if (cover) {
+        if (threadIdx.x == 0) atomicExch(&meta->slo_overflow, 1u);
+        return;
+    }
+    for (uint32_t i = threadIdx.x; i < kCtaSlots; i += blockDim.x) {
+        const uint32_t su = cset[i];
+        if (!su) continue;
+        uint32_t h = slo_hash(su, kSloSetBits);
+        for (uint32_t probe = 0; probe < kSloSetSize; ++probe) {
+            if (*(volatile uint32_t *)&meta->slo_distinct > kSloRankMax) { atomicExch(&meta->slo_overflow, 1u); break; }
+            const uint32_t old = atomicCAS(&slo_set[h], 0u, su);
+            if (old == 0u) { atomicAdd(&meta->slo_distinct, 1u); break; }
+            if (old == su) break;
+            h = (h + 1) & (kSloSetSize - 1);
+        }
+    }
 }
 
 cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
-                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, cudaStream_t st)
+                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, uint32_t *slo_set,
+                        cudaStream_t st)
 {
     if (n == 0) return cudaSuccess;
     uint64_t blocks = ceil_div(n, 256ull * 8);      // ~8 queries per thread
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     if (blocks < 1) blocks = 1;
-    k_load<<<(unsigned)blocks, 256, 0, st>>>(in, out, slo, n, keys, vals, meta);
+    k_load<<<(unsigned)blocks, 256, 0, st>>>(in, out, slo, n, keys, vals, meta, slo_set);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Rank table of the distinct SLO values (one CTA): table[r] = r-th smallest value,
+// rank_of_slot[h] = rank of the value stored in global-set slot h.
+__global__ void __launch_bounds__(1024) k_slo_table(const uint32_t *__restrict__ slo_set, uint32_t *__restrict__ table,
+                                                    uint32_t *__restrict__ rank_of_slot)
+{
+    __shared__ uint32_t vals[kSloRankMax];
+    __shared__ uint32_t cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (uint32_t h = threadIdx.x; h < kSloSetSize; h += blockDim.x) {
+        const uint32_t v = slo_set[h];
+        if (v) { const uint32_t k = atomicAdd(&cnt, 1u); if (k < kSloRankMax) vals[k] = v; }
+    }
+    __syncthreads();
+    const uint32_t K = min(cnt, kSloRankMax);
+    for (uint32_t h = threadIdx.x; h < kSloSetSize; h += blockDim.x) {
+        const uint32_t v = slo_set[h];
+        if (!v) continue;
+        uint32_t r = 0;
+        for (uint32_t f = 0; f < K; ++f) r += vals[f] < v;
+        rank_of_slot[h] = r;
+        table[r] = v;
+    }
+}
+
+// key32 = rank(slo_us) << ob | out
+__global__ void __launch_bounds__(256) k_repack(const unsigned long long *__restrict__ keys, uint64_t n,
+                                                const uint32_t *__restrict__ slo_set,
+                                                const uint32_t *__restrict__ rank_of_slot, int ob,
+                                                uint32_t *__restrict__ keys32)
+{
+    __shared__ uint32_t sset[kSloSetSize], srank[kSloSetSize];
+    for (uint32_t i = threadIdx.x; i < kSloSetSize; i += blockDim.x) { sset[i] = slo_set[i]; srank[i] = rank_of_slot[i]; }
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const unsigned long long key = keys[k];
+        const uint32_t su = (uint32_t)(key >> 32);
+        uint32_t h = slo_hash(su, kSloSetBits);
+        while (sset[h] != su) h = (h + 1) & (kSloSetSize - 1);
+        keys32[k] = (srank[h] << ob) | (uint32_t)key;
+    }
+}
+
+cudaError_t launch_slo_rank(const unsigned long long *keys, uint64_t n, const uint32_t *slo_set, uint32_t *table,
+                            uint32_t *rank_of_slot, int ob, uint32_t *keys32, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    k_slo_table<<<1, 1024, 0, st>>>(slo_set, table, rank_of_slot);
+    uint64_t blocks = ceil_div(n, 256ull * 8);
+    if (blocks > 148ull * 8) blocks = 148ull * 8;
+    k_repack<<<(unsigned)blocks, 256, 0, st>>>(keys, n, slo_set, rank_of_slot, ob, keys32);
     return cudaGetLastError();
 }
 
@@ -88,6 +200,27 @@ __global__ void __launch_bounds__(256) k_decode(const unsigned long long *__rest
     }
 }
 
+__global__ void __launch_bounds__(256) k_decode32(const uint32_t *__restrict__ keys, const uint32_t *__restrict__ vals,
+                                                  const uint32_t *__restrict__ in, uint64_t n,
+                                                  const uint32_t *__restrict__ table, int ob,
+                                                  uint32_t *__restrict__ rin, uint32_t *__restrict__ rout,
+                                                  uint32_t *__restrict__ rslo, uint32_t *__restrict__ order)
+{
+    __shared__ uint32_t st[kSloRankMax];
+    for (uint32_t i = threadIdx.x; i < kSloRankMax; i += blockDim.x) st[i] = table[i];
+    __syncthreads();
+    const uint32_t mask = ob >= 32 ? 0xffffffffu : ((1u << ob) - 1);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        const uint32_t key = keys[p];
+        const uint32_t idx = vals[p];
+        rslo[p] = st[ob >= 32 ? 0 : key >> ob];
+        rout[p] = key & mask;
+        rin[p] = __ldg(in + idx);
+        order[p] = idx;
+    }
+}
+
 cudaError_t launch_decode(const unsigned long long *keys, const uint32_t *vals, const uint32_t *in,
                           uint64_t n, uint32_t *rin, uint32_t *rout, uint32_t *rslo,
                           uint32_t *order, cudaStream_t st)
@@ -96,6 +229,17 @@ cudaError_t launch_decode(const unsigned long long *keys, const uint32_t *vals, 
     uint64_t blocks = ceil_div(n, 256ull * 4);
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     k_decode<<<(unsigned)blocks, 256, 0, st>>>(keys, vals, in, n, rin, rout, rslo, order);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const uint32_t *in, uint64_t n,
+                            const uint32_t *table, int ob, uint32_t *rin, uint32_t *rout, uint32_t *rslo,
+                            uint32_t *order, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = ceil_div(n, 256ull * 4);
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    k_decode32<<<(unsigned)blocks, 256, 0, st>>>(keys, vals, in, n, table, ob, rin, rout, rslo, order);
     return cudaGetLastError();
 }
 

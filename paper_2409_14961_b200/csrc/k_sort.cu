@@ -2,6 +2,11 @@
 // window (P:228 / P:256 "sort by SLO in ascending order", with the predicted length as
 // secondary key, R11).  8-bit digits; digits constant over all keys are skipped.
 //
+// Two key layouts (chosen on the host after load):
+//   u64  key = slo_us << 32 | out                           (any input)
+//   u32  key = rank(slo_us) << bits(max_out) | out           (few distinct SLO values: the rank
+//        of slo_us among the distinct values preserves the order exactly; 2 passes for c3/c4)
+//
 // Per pass (reduce-then-scan):
 //   k_sort_up    per 4096-key tile (tiles never cross a window): digit histogram, warp-
 //                aggregated with match.any (skewed class-valued SLO digits would otherwise
@@ -31,9 +36,9 @@ __device__ __forceinline__ void tile_range(uint64_t t, uint64_t n, uint64_t wind
     if (start > end) start = end;
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_sort_up(const unsigned long long *__restrict__ kin,
-                                                          uint32_t *__restrict__ hist, uint64_t n,
-                                                          uint64_t window, uint64_t tpw, int shift)
+template <class K>
+__global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ kin, uint32_t *__restrict__ hist,
+                                                          uint64_t n, uint64_t window, uint64_t tpw, int shift)
 {
     __shared__ uint32_t h[256];
     const int tid = threadIdx.x;
@@ -84,13 +89,11 @@ __global__ void __launch_bounds__(256) k_sort_scan(uint32_t *__restrict__ hist, 
     for (uint64_t k = 0; k < ntl; ++k) hist[(w * tpw + k) * 256 + d] += base;
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_sort_down(const unsigned long long *__restrict__ kin,
-                                                            const uint32_t *__restrict__ vin,
-                                                            unsigned long long *__restrict__ kout,
-                                                            uint32_t *__restrict__ vout,
-                                                            const uint32_t *__restrict__ hist,
-                                                            uint64_t n, uint64_t window, uint64_t tpw,
-                                                            int shift)
+template <class K>
+__global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
+                                                            K *__restrict__ kout, uint32_t *__restrict__ vout,
+                                                            const uint32_t *__restrict__ hist, uint64_t n,
+                                                            uint64_t window, uint64_t tpw, int shift)
 {
     constexpr int kWarps = kSortThreads / 32;
     constexpr int kPerWarpIters = kSortTile / kWarps / 32;     // 16
@@ -104,14 +107,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const unsigned long 
     tbase[tid] = hist[(uint64_t)blockIdx.x * 256 + tid];
     __syncthreads();
 
-    unsigned long long kr[kPerWarpIters];
+    K kr[kPerWarpIters];
     uint32_t vr[kPerWarpIters], rank[kPerWarpIters];
     const uint64_t base = start + (uint64_t)warp * (kPerWarpIters * 32);
 #pragma unroll
     for (int r = 0; r < kPerWarpIters; ++r) {
         uint64_t p = base + r * 32 + lane;
         bool valid = p < end;
-        kr[r] = valid ? kin[p] : 0ull;
+        kr[r] = valid ? kin[p] : (K)0;
         vr[r] = valid ? vin[p] : 0u;
     }
     const uint32_t lt = lanemask_lt();
@@ -153,25 +156,24 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const unsigned long 
     }
 }
 
-cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
-                               unsigned long long *keys_a, uint32_t *vals_a,
-                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
-                               uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
-                               int *passes, cudaStream_t st)
+template <class K>
+static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, K *keys_a, uint32_t *vals_a,
+                                   K *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n, uint64_t window,
+                                   uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st)
 {
     *passes = 0;
     if (n == 0) return cudaSuccess;
     const uint64_t tpw = ceil_div(window, kSortTile);
     const uint64_t tiles = tpw * nwin;
-    const unsigned long long *kin = *keys_io;
+    const K *kin = *keys_io;
     const uint32_t *vin = *vals_io;
-    for (int d = 0; d < 8; ++d) {
+    for (int d = 0; d < (int)sizeof(K); ++d) {
         if (!(digit_mask >> d & 1u)) continue;
-        unsigned long long *kout = (*passes & 1) ? keys_b : keys_a;
+        K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
-        k_sort_up<<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
+        k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
         k_sort_scan<<<(unsigned)nwin, 256, 0, st>>>(hist, n, window, tpw);
-        k_sort_down<<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw, 8 * d);
+        k_sort_down<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw, 8 * d);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         kin = kout;
@@ -181,6 +183,24 @@ cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_
     *keys_io = kin;
     *vals_io = vin;
     return cudaSuccess;
+}
+
+cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
+                               unsigned long long *keys_a, uint32_t *vals_a,
+                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
+                               uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
+                               int *passes, cudaStream_t st)
+{
+    return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window,
+                                               nwin, digit_mask, passes, st);
+}
+
+cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
+                                 uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
+                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st)
+{
+    return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window, nwin,
+                                     digit_mask, passes, st);
 }
 
 }  // namespace uellm

@@ -278,3 +278,25 @@ def test_sharded_ranks_equal_single_run():
     comb = D.combine_totals(torch.stack(rows))
     for f in D.TOTAL_FIELDS:
         assert comb[f] == full["totals"][f], f
+
+
+def test_sort_paths_compressed_and_generic():
+    """Class-valued SLOs take the rank-compressed 32-bit sort key; the paper's own protocol
+    (SLO uniform in [1, 350] s) overflows the distinct-value set and takes the 64-bit key.
+    Both must give the oracle's order; 1024 distinct values is the largest compressed case."""
+    inp, out, slo, cfg = W.c3(21, n=120_000)
+    r = assert_parity(inp, out, slo, cfg.replace(window=40_000))
+    assert r["diag"]["sort_key_bits"] < 32
+    slo_u = W.gen_uniform_slo(120_000, 21)
+    r = assert_parity(inp, out, slo_u, cfg.replace(window=40_000))
+    assert r["diag"]["sort_key_bits"] == 64
+    for k, expect_compressed in ((1024, True), (1025, False)):
+        rng = np.random.default_rng(k)
+        vals = np.sort(rng.choice(np.arange(1, 200_000), size=k, replace=False)).astype(np.float32) * np.float32(1e-3)
+        s2 = vals[rng.integers(0, k, size=60_000)]
+        if k == 1024:
+            s2[:k] = vals
+        else:
+            s2[:k] = vals
+        r = assert_parity(inp[:60_000], out[:60_000], s2, cfg.replace(window=0))
+        assert (r["diag"]["sort_key_bits"] < 64) == expect_compressed
