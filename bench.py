@@ -30,12 +30,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "queries scheduled/sec (device-timed, max over ranks)"
 UNIT = "queries/s"
-# per-candidate-evaluation lane-ops of the SEG-DP inner loop: the SASS of
-# one candidate round (loads, max updates, est, feasibility, D1 test, compaction) issues this
-# many instructions per live candidate; used to express the DP's work in lane-ops.
-DP_OPS_PER_EVAL = 64
+# SEG-DP issue roofline: warp instructions per candidate evaluation as
+# measured by ncu (fallback if profiles/ncu_summary.json is absent)
+DP_WARP_INST_PER_EVAL = 2.064
 SMS = 148
-LANES_PER_SM = 128
+ISSUE_PER_SM = 4
 
 
 def peaks():
@@ -72,7 +71,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
@@ -100,13 +99,14 @@ def compulsory_bytes(n: int, m: int) -> int:
     return 12 * n + 4 * n + 4 * (m + 1) + 80 * m + 112
 
 
+def ncu_summary() -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
 def ncu_traffic(kernel: str):
     """dram bytes per launch of `kernel` from the committed ncu summary, if present."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
-        return None
-    d = json.load(open(p))
-    k = d.get("kernels", {}).get(kernel)
+    k = ncu_summary().get("kernels", {}).get(kernel)
     return k.get("dram_bytes_per_launch") if k else None
 
 
@@ -156,7 +156,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="uellm", choices=["uellm", "reference"])
     ap.add_argument("--config", default="c4")
@@ -253,16 +253,20 @@ def main():
     # dominant kernel roofline
     dom = max(st_ms, key=st_ms.get)
     if dom in ("dp_local", "dp_fix", "dp_cascade"):
+        # SEG-DP is integer-issue-bound: units = candidate evaluations counted live by the kernel,
+        # per-unit cost = warp instructions per evaluation from the committed ncu capture
+        # (profiles/ncu_summary.json); peak = 148 SMs x 4 schedulers x 1 warp-instr/clk x max clock
         evals = diag["dp_candidate_evals"]
-        dp_ms = st_ms["dp_local"] + st_ms["dp_fix"] + st_ms["dp_cascade"]
-        achieved = evals * DP_OPS_PER_EVAL / (dp_ms / 1e3) / 1e12
-        peak = SMS * LANES_PER_SM * sm_max * 1e6 / 1e12
-        roof = {"bound": "alu", "kernel": "k_dp_local+k_dp_fix+k_dp_cascade", "achieved": achieved,
-                "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak,
+        per_eval = ncu_summary().get("dp_warp_inst_per_eval", DP_WARP_INST_PER_EVAL)
+        achieved = evals * per_eval / (st_ms["dp_local"] / 1e3) / 1e12
+        peak = SMS * ISSUE_PER_SM * sm_max * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "k_dp_local", "achieved": achieved,
+                "peak": peak, "unit": "T warp-instr/s", "frac": achieved / peak,
                 "traffic": ncu_traffic("k_dp_local"),
-                "work": f"{evals} candidate evaluations x {DP_OPS_PER_EVAL} lane-ops "
-                        f"({evals / n:.1f} per query)",
-                "peak_source": f"{SMS} SMs x {LANES_PER_SM} INT32/FP32 lanes x {sm_max:.0f} MHz (guide unit counts)"}
+                "work": f"{evals} candidate evaluations ({evals / n:.1f} per query) x {per_eval:.3f} "
+                        f"warp instructions each (ncu inst_executed / evaluations)",
+                "peak_source": f"{SMS} SMs x {ISSUE_PER_SM} issue slots/clk x {sm_max:.0f} MHz "
+                               f"(guide unit counts; MEASURED_PEAKS sm_max_mhz)"}
     else:
         # HBM-bound stages: algorithmic bytes per launch of the stage
         alg = {"sort": 24 * n * diag["sort_passes"], "decode": 24 * n, "stats": 12 * n + 80 * m,
