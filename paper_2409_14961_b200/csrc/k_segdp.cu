@@ -258,6 +258,7 @@ __device__ DpResult dp_warp(const DPParams &P, const WarpSlots &S, uint32_t s, u
 struct NarrowSlots {
     long long *cC;
     unsigned long long *cP;     // i | mo << 32 | mi << 48
+    uint32_t *rmq;              // per-block range-max table, 5 levels x 33 words
 };
 
 __device__ __forceinline__ unsigned long long pack_slot(uint32_t i, uint32_t mo, uint32_t mi)
@@ -402,60 +403,73 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             }
         };
         if (ext_slow) ext_pass(std::true_type{}); else ext_pass(std::false_type{});
-        // ---- 2. intra-block candidates, boundary by boundary
-        long long iC = 0;
-        uint32_t imo = 0, imi = 0;
-        long long o_C = 0;
-        uint32_t o_A = 0;
-        uint32_t kdone = B;
+        // ---- 2. intra-block candidates.  Lane = boundary again: the candidate born at boundary
+        //      j0+q+1 (final once lane q has seen every older candidate) is broadcast and every
+        //      later lane k evaluates it with the maxima of elements q+1..k, read in O(1) from a
+        //      per-block sparse table of packed (out << 16 | in) maxima.  Candidates arrive in
+        //      ascending i, so the strict '<' keeps the smallest minimising i.
+        uint32_t *T = S.rmq;
+        {
+            uint32_t cur = vl ? ((out_l << 16) | in_l) : 0u;
+            T[lane] = cur;
+#pragma unroll
+            for (int l = 1; l < 5; ++l) {        // T[l][x] = max over elements x .. x + 2^l - 1
+                cur = __vmaxu2(cur, __shfl_down_sync(0xffffffffu, cur, 1 << (l - 1)));
+                T[l * 33 + lane] = cur;
+            }
+        }
+        __syncwarp();
+        auto rmq = [&](uint32_t a, uint32_t bb) {  // max over elements a .. bb (a <= bb < 32)
+            const uint32_t lv = 31 - __clz(bb - a + 1);
+            return __vmaxu2(T[lv * 33 + a], T[lv * 33 + bb - (1u << lv) + 1]);
+        };
         auto intra_pass = [&](auto slow_tag) {
             constexpr bool SLOW = decltype(slow_tag)::value;
-            const uint32_t ci = j0 + 1 + lane;
-            for (uint32_t k = 0; k < B; ++k) {
-                const uint32_t ok = __shfl_sync(0xffffffffu, out_l, k), ik = __shfl_sync(0xffffffffu, in_l, k);
-                const uint32_t sk = __shfl_sync(0xffffffffu, slo_l, k);
-                const bool act = lane < k;
-                if (act) { imo = max(imo, ok); imi = max(imi, ik); }
-                const uint32_t j = j0 + k + 1;
-                const uint32_t b = k - lane;
-                const uint32_t est = t_b + t_it * imo + b * (t_tok * imo + t_pre * imi);
-                bool dead = !act | (b > W) | ((b > 1) & (b * (imo + imi) > cap32));
-                unsigned long long val = (unsigned long long)iC + est;
-                if (SLOW || split) {
-                    const uint32_t rsk = __shfl_sync(0xffffffffu, rs_l, k);
-                    dead |= split & (ci < rsk);
-                    if (LAM) {
-                        const uint32_t v = (ci >= rsk) ? ((sk < est) ? b : 0u)
-                                                       : (dead ? 0u : viol_count_slow(rslo, ci, j, est, sk));
-                        val += lam * v;
-                    }
-                } else if (LAM) {
-                    val += lam * ((sk < est) ? b : 0u);
+            for (uint32_t q = 0; q + 1 < B; ++q) {
+                const long long Cq = (long long)__shfl_sync(0xffffffffu, lb, q);
+                const bool act = vl && lane > q;
+                const uint32_t b = act ? lane - q : 1u;          // boundary jl minus candidate j0+1+q
+                const uint32_t m = rmq(act ? q + 1 : lane, lane);
+                const uint32_t mo = m >> 16, mi = m & 0xffffu;
+                const uint32_t ci = j0 + 1 + q;
+                const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
+                const bool dead = !act | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < rs_l));
+                unsigned long long tot = (unsigned long long)Cq + est;
+                if (LAM) {
+                    uint32_t v;
+                    if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
+                                               : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
+                    else v = (slo_l < est) ? b : 0u;
+                    tot += lam * v;
                 }
-                if (dead) val = ~0ull;
-                uint32_t idx = ci;
-                if (lane == k) { val = lb; idx = lbi; }
-                const uint32_t hi = (uint32_t)(val >> 32);
-                const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
-                const uint32_t lo = (hi == mhi) ? (uint32_t)val : 0xffffffffu;
-                const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
-                const uint32_t barg = __reduce_min_sync(0xffffffffu, (hi == mhi && (uint32_t)val == mlo) ? idx : 0xffffffffu);
-                const long long best = (long long)(((unsigned long long)mhi << 32) | mlo);
-                if (lane == k) { iC = best; o_C = best; o_A = j - barg; }
-                if (FIX) {
-                    const long long cl = __shfl_sync(0xffffffffu, cl_l, k);
-                    const long long dj = best - cl;
-                    if (dj == d_run) ++run; else { d_run = dj; run = 1; }
-                    if (run >= W && j >= stop_min) {
-                        R.conv = 1; R.conv_pos = j; R.fix_end = j; R.delta = d_run;
-                        stop = true;
-                        kdone = k + 1;
-                        break;
-                    }
-                }
+                if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
         };
         if (intra_slow) intra_pass(std::true_type{}); else intra_pass(std::false_type{});
+        const long long o_C = (long long)lb;
+        const long long iC = o_C;
+        const uint32_t o_A = jl - lbi;
+        uint32_t kdone = B;
+        if (FIX) {
+            // convergence: first boundary ending a run of W equal differences C_fix - C_local
+            const long long dk = o_C - cl_l;
+            long long dprev = __shfl_up_sync(0xffffffffu, dk, 1);
+            if (lane == 0) dprev = d_run;
+            const uint32_t brk = __ballot_sync(0xffffffffu, vl && dk != dprev);
+            const uint32_t upto = brk & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1));
+            const uint32_t runk = upto ? lane - (31 - __clz(upto)) + 1 : run + lane + 1;
+            const uint32_t cv = __ballot_sync(0xffffffffu, vl && runk >= W && jl >= stop_min);
+            if (cv) {
+                const uint32_t c = __ffs(cv) - 1;
+                R.conv = 1; R.conv_pos = j0 + c + 1; R.fix_end = R.conv_pos;
+                R.delta = __shfl_sync(0xffffffffu, dk, c);
+                stop = true;
+                kdone = c + 1;
+            } else {
+                d_run = __shfl_sync(0xffffffffu, dk, B - 1);
+                run = __shfl_sync(0xffffffffu, runk, B - 1);
+            }
+        }
         // outputs of this block
         if (lane < kdone) {
             (FIX ? P.CFx : P.Cx)[x] = o_C;
@@ -463,6 +477,9 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         }
         done = j0 + kdone;
         if (stop) break;
+        // maxima of the block's own candidates over [i, block end): elements q+1 .. B-1
+        uint32_t imo = 0, imi = 0;
+        if (lane + 1 < B) { const uint32_t m = rmq(lane + 1, B - 1); imo = m >> 16; imi = m & 0xffffu; }
         // ---- 3. extend the list by the block's candidates and prune at the block-end state
         const uint32_t jend = j0 + B;
         const uint32_t bmo = __shfl_sync(0xffffffffu, pmo, B - 1), bmi = __shfl_sync(0xffffffffu, pmi, B - 1);
@@ -521,17 +538,23 @@ __device__ __forceinline__ void tile_bounds(const DPParams &P, uint64_t t, uint3
     e = (uint32_t)min(ss + P.tile_len, w1);
 }
 
-__device__ __forceinline__ uint32_t slot_bytes(const DPParams &P) { return P.narrow ? 16u : 20u; }
+// shared memory per warp: narrow = 16 B slots + the 5 x 33-word range-max table; wide = 20 B slots
+constexpr uint32_t kRmqBytes = 5 * 33 * 4 + 12;    // 672, keeps 16-byte alignment
+static __host__ __device__ __forceinline__ uint32_t warp_smem_bytes(const DPParams &P)
+{
+    return P.narrow ? P.cap_slots * 16 + kRmqBytes : P.cap_slots * 20;
+}
 
 template <bool FIX>
 __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, uint32_t e,
                            const long long *src, uint32_t stop_min)
 {
     if (P.narrow) {
-        char *p = smem + (size_t)warp * P.cap_slots * 16;
+        char *p = smem + (size_t)warp * warp_smem_bytes(P);
         NarrowSlots S;
         S.cC = (long long *)p;
         S.cP = (unsigned long long *)(p + (size_t)P.cap_slots * 8);
+        S.rmq = (uint32_t *)(p + (size_t)P.cap_slots * 16);
         if (P.lambda) return dp_warp_blocked<FIX, true>(P, S, s, e, src, stop_min);
         return dp_warp_blocked<FIX, false>(P, S, s, e, src, stop_min);
     }
@@ -620,9 +643,8 @@ __global__ void k_dp_cascade(DPParams P)
     }
 }
 
-static uint32_t warps_per_cta(uint32_t cap_slots, uint32_t slot)
+static uint32_t warps_per_cta(uint32_t per)
 {
-    uint32_t per = cap_slots * slot;
     uint32_t wpc = kDpWarpsPerCta;
     while (wpc > 1 && wpc * per > 200 * 1024) --wpc;
     return wpc;
@@ -632,10 +654,10 @@ cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void 
 {
     *launches = 0;
     if (P.n == 0 || ntiles == 0) return cudaSuccess;
-    const uint32_t slot = P.narrow ? 16u : 20u;
-    const uint32_t wpc = warps_per_cta(P.cap_slots, slot);
-    const size_t smem = (size_t)wpc * P.cap_slots * slot;
-    const size_t smem1 = (size_t)P.cap_slots * slot;
+    const uint32_t per = warp_smem_bytes(P);
+    const uint32_t wpc = warps_per_cta(per);
+    const size_t smem = (size_t)wpc * per;
+    const size_t smem1 = (size_t)per;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_dp_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if ((e = cudaFuncSetAttribute(k_dp_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
