@@ -289,7 +289,8 @@ struct SlotWriter {            // writes a candidate slot with its derived cost 
 //     smaller i, which is always the external one);
 //  3. once per block the list is extended by the 32 new candidates and pruned at the block-end
 //     state (dead prefix + D1), which is valid for every later boundary.
-template <bool FIX, bool LAM>
+// LAMK: 0 = no SLO penalty, 1 = lambda < 2^32 (32x32 -> 64-bit product), 2 = 64-bit lambda.
+template <bool FIX, int LAMK, bool SPLIT>
 __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uint32_t s, uint32_t e,
                                     const long long *__restrict__ src, uint32_t stop_min)
 {
@@ -299,8 +300,12 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     const uint32_t cap32 = (uint32_t)min(P.cap_tok, 0xffffffffull);
     const uint32_t t_b = (uint32_t)P.t_batch, t_it = (uint32_t)P.t_iter, t_tok = (uint32_t)P.t_tok,
                    t_pre = (uint32_t)P.t_pre;
-    const bool split = P.split != 0;
+    constexpr bool LAM = LAMK != 0;
+    constexpr bool split = SPLIT;
     const unsigned long long lam = P.lambda;
+    auto penalty = [&](uint32_t v) -> unsigned long long {
+        return LAMK == 1 ? (unsigned long long)(uint32_t)lam * v : lam * v;
+    };
     const SlotWriter SW{t_b, t_it, t_tok, t_pre};
     const uint32_t *__restrict__ rin = P.rin;
     const uint32_t *__restrict__ rout = P.rout;
@@ -397,7 +402,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                     if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
                                                : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
                     else v = (slo_l < est) ? b : 0u;
-                    tot += lam * v;
+                    tot += penalty(v);
                 }
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
@@ -440,7 +445,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                     if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
                                                : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
                     else v = (slo_l < est) ? b : 0u;
-                    tot += lam * v;
+                    tot += penalty(v);
                 }
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
@@ -555,8 +560,15 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
         S.cC = (long long *)p;
         S.cP = (unsigned long long *)(p + (size_t)P.cap_slots * 8);
         S.rmq = (uint32_t *)(p + (size_t)P.cap_slots * 16);
-        if (P.lambda) return dp_warp_blocked<FIX, true>(P, S, s, e, src, stop_min);
-        return dp_warp_blocked<FIX, false>(P, S, s, e, src, stop_min);
+        const int lk = P.lambda == 0 ? 0 : (P.lambda < (1ull << 32) ? 1 : 2);
+        if (P.split) {
+            if (lk == 0) return dp_warp_blocked<FIX, 0, true>(P, S, s, e, src, stop_min);
+            if (lk == 1) return dp_warp_blocked<FIX, 1, true>(P, S, s, e, src, stop_min);
+            return dp_warp_blocked<FIX, 2, true>(P, S, s, e, src, stop_min);
+        }
+        if (lk == 0) return dp_warp_blocked<FIX, 0, false>(P, S, s, e, src, stop_min);
+        if (lk == 1) return dp_warp_blocked<FIX, 1, false>(P, S, s, e, src, stop_min);
+        return dp_warp_blocked<FIX, 2, false>(P, S, s, e, src, stop_min);
     }
     return dp_warp<FIX>(P, slots_for(smem, P.cap_slots, warp), s, e, src, stop_min);
 }
