@@ -55,6 +55,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     const uint64_t nblk = ceil_div(L.nwords, kScanBlock) + ceil_div(N, kScanBlock) + 2;
     L.blocksum = take(4 * nblk);
     L.blockagg = take(8 * nblk);
+    L.st_so = take(8 * N); L.st_pin = take(8 * N); L.st_pout = take(8 * N);
     L.hist = take(4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));
     L.meta = take(sizeof(LoadMeta)); L.diag = take(sizeof(Diag)); L.acc = take(sizeof(StatAcc));
     L.nb = take(8); L.totals = take(sizeof(uellm_totals));
@@ -407,6 +408,9 @@ uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg, 
     S.offsets = d_offs; S.num_batches = d_nb; S.n_cap = n; S.window = (uint32_t)L.window; S.nwin = (uint32_t)L.nwin;
     S.est = at<unsigned long long>(w, L.keys1); S.compl_ = at<unsigned long long>(w, L.keys2);
     S.blocksum_u32 = at<uint32_t>(w, L.blocksum); S.blockagg = at<unsigned long long>(w, L.blockagg);
+    S.so = at<unsigned long long>(w, L.st_so); S.pin = at<unsigned long long>(w, L.st_pin);
+    S.pout = at<unsigned long long>(w, L.st_pout);
+    S.sorted = cfg->mode != UELLM_MODE_FIFO;
     S.per_batch = per_batch; S.acc = at<StatAcc>(w, L.acc); S.totals = d_tot; S.n = n;
     S.kv_unit = (unsigned long long)cfg->kv_bytes_per_elem * cfg->n_layers * cfg->hidden;
     S.kv_cap = cfg->kv_cap_bytes;

@@ -73,6 +73,7 @@ struct WsLayout {
     uint64_t argx;                                // u16 per position
     uint64_t tiles;                               // TileRec[ntiles]
     uint64_t bitmap, wscan, blocksum, blockagg;   // boundary bitmap + scan scratch
+    uint64_t st_so, st_pin, st_pout;              // per-batch stats scratch (u64 each)
     uint64_t hist;                                // u32[sort_tiles * 256]
     uint64_t meta, diag, acc, nb, totals, wincost;
     uint64_t total;
@@ -170,6 +171,8 @@ struct StatsParams {
     uint64_t n_cap;                             // capacity bound of batches (n)
     uint32_t window, nwin;
     unsigned long long *est, *compl_;
+    unsigned long long *so, *pin, *pout;        // per batch: s | O << 32, input / output padding
+    uint32_t sorted;                            // members of a batch ascend in slo_us (all modes but FIFO)
     uint32_t *blocksum_u32;                     // scratch
     unsigned long long *blockagg;               // scratch
     uellm_batch_stat *per_batch;

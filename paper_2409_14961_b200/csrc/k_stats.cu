@@ -61,8 +61,30 @@ __global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
     const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < m; t += nw) {
         BatchCore c = batch_core(S, t);
-        if ((threadIdx.x & 31) == 0) S.est[t] = c.est;
+        if ((threadIdx.x & 31) == 0) {
+            S.est[t] = c.est;
+            S.so[t] = (unsigned long long)c.s | ((unsigned long long)c.O << 32);
+            S.pin[t] = (unsigned long long)c.b * c.s - c.sin;
+            S.pout[t] = (unsigned long long)c.b * c.O - c.sout;
+        }
     }
+}
+
+// #{k in [a, z) : rslo[k] < x} -- members ascend in slo_us when S.sorted (a contiguous range of
+// the (slo, out, index)-sorted window), else a plain count (FIFO batches keep arrival order).
+__device__ __forceinline__ uint32_t count_below(const StatsParams &S, uint32_t a, uint32_t z, unsigned long long x)
+{
+    if (S.sorted) {
+        uint32_t lo = a, hi = z;
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if ((unsigned long long)__ldg(S.rslo + mid) < x) lo = mid + 1; else hi = mid;
+        }
+        return lo - a;
+    }
+    uint32_t c = 0;
+    for (uint32_t k = a; k < z; ++k) c += (unsigned long long)__ldg(S.rslo + k) < x;
+    return c;
 }
 
 // ---- segmented inclusive scan of est by window (head flag = first batch of a window) ----
@@ -173,43 +195,49 @@ __global__ void __launch_bounds__(kScanBlock) k_seg_scan_apply(StatsParams S)
 // ---- all fields + totals ----
 __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
 {
+    // thread per batch: reads the pass-1 record, two binary searches for the violation counts
     __shared__ unsigned long long red[8][12];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t m = *S.num_batches;
-    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
     unsigned long long a_gen = 0, a_pin = 0, a_pout = 0, a_kv = 0, a_obj = 0, a_v1 = 0, a_v2 = 0, a_oc = 0,
                        a_mk = 0, a_llo = 0, a_lhi = 0, a_nb = 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < m; t += nw) {
-        const BatchCore c = batch_core(S, t);
-        const unsigned long long compl_us = S.compl_[t];
-        uint32_t v1 = 0, v2 = 0;
-        for (uint32_t k = c.a + lane; k < c.z; k += 32) {
-            const unsigned long long su = __ldg(S.rslo + k);
-            v1 += su < c.est;
-            v2 += su < compl_us;
-        }
-        v1 = warp_sum(v1);
-        v2 = warp_sum(v2);
-        const unsigned long long kv = S.kv_unit * (unsigned long long)c.b * ((unsigned long long)c.s + c.O);
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += nt) {
+        const uint32_t a = S.offsets[t], z = S.offsets[t + 1], b = z - a;
+        const unsigned long long so = S.so[t], est = S.est[t], compl_us = S.compl_[t];
+        const uint32_t s = (uint32_t)so, O = (uint32_t)(so >> 32);
+        const unsigned long long pin = S.pin[t], pout = S.pout[t];
+        const uint32_t v1 = count_below(S, a, z, est);
+        const uint32_t v2 = count_below(S, a, z, compl_us);
+        const unsigned long long kv = S.kv_unit * (unsigned long long)b * ((unsigned long long)s + O);
         const uint32_t oc = (S.kv_cap != 0 && kv > S.kv_cap) ? 1u : 0u;
-        const unsigned long long gen = (unsigned long long)c.b * c.O;
-        const unsigned long long pin = (unsigned long long)c.b * c.s - c.sin;
-        const unsigned long long pout = gen - c.sout;
-        if (lane == 0) {
-            if (S.per_batch) {
-                uellm_batch_stat r;
-                r.start = c.a; r.size = c.b; r.max_in = c.s; r.max_out = c.O;
-                r.gen_tokens = gen; r.pad_in = pin; r.pad_out = pout; r.kv_bytes = kv;
-                r.est_us = c.est; r.completion_us = compl_us;
-                r.viol_alone = v1; r.viol_seq = v2; r.over_cap = oc; r.window = c.a / S.window;
-                S.per_batch[t] = r;
-            }
-            a_gen += gen; a_pin += pin; a_pout += pout; a_kv = max(a_kv, kv);
-            a_obj += c.est + S.lambda * v1; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += c.est; a_nb += 1;
-            const unsigned long long lo = (unsigned long long)c.b * compl_us;
-            const unsigned long long hi = __umul64hi((unsigned long long)c.b, compl_us);
-            a_llo += lo; a_lhi += hi + (a_llo < lo ? 1ull : 0ull);
+        const unsigned long long gen = (unsigned long long)b * O;
+        if (S.per_batch) {
+            uellm_batch_stat r;
+            r.start = a; r.size = b; r.max_in = s; r.max_out = O;
+            r.gen_tokens = gen; r.pad_in = pin; r.pad_out = pout; r.kv_bytes = kv;
+            r.est_us = est; r.completion_us = compl_us;
+            r.viol_alone = v1; r.viol_seq = v2; r.over_cap = oc; r.window = a / S.window;
+            S.per_batch[t] = r;
         }
+        a_gen += gen; a_pin += pin; a_pout += pout; a_kv = max(a_kv, kv);
+        a_obj += est + S.lambda * v1; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += est; a_nb += 1;
+        const unsigned long long lo = (unsigned long long)b * compl_us;
+        const unsigned long long hi = __umul64hi((unsigned long long)b, compl_us);
+        a_llo += lo; a_lhi += hi + (a_llo < lo ? 1ull : 0ull);
+    }
+    // warp reduction (128-bit carry for the latency sum)
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        a_gen += __shfl_xor_sync(0xffffffffu, a_gen, d); a_pin += __shfl_xor_sync(0xffffffffu, a_pin, d);
+        a_pout += __shfl_xor_sync(0xffffffffu, a_pout, d); a_kv = max(a_kv, __shfl_xor_sync(0xffffffffu, a_kv, d));
+        a_obj += __shfl_xor_sync(0xffffffffu, a_obj, d); a_v1 += __shfl_xor_sync(0xffffffffu, a_v1, d);
+        a_v2 += __shfl_xor_sync(0xffffffffu, a_v2, d); a_oc += __shfl_xor_sync(0xffffffffu, a_oc, d);
+        a_mk += __shfl_xor_sync(0xffffffffu, a_mk, d); a_nb += __shfl_xor_sync(0xffffffffu, a_nb, d);
+        const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, a_llo, d), hi2 = __shfl_xor_sync(0xffffffffu, a_lhi, d);
+        const unsigned long long lo = a_llo + lo2;
+        a_lhi += hi2 + (lo < a_llo ? 1ull : 0ull);
+        a_llo = lo;
     }
     if (lane == 0) {
         unsigned long long *r = red[warp];

@@ -47,6 +47,29 @@ __global__ void k_trace_a(const uint16_t *__restrict__ argx, TileRec *tiles, uin
     tiles[t].exitA = i;
 }
 
+// Walk A with the tile's args staged in shared memory (one CTA per tile): the pointer chase
+// then costs a shared-memory latency per hop instead of a DRAM one.
+__global__ void __launch_bounds__(256) k_trace_a_smem(const uint16_t *__restrict__ argx, TileRec *tiles, uint32_t *bm)
+{
+    extern __shared__ uint16_t sa[];
+    const uint64_t t = blockIdx.x;
+    const TileRec r = tiles[t];
+    if (!r.valid) return;
+    const uint32_t len = r.e - r.s;              // sa[k] = delta of boundary s+1+k
+    for (uint32_t k = threadIdx.x; k < len; k += blockDim.x) sa[k] = argx[r.s + k];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    uint32_t j = r.e, i;
+    bm_set(bm, j);
+    for (;;) {
+        i = j - (uint32_t)sa[j - 1 - r.s];
+        if (i <= r.s) break;
+        bm_set(bm, i);
+        j = i;
+    }
+    tiles[t].exitA = i;
+}
+
 __global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t ntiles, uint64_t tpw,
                           uint32_t *bm, Diag *diag)
 {
@@ -112,7 +135,14 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 {
     if (P.n == 0) return cudaSuccess;
     const unsigned tb = 128;
-    k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
+    const size_t stage = (size_t)P.tile_len * sizeof(uint16_t);
+    if (stage <= 160 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_trace_a_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+        if (e != cudaSuccess) return e;
+        k_trace_a_smem<<<(unsigned)ntiles, 256, stage, st>>>(P.argx, P.tiles, bitmap);
+    } else {
+        k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
+    }
     k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag);
     k_trace_c<<<(unsigned)ceil_div(P.nwin, 64), 64, 0, st>>>(P.argx, P.tiles, P.tpw, P.nwin, P.window, bitmap,
                                                            P.diag);
