@@ -10,8 +10,8 @@
 namespace uellm {
 
 constexpr uint32_t kMaxBatchLimit = 4096;      // W limit of this build (UELLM_ERR_UNSUPPORTED)
-constexpr uint32_t kSortTile = 4096;           // keys per radix-sort CTA (256 threads x 16)
-constexpr uint32_t kSortThreads = 256;
+constexpr uint32_t kSortTile = 4096;           // keys per radix-sort CTA (512 threads x 8)
+constexpr uint32_t kSortThreads = 512;
 constexpr uint32_t kSortItems = kSortTile / kSortThreads;
 constexpr uint32_t kDpWarpsPerCta = 8;
 constexpr uint32_t kScanBlock = 1024;          // elements per CTA in the scan kernels

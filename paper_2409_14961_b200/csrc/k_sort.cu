@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ 
 {
     __shared__ uint32_t h[256];
     const int tid = threadIdx.x;
-    h[tid] = 0;
+    if (tid < 256) h[tid] = 0;
     __syncthreads();
     uint64_t start, end;
     tile_range(blockIdx.x, n, window, tpw, start, end);
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ 
         }
     }
     __syncthreads();
-    hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
+    if (tid < 256) hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
 }
 
 __global__ void __launch_bounds__(256) k_sort_scan(uint32_t *__restrict__ hist, uint64_t n,
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
     if (start >= end) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < kWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
-    tbase[tid] = hist[(uint64_t)blockIdx.x * 256 + tid];
+    if (tid < 256) tbase[tid] = hist[(uint64_t)blockIdx.x * 256 + tid];
     __syncthreads();
 
     K kr[kPerWarpIters];
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
         __syncwarp();
     }
     __syncthreads();
-    {   // exclusive scan over warps, per digit
+    if (tid < 256) {   // exclusive scan over warps, per digit
         uint32_t run = 0;
 #pragma unroll
         for (int wv = 0; wv < kWarps; ++wv) {
