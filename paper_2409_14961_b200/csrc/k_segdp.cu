@@ -296,15 +296,22 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
 {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t lt = lane_lt();
-    const uint32_t W = P.W;
-    const uint32_t cap32 = (uint32_t)min(P.cap_tok, 0xffffffffull);
-    const uint32_t t_b = (uint32_t)P.t_batch, t_it = (uint32_t)P.t_iter, t_tok = (uint32_t)P.t_tok,
-                   t_pre = (uint32_t)P.t_pre;
+    uint32_t W = P.W;
+    uint32_t cap32 = (uint32_t)min(P.cap_tok, 0xffffffffull);
+    uint32_t t_b = (uint32_t)P.t_batch, t_it = (uint32_t)P.t_iter, t_tok = (uint32_t)P.t_tok,
+             t_pre = (uint32_t)P.t_pre;
+    uint32_t lam32 = (uint32_t)P.lambda;
+    // keep the cost constants in registers (the compiler would otherwise re-load them from the
+    // constant bank inside the candidate loops, one issue slot each)
+    asm volatile("" : "+r"(W), "+r"(cap32), "+r"(t_b), "+r"(t_it), "+r"(t_tok), "+r"(t_pre), "+r"(lam32));
+    // a single query always satisfies the cap test when the cap exceeds any one query's tokens,
+    // so the b > 1 guard can be dropped (2 * 0xffff: narrow-path lengths are < 2^16)
+    const bool single_ok = cap32 >= 2u * 0xffffu;
     constexpr bool LAM = LAMK != 0;
     constexpr bool split = SPLIT;
     const unsigned long long lam = P.lambda;
     auto penalty = [&](uint32_t v) -> unsigned long long {
-        return LAMK == 1 ? (unsigned long long)(uint32_t)lam * v : lam * v;
+        return LAMK == 1 ? (unsigned long long)lam32 * v : lam * v;
     };
     const SlotWriter SW{t_b, t_it, t_tok, t_pre};
     const uint32_t *__restrict__ rin = P.rin;
@@ -384,8 +391,9 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         uint32_t lbi = 0xffffffffu;
         // candidates oldest -> newest; strict '<' keeps the smallest minimising i (R9)
         evals += L * B;
-        auto ext_pass = [&](auto slow_tag) {
+        auto ext_pass = [&](auto slow_tag, auto single_tag) {
             constexpr bool SLOW = decltype(slow_tag)::value;
+            constexpr bool SINGLE_OK = decltype(single_tag)::value;
 #pragma unroll 2
             for (uint32_t c = 0; c < L; ++c) {
                 const unsigned long long cp = S.cP[c];
@@ -395,7 +403,8 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, pmo);
                 const uint32_t mi = max((uint32_t)(cp >> 48), pmi);
                 const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
-                const bool dead = !vl | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < rs_l));
+                const bool dead = !vl | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
+                                  (split & (ci < rs_l));
                 unsigned long long tot = (unsigned long long)cC + est;
                 if (LAM) {
                     uint32_t v;
@@ -407,7 +416,11 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
         };
-        if (ext_slow) ext_pass(std::true_type{}); else ext_pass(std::false_type{});
+        if (ext_slow) {
+            if (single_ok) ext_pass(std::true_type{}, std::true_type{}); else ext_pass(std::true_type{}, std::false_type{});
+        } else {
+            if (single_ok) ext_pass(std::false_type{}, std::true_type{}); else ext_pass(std::false_type{}, std::false_type{});
+        }
         // ---- 2. intra-block candidates.  Lane = boundary again: the candidate born at boundary
         //      j0+q+1 (final once lane q has seen every older candidate) is broadcast and every
         //      later lane k evaluates it with the maxima of elements q+1..k, read in O(1) from a
@@ -428,8 +441,9 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             const uint32_t lv = 31 - __clz(bb - a + 1);
             return __vmaxu2(T[lv * 33 + a], T[lv * 33 + bb - (1u << lv) + 1]);
         };
-        auto intra_pass = [&](auto slow_tag) {
+        auto intra_pass = [&](auto slow_tag, auto single_tag) {
             constexpr bool SLOW = decltype(slow_tag)::value;
+            constexpr bool SINGLE_OK = decltype(single_tag)::value;
             for (uint32_t q = 0; q + 1 < B; ++q) {
                 const long long Cq = (long long)__shfl_sync(0xffffffffu, lb, q);
                 const bool act = vl && lane > q;
@@ -438,7 +452,8 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 const uint32_t mo = m >> 16, mi = m & 0xffffu;
                 const uint32_t ci = j0 + 1 + q;
                 const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
-                const bool dead = !act | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < rs_l));
+                const bool dead = !act | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
+                                  (split & (ci < rs_l));
                 unsigned long long tot = (unsigned long long)Cq + est;
                 if (LAM) {
                     uint32_t v;
@@ -450,7 +465,11 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
         };
-        if (intra_slow) intra_pass(std::true_type{}); else intra_pass(std::false_type{});
+        if (intra_slow) {
+            if (single_ok) intra_pass(std::true_type{}, std::true_type{}); else intra_pass(std::true_type{}, std::false_type{});
+        } else {
+            if (single_ok) intra_pass(std::false_type{}, std::true_type{}); else intra_pass(std::false_type{}, std::false_type{});
+        }
         const long long o_C = (long long)lb;
         const long long iC = o_C;
         const uint32_t o_A = jl - lbi;
