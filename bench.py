@@ -163,6 +163,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override query count (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -182,6 +183,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     desc, inp, out, slo, cfg = workload(args.config, rank, args.n)
+    if args.dp_tile:
+        cfg = cfg.replace(dp_tile=args.dp_tile)
     n = len(inp)
     d_in = torch.from_numpy(inp.view(np.int32)).to(dev)
     d_out = torch.from_numpy(out.view(np.int32)).to(dev)

@@ -356,6 +356,41 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         run = 1;
     }
     __syncwarp();
+    // Prune slots [0, Lt) at the state of boundary jend: slots below Lold first fold the block
+    // maxima (bmo, bmi).  Drops the dead prefix (b > W, KV cap, SLO split) and every candidate
+    // dominated (D1) by its successor; survivors are compacted in order.
+    auto prune = [&](uint32_t Lt, uint32_t Lold, uint32_t bmo, uint32_t bmi, uint32_t jend) {
+        uint32_t wr = 0;
+        for (uint32_t r = 0; r * 32 < Lt; ++r) {
+            const uint32_t k = r * 32 + lane;
+            const bool valid = k < Lt, has_next = k + 1 < Lt;
+            long long cC = 0, nC = 0;
+            unsigned long long cp = 0, np = 0;
+            if (valid) { cC = S.cC[k]; cp = S.cP[k]; }
+            if (has_next) { nC = S.cC[k + 1]; np = S.cP[k + 1]; }
+            const uint32_t ci = (uint32_t)cp;
+            uint32_t mo = (uint32_t)(cp >> 32) & 0xffffu, mi = (uint32_t)(cp >> 48);
+            if (k < Lold) { mo = max(mo, bmo); mi = max(mi, bmi); }
+            const uint32_t ni = (uint32_t)np;
+            uint32_t nmo = (uint32_t)(np >> 32) & 0xffffu, nmi = (uint32_t)(np >> 48);
+            if (k + 1 < Lold) { nmo = max(nmo, bmo); nmi = max(nmi, bmi); }
+            const uint32_t b = jend - ci;
+            const bool dead = !valid | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < run_start));
+            const uint32_t nS = t_tok * nmo + t_pre * nmi;
+            const bool dominated = has_next && (nC - cC < (long long)(unsigned long long)((ni - ci) * nS));
+            const bool keep = !dead && !dominated;
+            __syncwarp();
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const uint32_t pos = wr + __popc(bal & lt);
+                SW.put(S, pos, cC, ci, mo, mi);
+            }
+            wr += __popc(bal);
+            __syncwarp();
+        }
+        L = wr;
+    };
+    if (FIX) prune(L, L, 0, 0, s);      // the W fix-up candidates, pruned before the first block
     uint32_t evals = 0;
     bool stop = false;
     uint32_t done = s;
@@ -512,36 +547,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         if (vl) SW.put(S, L + lane, iC, j0 + 1 + lane, imo, imi);
         evals += B * (B - 1) / 2;
         __syncwarp();
-        const uint32_t Lt = L + B;
-        uint32_t wr = 0;
-        for (uint32_t r = 0; r * 32 < Lt; ++r) {
-            const uint32_t k = r * 32 + lane;
-            const bool valid = k < Lt, has_next = k + 1 < Lt;
-            long long cC = 0, nC = 0;
-            unsigned long long cp = 0, np = 0;
-            if (valid) { cC = S.cC[k]; cp = S.cP[k]; }
-            if (has_next) { nC = S.cC[k + 1]; np = S.cP[k + 1]; }
-            const uint32_t ci = (uint32_t)cp;
-            uint32_t mo = (uint32_t)(cp >> 32) & 0xffffu, mi = (uint32_t)(cp >> 48);
-            if (k < L) { mo = max(mo, bmo); mi = max(mi, bmi); }
-            const uint32_t ni = (uint32_t)np;
-            uint32_t nmo = (uint32_t)(np >> 32) & 0xffffu, nmi = (uint32_t)(np >> 48);
-            if (k + 1 < L) { nmo = max(nmo, bmo); nmi = max(nmi, bmi); }
-            const uint32_t b = jend - ci;
-            const bool dead = !valid | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < run_start));
-            const uint32_t nS = t_tok * nmo + t_pre * nmi;
-            const bool dominated = has_next && (nC - cC < (long long)(unsigned long long)((ni - ci) * nS));
-            const bool keep = !dead && !dominated;
-            __syncwarp();
-            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const uint32_t pos = wr + __popc(bal & lt);
-                SW.put(S, pos, cC, ci, mo, mi);
-            }
-            wr += __popc(bal);
-            __syncwarp();
-        }
-        L = wr;
+        prune(L + B, L, bmo, bmi, jend);
     }
     R.positions = done - s;
     R.evals = evals;
@@ -592,7 +598,7 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
     return dp_warp<FIX>(P, slots_for(smem, P.cap_slots, warp), s, e, src, stop_min);
 }
 
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 3) k_dp_local(DPParams P, uint64_t ntiles)
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_local(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
     const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -614,7 +620,7 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, 3) k_dp_local(DPParams P,
     }
 }
 
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 3) k_dp_fix(DPParams P, uint64_t ntiles)
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_fix(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
     const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
