@@ -198,8 +198,7 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     CU(cudaMemsetAsync(meta, 0, sizeof(LoadMeta), st));
     CU(cudaMemsetAsync(&meta->key_and, 0xff, sizeof(unsigned long long), st));
     CU(cudaMemsetAsync(at<uint32_t>(w, L.slo_set), 0, 4 * kSloSetSize, st));
-    CU(launch_load(din, dout, dslo, n, at<unsigned long long>(w, L.keys0), at<uint32_t>(w, L.vals0), meta,
-                   at<uint32_t>(w, L.slo_set), st));
+    CU(launch_load(din, dout, dslo, n, meta, at<uint32_t>(w, L.slo_set), st));
     LoadMeta hm;
     CU(cudaMemcpyAsync(&hm, meta, sizeof hm, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -213,7 +212,7 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     if (bound >= ((u128)1 << 63)) return UELLM_ERR_OVERFLOW;
     const u128 kv = (u128)cfg->kv_bytes_per_elem * cfg->n_layers * cfg->hidden * W * ((u128)hm.max_in + hm.max_out);
     if (kv >= ((u128)1 << 64)) return UELLM_ERR_OVERFLOW;
-    v.d_in = din; v.d_out = dout;
+    v.d_in = din; v.d_out = dout; v.d_slo = dslo;
     v.max_in = hm.max_in; v.max_out = hm.max_out; v.max_slo = hm.max_slo;
     v.key_or = hm.key_or; v.key_and = hm.key_and;
     v.slo_distinct = hm.slo_distinct; v.slo_overflow = hm.slo_overflow;
@@ -272,37 +271,54 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
     while (v.slo_distinct > 1 && rb < 32 && ((v.slo_distinct - 1) >> rb)) ++rb;   // bits(distinct - 1)
     const bool compressed = cfg->mode != UELLM_MODE_FIFO && !v.slo_overflow && v.slo_distinct >= 1 &&
                             v.slo_distinct <= kSloRankMax && rb + ob <= 32;
+    DecodeArgs D;
+    D.in = v.d_in; D.table = at<uint32_t>(w, L.slo_table); D.ob = ob;
+    D.rin = rin; D.rout = rout; D.rslo = rslo; D.order = d_order;
     if (compressed) {
+        // rank table, then keys rank << ob | out packed straight from the caller arrays together
+        // with the digit-0 histogram; the last pass writes the records (fused decode)
         uint32_t *kc = at<uint32_t>(w, L.keysc);
-        CU(launch_slo_rank(at<unsigned long long>(w, L.keys0), n, at<uint32_t>(w, L.slo_set),
-                           at<uint32_t>(w, L.slo_table), at<uint32_t>(w, L.slo_rank), ob, kc, st));
-        launches += 2;
+        uint32_t *vals0 = at<uint32_t>(w, L.vals0);
+        CU(launch_slo_table(at<uint32_t>(w, L.slo_set), at<uint32_t>(w, L.slo_table), at<uint32_t>(w, L.slo_rank), st));
         uint32_t mask = 0;
         for (int d = 0; d < 4; ++d) if (8 * d < rb + ob) mask |= 1u << d;
+        CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, L.nwin, at<uint32_t>(w, L.slo_set),
+                              at<uint32_t>(w, L.slo_rank), ob, kc, vals0, at<uint32_t>(w, L.hist), st));
+        launches += 2;
         const uint32_t *k32 = kc;
-        const uint32_t *vals = at<uint32_t>(w, L.vals0);
+        const uint32_t *vals = vals0;
         CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                 (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                                at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st));
-        launches += 3 * passes;
+                                at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st,
+                                (mask & 1u) != 0, &D));
+        launches += 3 * passes - ((mask & 1u) && passes ? 1 : 0);
         rec(v, UELLM_STAGE_SORT_END, st);
-        CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
+        if (passes == 0) {
+            CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
+            launches += 1;
+        }
     } else {
-        const unsigned long long *keys = at<unsigned long long>(w, L.keys0);
-        const uint32_t *vals = at<uint32_t>(w, L.vals0);
+        unsigned long long *k0 = at<unsigned long long>(w, L.keys0);
+        uint32_t *v0 = at<uint32_t>(w, L.vals0);
+        CU(launch_pack64(v.d_out, v.d_slo, n, k0, v0, st));
+        launches += 1;
+        const unsigned long long *keys = k0;
+        const uint32_t *vals = v0;
         if (cfg->mode != UELLM_MODE_FIFO) {
             const unsigned long long vary = v.key_or ^ v.key_and;
             uint32_t mask = 0;
             for (int d = 0; d < 8; ++d) if ((vary >> (8 * d)) & 0xffull) mask |= 1u << d;
             CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                   at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                                  at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st));
+                                  at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st, &D));
             launches += 3 * passes;
         }
         rec(v, UELLM_STAGE_SORT_END, st);
-        CU(launch_decode(keys, vals, v.d_in, n, rin, rout, rslo, d_order, st));
+        if (passes == 0) {
+            CU(launch_decode(keys, vals, v.d_in, n, rin, rout, rslo, d_order, st));
+            launches += 1;
+        }
     }
-    launches += 1;
     rec(v, UELLM_STAGE_DECODE_END, st);
     {
         unsigned long long sp[2] = {(unsigned long long)passes, compressed ? (unsigned long long)(rb + ob) : 64ull};

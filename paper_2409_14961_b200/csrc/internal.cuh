@@ -23,6 +23,19 @@ constexpr uint32_t kSloRankMax = 1024;         // rank-compress the sort key up 
 static inline __host__ __device__ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 static inline __host__ __device__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// a1 (R12): slo_us = rint(double(slo_s) * 1e6), round-half-to-even, valid iff in [1, 2^32-1].
+// Used by the load (validation) and by the key packers -- one definition, bit-identical.
+__device__ __forceinline__ uint32_t slo_to_us(float slo_s, bool &ok)
+{
+    const double x = (double)slo_s;
+    if (!(x > 0.0) || !isfinite(x)) { ok = false; return 0; }
+    const double r = rint(__dmul_rn(x, 1e6));      // one correctly rounded product
+    if (r < 1.0 || r > 4294967295.0) { ok = false; return 0; }
+    ok = true;
+    return (uint32_t)r;
+}
+__device__ __forceinline__ uint32_t slo_hash(uint32_t v, uint32_t bits) { return (v * 0x9E3779B1u) >> (32 - bits); }
+
 // --------------------------------------------------------------------------------------
 // Device-side validation record written by the load kernel (read back once, 64 bytes).
 struct LoadMeta {
@@ -93,7 +106,8 @@ struct ProfileView {
     uint64_t n_events;
     void *events[UELLM_STAGE_COUNT];              // caller cudaEvent_t handles (stage timing)
     uint32_t slo_distinct, slo_overflow;
-    uint64_t pad[10];
+    const float *d_slo;                           // caller device SLO array or its staging copy
+    uint64_t pad[9];
 };
 static_assert(sizeof(ProfileView) <= sizeof(uellm_profile), "ProfileView fits uellm_profile");
 
@@ -103,14 +117,26 @@ uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_ti
 // --------------------------------------------------------------------------------------
 // Kernel launchers (each returns cudaGetLastError()).
 cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
-                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, uint32_t *slo_set,
-                        cudaStream_t st);
-// Rank table of the distinct SLO values + u32 keys rank << ob | out.
-cudaError_t launch_slo_rank(const unsigned long long *keys, uint64_t n, const uint32_t *slo_set, uint32_t *table,
-                            uint32_t *rank_of_slot, int ob, uint32_t *keys32, cudaStream_t st);
+                        LoadMeta *meta, uint32_t *slo_set, cudaStream_t st);
+// key64 = slo_us << 32 | out, val = arrival index (generic sort key; FIFO records)
+cudaError_t launch_pack64(const uint32_t *out, const float *slo, uint64_t n, unsigned long long *keys,
+                          uint32_t *vals, cudaStream_t st);
+// decode arguments for the last radix pass (records written straight at the sorted position)
+struct DecodeArgs {
+    const uint32_t *in;        // caller input lengths (gathered by arrival index)
+    const uint32_t *table;     // compressed keys: rank -> slo_us (kSloRankMax entries)
+    int ob;                    // compressed keys: bits of max_out
+    uint32_t *rin, *rout, *rslo, *order;
+};
+// compressed path: rank table, then pack key32 = rank << ob | out with the digit-0 histogram
+cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, uint32_t *rank_of_slot, cudaStream_t st);
+cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t nwin,
+                               const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob, uint32_t *keys32,
+                               uint32_t *vals, uint32_t *hist0, cudaStream_t st);
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
-                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st);
+                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st,
+                                 bool hist0_ready = false, const DecodeArgs *dec = nullptr);
 cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const uint32_t *in, uint64_t n,
                             const uint32_t *table, int ob, uint32_t *rin, uint32_t *rout, uint32_t *rslo,
                             uint32_t *order, cudaStream_t st);
@@ -123,7 +149,7 @@ cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_
                                unsigned long long *keys_a, uint32_t *vals_a,
                                unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
                                uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
-                               int *passes, cudaStream_t st);
+                               int *passes, cudaStream_t st, const struct DecodeArgs *dec = nullptr);
 
 // Decode sorted keys into records: slo = key >> 32, out = key & 0xffffffff, idx = val.
 cudaError_t launch_decode(const unsigned long long *keys, const uint32_t *vals, const uint32_t *in,

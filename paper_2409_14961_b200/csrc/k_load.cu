@@ -16,11 +16,8 @@
 
 namespace uellm {
 
-__device__ __forceinline__ uint32_t slo_hash(uint32_t v, uint32_t bits) { return (v * 0x9E3779B1u) >> (32 - bits); }
-
 __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, const uint32_t *__restrict__ out,
                                               const float *__restrict__ slo, uint64_t n,
-                                              unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
                                               LoadMeta *meta, uint32_t *__restrict__ slo_set)
 {
     constexpr uint32_t kCtaSlots = 2048, kCtaBits = 11, kCtaMax = kSloRankMax;
@@ -39,19 +36,12 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
         uint32_t su = 0;
         if (v) {
             uint32_t a = __ldg(in + k), o = __ldg(out + k);
-            float sf = __ldg(slo + k);
-            double x = (double)sf;
+            bool ok;
+            su = slo_to_us(__ldg(slo + k), ok);
             if (a == 0) bad |= 1u;
             if (o == 0) bad |= 2u;
-            if (!(x > 0.0) || !isfinite(x)) {
-                bad |= 4u;
-            } else {
-                double r = rint(__dmul_rn(x, 1e6));      // one correctly rounded product, half-even
-                if (r < 1.0 || r > 4294967295.0) bad |= 4u; else su = (uint32_t)r;
-            }
-            unsigned long long key = ((unsigned long long)su << 32) | o;
-            keys[k] = key;
-            vals[k] = (uint32_t)k;
+            if (!ok) bad |= 4u;
+            const unsigned long long key = ((unsigned long long)su << 32) | o;
             mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
             kor |= key; kand &= key;
         }
@@ -114,14 +104,37 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
 }
 
 cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
-                        unsigned long long *keys, uint32_t *vals, LoadMeta *meta, uint32_t *slo_set,
-                        cudaStream_t st)
+                        LoadMeta *meta, uint32_t *slo_set, cudaStream_t st)
 {
     if (n == 0) return cudaSuccess;
     uint64_t blocks = ceil_div(n, 256ull * 8);      // ~8 queries per thread
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     if (blocks < 1) blocks = 1;
-    k_load<<<(unsigned)blocks, 256, 0, st>>>(in, out, slo, n, keys, vals, meta, slo_set);
+    k_load<<<(unsigned)blocks, 256, 0, st>>>(in, out, slo, n, meta, slo_set);
+    return cudaGetLastError();
+}
+
+// a2 (generic key): key64 = slo_us << 32 | out, payload = arrival index (inputs validated by load)
+__global__ void __launch_bounds__(256) k_pack64(const uint32_t *__restrict__ out, const float *__restrict__ slo,
+                                                uint64_t n, unsigned long long *__restrict__ keys,
+                                                uint32_t *__restrict__ vals)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        bool ok;
+        const uint32_t su = slo_to_us(__ldg(slo + k), ok);
+        keys[k] = ((unsigned long long)su << 32) | __ldg(out + k);
+        vals[k] = (uint32_t)k;
+    }
+}
+
+cudaError_t launch_pack64(const uint32_t *out, const float *slo, uint64_t n, unsigned long long *keys,
+                          uint32_t *vals, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = ceil_div(n, 256ull * 4);
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    k_pack64<<<(unsigned)blocks, 256, 0, st>>>(out, slo, n, keys, vals);
     return cudaGetLastError();
 }
 
@@ -151,33 +164,9 @@ __global__ void __launch_bounds__(1024) k_slo_table(const uint32_t *__restrict__
     }
 }
 
-// key32 = rank(slo_us) << ob | out
-__global__ void __launch_bounds__(256) k_repack(const unsigned long long *__restrict__ keys, uint64_t n,
-                                                const uint32_t *__restrict__ slo_set,
-                                                const uint32_t *__restrict__ rank_of_slot, int ob,
-                                                uint32_t *__restrict__ keys32)
+cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, uint32_t *rank_of_slot, cudaStream_t st)
 {
-    __shared__ uint32_t sset[kSloSetSize], srank[kSloSetSize];
-    for (uint32_t i = threadIdx.x; i < kSloSetSize; i += blockDim.x) { sset[i] = slo_set[i]; srank[i] = rank_of_slot[i]; }
-    __syncthreads();
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-        const unsigned long long key = keys[k];
-        const uint32_t su = (uint32_t)(key >> 32);
-        uint32_t h = slo_hash(su, kSloSetBits);
-        while (sset[h] != su) h = (h + 1) & (kSloSetSize - 1);
-        keys32[k] = (srank[h] << ob) | (uint32_t)key;
-    }
-}
-
-cudaError_t launch_slo_rank(const unsigned long long *keys, uint64_t n, const uint32_t *slo_set, uint32_t *table,
-                            uint32_t *rank_of_slot, int ob, uint32_t *keys32, cudaStream_t st)
-{
-    if (n == 0) return cudaSuccess;
     k_slo_table<<<1, 1024, 0, st>>>(slo_set, table, rank_of_slot);
-    uint64_t blocks = ceil_div(n, 256ull * 8);
-    if (blocks > 148ull * 8) blocks = 148ull * 8;
-    k_repack<<<(unsigned)blocks, 256, 0, st>>>(keys, n, slo_set, rank_of_slot, ob, keys32);
     return cudaGetLastError();
 }
 

@@ -89,22 +89,25 @@ __global__ void __launch_bounds__(256) k_sort_scan(uint32_t *__restrict__ hist, 
     for (uint64_t k = 0; k < ntl; ++k) hist[(w * tpw + k) * 256 + d] += base;
 }
 
-template <class K>
+template <class K, bool DECODE>
 __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                             K *__restrict__ kout, uint32_t *__restrict__ vout,
                                                             const uint32_t *__restrict__ hist, uint64_t n,
-                                                            uint64_t window, uint64_t tpw, int shift)
+                                                            uint64_t window, uint64_t tpw, int shift, DecodeArgs D)
 {
     constexpr int kWarps = kSortThreads / 32;
     constexpr int kPerWarpIters = kSortTile / kWarps / 32;     // 16
     __shared__ uint32_t whist[kWarps][256];
     __shared__ uint32_t tbase[256];
+    __shared__ uint32_t stab[DECODE && sizeof(K) == 4 ? kSloRankMax : 1];
     uint64_t start, end;
     tile_range(blockIdx.x, n, window, tpw, start, end);
     if (start >= end) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < kWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
     if (tid < 256) tbase[tid] = hist[(uint64_t)blockIdx.x * 256 + tid];
+    if (DECODE && sizeof(K) == 4)
+        for (int i = tid; i < (int)kSloRankMax; i += kSortThreads) stab[i] = D.table[i];
     __syncthreads();
 
     K kr[kPerWarpIters];
@@ -150,8 +153,22 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
         if (p < end) {
             uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
             uint32_t pos = tbase[d] + whist[warp][d] + rank[r];
-            kout[pos] = kr[r];
-            vout[pos] = vr[r];
+            if (DECODE) {       // a4 fused: records at the final scheduled position
+                const uint32_t idx = vr[r];
+                if (sizeof(K) == 8) {
+                    D.rslo[pos] = (uint32_t)((unsigned long long)kr[r] >> 32);
+                    D.rout[pos] = (uint32_t)kr[r];
+                } else {
+                    const uint32_t key = (uint32_t)kr[r];
+                    D.rslo[pos] = stab[D.ob >= 32 ? 0u : key >> D.ob];
+                    D.rout[pos] = D.ob >= 32 ? key : (key & ((1u << D.ob) - 1));
+                }
+                D.order[pos] = idx;
+                D.rin[pos] = __ldg(D.in + idx);
+            } else {
+                kout[pos] = kr[r];
+                vout[pos] = vr[r];
+            }
         }
     }
 }
@@ -159,7 +176,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
 template <class K>
 static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, K *keys_a, uint32_t *vals_a,
                                    K *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n, uint64_t window,
-                                   uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st)
+                                   uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st,
+                                   bool hist0_ready, const DecodeArgs *dec)
 {
     *passes = 0;
     if (n == 0) return cudaSuccess;
@@ -167,13 +185,22 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
     const uint64_t tiles = tpw * nwin;
     const K *kin = *keys_io;
     const uint32_t *vin = *vals_io;
+    int last = -1;
+    for (int d = 0; d < (int)sizeof(K); ++d) if (digit_mask >> d & 1u) last = d;
+    const DecodeArgs D0 = dec ? *dec : DecodeArgs{};
     for (int d = 0; d < (int)sizeof(K); ++d) {
         if (!(digit_mask >> d & 1u)) continue;
         K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
-        k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
+        if (!(hist0_ready && *passes == 0))
+            k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
         k_sort_scan<<<(unsigned)nwin, 256, 0, st>>>(hist, n, window, tpw);
-        k_sort_down<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw, 8 * d);
+        if (dec && d == last)
+            k_sort_down<K, true><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw,
+                                                                          8 * d, D0);
+        else
+            k_sort_down<K, false><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw,
+                                                                           8 * d, D0);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         kin = kout;
@@ -189,18 +216,70 @@ cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_
                                unsigned long long *keys_a, uint32_t *vals_a,
                                unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
                                uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
-                               int *passes, cudaStream_t st)
+                               int *passes, cudaStream_t st, const DecodeArgs *dec)
 {
     return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window,
-                                               nwin, digit_mask, passes, st);
+                                               nwin, digit_mask, passes, st, false, dec);
 }
 
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
-                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st)
+                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st,
+                                 bool hist0_ready, const DecodeArgs *dec)
 {
     return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window, nwin,
-                                     digit_mask, passes, st);
+                                     digit_mask, passes, st, hist0_ready, dec);
+}
+
+// a2 (compressed key) fused with the digit-0 histogram of the first radix pass:
+// key32 = rank(slo_us) << ob | out per 4096-query tile, payload = arrival index.
+__global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__restrict__ out,
+                                                              const float *__restrict__ slo, uint64_t n,
+                                                              uint64_t window, uint64_t tpw,
+                                                              const uint32_t *__restrict__ slo_set,
+                                                              const uint32_t *__restrict__ rank_of_slot, int ob,
+                                                              uint32_t *__restrict__ keys32, uint32_t *__restrict__ vals,
+                                                              uint32_t *__restrict__ hist)
+{
+    __shared__ uint32_t sset[kSloSetSize], srank[kSloSetSize];
+    __shared__ uint32_t h[256];
+    const int tid = threadIdx.x;
+    for (uint32_t i = tid; i < kSloSetSize; i += kSortThreads) { sset[i] = slo_set[i]; srank[i] = rank_of_slot[i]; }
+    if (tid < 256) h[tid] = 0;
+    __syncthreads();
+    uint64_t start, end;
+    tile_range(blockIdx.x, n, window, tpw, start, end);
+#pragma unroll 4
+    for (uint32_t i = 0; i < kSortItems; ++i) {
+        const uint64_t p = start + (uint64_t)i * kSortThreads + tid;
+        const bool valid = p < end;
+        const uint32_t act = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            bool ok;
+            const uint32_t su = slo_to_us(__ldg(slo + p), ok);
+            uint32_t hh = slo_hash(su, kSloSetBits);
+            while (sset[hh] != su) hh = (hh + 1) & (kSloSetSize - 1);
+            const uint32_t key = (srank[hh] << ob) | __ldg(out + p);
+            keys32[p] = key;
+            vals[p] = (uint32_t)p;
+            const uint32_t d = key & 0xffu;
+            const uint32_t peers = __match_any_sync(act, d);
+            if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    if (tid < 256) hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
+}
+
+cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t nwin,
+                               const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob, uint32_t *keys32,
+                               uint32_t *vals, uint32_t *hist0, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    const uint64_t tpw = ceil_div(window, kSortTile);
+    k_pack32_hist<<<(unsigned)(tpw * nwin), kSortThreads, 0, st>>>(out, slo, n, window, tpw, slo_set, rank_of_slot,
+                                                                  ob, keys32, vals, hist0);
+    return cudaGetLastError();
 }
 
 }  // namespace uellm
