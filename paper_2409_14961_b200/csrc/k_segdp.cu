@@ -419,27 +419,35 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         // is viol a single comparison.  Crossing intervals exist in this block only if the oldest
         // external candidate starts before the last run start (external), or a run starts inside
         // the block (intra); those rare blocks take the binary-search variant.
-        const bool ext_slow = LAM && !split && ((uint32_t)S.cP[0] < rs_last);
-        const bool intra_slow = LAM && !split && (rs_last > j0);
+        const bool one_run_ext = (uint32_t)S.cP[0] >= rs_last;     // every candidate and element in one run
+        const bool one_run_intra = rs_last <= j0;                   // every element of the block in one run
+        const bool ext_slow = LAM && !split && !one_run_ext;
+        const bool intra_slow = LAM && !split && !one_run_intra;
         // ---- 1. external candidates
         unsigned long long lb = ~0ull;
         uint32_t lbi = 0xffffffffu;
         // candidates oldest -> newest; strict '<' keeps the smallest minimising i (R9)
         evals += L * B;
-        auto ext_pass = [&](auto slow_tag, auto single_tag) {
+        // In one SLO run the elements ascend in predicted length (sort key), so the max output of
+        // any interval ending at the lane's element is that element's own: MO = pmo for every
+        // candidate and the lane-constant parts of est are computed once.
+        const uint32_t A_l = t_b + t_it * pmo, T_l = t_tok * pmo;
+        auto ext_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag) {
             constexpr bool SLOW = decltype(slow_tag)::value;
             constexpr bool SINGLE_OK = decltype(single_tag)::value;
+            constexpr bool ONERUN = decltype(onerun_tag)::value;
 #pragma unroll 2
             for (uint32_t c = 0; c < L; ++c) {
                 const unsigned long long cp = S.cP[c];
                 const uint32_t ci = (uint32_t)cp;
                 const long long cC = S.cC[c];
                 const uint32_t b = jl - ci;
-                const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, pmo);
+                const uint32_t mo = ONERUN ? pmo : max((uint32_t)(cp >> 32) & 0xffffu, pmo);
                 const uint32_t mi = max((uint32_t)(cp >> 48), pmi);
-                const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
+                const uint32_t est = ONERUN ? A_l + b * (T_l + t_pre * mi)
+                                            : t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
                 const bool dead = !vl | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
-                                  (split & (ci < rs_l));
+                                  (!ONERUN & split & (ci < rs_l));
                 unsigned long long tot = (unsigned long long)cC + est;
                 if (LAM) {
                     uint32_t v;
@@ -451,10 +459,14 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
         };
+        using T1 = std::true_type;
+        using F0 = std::false_type;
         if (ext_slow) {
-            if (single_ok) ext_pass(std::true_type{}, std::true_type{}); else ext_pass(std::true_type{}, std::false_type{});
+            if (single_ok) ext_pass(T1{}, T1{}, F0{}); else ext_pass(T1{}, F0{}, F0{});
+        } else if (one_run_ext) {
+            if (single_ok) ext_pass(F0{}, T1{}, T1{}); else ext_pass(F0{}, F0{}, T1{});
         } else {
-            if (single_ok) ext_pass(std::false_type{}, std::true_type{}); else ext_pass(std::false_type{}, std::false_type{});
+            if (single_ok) ext_pass(F0{}, T1{}, F0{}); else ext_pass(F0{}, F0{}, F0{});
         }
         // ---- 2. intra-block candidates.  Lane = boundary again: the candidate born at boundary
         //      j0+q+1 (final once lane q has seen every older candidate) is broadcast and every
@@ -476,19 +488,21 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             const uint32_t lv = 31 - __clz(bb - a + 1);
             return __vmaxu2(T[lv * 33 + a], T[lv * 33 + bb - (1u << lv) + 1]);
         };
-        auto intra_pass = [&](auto slow_tag, auto single_tag) {
+        auto intra_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag) {
             constexpr bool SLOW = decltype(slow_tag)::value;
             constexpr bool SINGLE_OK = decltype(single_tag)::value;
+            constexpr bool ONERUN = decltype(onerun_tag)::value;
             for (uint32_t q = 0; q + 1 < B; ++q) {
                 const long long Cq = (long long)__shfl_sync(0xffffffffu, lb, q);
                 const bool act = vl && lane > q;
                 const uint32_t b = act ? lane - q : 1u;          // boundary jl minus candidate j0+1+q
                 const uint32_t m = rmq(act ? q + 1 : lane, lane);
-                const uint32_t mo = m >> 16, mi = m & 0xffffu;
+                const uint32_t mo = ONERUN ? pmo : m >> 16, mi = m & 0xffffu;
                 const uint32_t ci = j0 + 1 + q;
-                const uint32_t est = t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
+                const uint32_t est = ONERUN ? A_l + b * (T_l + t_pre * mi)
+                                            : t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
                 const bool dead = !act | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
-                                  (split & (ci < rs_l));
+                                  (!ONERUN & split & (ci < rs_l));
                 unsigned long long tot = (unsigned long long)Cq + est;
                 if (LAM) {
                     uint32_t v;
@@ -501,9 +515,11 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             }
         };
         if (intra_slow) {
-            if (single_ok) intra_pass(std::true_type{}, std::true_type{}); else intra_pass(std::true_type{}, std::false_type{});
+            if (single_ok) intra_pass(T1{}, T1{}, F0{}); else intra_pass(T1{}, F0{}, F0{});
+        } else if (one_run_intra) {
+            if (single_ok) intra_pass(F0{}, T1{}, T1{}); else intra_pass(F0{}, F0{}, T1{});
         } else {
-            if (single_ok) intra_pass(std::false_type{}, std::true_type{}); else intra_pass(std::false_type{}, std::false_type{});
+            if (single_ok) intra_pass(F0{}, T1{}, F0{}); else intra_pass(F0{}, F0{}, F0{});
         }
         const long long o_C = (long long)lb;
         const long long iC = o_C;
