@@ -98,8 +98,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
     constexpr int kWarps = kSortThreads / 32;
     constexpr int kPerWarpIters = kSortTile / kWarps / 32;     // 16
     __shared__ uint32_t whist[kWarps][256];
-    __shared__ uint32_t tbase[256];
+    __shared__ uint32_t tbase[256], dstart[256];
     __shared__ uint32_t stab[DECODE && sizeof(K) == 4 ? kSloRankMax : 1];
+    extern __shared__ __align__(16) unsigned char dyn[];      // staging: K[kSortTile] + u32[kSortTile]
     uint64_t start, end;
     tile_range(blockIdx.x, n, window, tpw, start, end);
     if (start >= end) return;
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
         __syncwarp();
     }
     __syncthreads();
-    if (tid < 256) {   // exclusive scan over warps, per digit
+    if (tid < 256) {   // exclusive scan over warps, per digit; dstart = tile total of the digit
         uint32_t run = 0;
 #pragma unroll
         for (int wv = 0; wv < kWarps; ++wv) {
@@ -145,30 +146,50 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
             whist[wv][tid] = run;
             run += c;
         }
+        dstart[tid] = run;
     }
     __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {   // inclusive scan of the digit totals
+        uint32_t v = (tid < 256 && tid >= off) ? dstart[tid - off] : 0u;
+        __syncthreads();
+        if (tid < 256) dstart[tid] += v;
+        __syncthreads();
+    }
+    // stage the tile in shared memory in (digit, rank) order, then write every digit bucket as
+    // one contiguous run: consecutive threads store consecutive addresses
+    K *sk = reinterpret_cast<K *>(dyn);
+    uint32_t *sv = reinterpret_cast<uint32_t *>(dyn + kSortTile * sizeof(K));
 #pragma unroll
     for (int r = 0; r < kPerWarpIters; ++r) {
         uint64_t p = base + r * 32 + lane;
         if (p < end) {
-            uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
-            uint32_t pos = tbase[d] + whist[warp][d] + rank[r];
-            if (DECODE) {       // a4 fused: records at the final scheduled position
-                const uint32_t idx = vr[r];
-                if (sizeof(K) == 8) {
-                    D.rslo[pos] = (uint32_t)((unsigned long long)kr[r] >> 32);
-                    D.rout[pos] = (uint32_t)kr[r];
-                } else {
-                    const uint32_t key = (uint32_t)kr[r];
-                    D.rslo[pos] = stab[D.ob >= 32 ? 0u : key >> D.ob];
-                    D.rout[pos] = D.ob >= 32 ? key : (key & ((1u << D.ob) - 1));
-                }
-                D.order[pos] = idx;
-                D.rin[pos] = __ldg(D.in + idx);
+            const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
+            const uint32_t loc = (d ? dstart[d - 1] : 0u) + whist[warp][d] + rank[r];
+            sk[loc] = kr[r];
+            sv[loc] = vr[r];
+        }
+    }
+    __syncthreads();
+    const uint32_t cnt = (uint32_t)(end - start);
+    for (uint32_t i = tid; i < cnt; i += kSortThreads) {
+        const K key = sk[i];
+        const uint32_t d = (uint32_t)(key >> shift) & 0xffu;
+        const uint32_t pos = tbase[d] + i - (d ? dstart[d - 1] : 0u);
+        const uint32_t idx = sv[i];
+        if (DECODE) {           // a4 fused: records at the final scheduled position
+            if (sizeof(K) == 8) {
+                D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
+                D.rout[pos] = (uint32_t)key;
             } else {
-                kout[pos] = kr[r];
-                vout[pos] = vr[r];
+                const uint32_t k32 = (uint32_t)key;
+                D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
+                D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
             }
+            D.order[pos] = idx;
+            D.rin[pos] = __ldg(D.in + idx);
+        } else {
+            kout[pos] = key;
+            vout[pos] = idx;
         }
     }
 }
@@ -195,12 +216,16 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         if (!(hist0_ready && *passes == 0))
             k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
         k_sort_scan<<<(unsigned)nwin, 256, 0, st>>>(hist, n, window, tpw);
-        if (dec && d == last)
-            k_sort_down<K, true><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw,
-                                                                          8 * d, D0);
-        else
-            k_sort_down<K, false><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, hist, n, window, tpw,
-                                                                           8 * d, D0);
+        const size_t stage = kSortTile * (sizeof(K) + sizeof(uint32_t));
+        if (dec && d == last) {
+            cudaFuncSetAttribute(k_sort_down<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+            k_sort_down<K, true><<<(unsigned)tiles, kSortThreads, stage, st>>>(kin, vin, kout, vout, hist, n, window,
+                                                                              tpw, 8 * d, D0);
+        } else {
+            cudaFuncSetAttribute(k_sort_down<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+            k_sort_down<K, false><<<(unsigned)tiles, kSortThreads, stage, st>>>(kin, vin, kout, vout, hist, n, window,
+                                                                               tpw, 8 * d, D0);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         kin = kout;
