@@ -286,7 +286,8 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
                               at<uint32_t>(w, L.slo_rank), ob, kc, vals0, at<uint32_t>(w, L.hist), st));
         launches += 2;
         const uint32_t *k32 = kc;
-        const uint32_t *vals = vals0;
+        const uint32_t *vals = nullptr;            // identity payload (arrival index = position)
+        (void)vals0;
         CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                 (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
                                 at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st,

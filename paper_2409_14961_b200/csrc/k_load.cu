@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) k_decode32(const uint32_t *__restrict__ k
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
         const uint32_t key = keys[p];
-        const uint32_t idx = vals[p];
+        const uint32_t idx = vals ? vals[p] : (uint32_t)p;
         rslo[p] = st[ob >= 32 ? 0 : key >> ob];
         rout[p] = key & mask;
         rin[p] = __ldg(in + idx);

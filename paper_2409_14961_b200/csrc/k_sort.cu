@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
         uint64_t p = base + r * 32 + lane;
         bool valid = p < end;
         kr[r] = valid ? kin[p] : (K)0;
-        vr[r] = valid ? vin[p] : 0u;
+        vr[r] = valid ? (vin ? vin[p] : (uint32_t)p) : 0u;     // vin == NULL: identity payload
     }
     const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -285,8 +285,7 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
             uint32_t hh = slo_hash(su, kSloSetBits);
             while (sset[hh] != su) hh = (hh + 1) & (kSloSetSize - 1);
             const uint32_t key = (srank[hh] << ob) | __ldg(out + p);
-            keys32[p] = key;
-            vals[p] = (uint32_t)p;
+            keys32[p] = key;                       // payload = arrival index p: implicit (NULL vals)
             const uint32_t d = key & 0xffu;
             const uint32_t peers = __match_any_sync(act, d);
             if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));

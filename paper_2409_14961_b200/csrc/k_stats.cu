@@ -57,16 +57,23 @@ __device__ __forceinline__ BatchCore batch_core(const StatsParams &S, uint64_t t
 
 __global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
 {
+    // thread per batch: members are contiguous, each thread streams its own range
     const uint64_t m = *S.num_batches;
-    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < m; t += nw) {
-        BatchCore c = batch_core(S, t);
-        if ((threadIdx.x & 31) == 0) {
-            S.est[t] = c.est;
-            S.so[t] = (unsigned long long)c.s | ((unsigned long long)c.O << 32);
-            S.pin[t] = (unsigned long long)c.b * c.s - c.sin;
-            S.pout[t] = (unsigned long long)c.b * c.O - c.sout;
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += nt) {
+        const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
+        uint32_t s = 0, O = 0;
+        unsigned long long si = 0, so = 0;
+        for (uint32_t k = a; k < z; ++k) {
+            const uint32_t vi = __ldg(S.rin + k), vo = __ldg(S.rout + k);
+            s = max(s, vi); O = max(O, vo);
+            si += vi; so += vo;
         }
+        const unsigned long long b = z - a;
+        S.est[t] = S.t_batch + S.t_iter * O + S.t_tok * b * O + S.t_pre * b * s;
+        S.so[t] = (unsigned long long)s | ((unsigned long long)O << 32);
+        S.pin[t] = b * s - si;
+        S.pout[t] = b * O - so;
     }
 }
 
