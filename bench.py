@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
+    ap.add_argument("--mode", default="seg_dp", choices=["seg_dp", "slo_odbs", "fifo", "sort_only"],
+                    help="segmentation mode (default: the SEG-DP hot path)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -185,6 +187,11 @@ def main():
     desc, inp, out, slo, cfg = workload(args.config, rank, args.n)
     if args.dp_tile:
         cfg = cfg.replace(dp_tile=args.dp_tile)
+    if args.mode != "seg_dp":
+        import workloads as W
+        cfg = cfg.replace(mode={"slo_odbs": W.MODE_SLO_ODBS, "fifo": W.MODE_FIFO, "sort_only": W.MODE_SORT_ONLY}[args.mode],
+                          w1=1.0, w2=0.02, threshold=900.0)
+        desc += f"; mode {args.mode} (Alg. 1: w1=1, w2=0.02, threshold=900)" if args.mode == "slo_odbs" else f"; mode {args.mode}"
     n = len(inp)
     d_in = torch.from_numpy(inp.view(np.int32)).to(dev)
     d_out = torch.from_numpy(out.view(np.int32)).to(dev)

@@ -371,8 +371,8 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         A.w1 = cfg->w1; A.w2 = cfg->w2; A.l1 = cfg->l1; A.l2 = cfg->l2; A.threshold = cfg->threshold;
         A.eps = cfg->eps; A.eq2_additive = cfg->eq2_additive;
         rec(v, UELLM_STAGE_DP_LOCAL_END, st); rec(v, UELLM_STAGE_DP_FIX_END, st); rec(v, UELLM_STAGE_DP_CASCADE_END, st);
-        CU(launch_alg1(A, bm, st));
-        launches += 1;
+        CU(launch_alg1(A, bm, at<uint16_t>(w, L.argx), st));
+        launches += 2;
     } else {
         rec(v, UELLM_STAGE_DP_LOCAL_END, st); rec(v, UELLM_STAGE_DP_FIX_END, st); rec(v, UELLM_STAGE_DP_CASCADE_END, st);
         CU(launch_mark_fifo(bm, n, L.window, cfg->max_batch, cfg->mode == UELLM_MODE_SORT_ONLY, st));

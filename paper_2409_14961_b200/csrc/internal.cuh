@@ -184,7 +184,7 @@ struct Alg1Params {
     double w1, w2, l1, l2, threshold, eps;
     uint32_t eq2_additive;
 };
-cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, cudaStream_t st);
+cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_delta, cudaStream_t st);
 
 // Compaction of the boundary bitmap (n+1 bits) into batch_offsets, num_batches.
 cudaError_t run_compact(const uint32_t *bitmap, uint64_t n, uint32_t *wscan, uint32_t *blocksum,

@@ -150,59 +150,91 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 }
 
 // ---------------------------------------------------------------------------------------
-// Alg. 1 SLO-ODBS with readings R1-R6/R10/R12, one thread per window over the
-// sorted records (sequential scan, as printed).  Doubles with explicit round-to-nearest
-// intrinsics (no FMA contraction) so every decision matches the CPU oracle bit for bit.
-__global__ void k_alg1(Alg1Params A, uint32_t *bm)
+// Alg. 1 SLO-ODBS with readings R1-R6/R10/R12 -- parallel form.
+//
+// A flush always leaves an empty batch (line 14-19 seeds the next batch with q exactly as an
+// admission into an empty batch would; the line-20 dynamic-cap flush and the SLO-split flush
+// clear the state), so the batch that starts at position x evolves independently of how x was
+// reached: next(x), the start of the following batch, is a function of x alone (<= W steps).
+//   k_alg1_next   one thread per position: simulate Alg. 1 from a fresh batch at x -> next(x)
+//   k_alg1_chain  one CTA per window: follow w0 -> next(w0) -> ... through shared-memory
+//                 chunks of next(), marking every batch start.
+// Doubles with explicit round-to-nearest intrinsics (no FMA contraction): every decision is
+// bit-identical to the CPU oracle's sequential scan.
+__global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__restrict__ nd)
 {
-    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= A.nwin) return;
-    const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
-    uint64_t bsize = 0, MI = 0;
-    double L_CM = 0.0, O_CM = 0.0, CM = 0.0;
-    for (uint64_t x = w0; x < w1; ++x) {
-        const uint32_t su = A.rslo[x];
-        const double slo = __ddiv_rn((double)su, 1e6);
-        const double len = (double)A.rout[x];
-        const uint32_t inx = A.rin[x];
-        if (A.split && bsize > 0 && su != A.rslo[x - 1]) {
-            bsize = 0; L_CM = 0.0; O_CM = 0.0; CM = 0.0; MI = 0;
-        }
-        const double nb1 = (double)(bsize + 1);
-        const double T_l = __dmul_rn(__dmul_rn(__dadd_rn(slo, L_CM), nb1), A.l1);
-        double T_o = A.eq2_additive ? __dadd_rn(len, O_CM) : __dsub_rn(len, O_CM);
-        T_o = __dmul_rn(__dmul_rn(T_o, nb1), A.l2);
-        const double Total = __dadd_rn(__dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
-        bool admit = (bsize == 0);
-        if (!admit && Total <= A.threshold) {
-            const uint64_t s = max((uint64_t)inx, MI);
-            const uint64_t O = (uint64_t)(len > O_CM ? len : O_CM);
-            admit = (bsize + 1 <= 1) || ((bsize + 1) * (s + O) <= A.cap_tok);
-        }
-        const double cmq = __dadd_rn(__dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
-        if (admit) {
-            if (bsize == 0) bm_set(bm, (uint32_t)x);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < A.n; x += stride) {
+        const uint64_t w1 = min((x / A.window + 1) * A.window, (uint64_t)A.n);
+        uint64_t bsize = 0, MI = 0;
+        double L_CM = 0.0, O_CM = 0.0, CM = 0.0;
+        uint64_t p = x, next = w1;
+        for (; p < w1; ++p) {
+            const uint32_t su = A.rslo[p];
+            if (A.split && bsize > 0 && su != A.rslo[p - 1]) { next = p; break; }
+            const double slo = __ddiv_rn((double)su, 1e6);
+            const double len = (double)A.rout[p];
+            const uint32_t inx = A.rin[p];
+            const double nb1 = (double)(bsize + 1);
+            const double T_l = __dmul_rn(__dmul_rn(__dadd_rn(slo, L_CM), nb1), A.l1);
+            double T_o = A.eq2_additive ? __dadd_rn(len, O_CM) : __dsub_rn(len, O_CM);
+            T_o = __dmul_rn(__dmul_rn(T_o, nb1), A.l2);
+            const double Total = __dadd_rn(__dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
+            bool admit = (bsize == 0);
+            if (!admit && Total <= A.threshold) {
+                const uint64_t s = max((uint64_t)inx, MI);
+                const uint64_t O = (uint64_t)(len > O_CM ? len : O_CM);
+                admit = (bsize + 1) * (s + O) <= A.cap_tok;
+            }
+            if (!admit) { next = p; break; }                  // q seeds the next batch
+            const double cmq = __dadd_rn(__dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
             bsize += 1;
             if (slo > L_CM) L_CM = slo;
             if (len > O_CM) O_CM = len;
             if (cmq > CM) CM = cmq;
             if (inx > MI) MI = inx;
-        } else {
-            bm_set(bm, (uint32_t)x);
-            bsize = 1; L_CM = slo; O_CM = len; CM = cmq; MI = inx;
+            const double den = CM > A.eps ? CM : A.eps;
+            const double capd = floor(__ddiv_rn(A.threshold, den));
+            const uint64_t cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
+            if (bsize >= cap) { next = p + 1; break; }       // line 20: flush after q
         }
-        const double den = CM > A.eps ? CM : A.eps;
-        const double capd = floor(__ddiv_rn(A.threshold, den));
-        const uint64_t cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
-        if (bsize >= cap) { bsize = 0; L_CM = 0.0; O_CM = 0.0; CM = 0.0; MI = 0; }
+        nd[x] = (uint16_t)(next - x);                          // in [1, W]
     }
-    if (w == A.nwin - 1) bm_set(bm, A.n);
 }
 
-cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, cudaStream_t st)
+constexpr uint32_t kAlg1Chunk = 16384;                         // next() entries staged per chunk
+
+__global__ void __launch_bounds__(256) k_alg1_chain(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t *bm)
+{
+    __shared__ uint16_t sn[kAlg1Chunk];
+    __shared__ uint64_t sx;
+    const uint64_t w = blockIdx.x;
+    const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
+    if (threadIdx.x == 0) sx = w0;
+    __syncthreads();
+    for (;;) {
+        const uint64_t cb = sx;                                // chunk base: the current batch start
+        if (cb >= w1) break;
+        const uint64_t ce = min(cb + kAlg1Chunk, w1);
+        for (uint64_t k = cb + threadIdx.x; k < ce; k += blockDim.x) sn[k - cb] = nd[k];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t x = cb;
+            while (x < ce) { bm_set(bm, (uint32_t)x); x += sn[x - cb]; }
+            sx = x;
+        }
+        __syncthreads();
+    }
+    if (w == A.nwin - 1 && threadIdx.x == 0) bm_set(bm, A.n);
+}
+
+cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_delta, cudaStream_t st)
 {
     if (A.n == 0) return cudaSuccess;
-    k_alg1<<<(unsigned)ceil_div(A.nwin, 64), 64, 0, st>>>(A, bitmap);
+    uint64_t blocks = ceil_div(A.n, 256);
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    k_alg1_next<<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
+    k_alg1_chain<<<(unsigned)A.nwin, 256, 0, st>>>(A, next_delta, bitmap);
     return cudaGetLastError();
 }
 

@@ -300,3 +300,11 @@ def test_sort_paths_compressed_and_generic():
             s2[:k] = vals
         r = assert_parity(inp[:60_000], out[:60_000], s2, cfg.replace(window=0))
         assert (r["diag"]["sort_key_bits"] < 64) == expect_compressed
+
+
+@pytest.mark.parametrize("split", [0, 1])
+def test_mode_slo_odbs_large(split):
+    """Parallel Alg. 1 (next() per position + chunked chain walk) on several windows and chunks."""
+    inp, out, slo, cfg = W.c3(15, n=300_000, split=split)
+    cfg = cfg.replace(mode=W.MODE_SLO_ODBS, w1=1.0, w2=0.02, threshold=900.0, window=70_000, max_batch=128)
+    assert_parity(inp, out, slo, cfg)
