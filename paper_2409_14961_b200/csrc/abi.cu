@@ -58,6 +58,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.blocksum = take(4 * nblk);
     L.blockagg = take(8 * nblk);
     L.st_so = take(8 * N); L.st_pin = take(8 * N); L.st_pout = take(8 * N);
+    L.a1tiles = take(alg1_scratch_bytes(L.window, L.nwin, (uint32_t)L.W));
     L.hist = take(4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));
     L.meta = take(sizeof(LoadMeta)); L.diag = take(sizeof(Diag)); L.acc = take(sizeof(StatAcc));
     L.nb = take(8); L.totals = take(sizeof(uellm_totals));
@@ -371,8 +372,8 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         A.w1 = cfg->w1; A.w2 = cfg->w2; A.l1 = cfg->l1; A.l2 = cfg->l2; A.threshold = cfg->threshold;
         A.eps = cfg->eps; A.eq2_additive = cfg->eq2_additive;
         rec(v, UELLM_STAGE_DP_LOCAL_END, st); rec(v, UELLM_STAGE_DP_FIX_END, st); rec(v, UELLM_STAGE_DP_CASCADE_END, st);
-        CU(launch_alg1(A, bm, at<uint16_t>(w, L.argx), st));
-        launches += 2;
+        CU(launch_alg1(A, bm, at<uint16_t>(w, L.argx), at<uint2>(w, L.a1tiles), diag, st));
+        launches += 4;
     } else {
         rec(v, UELLM_STAGE_DP_LOCAL_END, st); rec(v, UELLM_STAGE_DP_FIX_END, st); rec(v, UELLM_STAGE_DP_CASCADE_END, st);
         CU(launch_mark_fifo(bm, n, L.window, cfg->max_batch, cfg->mode == UELLM_MODE_SORT_ONLY, st));

@@ -87,6 +87,7 @@ struct WsLayout {
     uint64_t tiles;                               // TileRec[ntiles]
     uint64_t bitmap, wscan, blocksum, blockagg;   // boundary bitmap + scan scratch
     uint64_t st_so, st_pin, st_pout;              // per-batch stats scratch (u64 each)
+    uint64_t a1tiles;                             // Alg. 1 chain-walk tile exits (uint2)
     uint64_t hist;                                // u32[sort_tiles * 256]
     uint64_t meta, diag, acc, nb, totals, wincost;
     uint64_t total;
@@ -184,7 +185,9 @@ struct Alg1Params {
     double w1, w2, l1, l2, threshold, eps;
     uint32_t eq2_additive;
 };
-cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_delta, cudaStream_t st);
+cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_delta, uint2 *tile_exits, Diag *diag,
+                        cudaStream_t st);
+uint64_t alg1_scratch_bytes(uint64_t window, uint64_t nwin, uint32_t W);
 
 // Compaction of the boundary bitmap (n+1 bits) into batch_offsets, num_batches.
 cudaError_t run_compact(const uint32_t *bitmap, uint64_t n, uint32_t *wscan, uint32_t *blocksum,

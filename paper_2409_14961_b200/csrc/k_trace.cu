@@ -157,8 +157,7 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 // clear the state), so the batch that starts at position x evolves independently of how x was
 // reached: next(x), the start of the following batch, is a function of x alone (<= W steps).
 //   k_alg1_next   one thread per position: simulate Alg. 1 from a fresh batch at x -> next(x)
-//   k_alg1_chain  one CTA per window: follow w0 -> next(w0) -> ... through shared-memory
-//                 chunks of next(), marking every batch start.
+//   k_a1_*        mark the chain w0 -> next(w0) -> ... by binary lifting (below).
 // Doubles with explicit round-to-nearest intrinsics (no FMA contraction): every decision is
 // bit-identical to the CPU oracle's sequential scan.
 __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__restrict__ nd)
@@ -202,41 +201,137 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
     }
 }
 
-constexpr uint32_t kAlg1Chunk = 16384;                         // next() entries staged per chunk
+// Chain marking w0 -> next(w0) -> ... without a serial walk.  Greedy chains started at
+// different positions phase-lock on the dynamic cap and rarely re-merge, so the walk is split
+// by binary lifting instead, per sub-tile of T positions (T a power of two >= W):
+//   k_a1_lift<false>  lift tables L[k][x] = next^(2^k)(x) inside the sub-tile (EXIT once it
+//                     leaves), then for each possible entry x < W the exit offset into the next
+//                     sub-tile;
+//   k_a1_entries      per window, sub-tile entries in order (one table lookup per sub-tile);
+//   k_a1_lift<true>   rebuild the tables; x is on the chain from entry e iff it has the same
+//                     exit, is no deeper, and lift(e, depth(e) - depth(x)) == x.
+constexpr uint16_t kExit = 0xffff;
 
-__global__ void __launch_bounds__(256) k_alg1_chain(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t *bm)
+template <bool MARK>
+__global__ void __launch_bounds__(256) k_a1_lift(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t T, uint32_t K,
+                                                 uint64_t spw, uint16_t *__restrict__ exit_first,
+                                                 const uint32_t *__restrict__ entries, uint32_t *bm)
 {
-    __shared__ uint16_t sn[kAlg1Chunk];
-    __shared__ uint64_t sx;
-    const uint64_t w = blockIdx.x;
+    extern __shared__ uint16_t sl[];            // K levels x T, then E0[T] (exit offset of the last hop)
+    uint16_t *E0 = sl + (size_t)K * T;
+    const uint64_t t = blockIdx.x, w = t / spw, kk = t % spw;
     const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
-    if (threadIdx.x == 0) sx = w0;
+    const uint64_t s = w0 + kk * T;
+    if (s >= w1) return;
+    const uint32_t len = (uint32_t)min((uint64_t)T, w1 - s);
+    for (uint32_t x = threadIdx.x; x < len; x += blockDim.x) {
+        const uint32_t nx = x + nd[s + x];
+        sl[x] = nx < len ? (uint16_t)nx : kExit;
+        E0[x] = nx < len ? 0 : (uint16_t)(nx - len);
+    }
     __syncthreads();
-    for (;;) {
-        const uint64_t cb = sx;                                // chunk base: the current batch start
-        if (cb >= w1) break;
-        const uint64_t ce = min(cb + kAlg1Chunk, w1);
-        for (uint64_t k = cb + threadIdx.x; k < ce; k += blockDim.x) sn[k - cb] = nd[k];
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t x = cb;
-            while (x < ce) { bm_set(bm, (uint32_t)x); x += sn[x - cb]; }
-            sx = x;
+    for (uint32_t lv = 1; lv < K; ++lv) {
+        for (uint32_t x = threadIdx.x; x < len; x += blockDim.x) {
+            const uint16_t a = sl[(lv - 1) * T + x];
+            sl[lv * T + x] = a == kExit ? kExit : sl[(lv - 1) * T + a];
         }
         __syncthreads();
     }
-    if (w == A.nwin - 1 && threadIdx.x == 0) bm_set(bm, A.n);
+    auto climb = [&](uint32_t x, uint32_t &depth, uint32_t &ex) {     // hops until the exit
+        uint32_t y = x, h = 0;
+        for (int lv = (int)K - 1; lv >= 0; --lv) {
+            const uint16_t a = sl[lv * T + y];
+            if (a != kExit) { y = a; h += 1u << lv; }
+        }
+        depth = h + 1;
+        ex = E0[y];
+    };
+    const uint32_t Wf = min(A.W, len);
+    if (!MARK) {
+        for (uint32_t x = threadIdx.x; x < Wf; x += blockDim.x) {
+            uint32_t d, ex;
+            climb(x, d, ex);
+            exit_first[t * A.W + x] = (uint16_t)ex;
+        }
+        return;
+    }
+    const uint32_t e = (uint32_t)(entries[t] - s);
+    uint32_t De, Ee;
+    climb(e, De, Ee);
+    for (uint32_t x0 = 0; x0 < len; x0 += blockDim.x) {
+        const uint32_t x = x0 + threadIdx.x;
+        bool on = false;
+        if (x < len && x >= e) {
+            uint32_t Dx, Ex;
+            climb(x, Dx, Ex);
+            if (Ex == Ee && Dx <= De) {
+                uint32_t y = e, h = De - Dx;
+                for (uint32_t lv = 0; h; ++lv, h >>= 1)
+                    if (h & 1u) y = sl[lv * T + y];
+                on = (y == x);
+            }
+        }
+        if (on) bm_set(bm, (uint32_t)(s + x));
+    }
+    if (s + len == A.n && threadIdx.x == 0) bm_set(bm, A.n);
 }
 
-cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_delta, cudaStream_t st)
+__global__ void k_a1_entries(Alg1Params A, uint32_t T, uint64_t spw, const uint16_t *__restrict__ exit_first,
+                             uint32_t *entries)
 {
+    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= A.nwin) return;
+    const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
+    uint64_t e = w0;
+    for (uint64_t k = 0; k < spw; ++k) {
+        const uint64_t s = w0 + k * T;
+        if (s >= w1) break;
+        const uint64_t t = w * spw + k;
+        entries[t] = (uint32_t)e;
+        const uint64_t len = min((uint64_t)T, w1 - s);
+        e = s + len + exit_first[t * A.W + (e - s)];
+    }
+}
+
+static uint32_t a1_sub(uint32_t W)
+{
+    uint32_t T = 2048;
+    while (T < W) T <<= 1;
+    return T;
+}
+
+cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_delta, uint2 *tile_exits, Diag *diag,
+                        cudaStream_t st)
+{
+    (void)diag;
     if (A.n == 0) return cudaSuccess;
     uint64_t blocks = ceil_div(A.n, 256);
     if (blocks > 148ull * 64) blocks = 148ull * 64;
     k_alg1_next<<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
-    k_alg1_chain<<<(unsigned)A.nwin, 256, 0, st>>>(A, next_delta, bitmap);
+    const uint32_t T = a1_sub(A.W);
+    uint32_t K = 0;
+    while ((1u << K) < T) ++K;
+    const uint64_t spw = ceil_div(A.window, T), nt = spw * A.nwin;
+    // scratch inside the Alg. 1 tile area: entries (u32 per sub-tile), exit_first (u16 x W per sub-tile)
+    uint32_t *entries = reinterpret_cast<uint32_t *>(tile_exits);
+    uint16_t *exit_first = reinterpret_cast<uint16_t *>(entries + nt + 1);
+    const size_t smem = ((size_t)K + 1) * T * sizeof(uint16_t);
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_a1_lift<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_a1_lift<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    k_a1_lift<false><<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
+    k_a1_entries<<<(unsigned)ceil_div(A.nwin, 64), 64, 0, st>>>(A, T, spw, exit_first, entries);
+    k_a1_lift<true><<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
     return cudaGetLastError();
 }
+
+// bytes of Alg. 1 scratch: per sub-tile an entry (u32) and W exit offsets (u16)
+uint64_t alg1_scratch_bytes(uint64_t window, uint64_t nwin, uint32_t W)
+{
+    const uint64_t nt = ceil_div(window, a1_sub(W)) * nwin;
+    return 4 * (nt + 1) + 2ull * W * nt + 16;
+}
+
 
 // ---------------------------------------------------------------------------------------
 // Compaction: batch_offsets = ascending positions of the set bits; num_batches = count - 1.

@@ -308,3 +308,9 @@ def test_mode_slo_odbs_large(split):
     inp, out, slo, cfg = W.c3(15, n=300_000, split=split)
     cfg = cfg.replace(mode=W.MODE_SLO_ODBS, w1=1.0, w2=0.02, threshold=900.0, window=70_000, max_batch=128)
     assert_parity(inp, out, slo, cfg)
+
+
+def test_mode_slo_odbs_single_window_many_tiles():
+    inp, out, slo, cfg = W.c2(16, n=250_000)
+    cfg = cfg.replace(mode=W.MODE_SLO_ODBS, w1=1.0, w2=0.05, threshold=400.0, window=0)
+    assert_parity(inp, out, slo, cfg, nthreads=1)
