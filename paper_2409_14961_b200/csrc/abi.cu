@@ -344,7 +344,6 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         P.wincost = at<unsigned long long>(w, L.wincost);
         P.n = (uint32_t)n; P.window = (uint32_t)L.window; P.nwin = (uint32_t)L.nwin;
         P.tile_len = (uint32_t)L.tile_len; P.tpw = (uint32_t)L.tpw; P.W = cfg->max_batch;
-        P.cap_slots = (uint32_t)align_up(cfg->max_batch + 33, 32);
         P.split = cfg->split_on_slo_change;
         P.cap_tok = cap_tok;
         P.t_batch = cfg->t_batch_us; P.t_iter = cfg->t_iter_us; P.t_tok = cfg->t_tok_us;
@@ -355,6 +354,9 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
                            ((u128)cfg->t_tok_us * v.max_out + (u128)cfg->t_prefill_us * v.max_in) * cfg->max_batch;
             P.narrow = (v.max_in < 65536u && v.max_out < 65536u && E < ((u128)1 << 32) && !(cfg->flags & 1u)) ? 1u : 0u;
         }
+        // candidate slots per warp: the blocked path holds at most W live + 32 new candidates; the
+        // generic path at most W + 1 and reads one slot ahead
+        P.cap_slots = (uint32_t)align_up(cfg->max_batch + (P.narrow ? 32 : 33), 32);
         void *ev[3] = {nullptr, nullptr, nullptr};
         for (int k = 0; k < 3; ++k)
             if ((uint64_t)(UELLM_STAGE_DP_LOCAL_END + k) < v.n_events) ev[k] = v.events[UELLM_STAGE_DP_LOCAL_END + k];

@@ -254,12 +254,13 @@ __device__ DpResult dp_warp(const DPParams &P, const WarpSlots &S, uint32_t s, u
 // Fast path ("narrow"): valid when max_in, max_out < 2^16 and
 //   E = t_batch + t_iter*max_out + W*(t_tok*max_out + t_prefill*max_in) < 2^32,
 // so est, S = t_tok*MO + t_prefill*MI, b*S and b*(MI+MO) all fit 32 bits (checked on the host).
-// A candidate slot is 16 bytes: C (i64) and (i | MO << 32 | MI << 48).
+// A candidate slot is 16 bytes, one LDS.128: C (i64) and (i | MO << 32 | MI << 48).
 struct NarrowSlots {
-    long long *cC;
-    unsigned long long *cP;     // i | mo << 32 | mi << 48
-    uint32_t *rmq;              // per-block range-max table, 5 levels x 33 words
+    longlong2 *sl;              // .x = C, .y = i | mo << 32 | mi << 48
+    uint32_t *tri;              // per-block triangular max table M[q][k], q < k < 32 (496 words)
 };
+// offset of row q of the triangular table (row q holds k = q+1 .. 31)
+__host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
 
 __device__ __forceinline__ unsigned long long pack_slot(uint32_t i, uint32_t mo, uint32_t mi)
 {
@@ -271,8 +272,7 @@ struct SlotWriter {            // writes a candidate slot with its derived cost 
     __device__ __forceinline__ void put(const NarrowSlots &S, uint32_t pos, long long C, uint32_t i, uint32_t mo,
                                         uint32_t mi) const
     {
-        S.cC[pos] = C;
-        S.cP[pos] = pack_slot(i, mo, mi);
+        S.sl[pos] = make_longlong2(C, (long long)pack_slot(i, mo, mi));
     }
 };
 
@@ -363,21 +363,33 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         uint32_t wr = 0;
         for (uint32_t r = 0; r * 32 < Lt; ++r) {
             const uint32_t k = r * 32 + lane;
-            const bool valid = k < Lt, has_next = k + 1 < Lt;
-            long long cC = 0, nC = 0;
-            unsigned long long cp = 0, np = 0;
-            if (valid) { cC = S.cC[k]; cp = S.cP[k]; }
-            if (has_next) { nC = S.cC[k + 1]; np = S.cP[k + 1]; }
+            const bool valid = k < Lt;
+            longlong2 sv = make_longlong2(0, 0);
+            if (valid) sv = S.sl[k];
+            const long long cC = sv.x;
+            const unsigned long long cp = (unsigned long long)sv.y;
             const uint32_t ci = (uint32_t)cp;
             uint32_t mo = (uint32_t)(cp >> 32) & 0xffffu, mi = (uint32_t)(cp >> 48);
             if (k < Lold) { mo = max(mo, bmo); mi = max(mi, bmi); }
-            const uint32_t ni = (uint32_t)np;
-            uint32_t nmo = (uint32_t)(np >> 32) & 0xffffu, nmi = (uint32_t)(np >> 48);
-            if (k + 1 < Lold) { nmo = max(nmo, bmo); nmi = max(nmi, bmi); }
             const uint32_t b = jend - ci;
             const bool dead = !valid | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < run_start));
-            const uint32_t nS = t_tok * nmo + t_pre * nmi;
-            const bool dominated = has_next && (nC - cC < (long long)(unsigned long long)((ni - ci) * nS));
+            // D1 against the successors at list distance 1, 8 and 32 (any later candidate is a valid
+            // dominator: strict dominance is transitive and a later candidate outlives an earlier
+            // one, so dropping i needs no dominator to be kept).  (n_i - i) * S < W * S <= E < 2^32.
+            auto dominated_by = [&](uint32_t k2) -> bool {
+                const longlong2 nv = S.sl[k2];
+                const unsigned long long np = (unsigned long long)nv.y;
+                uint32_t nmo = (uint32_t)(np >> 32) & 0xffffu, nmi = (uint32_t)(np >> 48);
+                if (k2 < Lold) { nmo = max(nmo, bmo); nmi = max(nmi, bmi); }
+                const uint32_t nS = t_tok * nmo + t_pre * nmi;
+                return nv.x - cC < (long long)(unsigned long long)(((uint32_t)np - ci) * nS);
+            };
+            bool dominated = false;
+            if (!dead) {
+                if (k + 1 < Lt) dominated = dominated_by(k + 1);
+                if (!dominated && k + 8 < Lt) dominated = dominated_by(k + 8);
+                if (!dominated && k + 32 < Lt) dominated = dominated_by(k + 32);
+            }
             const bool keep = !dead && !dominated;
             __syncwarp();
             const uint32_t bal = __ballot_sync(0xffffffffu, keep);
@@ -419,7 +431,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         // is viol a single comparison.  Crossing intervals exist in this block only if the oldest
         // external candidate starts before the last run start (external), or a run starts inside
         // the block (intra); those rare blocks take the binary-search variant.
-        const bool one_run_ext = (uint32_t)S.cP[0] >= rs_last;     // every candidate and element in one run
+        const bool one_run_ext = (uint32_t)S.sl[0].y >= rs_last;     // every candidate and element in one run
         const bool one_run_intra = rs_last <= j0;                   // every element of the block in one run
         const bool ext_slow = LAM && !split && !one_run_ext;
         const bool intra_slow = LAM && !split && !one_run_intra;
@@ -432,15 +444,16 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         // any interval ending at the lane's element is that element's own: MO = pmo for every
         // candidate and the lane-constant parts of est are computed once.
         const uint32_t A_l = t_b + t_it * pmo, T_l = t_tok * pmo;
-        auto ext_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag) {
+        auto ext_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag, uint32_t c0, uint32_t c1) {
             constexpr bool SLOW = decltype(slow_tag)::value;
             constexpr bool SINGLE_OK = decltype(single_tag)::value;
             constexpr bool ONERUN = decltype(onerun_tag)::value;
 #pragma unroll 2
-            for (uint32_t c = 0; c < L; ++c) {
-                const unsigned long long cp = S.cP[c];
+            for (uint32_t c = c0; c < c1; ++c) {
+                const longlong2 sv = S.sl[c];
+                const unsigned long long cp = (unsigned long long)sv.y;
                 const uint32_t ci = (uint32_t)cp;
-                const long long cC = S.cC[c];
+                const long long cC = sv.x;
                 const uint32_t b = jl - ci;
                 const uint32_t mo = ONERUN ? pmo : max((uint32_t)(cp >> 32) & 0xffffu, pmo);
                 const uint32_t mi = max((uint32_t)(cp >> 48), pmi);
@@ -459,51 +472,95 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
         };
+        // In one SLO run the only deaths are the monotone ones (b > W, KV cap): a candidate alive
+        // at the block-end state (b and maxima largest) is alive for every boundary of the block,
+        // and the candidates dead there form a prefix of the list.  Only that prefix (Pd slots)
+        // needs the feasibility test; the rest take the lean loop.
+        auto ext_lean = [&](uint32_t c0, uint32_t c1) {
+#pragma unroll 4
+            for (uint32_t c = c0; c < c1; ++c) {
+                const longlong2 sv = S.sl[c];
+                const uint32_t ci = (uint32_t)sv.y;
+                const uint32_t b = jl - ci;
+                const uint32_t mi = max((uint32_t)((unsigned long long)sv.y >> 48), pmi);
+                const uint32_t est = A_l + b * (T_l + t_pre * mi);
+                unsigned long long tot = (unsigned long long)sv.x + est;
+                if (LAM) tot += penalty((slo_l < est) ? b : 0u);
+                if (tot < lb) { lb = tot; lbi = ci; }
+            }
+        };
         using T1 = std::true_type;
         using F0 = std::false_type;
         if (ext_slow) {
-            if (single_ok) ext_pass(T1{}, T1{}, F0{}); else ext_pass(T1{}, F0{}, F0{});
+            if (single_ok) ext_pass(T1{}, T1{}, F0{}, 0, L); else ext_pass(T1{}, F0{}, F0{}, 0, L);
         } else if (one_run_ext) {
-            if (single_ok) ext_pass(F0{}, T1{}, T1{}); else ext_pass(F0{}, F0{}, T1{});
+            const uint32_t jend = j0 + B;
+            const uint32_t bmo = __shfl_sync(0xffffffffu, pmo, B - 1), bmi = __shfl_sync(0xffffffffu, pmi, B - 1);
+            uint32_t Pd = 0;
+            for (uint32_t r = 0; r * 32 < L; ++r) {
+                const uint32_t k = r * 32 + lane;
+                bool d = false;
+                if (k < L) {
+                    const unsigned long long cp = (unsigned long long)S.sl[k].y;
+                    const uint32_t ci = (uint32_t)cp, b = jend - ci;
+                    const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, bmo), mi = max((uint32_t)(cp >> 48), bmi);
+                    d = (b > W) | ((b > 1) & (b * (mo + mi) > cap32));
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, d);
+                Pd += __popc(bal);
+                if (bal != 0xffffffffu) break;             // dead slots are a prefix
+            }
+            if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd);
+            ext_lean(Pd, L);
         } else {
-            if (single_ok) ext_pass(F0{}, T1{}, F0{}); else ext_pass(F0{}, F0{}, F0{});
+            if (single_ok) ext_pass(F0{}, T1{}, F0{}, 0, L); else ext_pass(F0{}, F0{}, F0{}, 0, L);
         }
         // ---- 2. intra-block candidates.  Lane = boundary again: the candidate born at boundary
         //      j0+q+1 (final once lane q has seen every older candidate) is broadcast and every
-        //      later lane k evaluates it with the maxima of elements q+1..k, read in O(1) from a
-        //      per-block sparse table of packed (out << 16 | in) maxima.  Candidates arrive in
-        //      ascending i, so the strict '<' keeps the smallest minimising i.
-        uint32_t *T = S.rmq;
+        //      later lane k evaluates it with the maxima of elements q+1..k, one shared load from a
+        //      triangular table M[q][k] of packed (out << 16 | in) maxima built backwards
+        //      (M[q][k] = max(M[q+1][k], element q+1)).  Candidates arrive in ascending i, so the
+        //      strict '<' keeps the smallest minimising i.
+        uint32_t *M = S.tri;
+        const uint32_t pk_l = vl ? ((out_l << 16) | in_l) : 0u;
         {
-            uint32_t cur = vl ? ((out_l << 16) | in_l) : 0u;
-            T[lane] = cur;
+            uint32_t m = pk_l;
 #pragma unroll
-            for (int l = 1; l < 5; ++l) {        // T[l][x] = max over elements x .. x + 2^l - 1
-                cur = __vmaxu2(cur, __shfl_down_sync(0xffffffffu, cur, 1 << (l - 1)));
-                T[l * 33 + lane] = cur;
+            for (int q = 30; q >= 0; --q) {
+                const uint32_t el = __shfl_sync(0xffffffffu, pk_l, q + 1);
+                if ((int)lane > q) { m = __vmaxu2(m, el); M[tri_off(q) + lane - q - 1] = m; }
             }
         }
         __syncwarp();
-        auto rmq = [&](uint32_t a, uint32_t bb) {  // max over elements a .. bb (a <= bb < 32)
-            const uint32_t lv = 31 - __clz(bb - a + 1);
-            return __vmaxu2(T[lv * 33 + a], T[lv * 33 + bb - (1u << lv) + 1]);
-        };
-        auto intra_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag) {
+        // block-end maxima of this lane's own candidate (elements lane+1 .. B-1), reused below
+        const uint32_t mend = (lane + 1 < B) ? M[tri_off(lane) + B - 2 - lane] : 0u;
+        // steps q in [q0, q1); the table offset of (q, lane) advances by 30 - q per step
+        auto intra_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag, auto check_tag, uint32_t q0,
+                              uint32_t q1) {
             constexpr bool SLOW = decltype(slow_tag)::value;
             constexpr bool SINGLE_OK = decltype(single_tag)::value;
             constexpr bool ONERUN = decltype(onerun_tag)::value;
-            for (uint32_t q = 0; q + 1 < B; ++q) {
+            constexpr bool CHECK = decltype(check_tag)::value;
+            uint32_t off = tri_off((int)q0) + lane - q0 - 1;
+#pragma unroll 2
+            for (uint32_t q = q0; q < q1; ++q) {
                 const long long Cq = (long long)__shfl_sync(0xffffffffu, lb, q);
-                const bool act = vl && lane > q;
-                const uint32_t b = act ? lane - q : 1u;          // boundary jl minus candidate j0+1+q
-                const uint32_t m = rmq(act ? q + 1 : lane, lane);
+                const bool act = lane > q;
+                const uint32_t b = lane - q;                     // boundary jl minus candidate j0+1+q
+                const uint32_t m = act ? M[off] : 0u;
+                off += 30 - q;
                 const uint32_t mo = ONERUN ? pmo : m >> 16, mi = m & 0xffffu;
                 const uint32_t ci = j0 + 1 + q;
                 const uint32_t est = ONERUN ? A_l + b * (T_l + t_pre * mi)
                                             : t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
+                unsigned long long tot = (unsigned long long)Cq + est;
+                if (!CHECK) {                                    // alive at the block end: alive here
+                    if (LAM) tot += penalty((slo_l < est) ? b : 0u);
+                    if (act && tot < lb) { lb = tot; lbi = ci; }
+                    continue;
+                }
                 const bool dead = !act | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
                                   (!ONERUN & split & (ci < rs_l));
-                unsigned long long tot = (unsigned long long)Cq + est;
                 if (LAM) {
                     uint32_t v;
                     if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
@@ -514,12 +571,24 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if (!dead && tot < lb) { lb = tot; lbi = ci; }
             }
         };
+        const uint32_t QB = B - 1;                   // intra candidates q = 0 .. B-2
         if (intra_slow) {
-            if (single_ok) intra_pass(T1{}, T1{}, F0{}); else intra_pass(T1{}, F0{}, F0{});
+            if (single_ok) intra_pass(T1{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(T1{}, F0{}, F0{}, T1{}, 0, QB);
         } else if (one_run_intra) {
-            if (single_ok) intra_pass(F0{}, T1{}, T1{}); else intra_pass(F0{}, F0{}, T1{});
+            // deaths inside one run are monotone (b > W, KV cap): candidates dead at the block end
+            // form a prefix q < Qd; the rest need no feasibility test
+            bool dend = false;
+            if (lane + 1 < B) {
+                const uint32_t be = B - 1 - lane, mo_e = mend >> 16, mi_e = mend & 0xffffu;
+                dend = (be > W) | ((be > 1) & (be * (mo_e + mi_e) > cap32));
+            }
+            const uint32_t Qd = __popc(__ballot_sync(0xffffffffu, dend));
+            if (Qd) {
+                if (single_ok) intra_pass(F0{}, T1{}, T1{}, T1{}, 0, Qd); else intra_pass(F0{}, F0{}, T1{}, T1{}, 0, Qd);
+            }
+            intra_pass(F0{}, F0{}, T1{}, F0{}, Qd, QB);
         } else {
-            if (single_ok) intra_pass(F0{}, T1{}, F0{}); else intra_pass(F0{}, F0{}, F0{});
+            if (single_ok) intra_pass(F0{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(F0{}, F0{}, F0{}, T1{}, 0, QB);
         }
         const long long o_C = (long long)lb;
         const long long iC = o_C;
@@ -553,8 +622,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         done = j0 + kdone;
         if (stop) break;
         // maxima of the block's own candidates over [i, block end): elements q+1 .. B-1
-        uint32_t imo = 0, imi = 0;
-        if (lane + 1 < B) { const uint32_t m = rmq(lane + 1, B - 1); imo = m >> 16; imi = m & 0xffffu; }
+        const uint32_t imo = mend >> 16, imi = mend & 0xffffu;
         // ---- 3. extend the list by the block's candidates and prune at the block-end state
         const uint32_t jend = j0 + B;
         const uint32_t bmo = __shfl_sync(0xffffffffu, pmo, B - 1), bmi = __shfl_sync(0xffffffffu, pmi, B - 1);
@@ -584,8 +652,8 @@ __device__ __forceinline__ void tile_bounds(const DPParams &P, uint64_t t, uint3
     e = (uint32_t)min(ss + P.tile_len, w1);
 }
 
-// shared memory per warp: narrow = 16 B slots + the 5 x 33-word range-max table; wide = 20 B slots
-constexpr uint32_t kRmqBytes = 5 * 33 * 4 + 12;    // 672, keeps 16-byte alignment
+// shared memory per warp: narrow = 16 B slots + the 496-word triangular max table; wide = 20 B slots
+constexpr uint32_t kRmqBytes = 496 * 4;            // 1984, keeps 16-byte alignment
 static __host__ __device__ __forceinline__ uint32_t warp_smem_bytes(const DPParams &P)
 {
     return P.narrow ? P.cap_slots * 16 + kRmqBytes : P.cap_slots * 20;
@@ -598,9 +666,8 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
     if (P.narrow) {
         char *p = smem + (size_t)warp * warp_smem_bytes(P);
         NarrowSlots S;
-        S.cC = (long long *)p;
-        S.cP = (unsigned long long *)(p + (size_t)P.cap_slots * 8);
-        S.rmq = (uint32_t *)(p + (size_t)P.cap_slots * 16);
+        S.sl = (longlong2 *)p;
+        S.tri = (uint32_t *)(p + (size_t)P.cap_slots * 16);
         const int lk = P.lambda == 0 ? 0 : (P.lambda < (1ull << 32) ? 1 : 2);
         if (P.split) {
             if (lk == 0) return dp_warp_blocked<FIX, 0, true>(P, S, s, e, src, stop_min);
