@@ -491,12 +491,29 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         };
         using T1 = std::true_type;
         using F0 = std::false_type;
-        if (ext_slow) {
-            if (single_ok) ext_pass(T1{}, T1{}, F0{}, 0, L); else ext_pass(T1{}, F0{}, F0{}, 0, L);
-        } else if (one_run_ext) {
+        // ---- 2. intra-block candidates.  Lane = boundary again: the candidate born at boundary
+        //      j0+q+1 (final once lane q has seen every older candidate) is broadcast and every
+        //      later lane k evaluates it with the maxima of elements q+1..k, one shared load from a
+        //      triangular table M[q][k] of packed (out << 16 | in) maxima built backwards
+        //      (M[q][k] = max(M[q+1][k], element q+1)).  Candidates arrive in ascending i, so the
+        //      strict '<' keeps the smallest minimising i.
+        uint32_t *M = S.tri + 1;                   // S.tri[0] is padding (read by idle lanes)
+        const uint32_t pk_l = vl ? ((out_l << 16) | in_l) : 0u;
+        {
+            uint32_t m = pk_l;
+#pragma unroll
+            for (int q = 30; q >= 0; --q) {
+                const uint32_t el = __shfl_sync(0xffffffffu, pk_l, q + 1);
+                if ((int)lane > q) { m = __vmaxu2(m, el); M[tri_off(q) + lane - q - 1] = m; }
+            }
+        }
+        __syncwarp();
+        // block-end maxima of this lane's own candidate (elements lane+1 .. B-1), reused below
+        const uint32_t mend = (lane + 1 < B) ? M[tri_off(lane) + B - 2 - lane] : 0u;
+        uint32_t Pd = 0;
+        if (one_run_ext) {
             const uint32_t jend = j0 + B;
             const uint32_t bmo = __shfl_sync(0xffffffffu, pmo, B - 1), bmi = __shfl_sync(0xffffffffu, pmi, B - 1);
-            uint32_t Pd = 0;
             for (uint32_t r = 0; r * 32 < L; ++r) {
                 const uint32_t k = r * 32 + lane;
                 bool d = false;
@@ -510,85 +527,134 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 Pd += __popc(bal);
                 if (bal != 0xffffffffu) break;             // dead slots are a prefix
             }
-            if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd);
-            ext_lean(Pd, L);
-        } else {
-            if (single_ok) ext_pass(F0{}, T1{}, F0{}, 0, L); else ext_pass(F0{}, F0{}, F0{}, 0, L);
         }
-        // ---- 2. intra-block candidates.  Lane = boundary again: the candidate born at boundary
-        //      j0+q+1 (final once lane q has seen every older candidate) is broadcast and every
-        //      later lane k evaluates it with the maxima of elements q+1..k, one shared load from a
-        //      triangular table M[q][k] of packed (out << 16 | in) maxima built backwards
-        //      (M[q][k] = max(M[q+1][k], element q+1)).  Candidates arrive in ascending i, so the
-        //      strict '<' keeps the smallest minimising i.
-        uint32_t *M = S.tri;
-        const uint32_t pk_l = vl ? ((out_l << 16) | in_l) : 0u;
-        {
-            uint32_t m = pk_l;
-#pragma unroll
-            for (int q = 30; q >= 0; --q) {
-                const uint32_t el = __shfl_sync(0xffffffffu, pk_l, q + 1);
-                if ((int)lane > q) { m = __vmaxu2(m, el); M[tri_off(q) + lane - q - 1] = m; }
-            }
+        // ---- fast block: one SLO run, no SLO violation possible for any (lane, candidate) and
+        //      every candidate cost within 2^32 of base = C of the oldest live candidate.  C is
+        //      non-decreasing in the boundary (a batch's cost only grows with its members), so
+        //      every C that can win here lies in [base, base + 2^32): costs are compared as 32-bit
+        //      offsets from base (one add, one compare, two selects per candidate).
+        bool fast = false;
+        long long base = 0;
+        if (one_run_ext && one_run_intra && Pd < L) {
+            const longlong2 sP = S.sl[Pd];
+            base = sP.x;
+            const long long cmax = S.sl[L - 1].x;
+            const uint32_t bP = jl - (uint32_t)sP.y;
+            const uint32_t eP = A_l + bP * (T_l + t_pre * max((uint32_t)((unsigned long long)sP.y >> 48), pmi));
+            // eP bounds est of every lean external and every intra candidate of this lane (largest
+            // b and maxima); intra C values are bounded by the lane-(B-2) external minimum
+            const unsigned long long span = (unsigned long long)(cmax - base) + 2ull * eP;
+            const bool ok = !vl || ((!LAM || eP <= slo_l) && span < 0xfffffff0ull);
+            fast = __all_sync(0xffffffffu, ok);
         }
-        __syncwarp();
-        // block-end maxima of this lane's own candidate (elements lane+1 .. B-1), reused below
-        const uint32_t mend = (lane + 1 < B) ? M[tri_off(lane) + B - 2 - lane] : 0u;
-        // steps q in [q0, q1); the table offset of (q, lane) advances by 30 - q per step
-        auto intra_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag, auto check_tag, uint32_t q0,
-                              uint32_t q1) {
-            constexpr bool SLOW = decltype(slow_tag)::value;
-            constexpr bool SINGLE_OK = decltype(single_tag)::value;
-            constexpr bool ONERUN = decltype(onerun_tag)::value;
-            constexpr bool CHECK = decltype(check_tag)::value;
-            uint32_t off = tri_off((int)q0) + lane - q0 - 1;
-#pragma unroll 2
-            for (uint32_t q = q0; q < q1; ++q) {
-                const long long Cq = (long long)__shfl_sync(0xffffffffu, lb, q);
-                const bool act = lane > q;
-                const uint32_t b = lane - q;                     // boundary jl minus candidate j0+1+q
-                const uint32_t m = act ? M[off] : 0u;
-                off += 30 - q;
-                const uint32_t mo = ONERUN ? pmo : m >> 16, mi = m & 0xffffu;
-                const uint32_t ci = j0 + 1 + q;
-                const uint32_t est = ONERUN ? A_l + b * (T_l + t_pre * mi)
-                                            : t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
-                unsigned long long tot = (unsigned long long)Cq + est;
-                if (!CHECK) {                                    // alive at the block end: alive here
-                    if (LAM) tot += penalty((slo_l < est) ? b : 0u);
-                    if (act && tot < lb) { lb = tot; lbi = ci; }
-                    continue;
-                }
-                const bool dead = !act | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
-                                  (!ONERUN & split & (ci < rs_l));
-                if (LAM) {
-                    uint32_t v;
-                    if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
-                                               : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
-                    else v = (slo_l < est) ? b : 0u;
-                    tot += penalty(v);
-                }
-                if (!dead && tot < lb) { lb = tot; lbi = ci; }
+        if (fast) {
+            if (Pd) { if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd); }
+            const uint32_t base_lo = (uint32_t)base;
+            uint32_t r32 = 0xffffffffu, ri = 0xffffffffu;
+#pragma unroll 4
+            for (uint32_t c = Pd; c < L; ++c) {
+                const longlong2 sv = S.sl[c];
+                const uint32_t ci = (uint32_t)sv.y;
+                const uint32_t b = jl - ci;
+                const uint32_t mi = max((uint32_t)((unsigned long long)sv.y >> 48), pmi);
+                const uint32_t tot = ((uint32_t)sv.x - base_lo) + A_l + b * (T_l + t_pre * mi);
+                if (tot < r32) { r32 = tot; ri = ci; }
             }
-        };
-        const uint32_t QB = B - 1;                   // intra candidates q = 0 .. B-2
-        if (intra_slow) {
-            if (single_ok) intra_pass(T1{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(T1{}, F0{}, F0{}, T1{}, 0, QB);
-        } else if (one_run_intra) {
-            // deaths inside one run are monotone (b > W, KV cap): candidates dead at the block end
-            // form a prefix q < Qd; the rest need no feasibility test
+            // the dying prefix (older, wins ties) was evaluated in 64 bits: lb >= C(jl) >= base
+            if (lb <= (unsigned long long)base + r32) { r32 = (uint32_t)(lb - (unsigned long long)base); ri = lbi; }
+            // intra candidates in 32-bit offsets: dead prefix q < Qd checked, the rest lean
             bool dend = false;
             if (lane + 1 < B) {
                 const uint32_t be = B - 1 - lane, mo_e = mend >> 16, mi_e = mend & 0xffffu;
                 dend = (be > W) | ((be > 1) & (be * (mo_e + mi_e) > cap32));
             }
             const uint32_t Qd = __popc(__ballot_sync(0xffffffffu, dend));
-            if (Qd) {
-                if (single_ok) intra_pass(F0{}, T1{}, T1{}, T1{}, 0, Qd); else intra_pass(F0{}, F0{}, T1{}, T1{}, 0, Qd);
+            int off = (int)lane - 1;                 // M[tri_off(q) + lane - q - 1], M[-1] is padding
+            for (uint32_t q = 0; q < Qd; ++q) {
+                const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
+                const uint32_t b = lane - q;
+                const uint32_t mi = M[off] & 0xffffu;
+                off += 30 - (int)q;
+                const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
+                const bool dead = (lane <= q) | (b > W) | ((single_ok | (b > 1)) & (b * (pmo + mi) > cap32));
+                if (!dead && tot < r32) { r32 = tot; ri = j0 + 1 + q; }
             }
-            intra_pass(F0{}, F0{}, T1{}, F0{}, Qd, QB);
+#pragma unroll 4
+            for (uint32_t q = Qd; q + 1 < B; ++q) {
+                const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
+                const uint32_t b = lane - q;
+                const uint32_t mi = M[off] & 0xffffu;
+                off += 30 - (int)q;
+                const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
+                if (lane > q && tot < r32) { r32 = tot; ri = j0 + 1 + q; }
+            }
+            lb = (unsigned long long)base + r32;
+            lbi = ri;
         } else {
-            if (single_ok) intra_pass(F0{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(F0{}, F0{}, F0{}, T1{}, 0, QB);
+                    if (ext_slow) {
+                if (single_ok) ext_pass(T1{}, T1{}, F0{}, 0, L); else ext_pass(T1{}, F0{}, F0{}, 0, L);
+            } else if (one_run_ext) {
+                if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd);
+                ext_lean(Pd, L);
+            } else {
+                if (single_ok) ext_pass(F0{}, T1{}, F0{}, 0, L); else ext_pass(F0{}, F0{}, F0{}, 0, L);
+            }
+            // steps q in [q0, q1); the table offset of (q, lane) advances by 30 - q per step
+            auto intra_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag, auto check_tag, uint32_t q0,
+                                  uint32_t q1) {
+                constexpr bool SLOW = decltype(slow_tag)::value;
+                constexpr bool SINGLE_OK = decltype(single_tag)::value;
+                constexpr bool ONERUN = decltype(onerun_tag)::value;
+                constexpr bool CHECK = decltype(check_tag)::value;
+                uint32_t off = tri_off((int)q0) + lane - q0 - 1;
+    #pragma unroll 2
+                for (uint32_t q = q0; q < q1; ++q) {
+                    const long long Cq = (long long)__shfl_sync(0xffffffffu, lb, q);
+                    const bool act = lane > q;
+                    const uint32_t b = lane - q;                     // boundary jl minus candidate j0+1+q
+                    const uint32_t m = act ? M[off] : 0u;
+                    off += 30 - q;
+                    const uint32_t mo = ONERUN ? pmo : m >> 16, mi = m & 0xffffu;
+                    const uint32_t ci = j0 + 1 + q;
+                    const uint32_t est = ONERUN ? A_l + b * (T_l + t_pre * mi)
+                                                : t_b + t_it * mo + b * (t_tok * mo + t_pre * mi);
+                    unsigned long long tot = (unsigned long long)Cq + est;
+                    if (!CHECK) {                                    // alive at the block end: alive here
+                        if (LAM) tot += penalty((slo_l < est) ? b : 0u);
+                        if (act && tot < lb) { lb = tot; lbi = ci; }
+                        continue;
+                    }
+                    const bool dead = !act | (b > W) | ((SINGLE_OK | (b > 1)) & (b * (mo + mi) > cap32)) |
+                                      (!ONERUN & split & (ci < rs_l));
+                    if (LAM) {
+                        uint32_t v;
+                        if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
+                                                   : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
+                        else v = (slo_l < est) ? b : 0u;
+                        tot += penalty(v);
+                    }
+                    if (!dead && tot < lb) { lb = tot; lbi = ci; }
+                }
+            };
+            const uint32_t QB = B - 1;                   // intra candidates q = 0 .. B-2
+            if (intra_slow) {
+                if (single_ok) intra_pass(T1{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(T1{}, F0{}, F0{}, T1{}, 0, QB);
+            } else if (one_run_intra) {
+                // deaths inside one run are monotone (b > W, KV cap): candidates dead at the block end
+                // form a prefix q < Qd; the rest need no feasibility test
+                bool dend = false;
+                if (lane + 1 < B) {
+                    const uint32_t be = B - 1 - lane, mo_e = mend >> 16, mi_e = mend & 0xffffu;
+                    dend = (be > W) | ((be > 1) & (be * (mo_e + mi_e) > cap32));
+                }
+                const uint32_t Qd = __popc(__ballot_sync(0xffffffffu, dend));
+                if (Qd) {
+                    if (single_ok) intra_pass(F0{}, T1{}, T1{}, T1{}, 0, Qd); else intra_pass(F0{}, F0{}, T1{}, T1{}, 0, Qd);
+                }
+                intra_pass(F0{}, F0{}, T1{}, F0{}, Qd, QB);
+            } else {
+                if (single_ok) intra_pass(F0{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(F0{}, F0{}, F0{}, T1{}, 0, QB);
+            }
         }
         const long long o_C = (long long)lb;
         const long long iC = o_C;
@@ -653,7 +719,7 @@ __device__ __forceinline__ void tile_bounds(const DPParams &P, uint64_t t, uint3
 }
 
 // shared memory per warp: narrow = 16 B slots + the 496-word triangular max table; wide = 20 B slots
-constexpr uint32_t kRmqBytes = 496 * 4;            // 1984, keeps 16-byte alignment
+constexpr uint32_t kRmqBytes = 500 * 4;            // 1 pad word + 496 + 3, keeps 16-byte alignment
 static __host__ __device__ __forceinline__ uint32_t warp_smem_bytes(const DPParams &P)
 {
     return P.narrow ? P.cap_slots * 16 + kRmqBytes : P.cap_slots * 20;
