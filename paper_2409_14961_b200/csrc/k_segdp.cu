@@ -510,33 +510,42 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         __syncwarp();
         // block-end maxima of this lane's own candidate (elements lane+1 .. B-1), reused below
         const uint32_t mend = (lane + 1 < B) ? M[tri_off(lane) + B - 2 - lane] : 0u;
-        uint32_t Pd = 0;
+        // Pd = candidates dead at the block end (a prefix); V = candidates that violate the SLO at
+        // the block's last boundary (also a prefix in one run: est shrinks with i).  In one run all
+        // lanes share the SLO and est grows with the boundary, so candidates >= V violate for no lane.
+        uint32_t Pd = 0, V = 0;
         if (one_run_ext) {
             const uint32_t jend = j0 + B;
             const uint32_t bmo = __shfl_sync(0xffffffffu, pmo, B - 1), bmi = __shfl_sync(0xffffffffu, pmi, B - 1);
+            const uint32_t slo_run = __shfl_sync(0xffffffffu, slo_l, B - 1);
+            const uint32_t A_e = t_b + t_it * bmo, T_e = t_tok * bmo;
             for (uint32_t r = 0; r * 32 < L; ++r) {
                 const uint32_t k = r * 32 + lane;
-                bool d = false;
+                bool d = false, v = false;
                 if (k < L) {
                     const unsigned long long cp = (unsigned long long)S.sl[k].y;
                     const uint32_t ci = (uint32_t)cp, b = jend - ci;
                     const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, bmo), mi = max((uint32_t)(cp >> 48), bmi);
                     d = (b > W) | ((b > 1) & (b * (mo + mi) > cap32));
+                    v = LAM && (d || slo_run < A_e + b * (T_e + t_pre * mi));
                 }
-                const uint32_t bal = __ballot_sync(0xffffffffu, d);
-                Pd += __popc(bal);
-                if (bal != 0xffffffffu) break;             // dead slots are a prefix
+                const uint32_t bd = __ballot_sync(0xffffffffu, d), bv = __ballot_sync(0xffffffffu, v);
+                Pd += __popc(bd);
+                V += __popc(bv);
+                if (bd != 0xffffffffu && bv != 0xffffffffu) break;   // both are prefixes
             }
         }
-        // ---- fast block: one SLO run, no SLO violation possible for any (lane, candidate) and
-        //      every candidate cost within 2^32 of base = C of the oldest live candidate.  C is
-        //      non-decreasing in the boundary (a batch's cost only grows with its members), so
-        //      every C that can win here lies in [base, base + 2^32): costs are compared as 32-bit
-        //      offsets from base (one add, one compare, two selects per candidate).
+        const uint32_t Vs = max(Pd, V);
+        // ---- fast block (one SLO run): candidates from Vs on and all intra candidates violate for
+        //      no lane, so their costs are C + est with C >= base = C of candidate Vs.  C is
+        //      non-decreasing in the boundary (a batch's cost only grows with its members), so when
+        //      every such cost lies within 2^32 of base they are compared as 32-bit offsets (one
+        //      add, one compare, two selects per candidate); the older candidates [0, Vs) are
+        //      evaluated in 64 bits first and merged (they win ties: smaller i).
         bool fast = false;
         long long base = 0;
-        if (one_run_ext && one_run_intra && Pd < L) {
-            const longlong2 sP = S.sl[Pd];
+        if (one_run_ext && one_run_intra && Vs < L) {
+            const longlong2 sP = S.sl[Vs];
             base = sP.x;
             const long long cmax = S.sl[L - 1].x;
             const uint32_t bP = jl - (uint32_t)sP.y;
@@ -544,15 +553,16 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             // eP bounds est of every lean external and every intra candidate of this lane (largest
             // b and maxima); intra C values are bounded by the lane-(B-2) external minimum
             const unsigned long long span = (unsigned long long)(cmax - base) + 2ull * eP;
-            const bool ok = !vl || ((!LAM || eP <= slo_l) && span < 0xfffffff0ull);
+            const bool ok = !vl || span < 0xfffffff0ull;
             fast = __all_sync(0xffffffffu, ok);
         }
         if (fast) {
             if (Pd) { if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd); }
+            if (Vs > Pd) ext_lean(Pd, Vs);             // may violate: 64-bit with the penalty
             const uint32_t base_lo = (uint32_t)base;
             uint32_t r32 = 0xffffffffu, ri = 0xffffffffu;
 #pragma unroll 4
-            for (uint32_t c = Pd; c < L; ++c) {
+            for (uint32_t c = Vs; c < L; ++c) {
                 const longlong2 sv = S.sl[c];
                 const uint32_t ci = (uint32_t)sv.y;
                 const uint32_t b = jl - ci;
@@ -560,7 +570,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 const uint32_t tot = ((uint32_t)sv.x - base_lo) + A_l + b * (T_l + t_pre * mi);
                 if (tot < r32) { r32 = tot; ri = ci; }
             }
-            // the dying prefix (older, wins ties) was evaluated in 64 bits: lb >= C(jl) >= base
+            // the older candidates (win ties) were evaluated in 64 bits: lb >= C(jl) >= base
             if (lb <= (unsigned long long)base + r32) { r32 = (uint32_t)(lb - (unsigned long long)base); ri = lbi; }
             // intra candidates in 32-bit offsets: dead prefix q < Qd checked, the rest lean
             bool dend = false;
