@@ -53,6 +53,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.order = take(4 * N); L.offsets = take(4 * (N + 1));
     L.argx = take(2 * N);
     L.tiles = take(sizeof(TileRec) * (L.ntiles ? L.ntiles : 1));
+    L.tflags = take(4 * (L.ntiles + 2));
     L.bitmap = take(4 * L.nwords); L.wscan = take(4 * L.nwords);
     const uint64_t nblk = ceil_div(L.nwords, kScanBlock) + ceil_div(N, kScanBlock) + 2;
     L.blocksum = take(4 * nblk);
@@ -340,6 +341,7 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         P.Cx = at<long long>(w, L.keys1); P.CFx = at<long long>(w, L.keys2);
         P.argx = at<uint16_t>(w, L.argx);
         P.tiles = at<TileRec>(w, L.tiles);
+        P.tflags = at<uint32_t>(w, L.tflags);
         P.diag = diag;
         P.wincost = at<unsigned long long>(w, L.wincost);
         P.n = (uint32_t)n; P.window = (uint32_t)L.window; P.nwin = (uint32_t)L.nwin;

@@ -85,6 +85,7 @@ struct WsLayout {
     uint64_t order, offsets;                      // internal copies of the schedule
     uint64_t argx;                                // u16 per position
     uint64_t tiles;                               // TileRec[ntiles]
+    uint64_t tflags;                              // u32[ntiles + 2]: local-done flags + 2 work counters
     uint64_t bitmap, wscan, blocksum, blockagg;   // boundary bitmap + scan scratch
     uint64_t st_so, st_pin, st_pout;              // per-batch stats scratch (u64 each)
     uint64_t a1tiles;                             // Alg. 1 chain-walk tile exits (uint2)
@@ -162,6 +163,7 @@ struct DPParams {
     long long *Cx, *CFx;
     uint16_t *argx;
     TileRec *tiles;
+    uint32_t *tflags;                            // [ntiles] local-done flags, then the local / fix-up work counters
     Diag *diag;
     unsigned long long *wincost;
     uint32_t n, window, nwin, tile_len, tpw, W, cap_slots, split;

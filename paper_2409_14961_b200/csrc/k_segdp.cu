@@ -28,6 +28,17 @@
 
 namespace uellm {
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 struct WarpSlots {
     long long *cC;
     uint32_t *ci, *mo, *mi;
@@ -122,16 +133,16 @@ __device__ DpResult dp_warp(const DPParams &P, const WarpSlots &S, uint32_t s, u
             vo = max(vo, cmo); vi = max(vi, cmi);
             if (valid) {
                 uint32_t q = p - i0;
-                S.ci[q] = p; S.mo[q] = vo; S.mi[q] = vi; S.cC[q] = src[p - 1];
+                S.ci[q] = p; S.mo[q] = vo; S.mi[q] = vi; S.cC[q] = __ldcg(src + p - 1);
             }
             cmo = __shfl_sync(0xffffffffu, vo, 31);
             cmi = __shfl_sync(0xffffffffu, vi, 31);
         }
-        if (lane == 0) { S.ci[W - 1] = s; S.mo[W - 1] = 0; S.mi[W - 1] = 0; S.cC[W - 1] = src[s - 1]; }
+        if (lane == 0) { S.ci[W - 1] = s; S.mo[W - 1] = 0; S.mi[W - 1] = 0; S.cC[W - 1] = __ldcg(src + s - 1); }
         L = W;
         run_start = __reduce_max_sync(0xffffffffu, rs);
         prev_slo = __ldg(P.rslo + s - 1);
-        Cprev = src[s - 1];
+        Cprev = __ldcg(src + s - 1);
         d_run = Cprev;          // local C at boundary s is 0
         run = 1;
     }
@@ -344,15 +355,15 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if ((int)lane >= d) { vo = max(vo, to); vi = max(vi, ti); }
             }
             vo = max(vo, cmo); vi = max(vi, cmi);
-            if (valid) SW.put(S, p - i0, src[p - 1], p, vo, vi);
+            if (valid) SW.put(S, p - i0, __ldcg(src + p - 1), p, vo, vi);
             cmo = __shfl_sync(0xffffffffu, vo, 31);
             cmi = __shfl_sync(0xffffffffu, vi, 31);
         }
-        if (lane == 0) SW.put(S, W - 1, src[s - 1], s, 0, 0);
+        if (lane == 0) SW.put(S, W - 1, __ldcg(src + s - 1), s, 0, 0);
         L = W;
         run_start = __reduce_max_sync(0xffffffffu, rs);
         prev_slo = __ldg(rslo + s - 1);
-        d_run = src[s - 1];           // local C at boundary s is 0
+        d_run = __ldcg(src + s - 1);  // local C at boundary s is 0
         run = 1;
     }
     __syncwarp();
@@ -757,45 +768,70 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
     return dp_warp<FIX>(P, slots_for(smem, P.cap_slots, warp), s, e, src, stop_min);
 }
 
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_local(DPParams P, uint64_t ntiles)
+// Local run and fix-up fused in one persistent kernel.  Warps first claim local runs in tile
+// order from one counter; a finished local run is published (flag[t], release).  Once the local
+// runs are all claimed, warps claim fix-ups in tile order from a second counter; the fix-up of
+// tile t waits (acquire) for tile t-1's flag and runs from t-1's local values.  Every claimed
+// local run belongs to a running warp that sets its flag before claiming anything else, so the
+// waits always end; the fix-ups fill the SMs as the local runs drain instead of a second,
+// tail-bound launch.
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_tiles(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
-    const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (t >= ntiles) return;
-    uint32_t s, e, k, w; bool valid;
-    tile_bounds(P, t, s, e, k, w, valid);
     const uint32_t lane = threadIdx.x & 31;
-    if (!valid) {
-        if (lane == 0) { TileRec r = {}; r.valid = 0; P.tiles[t] = r; }
-        return;
+    const int warp = threadIdx.x >> 5;
+    uint32_t *counter = P.tflags + ntiles;          // [0] local runs, [1] fix-ups
+    unsigned long long evals = 0;
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntiles) break;
+        uint32_t s, e, k, w; bool valid;
+        tile_bounds(P, t, s, e, k, w, valid);
+        if (!valid) {
+            if (lane == 0) { TileRec r = {}; r.valid = 0; P.tiles[t] = r; }
+            __syncwarp();
+            __threadfence();
+            if (lane == 0) st_release(P.tflags + t, 1u);
+            continue;
+        }
+        DpResult R = dp_run<false>(P, smem, warp, s, e, nullptr, 0);
+        evals += R.evals;
+        if (lane == 0) {
+            TileRec r = {};
+            r.s = s; r.e = e; r.valid = 1;
+            r.conv = (k == 0); r.conv_pos = s; r.fix_end = s;
+            P.tiles[t] = r;
+        }
+        __syncwarp();
+        __threadfence();
+        if (lane == 0) st_release(P.tflags + t, 1u);
     }
-    DpResult R = dp_run<false>(P, smem, threadIdx.x >> 5, s, e, nullptr, 0);
-    if (lane == 0) {
-        atomicAdd(&P.diag->dp_evals, (unsigned long long)R.evals);
-        TileRec r = {};
-        r.s = s; r.e = e; r.valid = 1;
-        r.conv = (k == 0); r.conv_pos = s; r.fix_end = s;
-        P.tiles[t] = r;
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(counter + 1, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntiles) break;
+        uint32_t s, e, k, w; bool valid;
+        tile_bounds(P, t, s, e, k, w, valid);
+        if (!valid || k == 0) continue;
+        if (lane == 0) {
+            while (ld_acquire(P.tflags + t - 1) == 0u) __nanosleep(64);
+            while (ld_acquire(P.tflags + t) == 0u) __nanosleep(64);
+        }
+        __syncwarp();
+        __threadfence();
+        DpResult F = dp_run<true>(P, smem, warp, s, e, P.Cx, 0);
+        evals += F.evals;
+        if (lane == 0) {
+            TileRec &r = P.tiles[t];
+            r.conv = F.conv; r.conv_pos = F.conv_pos; r.fix_end = F.fix_end; r.delta = F.delta;
+            atomicAdd(&P.diag->fixup_positions, (unsigned long long)F.positions);
+            if (!F.conv) atomicAdd(&P.diag->fixups_unconverged, 1ull);
+        }
     }
-}
-
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_fix(DPParams P, uint64_t ntiles)
-{
-    extern __shared__ __align__(16) char smem[];
-    const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (t >= ntiles) return;
-    uint32_t s, e, k, w; bool valid;
-    tile_bounds(P, t, s, e, k, w, valid);
-    if (!valid || k == 0) return;
-    const uint32_t lane = threadIdx.x & 31;
-    DpResult R = dp_run<true>(P, smem, threadIdx.x >> 5, s, e, P.Cx, 0);
-    if (lane == 0) {
-        TileRec &r = P.tiles[t];
-        r.conv = R.conv; r.conv_pos = R.conv_pos; r.fix_end = R.fix_end; r.delta = R.delta;
-        atomicAdd(&P.diag->fixup_positions, (unsigned long long)R.positions);
-        atomicAdd(&P.diag->dp_evals, (unsigned long long)R.evals);
-        if (!R.conv) atomicAdd(&P.diag->fixups_unconverged, 1ull);
-    }
+    if (lane == 0 && evals) atomicAdd(&P.diag->dp_evals, evals);
 }
 
 // One warp per window: resolve tiles whose predecessor did not converge, compute the frame
@@ -855,14 +891,20 @@ cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void 
     const size_t smem = (size_t)wpc * per;
     const size_t smem1 = (size_t)per;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_dp_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_dp_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_dp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if ((e = cudaFuncSetAttribute(k_dp_cascade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1))) return e;
-    const unsigned blocks = (unsigned)ceil_div(ntiles, wpc);
-    k_dp_local<<<blocks, wpc * 32, smem, st>>>(P, ntiles);
+    int dev = 0, nsm = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dp_tiles, (int)(wpc * 32), smem))) return e;
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t want = ceil_div(ntiles, wpc);
+    const uint64_t cap = (uint64_t)nsm * (uint64_t)per_sm;
+    const unsigned blocks = (unsigned)(want < cap ? want : cap);
+    if ((e = cudaMemsetAsync(P.tflags, 0, 4 * (ntiles + 2), st))) return e;
+    k_dp_tiles<<<blocks, wpc * 32, smem, st>>>(P, ntiles);
     ++*launches;
     if (ev[0]) cudaEventRecord((cudaEvent_t)ev[0], st);
-    if (P.tpw > 1) { k_dp_fix<<<blocks, wpc * 32, smem, st>>>(P, ntiles); ++*launches; }
     if (ev[1]) cudaEventRecord((cudaEvent_t)ev[1], st);
     k_dp_cascade<<<P.nwin, 32, smem1, st>>>(P);
     ++*launches;
