@@ -28,44 +28,50 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
     __syncthreads();
     uint32_t bad = 0, mx_in = 0, mx_out = 0, mx_slo = 0;
     unsigned long long kor = 0, kand = ~0ull;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t iters = ceil_div(n, stride);
-    for (uint64_t it = 0; it < iters; ++it) {
-        const uint64_t k = it * stride + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        const bool v = k < n;
-        uint32_t su = 0;
-        if (v) {
-            uint32_t a = __ldg(in + k), o = __ldg(out + k);
-            bool ok;
-            su = slo_to_us(__ldg(slo + k), ok);
-            if (a == 0) bad |= 1u;
-            if (o == 0) bad |= 2u;
-            if (!ok) bad |= 4u;
-            const unsigned long long key = ((unsigned long long)su << 32) | o;
-            mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
-            kor |= key; kand &= key;
-        }
-        // distinct-SLO collection (warp-deduplicated; stops once the CTA saw > kCtaMax values)
-        const uint32_t cv = __shfl_sync(0xffffffffu, *(volatile uint32_t *)&cover, 0);
-        if (!cv) {
-            const uint32_t act = __ballot_sync(0xffffffffu, v && su != 0);
-            if (v && su != 0) {
-                const uint32_t peers = __match_any_sync(act, su);
-                if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
-                    uint32_t h = slo_hash(su, kCtaBits);
-                    for (uint32_t probe = 0; probe < kCtaSlots; ++probe) {
-                        const uint32_t old = atomicCAS(&cset[h], 0u, su);
-                        if (old == 0u) {
-                            if (atomicAdd(&ccount, 1u) + 1 > kCtaMax) cover = 1;
-                            break;
-                        }
-                        if (old == su) break;
-                        h = (h + 1) & (kCtaSlots - 1);
-                    }
-                }
+    // distinct-SLO collection: a read-only probe first (class-valued SLOs hit at once), the CAS
+    // insert only on a miss; stops once the CTA saw more than kCtaMax values
+    auto consume = [&](uint32_t a, uint32_t o, float sf, bool cv) {
+        bool ok;
+        const uint32_t su = slo_to_us(sf, ok);
+        if (a == 0) bad |= 1u;
+        if (o == 0) bad |= 2u;
+        if (!ok) bad |= 4u;
+        const unsigned long long key = ((unsigned long long)su << 32) | o;
+        mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
+        kor |= key; kand &= key;
+        if (cv || su == 0) return;
+        uint32_t h = slo_hash(su, kCtaBits);
+        if (((volatile uint32_t *)cset)[h] == su) return;
+        for (uint32_t probe = 0; probe < kCtaSlots; ++probe) {
+            const uint32_t old = atomicCAS(&cset[h], 0u, su);
+            if (old == 0u) {
+                if (atomicAdd(&ccount, 1u) + 1 > kCtaMax) cover = 1;
+                break;
             }
+            if (old == su) break;
+            h = (h + 1) & (kCtaSlots - 1);
         }
+    };
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t head = 0;                          // elements handled by the vector loop
+    if ((((uintptr_t)in | (uintptr_t)out | (uintptr_t)slo) & 15u) == 0) {
+        const uint64_t n4 = n / 4;
+        const uint4 *in4 = reinterpret_cast<const uint4 *>(in), *out4 = reinterpret_cast<const uint4 *>(out);
+        const float4 *slo4 = reinterpret_cast<const float4 *>(slo);
+        for (uint64_t g = tid; g < n4; g += stride) {
+            const uint4 a = __ldg(in4 + g), o = __ldg(out4 + g);
+            const float4 f = __ldg(slo4 + g);
+            const bool cv = *(volatile uint32_t *)&cover;
+            consume(a.x, o.x, f.x, cv);
+            consume(a.y, o.y, f.y, cv);
+            consume(a.z, o.z, f.z, cv);
+            consume(a.w, o.w, f.w, cv);
+        }
+        head = n4 * 4;
     }
+    for (uint64_t k = head + tid; k < n; k += stride)
+        consume(__ldg(in + k), __ldg(out + k), __ldg(slo + k), *(volatile uint32_t *)&cover);
     // warp reductions, one atomic per warp
     for (int d = 16; d; d >>= 1) {
         bad |= __shfl_xor_sync(0xffffffffu, bad, d);

@@ -61,32 +61,58 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ 
     if (tid < 256) hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
 }
 
-__global__ void __launch_bounds__(256) k_sort_scan(uint32_t *__restrict__ hist, uint64_t n,
-                                                   uint64_t window, uint64_t tpw)
+// 1024 threads per window: thread (g, d) owns digit d of the g-th quarter of the window's tiles.
+// Column loads are issued 8 at a time (independent), so the pass is bandwidth- not latency-bound.
+constexpr int kScanGroups = 4;
+__global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__restrict__ hist, uint64_t n,
+                                                                 uint64_t window, uint64_t tpw)
 {
+    __shared__ uint32_t gs[kScanGroups][256];
     __shared__ uint32_t s[256];
     const uint64_t w = blockIdx.x;
-    const int d = threadIdx.x;
+    const int d = threadIdx.x & 255, g = threadIdx.x >> 8;
     const uint64_t w0 = w * window;
     const uint64_t L = min(window, n - w0);
-    const uint64_t ntl = ceil_div(L, kSortTile);
-    uint32_t run = 0;
-    for (uint64_t k = 0; k < ntl; ++k) {
-        uint32_t *c = hist + (w * tpw + k) * 256 + d;
-        uint32_t v = *c;
-        *c = run;
-        run += v;
+    const uint32_t ntl = (uint32_t)ceil_div(L, kSortTile);
+    const uint32_t per = (ntl + kScanGroups - 1) / kScanGroups;
+    const uint32_t k0 = min(ntl, g * per), k1 = min(ntl, k0 + per);
+    uint32_t *col = hist + (w * tpw) * 256 + d;
+    uint32_t sum = 0;
+    uint32_t k = k0;
+    for (; k + 8 <= k1; k += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = col[(uint64_t)(k + u) * 256];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += v[u];
     }
-    s[d] = run;
+    for (; k < k1; ++k) sum += col[(uint64_t)k * 256];
+    gs[g][d] = sum;
+    __syncthreads();
+    if (g == 0) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < kScanGroups; ++q) tot += gs[q][d];
+        s[d] = tot;
+    }
     __syncthreads();
     for (int off = 1; off < 256; off <<= 1) {   // Hillis-Steele inclusive scan over digits
-        uint32_t v = d >= off ? s[d - off] : 0;
+        uint32_t v = 0;
+        if (g == 0 && d >= off) v = s[d - off];
         __syncthreads();
-        s[d] += v;
+        if (g == 0) s[d] += v;
         __syncthreads();
     }
-    const uint32_t base = (uint32_t)w0 + s[d] - run;
-    for (uint64_t k = 0; k < ntl; ++k) hist[(w * tpw + k) * 256 + d] += base;
+    uint32_t run = (uint32_t)w0 + (d ? s[d - 1] : 0u);
+    for (int q = 0; q < g; ++q) run += gs[q][d];
+    for (k = k0; k + 8 <= k1; k += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = col[(uint64_t)(k + u) * 256];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { col[(uint64_t)(k + u) * 256] = run; run += v[u]; }
+    }
+    for (; k < k1; ++k) { const uint32_t v = col[(uint64_t)k * 256]; col[(uint64_t)k * 256] = run; run += v; }
 }
 
 template <class K, bool DECODE>
@@ -215,7 +241,7 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
         if (!(hist0_ready && *passes == 0))
             k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
-        k_sort_scan<<<(unsigned)nwin, 256, 0, st>>>(hist, n, window, tpw);
+        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hist, n, window, tpw);
         const size_t stage = kSortTile * (sizeof(K) + sizeof(uint32_t));
         if (dec && d == last) {
             cudaFuncSetAttribute(k_sort_down<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
