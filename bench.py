@@ -270,9 +270,9 @@ def main():
         per_eval = ncu_summary().get("dp_warp_inst_per_eval", DP_WARP_INST_PER_EVAL)
         achieved = evals * per_eval / (st_ms["dp_local"] / 1e3) / 1e12
         peak = SMS * ISSUE_PER_SM * sm_max * 1e6 / 1e12
-        roof = {"bound": "alu", "kernel": "k_dp_local", "achieved": achieved,
+        roof = {"bound": "alu", "kernel": "k_dp_tiles", "achieved": achieved,
                 "peak": peak, "unit": "T warp-instr/s", "frac": achieved / peak,
-                "traffic": ncu_traffic("k_dp_local"),
+                "traffic": ncu_traffic("k_dp_tiles"),
                 "work": f"{evals} candidate evaluations ({evals / n:.1f} per query) x {per_eval:.3f} "
                         f"warp instructions each (ncu inst_executed / evaluations)",
                 "peak_source": f"{SMS} SMs x {ISSUE_PER_SM} issue slots/clk x {sm_max:.0f} MHz "
@@ -343,7 +343,9 @@ def main():
                        "l2": "inputs 1.2 GB/rank >> 126 MB L2; no flush needed",
                        "parallelism": f"{world} rank(s), windows independent, one allgather of totals"},
             "roofline": roof, "step_hbm_roofline": step_hbm, "stage_ms": st_ms,
-            "gpu_launches": int(diag["sched_launches"] + diag["stats_launches"] + 1),
+            # our kernels launched inside the timed region: K steps x (load + schedule + stats)
+            "gpu_launches": K * int(diag["sched_launches"] + diag["stats_launches"] + 1),
+            "gpu_launches_per_step": int(diag["sched_launches"] + diag["stats_launches"] + 1),
             "diagnostics": diag, "batches": m, "dp_cost": res["totals"]["dp_cost"],
             "job_totals": ({k: v for k, v in combine_totals(gather_buf.view(world, GATHER_WORDS)).items()
                             if k in ("n", "batches", "dp_cost", "viol_alone")} if world > 1 else None),

@@ -79,7 +79,7 @@ def main():
     summ = {"round": a.tag, "source": f"ncu --set full --clock-control none; {os.path.basename(a.rep)}; "
                                      "bench.py c4 (1e8 queries, seed 0), one step",
             "dp_candidate_evals_c4_seed0": evals,
-            "dp_warp_inst_per_eval": K["k_dp_local"]["inst_executed"] / evals, "kernels": K}
+            "dp_warp_inst_per_eval": K["k_dp_tiles"]["inst_executed"] / evals, "kernels": K}
     json.dump(summ, open(os.path.join(HERE, "ncu_summary.json"), "w"), indent=1)
     md = [f"# {a.tag} ncu summary (B200, c4 = 10^8 queries, one step)", "",
           f"Bench line of the same code: {bench['value']:.3e} q/s, {bench['ms_per_step']:.2f} ms/step "
@@ -90,7 +90,7 @@ def main():
         md.append(f"| {k} | {v['duration_ms']:.3f} | {v['dram_read_bytes'] / 1e9:.3f} | "
                   f"{v['dram_write_bytes'] / 1e9:.3f} | {v['dram_gbs']:.0f} | {v['issue_active_pct']:.1f} | "
                   f"{v['warps_active_pct']:.1f} | {v['registers']} |")
-    md += ["", f"SEG-DP: {K['k_dp_local']['inst_executed'] / 1e8:.1f} warp instructions per query, "
+    md += ["", f"SEG-DP: {K['k_dp_tiles']['inst_executed'] / 1e8:.1f} warp instructions per query, "
                f"{summ['dp_warp_inst_per_eval']:.3f} per candidate evaluation ({evals / 1e8:.1f} evaluations per query)."]
     open(os.path.join(HERE, f"{a.tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md))
