@@ -163,6 +163,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override query count (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sim", action="store_true", help="skip the NEXT f2 simulator timing")
     ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
     ap.add_argument("--mode", default="seg_dp", choices=["seg_dp", "slo_odbs", "fifo", "sort_only"],
                     help="segmentation mode (default: the SEG-DP hot path)")
@@ -328,6 +329,34 @@ def main():
                "ms_per_step": float(te.item())}
         assert mh == m, "host-buffer path disagrees with the device path"
 
+    # NEXT f2: the sequential-execution simulator over this step's schedule, timed on its own
+    # (not part of the a1-a9 step): Poisson arrivals resident in HBM, per-batch ends and
+    # per-query latencies written
+    next_rows = {}
+    if not args.no_sim:
+        import workloads as W
+        arr = W.poisson_arrivals(n, rank, W.MEAN_GAP_US.get(args.config, 21_000))
+        d_arr = torch.from_numpy(arr.view(np.int64)).to(dev)
+        for _ in range(max(Wm, 1)):
+            g.simulate(d_arr, stream)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(K):
+            g.simulate(d_arr, stream)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        sim_ms = s0.elapsed_time(s1) / K
+        sim = g.sim_results()["totals"]
+        alg_b = 32 * n + 12 * m          # arrival 8 + order/in/out/slo 4 each + latency 8 per query; offsets 4 + end 8 per batch
+        next_rows["f2_simulate"] = {
+            "ms": sim_ms, "queries_per_s": n / (sim_ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": alg_b / (sim_ms / 1e3) / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                         "frac": alg_b / (sim_ms / 1e3) / 1e9 / hbm_gbs, "algorithmic_bytes": alg_b},
+            "arrivals": f"Poisson, mean gap {W.MEAN_GAP_US.get(args.config, 21_000)} us",
+            "totals": {k: sim[k] for k in ("makespan_us", "idle_us", "viol", "mean_latency_s",
+                                            "slo_violation_rate", "utilization", "throughput_tok_s")}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
@@ -349,7 +378,7 @@ def main():
             "diagnostics": diag, "batches": m, "dp_cost": res["totals"]["dp_cost"],
             "job_totals": ({k: v for k, v in combine_totals(gather_buf.view(world, GATHER_WORDS)).items()
                             if k in ("n", "batches", "dp_cost", "viol_alone")} if world > 1 else None),
-            "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "next_rows": next_rows,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -178,7 +178,8 @@ typedef struct {
 
 /* ABI version (UELLM_ABI_VERSION) and struct sizes, for bindings to check their layouts. [host] */
 uint32_t uellm_abi_version(void);
-uint64_t uellm_sizeof(int which);   /* 0 config, 1 batch_stat, 2 totals, 3 profile, 4 diagnostics */
+uint64_t uellm_sizeof(int which);   /* 0 config, 1 batch_stat, 2 totals, 3 profile, 4 diagnostics,
+                                       5 sim_totals */
 
 /* Human-readable name of a status code.  [host]  Never NULL; static storage. */
 const char *uellm_status_string(uellm_status s);
@@ -229,6 +230,49 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
 uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg,
                                const uint32_t *batch_offsets, const uint64_t *num_batches,
                                uellm_batch_stat *per_batch, uellm_totals *totals, void *stream);
+
+/* Totals of a simulated execution (uellm_simulate, NEXT f2). */
+typedef struct {
+    uint64_t n, batches;
+    uint64_t makespan_us;           /* end of the last batch; the timeline starts at 0             */
+    uint64_t busy_us;               /* sum of est_us                                        */
+    uint64_t idle_us;               /* makespan_us - busy_us: waits for arrivals            */
+    uint64_t gen_tokens;            /* sum b x O                                            */
+    uint64_t viol;                  /* queries with latency_us > slo_us                     */
+    uint64_t latency_max_us;
+    uint64_t latency_sum_lo, latency_sum_hi;   /* exact 128-bit sum of latencies (us)           */
+    double mean_latency_s;          /* latency sum / n * 1e-6 ("Latency")                     */
+    double slo_violation_rate;      /* viol / n                                      */
+    double utilization;             /* busy_us / makespan_us                                */
+    double throughput_tok_s;        /* gen_tokens / (makespan_us * 1e-6)                    */
+    uint32_t status;                /* UELLM_OK, or UELLM_ERR_OVERFLOW if some batch end reached
+                                       2^63 us (all other fields are then unspecified)            */
+    uint32_t pad;
+} uellm_sim_totals;
+
+/* Sequential execution of a schedule on one replica with query arrivals (NEXT f2; PAPER.md
+ * P:499 metrics, R19).  Batches run one after another in scan order
+ * (windows ascending, then batch order) on one continuous timeline that starts at 0:
+ *     start_t = max(end_{t-1}, max_{k in batch t} arrival_us[k])   ("a batch cannot start
+ *               before the latest arrival among its members"), end_{-1} = 0,
+ *     end_t   = start_t + est_us(t)                                 (service model R7),
+ *     latency_k = end_{t(k)} - arrival_us[k], violation iff latency_k > slo_us[k].
+ *   p, cfg         as for uellm_batch_stats; the schedule of the last uellm_schedule_batches.
+ *   arrival_us     [host|device] n x u64, arrival time of caller query k in microseconds
+ *                  (any order; values < 2^63).  Host arrays are staged through the workspace.
+ *   order, batch_offsets, num_batches
+ *                  [host|device] that schedule call's outputs (host pointers: only when that call
+ *                  returned them to host memory; the workspace copies are read).
+ *   batch_end_us   [device] capacity num_batches x u64 (end_t), or NULL.
+ *   latency_us     [device] n x u64 indexed by CALLER index, or NULL.
+ *   totals         [host|device] 1 x uellm_sim_totals.
+ * Integer results are exact; the doubles are formed once from exact integer sums.  Overflow of
+ * the 2^63-us timeline is reported in totals->status (the call itself does not synchronise
+ * unless totals is a host pointer). */
+uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, const uint64_t *arrival_us,
+                            const uint32_t *order, const uint32_t *batch_offsets,
+                            const uint64_t *num_batches, uint64_t *batch_end_us, uint64_t *latency_us,
+                            uellm_sim_totals *totals, void *stream);
 
 /* Attach (n <= UELLM_STAGE_COUNT) caller-owned cudaEvent_t handles (void*, created with timing
  * enabled; NULL entries are skipped) to the profile; subsequent schedule/stats calls record

@@ -63,6 +63,19 @@ class OrcTotals(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class OrcSimTotals(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("n", "batches", "makespan_us", "busy_us", "idle_us",
+                                          "gen_tokens", "viol", "latency_max_us",
+                                          "latency_sum_lo", "latency_sum_hi")] + \
+               [(k, C.c_double) for k in ("mean_latency_s", "slo_violation_rate", "utilization",
+                                          "throughput_tok_s")]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["latency_sum_us"] = d["latency_sum_lo"] + (d["latency_sum_hi"] << 64)
+        return d
+
+
 _lib = None
 
 
@@ -80,11 +93,17 @@ def lib():
                                       C.c_int]
         _lib.orc_stats.argtypes = [C.c_uint64, u32p, u32p, f32p, C.POINTER(OrcConfig),
                                    u32p, u32p, C.c_uint64, C.c_void_p, C.POINTER(OrcTotals)]
-        for f in ("orc_sizeof_config", "orc_sizeof_batch_stat", "orc_sizeof_totals"):
+        u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+        _lib.orc_simulate.argtypes = [C.c_uint64, u32p, u32p, f32p, C.POINTER(OrcConfig),
+                                      u32p, u32p, C.c_uint64, u64p, C.c_void_p, C.c_void_p,
+                                      C.POINTER(OrcSimTotals)]
+        for f in ("orc_sizeof_config", "orc_sizeof_batch_stat", "orc_sizeof_totals",
+                  "orc_sizeof_sim_totals"):
             getattr(_lib, f).restype = C.c_uint64
         assert _lib.orc_sizeof_config() == C.sizeof(OrcConfig)
         assert _lib.orc_sizeof_batch_stat() == BATCH_STAT_DTYPE.itemsize
         assert _lib.orc_sizeof_totals() == C.sizeof(OrcTotals)
+        assert _lib.orc_sizeof_sim_totals() == C.sizeof(OrcSimTotals)
     return _lib
 
 
@@ -153,3 +172,29 @@ def stats(inp, out, slo, cfg, order, offsets):
     if st:
         raise OracleError(st, "stats")
     return pb[:m], tot.as_dict()
+
+
+def simulate(inp, out, slo, cfg, order, offsets, arrival_us):
+    """O8 (NEXT f2): sequential execution with arrivals -> (batch_end u64[m], latency u64[n]
+    by caller index, totals dict)."""
+    inp, out, slo = _arrays(inp, out, slo)
+    n = inp.shape[0]
+    order = np.ascontiguousarray(order, np.uint32)
+    offsets = np.ascontiguousarray(offsets, np.uint32)
+    arr = np.ascontiguousarray(arrival_us, np.uint64)
+    m = offsets.shape[0] - 1
+    ends = np.zeros(max(m, 1), np.uint64)
+    lat = np.zeros(max(n, 1), np.uint64)
+    tot = OrcSimTotals()
+    c = to_config(cfg)
+    if n == 0:
+        order = np.zeros(1, np.uint32)
+        inp = out = np.zeros(1, np.uint32)
+        slo = np.zeros(1, np.float32)
+        arr = np.zeros(1, np.uint64)
+    st = lib().orc_simulate(n, inp, out, slo, C.byref(c), order, offsets, m, arr,
+                            ends.ctypes.data_as(C.c_void_p), lat.ctypes.data_as(C.c_void_p),
+                            C.byref(tot))
+    if st:
+        raise OracleError(st, "simulate")
+    return ends[:m], lat[:n], tot.as_dict()

@@ -20,6 +20,9 @@
  *                       O5   Alg. 1 SLO-ODBS, literal (R1-R5)
  *                       O6   FIFO baseline
  *   orc_stats           O7   per-batch padding / tokens / KV / latency stats
+ *   orc_simulate        O8   sequential execution of a schedule with arrivals
+ *                            (NEXT f2; latency, SLO violations, utilisation,
+ *                            throughput)
  *
  * Parity pins (tests/test_oracle_*.py, -m "not gpu"): brute-force enumeration of all
  * 2^(n-1) segmentations (n <= 12), closed forms (identical queries), special cases
@@ -484,7 +487,82 @@ int orc_stats(uint64_t n, const uint32_t *in, const uint32_t *out, const float *
     return ORC_OK;
 }
 
+
+/* ======================================================================== */
+/* O8  sequential-execution simulator with arrivals (NEXT f2; R19).
+ * P:499 names the paper's metrics (latency = "time taken for the system to respond", SLO
+ * violation, GPU utilisation, throughput); S:445-457 fixes the execution model:
+ *   - batches execute sequentially on one replica, in scan order (windows ascending,
+ *     P:245), the service time of batch t is est_us(t) (R7);
+ *   - "a batch cannot start before the latest arrival among its members":
+ *         start_t = max(end_{t-1}, max_{k in t} arrival_k),   end_{-1} = 0,
+ *         end_t   = start_t + est_us(t);
+ *   - latency_k = end_{t(k)} - arrival_k; a violation is latency_k > slo_us_k
+ *     ("latency > slo");
+ *   - makespan = end of the last batch (the timeline starts at 0), busy = sum est,
+ *     idle = makespan - busy (S:471 work conservation), utilisation = busy / makespan,
+ *     throughput = sum b*O / makespan.
+ * One continuous timeline over all windows of the call.  Integers are exact; a batch end at
+ * or beyond 2^63 us is an overflow error (the limit include/uellm.h states); the four doubles
+ * are formed once at the end.                                                              */
+typedef struct {
+    uint64_t n, batches, makespan_us, busy_us, idle_us, gen_tokens, viol, latency_max_us;
+    uint64_t latency_sum_lo, latency_sum_hi;      /* exact 128-bit sum of latencies (us) */
+    double   mean_latency_s, slo_violation_rate, utilization, throughput_tok_s;
+} orc_sim_totals;
+
+int orc_simulate(uint64_t n, const uint32_t *in, const uint32_t *out, const float *slo_s,
+                 const orc_config *cfg, const uint32_t *order, const uint32_t *offsets,
+                 uint64_t m, const uint64_t *arrival_us, uint64_t *batch_end_us,
+                 uint64_t *latency_us, orc_sim_totals *tot)
+{
+    if (!cfg || !tot) return ORC_ERR_ARG;
+    if (n > 0 && (!in || !out || !slo_s || !order || !offsets || !arrival_us)) return ORC_ERR_ARG;
+    memset(tot, 0, sizeof *tot);
+    tot->n = n;
+    tot->batches = m;
+    if (n == 0) return ORC_OK;
+    uint64_t end = 0;                       /* end_{t-1}; the server is free from time 0 */
+    unsigned __int128 lat_sum = 0;
+    for (uint64_t t = 0; t < m; ++t) {
+        uint64_t a = offsets[t], z = offsets[t + 1];
+        if (z <= a || z > n) return ORC_ERR_ARG;
+        uint64_t b = z - a, s = 0, O = 0, last_arrival = 0, e;
+        for (uint64_t k = a; k < z; ++k) {
+            uint32_t x = order[k];
+            if (in[x] > s) s = in[x];
+            if (out[x] > O) O = out[x];
+            if (arrival_us[x] > last_arrival) last_arrival = arrival_us[x];
+        }
+        if (est_us(cfg, b, s, O, &e) != ORC_OK) return ORC_ERR_OVERFLOW;
+        uint64_t start = end > last_arrival ? end : last_arrival;
+        tot->idle_us += start - end;
+        if (__builtin_add_overflow(start, e, &end) || end >= (1ull << 63)) return ORC_ERR_OVERFLOW;
+        if (batch_end_us) batch_end_us[t] = end;
+        tot->busy_us += e;
+        tot->gen_tokens += b * O;
+        for (uint64_t k = a; k < z; ++k) {
+            uint32_t x = order[k], su;
+            if (orc_slo_us(slo_s[x], &su) != ORC_OK) return ORC_ERR_CONTRACT;
+            uint64_t lat = end - arrival_us[x];
+            if (latency_us) latency_us[x] = lat;
+            if (lat > su) tot->viol++;
+            if (lat > tot->latency_max_us) tot->latency_max_us = lat;
+            lat_sum += lat;
+        }
+    }
+    tot->makespan_us = end;
+    tot->latency_sum_lo = (uint64_t)lat_sum;
+    tot->latency_sum_hi = (uint64_t)(lat_sum >> 64);
+    tot->mean_latency_s = (double)lat_sum / (double)n * 1e-6;
+    tot->slo_violation_rate = (double)tot->viol / (double)n;
+    tot->utilization = end ? (double)tot->busy_us / (double)end : 0.0;
+    tot->throughput_tok_s = end ? (double)tot->gen_tokens / ((double)end * 1e-6) : 0.0;
+    return ORC_OK;
+}
+
 /* ABI self-description for the Python side (sizes checked by tests). */
 uint64_t orc_sizeof_config(void) { return sizeof(orc_config); }
 uint64_t orc_sizeof_batch_stat(void) { return sizeof(orc_batch_stat); }
 uint64_t orc_sizeof_totals(void) { return sizeof(orc_totals); }
+uint64_t orc_sizeof_sim_totals(void) { return sizeof(orc_sim_totals); }

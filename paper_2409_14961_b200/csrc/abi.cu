@@ -64,6 +64,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.meta = take(sizeof(LoadMeta)); L.diag = take(sizeof(Diag)); L.acc = take(sizeof(StatAcc));
     L.nb = take(8); L.totals = take(sizeof(uellm_totals));
     L.wincost = take(8 * (L.nwin ? L.nwin : 1));
+    L.simacc = take(sizeof(SimAcc)); L.simtot = take(sizeof(uellm_sim_totals));
     L.total = off;
     return L;
 }
@@ -132,6 +133,7 @@ uint64_t uellm_sizeof(int which)
     case 2: return sizeof(uellm_totals);
     case 3: return sizeof(uellm_profile);
     case 4: return sizeof(uellm_diagnostics);
+    case 5: return sizeof(uellm_sim_totals);
     default: return 0;
     }
 }
@@ -449,6 +451,64 @@ uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg, 
     }
     if (!dev_tot) {
         CU(cudaMemcpyAsync(totals, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    return UELLM_OK;
+}
+
+uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, const uint64_t *arrival_us,
+                            const uint32_t *order, const uint32_t *batch_offsets, const uint64_t *num_batches,
+                            uint64_t *batch_end_us, uint64_t *latency_us, uellm_sim_totals *totals, void *stream)
+{
+    if (!p || !cfg || !totals || !batch_offsets || !num_batches) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
+    uellm_status s = check_config(cfg);
+    if (s != UELLM_OK) return s;
+    const uint64_t n = v.n;
+    if (n > 0 && (!arrival_us || !order)) return UELLM_ERR_ARG;
+    if ((batch_end_us && !is_device_ptr(batch_end_us)) || (latency_us && !is_device_ptr(latency_us)))
+        return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = v.ws;
+    const WsLayout L = make_layout(n, *cfg);
+    if (L.total > v.ws_bytes) return UELLM_ERR_ARG;
+    const bool dev_tot = is_device_ptr(totals);
+    SimParams S;
+    std::memset(&S, 0, sizeof S);
+    if (n > 0) {
+        const unsigned long long *arr = (const unsigned long long *)arrival_us;
+        if (!is_device_ptr(arrival_us)) {
+            // host arrivals: staged through keys2 (free scratch once the schedule is done)
+            CU(cudaMemcpyAsync(at<unsigned long long>(w, L.keys2), arrival_us, 8 * n, cudaMemcpyHostToDevice, st));
+            arr = at<unsigned long long>(w, L.keys2);
+        }
+        S.arrival = arr;
+        S.order = is_device_ptr(order) ? order : at<uint32_t>(w, L.order);
+        S.offsets = is_device_ptr(batch_offsets) ? batch_offsets : at<uint32_t>(w, L.offsets);
+        S.num_batches = is_device_ptr(num_batches) ? (const unsigned long long *)num_batches
+                                                   : at<unsigned long long>(w, L.nb);
+    } else {
+        S.num_batches = at<unsigned long long>(w, L.nb);
+        CU(cudaMemsetAsync(at<unsigned long long>(w, L.nb), 0, 8, st));
+    }
+    S.rin = at<uint32_t>(w, L.rin); S.rout = at<uint32_t>(w, L.rout); S.rslo = at<uint32_t>(w, L.rslo);
+    S.est = at<unsigned long long>(w, L.st_so);
+    S.inc_a = at<unsigned long long>(w, L.st_pin);
+    S.inc_b = at<unsigned long long>(w, L.st_pout);
+    const uint64_t nch = ceil_div(n ? n : 1, kScanBlock);
+    S.chunk_a = at<unsigned long long>(w, L.keys1);
+    S.chunk_b = S.chunk_a + nch;
+    S.carry = S.chunk_b + nch;
+    S.batch_end = (unsigned long long *)batch_end_us;
+    S.latency = (unsigned long long *)latency_us;
+    S.acc = at<SimAcc>(w, L.simacc);
+    S.totals = dev_tot ? totals : at<uellm_sim_totals>(w, L.simtot);
+    S.n = n; S.n_cap = n;
+    S.t_batch = cfg->t_batch_us; S.t_iter = cfg->t_iter_us; S.t_tok = cfg->t_tok_us; S.t_pre = cfg->t_prefill_us;
+    CU(run_simulate(S, st, nullptr));
+    if (!dev_tot) {
+        CU(cudaMemcpyAsync(totals, S.totals, sizeof(uellm_sim_totals), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }
     return UELLM_OK;

@@ -72,6 +72,11 @@ struct StatAcc {
         makespan, lat_lo, lat_hi, batches;
 };
 
+// Accumulators of uellm_simulate (exact 128-bit latency sum).
+struct SimAcc {
+    unsigned long long busy, gen, viol, lat_max, lat_lo, lat_hi, makespan, pad;
+};
+
 // --------------------------------------------------------------------------------------
 // Workspace layout (byte offsets from the workspace base, 256-B aligned).
 struct WsLayout {
@@ -91,6 +96,7 @@ struct WsLayout {
     uint64_t a1tiles;                             // Alg. 1 chain-walk tile exits (uint2)
     uint64_t hist;                                // u32[sort_tiles * 256]
     uint64_t meta, diag, acc, nb, totals, wincost;
+    uint64_t simacc, simtot;                      // uellm_simulate accumulators / host-totals staging
     uint64_t total;
 };
 
@@ -215,5 +221,20 @@ struct StatsParams {
     unsigned long long t_batch, t_iter, t_tok, t_pre, lambda;
 };
 cudaError_t run_stats(const StatsParams &S, cudaStream_t st);
+
+struct SimParams {
+    const uint32_t *rin, *rout, *rslo;          // scheduled-order records
+    const uint32_t *order, *offsets;
+    const unsigned long long *num_batches;
+    const unsigned long long *arrival;          // caller index -> arrival time (us)
+    unsigned long long *est, *inc_a, *inc_b;    // per batch: est, CTA-local inclusive map
+    unsigned long long *chunk_a, *chunk_b, *carry;   // per chunk of kScanBlock batches
+    unsigned long long *batch_end, *latency;    // optional outputs (NULL = not requested)
+    SimAcc *acc;
+    uellm_sim_totals *totals;
+    uint64_t n, n_cap;
+    unsigned long long t_batch, t_iter, t_tok, t_pre;
+};
+cudaError_t run_simulate(const SimParams &S, cudaStream_t st, int *launches);
 
 }  // namespace uellm

@@ -45,6 +45,25 @@ class GpuScheduler:
         U.batch_stats(self.profile, self.cfg, self.offsets, self.num_batches, self.per_batch,
                       self.totals, stream)
 
+    def simulate(self, arrival_us, stream=None, per_batch: bool = True, per_query: bool = True):
+        """NEXT f2: sequential execution of the current schedule with arrivals (u64 us by caller
+        index, torch int64/uint64 device tensor or numpy array)."""
+        if not hasattr(self, "sim_totals"):
+            self.sim_totals = torch.zeros(U.SIM_TOTALS_BYTES, dtype=torch.uint8, device=self.device)
+            self.batch_end = torch.empty(max(self.n, 1), dtype=torch.int64, device=self.device)
+            self.latency = torch.empty(max(self.n, 1), dtype=torch.int64, device=self.device)
+        U.simulate(self.profile, self.cfg, arrival_us, self.order, self.offsets, self.num_batches,
+                   self.batch_end if per_batch else None, self.latency if per_query else None,
+                   self.sim_totals, stream)
+
+    def sim_results(self) -> dict:
+        torch.cuda.synchronize(self.device)
+        m = int(self.num_batches.item())
+        tot = U.SimTotals.from_buffer_copy(self.sim_totals.cpu().numpy().tobytes())
+        return {"batch_end": self.batch_end[:m].cpu().numpy().view(np.uint64),
+                "latency": self.latency[: self.n].cpu().numpy().view(np.uint64),
+                "totals": tot.as_dict()}
+
     def run(self, input_len, pred_out_len, slo_s, stream=None):
         self.load(input_len, pred_out_len, slo_s, stream)
         self.schedule(stream)

@@ -52,6 +52,20 @@ class Totals(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class SimTotals(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("n", "batches", "makespan_us", "busy_us", "idle_us",
+                                          "gen_tokens", "viol", "latency_max_us",
+                                          "latency_sum_lo", "latency_sum_hi")] + \
+               [(k, C.c_double) for k in ("mean_latency_s", "slo_violation_rate", "utilization",
+                                          "throughput_tok_s")] + \
+               [("status", C.c_uint32), ("pad", C.c_uint32)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+        d["latency_sum_us"] = d["latency_sum_lo"] + (d["latency_sum_hi"] << 64)
+        return d
+
+
 class Profile(C.Structure):
     _fields_ = [("opaque", C.c_uint64 * 40)]
 
@@ -72,6 +86,7 @@ BATCH_STAT_DTYPE = np.dtype([
     ("est_us", "<u8"), ("completion_us", "<u8"),
     ("viol_alone", "<u4"), ("viol_seq", "<u4"), ("over_cap", "<u4"), ("window", "<u4")])
 TOTALS_BYTES = C.sizeof(Totals)
+SIM_TOTALS_BYTES = C.sizeof(SimTotals)
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"libuellm.so not built ({_LIB_PATH}); run __graft_entry__.build()")
@@ -92,6 +107,8 @@ _lib.uellm_schedule_batches.argtypes = [C.POINTER(Profile), C.POINTER(Config), C
 _lib.uellm_batch_stats.restype = C.c_int32
 _lib.uellm_batch_stats.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p]
+_lib.uellm_simulate.restype = C.c_int32
+_lib.uellm_simulate.argtypes = [C.POINTER(Profile), C.POINTER(Config)] + [C.c_void_p] * 8
 _lib.uellm_set_stage_events.restype = C.c_int32
 _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
 _lib.uellm_get_diagnostics.restype = C.c_int32
@@ -103,6 +120,7 @@ assert _lib.uellm_sizeof(1) == BATCH_STAT_DTYPE.itemsize == 80
 assert _lib.uellm_sizeof(2) == C.sizeof(Totals)
 assert _lib.uellm_sizeof(3) == C.sizeof(Profile)
 assert _lib.uellm_sizeof(4) == C.sizeof(Diagnostics)
+assert _lib.uellm_sizeof(5) == C.sizeof(SimTotals)
 
 LIBRARY_PATH = _LIB_PATH
 
@@ -172,6 +190,13 @@ def batch_stats(p: Profile, cfg: Config, batch_offsets, num_batches, per_batch, 
     _check(_lib.uellm_batch_stats(C.byref(p), C.byref(cfg), _ptr(batch_offsets), _ptr(num_batches),
                                   _ptr(per_batch), _ptr(totals), _stream_handle(stream)),
            "uellm_batch_stats")
+
+
+def simulate(p: Profile, cfg: Config, arrival_us, order, batch_offsets, num_batches, batch_end_us,
+             latency_us, totals, stream=None):
+    _check(_lib.uellm_simulate(C.byref(p), C.byref(cfg), _ptr(arrival_us), _ptr(order), _ptr(batch_offsets),
+                               _ptr(num_batches), _ptr(batch_end_us), _ptr(latency_us), _ptr(totals),
+                               _stream_handle(stream)), "uellm_simulate")
 
 
 STAGES = ["sched_begin", "sort_end", "decode_end", "dp_local_end", "dp_fix_end", "dp_cascade_end",

@@ -66,3 +66,59 @@ def brute_segmentation(inp, out, slo, cfg):
         if best is None or key < best:
             best = key
     return order, best[1][::-1], best[0]
+
+
+def brute_simulate(inp, out, slo, cfg, order, offsets, arrival):
+    """Discrete-event reference of the sequential-execution simulator (NEXT f2):
+    one server, batches taken in plan order; a batch starts when the server is idle AND every
+    member has arrived; its service time is est(B) (R7).  Formulated as an event loop
+    over arrival / completion events with a heap (not as the max-plus recurrence the oracle
+    and the GPU use).  Returns (batch_end list, latency dict by caller index, totals dict)."""
+    import heapq
+    n = len(inp)
+    m = len(offsets) - 1
+    members = [[int(order[k]) for k in range(int(offsets[t]), int(offsets[t + 1]))] for t in range(m)]
+    batch_of = {x: t for t in range(m) for x in members[t]}
+    missing = [len(ms) for ms in members]
+
+    def est(ms):
+        b = len(ms)
+        s = max(int(inp[x]) for x in ms)
+        O = max(int(out[x]) for x in ms)
+        return cfg.t_batch_us + cfg.t_iter_us * O + cfg.t_tok_us * b * O + cfg.t_prefill_us * b * s
+
+    ev = [(int(arrival[x]), 0, x) for x in range(n)]      # (time, kind 0 = arrival, query)
+    heapq.heapify(ev)
+    nxt, busy, ends, lat = 0, False, [None] * m, {}
+    while ev:
+        now = ev[0][0]
+        while ev and ev[0][0] == now:                      # all events at this instant
+            _, kind, x = heapq.heappop(ev)
+            if kind == 0:
+                missing[batch_of[x]] -= 1
+            else:
+                busy = False
+                ends[x] = now
+                for q in members[x]:
+                    lat[q] = now - int(arrival[q])
+            while not busy and nxt < m and missing[nxt] == 0:
+                e = est(members[nxt])
+                if e == 0:                                 # zero service time: done at once
+                    ends[nxt] = now
+                    for q in members[nxt]:
+                        lat[q] = now - int(arrival[q])
+                    nxt += 1
+                    continue
+                heapq.heappush(ev, (now + e, 1, nxt))
+                busy = True
+                nxt += 1
+    assert nxt == m and all(e is not None for e in ends)
+    su = [slo_us_ref(s) for s in slo]
+    busy_us = sum(est(ms) for ms in members)
+    mk = ends[-1] if m else 0
+    tot = {"makespan_us": mk, "busy_us": busy_us, "idle_us": mk - busy_us,
+           "gen_tokens": sum(len(ms) * max(int(out[x]) for x in ms) for ms in members),
+           "viol": sum(1 for x in range(n) if lat[x] > su[x]),
+           "latency_max_us": max(lat.values()) if n else 0,
+           "latency_sum_us": sum(lat.values())}
+    return ends, lat, tot

@@ -185,6 +185,27 @@ def c5(seed: int, n: int = 10_000_000, window: int = 1_000_000, lam: int = 10**9
     return inp, out, slo, cfg
 
 
+# Mean inter-arrival gaps (us) for the simulator (NEXT f2): about one query's share of the
+# makespan the R7 service model gives the SEG-DP schedules of these shapes (c2 ~10 ms/query,
+# c3/c4 ~21.6 ms/query), i.e. a replica loaded close to saturation.
+MEAN_GAP_US = {"c2": 10_000, "c3": 21_000, "c4": 21_000}
+
+
+def poisson_arrivals(n: int, seed: int, mean_gap_us: float, stream: int = 11) -> np.ndarray:
+    """Arrival times (u64 us, nondecreasing in arrival index): cumulative sums of rounded
+    exponential gaps (a Poisson stream; the paper states none)."""
+    rng = _rng(seed, stream)
+    gaps = np.rint(rng.exponential(mean_gap_us, size=n)).astype(np.int64)
+    return np.cumsum(gaps).astype(np.uint64)
+
+
+def random_arrivals(n: int, seed: int, hi: int, stream: int = 12) -> np.ndarray:
+    """Arrivals in any order (uniform in [0, hi)): exercises batches whose latest member arrives
+    after the previous batch ends."""
+    rng = _rng(seed, stream)
+    return rng.integers(0, max(hi, 1), size=n).astype(np.uint64)
+
+
 def random_small(seed: int, n: int, pattern: str = "rand"):
     """Tiny brute-force-checkable instances with a random configuration.
     pattern: rand | ties | bucket | identical | descending | classes."""
