@@ -357,6 +357,42 @@ def main():
             "totals": {k: sim[k] for k in ("makespan_us", "idle_us", "viol", "mean_latency_s",
                                             "slo_violation_rate", "utilization", "throughput_tok_s")}}
 
+    # NEXT f4: profiler stand-ins + monitor producing the predicted lengths of a stream of this
+    # step's size (true lengths resident in HBM; one monitor epoch per scheduling window)
+    if not args.no_sim:
+        import workloads as W
+        tl = torch.from_numpy(W.true_output_lengths(n, rank).view(np.int32)).to(dev)
+        pr = torch.empty(n, dtype=torch.int32, device=dev)
+        st0 = U.MonitorState()
+        st0.inflation_factor = 1.0
+        init = torch.frombuffer(bytearray(bytes(st0)), dtype=torch.uint8).to(dev)
+        state = init.clone()
+        pc = W.PredictorConfig(variant=2, error_rate=0.0049, bucket_width=16, window=cfg.window or n, seed=rank)
+        cp = U.make_predictor(pc)
+
+        def f4_step():
+            with torch.cuda.stream(stream):
+                state.copy_(init)
+            U.predict_lengths(n, tl, cp, state, pr, None, stream)
+        for _ in range(max(Wm, 1)):
+            f4_step()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(K):
+            f4_step()
+        p1.record(stream)
+        torch.cuda.synchronize(dev)
+        pms = p0.elapsed_time(p1) / K
+        fin = U.MonitorState.from_buffer_copy(state.cpu().numpy().tobytes())
+        next_rows["f4_predict"] = {
+            "ms": pms, "queries_per_s": n / (pms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": 8 * n / (pms / 1e3) / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                         "frac": 8 * n / (pms / 1e3) / 1e9 / hbm_gbs, "algorithmic_bytes": 8 * n},
+            "predictor": "noisy, error 0.0049, 16-token buckets, monitor gamma 1.1 cap 2.0, epoch = window",
+            "launches": (n + (cfg.window or n) - 1) // (cfg.window or n),
+            "final_state": {"corrections": fin.corrections, "inflation_factor": fin.inflation_factor}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1

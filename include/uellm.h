@@ -12,6 +12,12 @@
  *   uellm_batch_stats       per-batch padding, generated tokens (b x O), KV-cache peak
  *                           bytes (4*b*l*h*(s+n)), estimated latency and SLO violations
  *
+ * and the adjacent steps of SURVEY.md section 8(f):
+ *   uellm_simulate          (f2) sequential execution of a schedule with arrivals: latency, SLO
+ *                           violations, utilisation, throughput
+ *   uellm_predict_lengths   (f4) profiler stand-ins + misprediction monitor that produce the
+ *                           predicted output lengths
+ *
  * Citations: P:NNN = /root/reference/PAPER.md line; S:NNN = SPEC.md line; Rk = reading k in
  * DESIGN.md.  The C ABI is plain: no exceptions, no C++ or torch types, no global state, no
  * allocation.  All device work is stream-ordered on `stream` (a cudaStream_t passed as void*,
@@ -179,7 +185,7 @@ typedef struct {
 /* ABI version (UELLM_ABI_VERSION) and struct sizes, for bindings to check their layouts. [host] */
 uint32_t uellm_abi_version(void);
 uint64_t uellm_sizeof(int which);   /* 0 config, 1 batch_stat, 2 totals, 3 profile, 4 diagnostics,
-                                       5 sim_totals */
+                                       5 sim_totals, 6 predictor, 7 monitor_state */
 
 /* Human-readable name of a status code.  [host]  Never NULL; static storage. */
 const char *uellm_status_string(uellm_status s);
@@ -273,6 +279,57 @@ uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, con
                             const uint32_t *order, const uint32_t *batch_offsets,
                             const uint64_t *num_batches, uint64_t *batch_end_us, uint64_t *latency_us,
                             uellm_sim_totals *totals, void *stream);
+
+/* Profiler stand-ins (NEXT f4; R20).  The paper's
+ * predictor is a fine-tuned ChatGLM3-6B that classifies output lengths into buckets (out of
+ * scope); these stand-ins turn a true output length into the predicted one the scheduler
+ * consumes. */
+enum {
+    UELLM_PREDICT_ORACLE = 0,       /* pred = true length                                          */
+    UELLM_PREDICT_BUCKETED = 1,     /* pred = max(1, ceil(true / w)) * w                   */
+    UELLM_PREDICT_NOISY = 2,        /* bucketed, moved one bucket up or down with probability
+                                       error_rate (never below the first bucket, R20)       */
+    UELLM_PREDICT_CONSTANT = 3      /* pred = constant_tokens                                      */
+};
+typedef struct {
+    uint32_t variant;               /* UELLM_PREDICT_*                                             */
+    uint32_t bucket_width;          /* w >= 1 (bucketed, noisy)                                    */
+    uint32_t constant_tokens;       /* >= 1 (constant)                                             */
+    uint32_t window;                /* monitor epoch in queries (R20); 0 = one epoch of all n      */
+    double error_rate;              /* noisy: probability in [0, 1] (0.0049 mimics P:195's 99.51 %) */
+    double gamma;                   /* monitor multiplier >= 1 (S:216 default 1.1)                 */
+    double cap;                     /* monitor inflation cap >= 1 (S:216 default 2.0)              */
+    uint64_t seed;                  /* noisy: counter-based draw splitmix64(seed ^ k * 0x9E3779B97F4A7C15)
+                                       for caller index k; u = (z >> 11) * 2^-53, moved iff
+                                       u < error_rate, up iff z is odd                             */
+    uint32_t monitor;               /* 0|1: apply the misprediction monitor      */
+    uint32_t pad;
+} uellm_predictor;
+
+/* Misprediction-monitor state, device-resident so that consecutive windows chain on the
+ * stream without host round trips. */
+typedef struct {
+    uint64_t corrections;           /* observed under-predictions                          */
+    double inflation_factor;        /* >= 1, multiplies every prediction                   */
+    uint64_t scratch[2];            /* library scratch: zero before the first call, left zero      */
+} uellm_monitor_state;
+
+/* Predicted output lengths for n queries in windows of pc->window (R20): window w is predicted
+ * with the inflation factor in force at its start,
+ *     pred_k = min(ceil(base_k * factor), 2^32 - 1),   base_k from the variant above,
+ * then its completions are observed (true length = actual): every under-prediction
+ * (true_k > pred_k) increments corrections and sets factor <- min(factor * gamma, cap), one
+ * observation at a time, before window w + 1 is predicted.
+ *   true_out_len   [device] n x u32, true (generated) output length of caller query k.
+ *   pc             [host] predictor; UELLM_ERR_CONFIG if a field is out of range.
+ *   state          [device] 1 x uellm_monitor_state, read and updated on the stream.
+ *   pred_out_len   [device] n x u32 output (feeds uellm_queries.pred_out_len).
+ *   window_factors [device] capacity nwin + 1 x f64 or NULL: factor used by each window, then
+ *                  the final factor.
+ * One kernel launch per window; never synchronises. */
+uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, const uellm_predictor *pc,
+                                   uellm_monitor_state *state, uint32_t *pred_out_len,
+                                   double *window_factors, void *stream);
 
 /* Attach (n <= UELLM_STAGE_COUNT) caller-owned cudaEvent_t handles (void*, created with timing
  * enabled; NULL entries are skipped) to the profile; subsequent schedule/stats calls record

@@ -76,6 +76,12 @@ class OrcSimTotals(C.Structure):
         return d
 
 
+class OrcPredictor(C.Structure):
+    _fields_ = [("variant", C.c_uint32), ("bucket_width", C.c_uint32), ("constant_tokens", C.c_uint32),
+                ("window", C.c_uint32), ("error_rate", C.c_double), ("gamma", C.c_double),
+                ("cap", C.c_double), ("seed", C.c_uint64), ("monitor", C.c_uint32), ("pad", C.c_uint32)]
+
+
 _lib = None
 
 
@@ -97,13 +103,20 @@ def lib():
         _lib.orc_simulate.argtypes = [C.c_uint64, u32p, u32p, f32p, C.POINTER(OrcConfig),
                                       u32p, u32p, C.c_uint64, u64p, C.c_void_p, C.c_void_p,
                                       C.POINTER(OrcSimTotals)]
+        _lib.orc_predict.argtypes = [C.c_uint64, C.c_uint64, u32p, C.POINTER(OrcPredictor), C.c_double, u32p]
+        _lib.orc_monitor_observe.argtypes = [C.c_uint64, u32p, u32p, C.c_double, C.c_double,
+                                             C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        _lib.orc_profile_stream.argtypes = [C.c_uint64, u32p, C.POINTER(OrcPredictor), C.c_double, u32p, f64p,
+                                            C.POINTER(C.c_uint64)]
         for f in ("orc_sizeof_config", "orc_sizeof_batch_stat", "orc_sizeof_totals",
-                  "orc_sizeof_sim_totals"):
+                  "orc_sizeof_sim_totals", "orc_sizeof_predictor"):
             getattr(_lib, f).restype = C.c_uint64
         assert _lib.orc_sizeof_config() == C.sizeof(OrcConfig)
         assert _lib.orc_sizeof_batch_stat() == BATCH_STAT_DTYPE.itemsize
         assert _lib.orc_sizeof_totals() == C.sizeof(OrcTotals)
         assert _lib.orc_sizeof_sim_totals() == C.sizeof(OrcSimTotals)
+        assert _lib.orc_sizeof_predictor() == C.sizeof(OrcPredictor)
     return _lib
 
 
@@ -198,3 +211,54 @@ def simulate(inp, out, slo, cfg, order, offsets, arrival_us):
     if st:
         raise OracleError(st, "simulate")
     return ends[:m], lat[:n], tot.as_dict()
+
+
+PREDICTORS = {"oracle": 0, "bucketed": 1, "noisy": 2, "constant": 3}
+
+
+def to_predictor(pc) -> OrcPredictor:
+    p = OrcPredictor()
+    for name, _ in OrcPredictor._fields_:
+        if name != "pad":
+            setattr(p, name, getattr(pc, name))
+    return p
+
+
+def predict(true_len, pc, factor: float = 1.0, index0: int = 0):
+    """O9 (NEXT f4): predicted output lengths of queries index0.. with inflation `factor`."""
+    t = np.ascontiguousarray(true_len, np.uint32)
+    pred = np.zeros(max(len(t), 1), np.uint32)
+    st = lib().orc_predict(len(t), index0, t if len(t) else np.zeros(1, np.uint32), C.byref(to_predictor(pc)),
+                           factor, pred)
+    if st:
+        raise OracleError(st, "predict")
+    return pred[: len(t)]
+
+
+def monitor_observe(pred, actual, gamma: float, cap: float, corrections: int = 0, factor: float = 1.0):
+    """O10 (NEXT f4): -> (corrections, factor) after observing every (pred, actual) in order."""
+    p = np.ascontiguousarray(pred, np.uint32)
+    a = np.ascontiguousarray(actual, np.uint32)
+    c = C.c_uint64(corrections)
+    f = C.c_double(factor)
+    st = lib().orc_monitor_observe(len(p), p if len(p) else np.zeros(1, np.uint32),
+                                   a if len(a) else np.zeros(1, np.uint32), gamma, cap, C.byref(c), C.byref(f))
+    if st:
+        raise OracleError(st, "monitor_observe")
+    return c.value, f.value
+
+
+def profile_stream(true_len, pc, factor0: float = 1.0):
+    """O11 (NEXT f4, R20): -> (pred u32[n], factors f64[nwin + 1], corrections)."""
+    t = np.ascontiguousarray(true_len, np.uint32)
+    n = len(t)
+    wl = pc.window or max(n, 1)
+    nwin = (n + wl - 1) // wl
+    pred = np.zeros(max(n, 1), np.uint32)
+    factors = np.zeros(nwin + 1, np.float64)
+    c = C.c_uint64()
+    st = lib().orc_profile_stream(n, t if n else np.zeros(1, np.uint32), C.byref(to_predictor(pc)), factor0, pred,
+                                  factors, C.byref(c))
+    if st:
+        raise OracleError(st, "profile_stream")
+    return pred[:n], factors, c.value

@@ -23,6 +23,10 @@
  *   orc_simulate        O8   sequential execution of a schedule with arrivals
  *                            (NEXT f2; latency, SLO violations, utilisation,
  *                            throughput)
+ *   orc_predict         O9   profiler stand-ins: oracle / bucketed / noisy /      P:195
+ *                            constant predicted output length (NEXT f4)
+ *   orc_monitor_observe O10  misprediction monitor, gamma-inflation (NEXT f4)
+ *   orc_profile_stream  O11  predict + observe, one monitor epoch per window      R20
  *
  * Parity pins (tests/test_oracle_*.py, -m "not gpu"): brute-force enumeration of all
  * 2^(n-1) segmentations (n <= 12), closed forms (identical queries), special cases
@@ -561,8 +565,136 @@ int orc_simulate(uint64_t n, const uint32_t *in, const uint32_t *out, const floa
     return ORC_OK;
 }
 
+/* ======================================================================== */
+/* O9-O11  profiler stand-ins and the misprediction monitor (NEXT f4; R20).
+ * the resource profiler "categorize[s] the output lengths" of requests into buckets (a
+ * fine-tuned ChatGLM3-6B, out of scope); a backend monitor "detect[s] erroneous
+ * predictions and adjust[s] the allocated memory size".  SPEC S:200-207 / S:211-218 fix the
+ * stand-ins used here:
+ *   oracle      pred = true length
+ *   bucketed(w) pred = true length rounded up to the bucket ceiling (R20: at least one bucket)
+ *   noisy(e, w) the bucketed value displaced by +-1 bucket with probability e (seeded,
+ *               reproducible; R20: never below the first bucket)
+ *   constant(v) pred = v
+ * then "multiplied by monitor.inflation_factor and rounded up"; R20 saturates at
+ * 2^32 - 1.  The monitor: on actual > predicted, corrections += 1 and
+ * factor <- min(factor * gamma, cap).
+ * Random draws: a counter-based generator (splitmix64 finaliser of seed ^ (index * golden
+ * gamma)); u = (z >> 11) * 2^-53, displaced iff u < e, direction + iff z is odd.  The CUDA path
+ * implements the same generator independently (③: same counter-based generator on each side). */
+typedef struct {
+    uint32_t variant;          /* 0 oracle, 1 bucketed, 2 noisy, 3 constant */
+    uint32_t bucket_width;     /* >= 1 for bucketed / noisy */
+    uint32_t constant_tokens;  /* >= 1 for constant */
+    uint32_t window;           /* monitor epoch in queries (0 = all) */
+    double   error_rate;       /* [0, 1] */
+    double   gamma;            /* >= 1 */
+    double   cap;              /* >= 1 */
+    uint64_t seed;
+    uint32_t monitor;          /* 0|1 */
+    uint32_t pad;
+} orc_predictor;
+
+static uint64_t orc_mix64(uint64_t seed, uint64_t index)
+{
+    uint64_t z = seed ^ (index * 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static int check_predictor(const orc_predictor *p)
+{
+    if (p->variant > 3) return ORC_ERR_CONFIG;
+    if ((p->variant == 1 || p->variant == 2) && p->bucket_width < 1) return ORC_ERR_CONFIG;
+    if (p->variant == 3 && p->constant_tokens < 1) return ORC_ERR_CONFIG;
+    if (!(p->error_rate >= 0.0 && p->error_rate <= 1.0)) return ORC_ERR_CONFIG;
+    if (p->monitor > 1) return ORC_ERR_CONFIG;
+    if (p->monitor && !(p->gamma >= 1.0 && p->cap >= 1.0 && isfinite(p->gamma) && isfinite(p->cap)))
+        return ORC_ERR_CONFIG;
+    return ORC_OK;
+}
+
+/* O9: prediction for query `index` (global caller index) with inflation `factor` */
+static uint32_t predict_one(const orc_predictor *p, uint64_t index, uint32_t true_len, double factor)
+{
+    uint64_t base;
+    if (p->variant == 0) {
+        base = true_len;
+    } else if (p->variant == 3) {
+        base = p->constant_tokens;
+    } else {
+        uint64_t w = p->bucket_width;
+        uint64_t k = (true_len + w - 1) / w;          /* bucket of the true length (ceiling) */
+        if (k < 1) k = 1;
+        if (p->variant == 2) {
+            uint64_t z = orc_mix64(p->seed, index);
+            double u = (double)(z >> 11) * 0x1.0p-53;
+            if (u < p->error_rate) {
+                if (z & 1) k += 1;
+                else if (k > 1) k -= 1;
+            }
+        }
+        base = k * w;
+    }
+    double x = ceil((double)base * factor);           /* "multiplied ... and rounded up" */
+    return x >= 4294967295.0 ? 4294967295u : (uint32_t)x;
+}
+
+int orc_predict(uint64_t n, uint64_t index0, const uint32_t *true_len, const orc_predictor *p,
+                double factor, uint32_t *pred)
+{
+    if (!p || (n && (!true_len || !pred))) return ORC_ERR_ARG;
+    int s = check_predictor(p);
+    if (s != ORC_OK) return s;
+    if (!(factor >= 1.0) || !isfinite(factor)) return ORC_ERR_CONFIG;
+    for (uint64_t k = 0; k < n; ++k) pred[k] = predict_one(p, index0 + k, true_len[k], factor);
+    return ORC_OK;
+}
+
+/* O10: S:211-218, one observation at a time, in order */
+int orc_monitor_observe(uint64_t n, const uint32_t *pred, const uint32_t *actual, double gamma,
+                        double cap, uint64_t *corrections, double *factor)
+{
+    if (!corrections || !factor || (n && (!pred || !actual))) return ORC_ERR_ARG;
+    for (uint64_t k = 0; k < n; ++k) {
+        if (actual[k] > pred[k]) {
+            *corrections += 1;
+            double f = *factor * gamma;
+            *factor = f < cap ? f : cap;
+        }
+    }
+    return ORC_OK;
+}
+
+/* O11 (R20): the profiler and the monitor over a stream cut into windows (the scheduling
+ * windows, R15).  Window w is predicted with the factor in force when it starts; its
+ * completions are then observed (true length = actual) before window w + 1 is predicted.
+ * factors[w] = factor used for window w (nwin entries), factors[nwin] = final factor. */
+int orc_profile_stream(uint64_t n, const uint32_t *true_len, const orc_predictor *p, double factor0,
+                       uint32_t *pred, double *factors, uint64_t *corrections)
+{
+    if (!p || !corrections || (n && (!true_len || !pred || !factors))) return ORC_ERR_ARG;
+    int s = check_predictor(p);
+    if (s != ORC_OK) return s;
+    uint64_t wl = p->window ? p->window : (n ? n : 1);
+    double f = factor0;
+    uint64_t w = 0;
+    *corrections = 0;
+    for (uint64_t a = 0; a < n; a += wl, ++w) {
+        uint64_t z = a + wl < n ? a + wl : n;
+        factors[w] = f;
+        s = orc_predict(z - a, a, true_len + a, p, f, pred + a);
+        if (s != ORC_OK) return s;
+        if (p->monitor) orc_monitor_observe(z - a, pred + a, true_len + a, p->gamma, p->cap, corrections, &f);
+    }
+    if (factors) factors[w] = f;
+    return ORC_OK;
+}
+
 /* ABI self-description for the Python side (sizes checked by tests). */
 uint64_t orc_sizeof_config(void) { return sizeof(orc_config); }
 uint64_t orc_sizeof_batch_stat(void) { return sizeof(orc_batch_stat); }
 uint64_t orc_sizeof_totals(void) { return sizeof(orc_totals); }
 uint64_t orc_sizeof_sim_totals(void) { return sizeof(orc_sim_totals); }
+uint64_t orc_sizeof_predictor(void) { return sizeof(orc_predictor); }

@@ -134,6 +134,8 @@ uint64_t uellm_sizeof(int which)
     case 3: return sizeof(uellm_profile);
     case 4: return sizeof(uellm_diagnostics);
     case 5: return sizeof(uellm_sim_totals);
+    case 6: return sizeof(uellm_predictor);
+    case 7: return sizeof(uellm_monitor_state);
     default: return 0;
     }
 }
@@ -500,6 +502,8 @@ uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, con
     S.chunk_a = at<unsigned long long>(w, L.keys1);
     S.chunk_b = S.chunk_a + nch;
     S.carry = S.chunk_b + nch;
+    S.arr_s = at<unsigned long long>(w, L.keys0);       // keys0: sort scratch, free after the schedule
+    S.lat_s = at<unsigned long long>(w, L.keys2);       // keys2: read by the gather before it is reused
     S.batch_end = (unsigned long long *)batch_end_us;
     S.latency = (unsigned long long *)latency_us;
     S.acc = at<SimAcc>(w, L.simacc);
@@ -511,6 +515,34 @@ uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, con
         CU(cudaMemcpyAsync(totals, S.totals, sizeof(uellm_sim_totals), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }
+    return UELLM_OK;
+}
+
+uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, const uellm_predictor *pc,
+                                   uellm_monitor_state *state, uint32_t *pred_out_len, double *window_factors,
+                                   void *stream)
+{
+    if (!pc || !state || !is_device_ptr(state)) return UELLM_ERR_ARG;
+    if (n >= 0xffffffffull) return UELLM_ERR_ARG;
+    if (n > 0 && (!true_out_len || !pred_out_len || !is_device_ptr(true_out_len) || !is_device_ptr(pred_out_len)))
+        return UELLM_ERR_ARG;
+    if (window_factors && !is_device_ptr(window_factors)) return UELLM_ERR_ARG;
+    if (pc->variant > UELLM_PREDICT_CONSTANT || pc->monitor > 1) return UELLM_ERR_CONFIG;
+    if ((pc->variant == UELLM_PREDICT_BUCKETED || pc->variant == UELLM_PREDICT_NOISY) && pc->bucket_width < 1)
+        return UELLM_ERR_CONFIG;
+    if (pc->variant == UELLM_PREDICT_CONSTANT && pc->constant_tokens < 1) return UELLM_ERR_CONFIG;
+    if (!(pc->error_rate >= 0.0 && pc->error_rate <= 1.0)) return UELLM_ERR_CONFIG;
+    if (pc->monitor && !(pc->gamma >= 1.0 && pc->cap >= 1.0 && pc->gamma < 1e308 && pc->cap < 1e308))
+        return UELLM_ERR_CONFIG;
+    const uint64_t window = pc->window ? (pc->window < n ? pc->window : n) : (n ? n : 1);
+    PredictParams P;
+    std::memset(&P, 0, sizeof P);
+    P.true_len = true_out_len; P.pred = pred_out_len; P.state = state; P.factors = window_factors;
+    P.nwin = n ? ceil_div(n, window) : 0;
+    P.variant = pc->variant; P.bucket_width = pc->bucket_width; P.constant_tokens = pc->constant_tokens;
+    P.monitor = pc->monitor; P.error_rate = pc->error_rate; P.gamma = pc->gamma; P.cap = pc->cap;
+    P.seed = pc->seed;
+    CU(run_predict(P, n, window, (cudaStream_t)stream, nullptr));
     return UELLM_OK;
 }
 

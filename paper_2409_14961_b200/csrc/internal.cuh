@@ -227,6 +227,7 @@ struct SimParams {
     const uint32_t *order, *offsets;
     const unsigned long long *num_batches;
     const unsigned long long *arrival;          // caller index -> arrival time (us)
+    unsigned long long *arr_s, *lat_s;          // arrival / latency in scheduled order (scratch)
     unsigned long long *est, *inc_a, *inc_b;    // per batch: est, CTA-local inclusive map
     unsigned long long *chunk_a, *chunk_b, *carry;   // per chunk of kScanBlock batches
     unsigned long long *batch_end, *latency;    // optional outputs (NULL = not requested)
@@ -236,5 +237,17 @@ struct SimParams {
     unsigned long long t_batch, t_iter, t_tok, t_pre;
 };
 cudaError_t run_simulate(const SimParams &S, cudaStream_t st, int *launches);
+
+struct PredictParams {
+    const uint32_t *true_len;
+    uint32_t *pred;
+    uellm_monitor_state *state;
+    double *factors;                            // per-window factors (nwin + 1) or NULL
+    uint64_t nwin;
+    uint32_t variant, bucket_width, constant_tokens, monitor;
+    double error_rate, gamma, cap;
+    unsigned long long seed;
+};
+cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cudaStream_t st, int *launches);
 
 }  // namespace uellm

@@ -1,0 +1,134 @@
+// k_profiler.cu -- NEXT f4: profiler stand-ins and the misprediction monitor (PAPER.md P:73,
+// P:195; R20).  The step before the scheduling path: predicted output
+// lengths for a stream of queries, one monitor epoch per window.
+//
+//   variant oracle      pred = true length
+//           bucketed(w) pred = max(1, ceil(true / w)) * w
+//           noisy(e, w) the bucketed value moved one bucket up or down with probability e
+//                       (counter-based draw per caller index; never below the first bucket)
+//           constant(v) pred = v
+//   then pred = min(ceil(pred * factor), 2^32 - 1) ("multiplied by the inflation factor
+//   and rounded up").  Monitor: every under-prediction (true > pred) counts one
+//   correction and factor <- min(factor * gamma, cap).
+//
+// k_predict_window (one launch per window, position-linear): predictions with the factor in
+// force at the window's start, under-prediction count reduced per CTA; the last CTA to finish
+// (threadfence + arrival counter) applies the monitor update for the window's corrections and
+// publishes the next window's factor in the device-resident monitor state.
+#include "internal.cuh"
+
+namespace uellm {
+
+namespace {
+
+// counter-based draw (splitmix64 finaliser of seed ^ index * golden gamma)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long seed, unsigned long long index)
+{
+    unsigned long long z = seed ^ (index * 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint32_t predict_one(const PredictParams &P, unsigned long long index, uint32_t t,
+                                                double factor)
+{
+    unsigned long long base;
+    if (P.variant == UELLM_PREDICT_ORACLE) {
+        base = t;
+    } else if (P.variant == UELLM_PREDICT_CONSTANT) {
+        base = P.constant_tokens;
+    } else {
+        const unsigned long long w = P.bucket_width;
+        unsigned long long k = ((unsigned long long)t + w - 1) / w;
+        k = k < 1 ? 1 : k;
+        if (P.variant == UELLM_PREDICT_NOISY) {
+            const unsigned long long z = mix64(P.seed, index);
+            const double u = (double)(z >> 11) * 0x1.0p-53;
+            if (u < P.error_rate) {
+                if (z & 1ull) k += 1;
+                else if (k > 1) k -= 1;
+            }
+        }
+        base = k * w;
+    }
+    const double x = ceil(__dmul_rn((double)base, factor));
+    return x >= 4294967295.0 ? 4294967295u : (uint32_t)x;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_predict_window(PredictParams P, uint64_t a, uint64_t z, uint64_t w)
+{
+    __shared__ unsigned long long red[8];
+    __shared__ bool last;
+    uellm_monitor_state *M = P.state;
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(M->scratch);   // [0] under, [1] CTAs done
+    const double f = M->inflation_factor;       // read before this CTA's arrival below
+    unsigned long long under = 0;
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = a + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < z; k += nt) {
+        const uint32_t t = __ldg(P.true_len + k);
+        const uint32_t p = predict_one(P, k, t, f);
+        P.pred[k] = p;
+        under += t > p;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) under += __shfl_xor_sync(0xffffffffu, under, d);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = under;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long c = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) c += red[i];
+        if (c) atomicAdd(&cnt[0], c);
+        __threadfence();
+        last = atomicAdd(&cnt[1], 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned long long k = atomicAdd(&cnt[0], 0ull);   // every CTA's count is in
+    double g = f;
+    if (P.monitor) {
+        for (unsigned long long i = 0; i < k; ++i) {     // S:216, one observation at a time
+            const double h = __dmul_rn(g, P.gamma);
+            const double n2 = h < P.cap ? h : P.cap;
+            if (n2 == g) break;                          // fixpoint (cap reached or gamma == 1)
+            g = n2;
+        }
+        M->corrections += k;
+        M->inflation_factor = g;
+    }
+    if (P.factors) {
+        P.factors[w] = f;
+        if (w + 1 == P.nwin) P.factors[w + 1] = g;
+    }
+    cnt[0] = 0;
+    cnt[1] = 0;
+}
+
+__global__ void k_predict_empty(PredictParams P)
+{
+    if (P.factors) P.factors[0] = P.state->inflation_factor;
+}
+
+cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cudaStream_t st, int *launches)
+{
+    int l = 0;
+    if (n == 0) {
+        k_predict_empty<<<1, 1, 0, st>>>(P);
+        l = 1;
+    } else {
+        for (uint64_t w = 0, a = 0; a < n; a += window, ++w) {
+            const uint64_t z = a + window < n ? a + window : n;
+            const uint64_t nb = ceil_div(z - a, 256 * 4);
+            const unsigned blocks = (unsigned)(nb < 148 * 8 ? nb : 148 * 8);
+            k_predict_window<<<blocks, 256, 0, st>>>(P, a, z, w);
+            ++l;
+        }
+    }
+    if (launches) *launches = l;
+    return cudaGetLastError();
+}
+
+}  // namespace uellm

@@ -15,11 +15,16 @@
 // saturated scan equals min(true value, 2^63) exactly); ends are nondecreasing in t, so the
 // timeline overflowed iff the last end reached 2^63.
 //
+//   k_sim_gather   position-linear: arrival in scheduled order, arr_s[k] = arrival[order[k]]
+//                  (the random gather stays inside the window the resident CTAs work on, so it
+//                  is served from L2; everything after it streams coalesced)
 //   k_sim_batches  thread per batch (chunks of kScanBlock batches per CTA): s, O, A_t from the
 //                  members, est_t; CTA-wide inclusive scan of the maps; chunk aggregates
 //   k_sim_chunks   one CTA: exclusive scan of the chunk aggregates -> end value entering chunk
-//   k_sim_members  thread per batch: end_t, member latencies / violations, block-aggregated
-//                  totals (exact 128-bit latency sum)
+//   k_sim_members  thread per batch: end_t, member latencies (scheduled order) / violations,
+//                  block-aggregated totals (exact 128-bit latency sum)
+//   k_sim_scatter  position-linear (only when per-query latencies are requested):
+//                  latency[order[k]] = lat_s[k]
 //   k_sim_totals   one thread: uellm_sim_totals
 #include "internal.cuh"
 
@@ -98,6 +103,20 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v)
 
 }  // namespace
 
+__global__ void __launch_bounds__(256) k_sim_gather(SimParams S)
+{
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S.n; k += nt)
+        S.arr_s[k] = __ldg(S.arrival + __ldg(S.order + k));
+}
+
+__global__ void __launch_bounds__(256) k_sim_scatter(SimParams S)
+{
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S.n; k += nt)
+        S.latency[__ldg(S.order + k)] = S.lat_s[k];
+}
+
 __global__ void __launch_bounds__(kScanBlock) k_sim_batches(SimParams S)
 {
     const uint64_t m = *S.num_batches;
@@ -113,7 +132,7 @@ __global__ void __launch_bounds__(kScanBlock) k_sim_batches(SimParams S)
             for (uint32_t k = a; k < z; ++k) {
                 s = max(s, __ldg(S.rin + k));
                 O = max(O, __ldg(S.rout + k));
-                A = max(A, __ldg(S.arrival + __ldg(S.order + k)));
+                A = max(A, __ldg(S.arr_s + k));
             }
             const unsigned long long b = z - a;
             const unsigned long long est = S.t_batch + S.t_iter * O + S.t_tok * b * O + S.t_pre * b * s;
@@ -181,14 +200,13 @@ __global__ void __launch_bounds__(256) k_sim_members(SimParams S)
         if (t == m - 1) S.acc->makespan = end;
         const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
         for (uint32_t k = a; k < z; ++k) {
-            const uint32_t x = __ldg(S.order + k);
-            const unsigned long long arr = __ldg(S.arrival + x);
+            const unsigned long long arr = __ldg(S.arr_s + k);
             const unsigned long long lat = end > arr ? end - arr : 0ull;
             viol += lat > (unsigned long long)__ldg(S.rslo + k);
             lmax = max(lmax, lat);
             llo += lat;
             lhi += llo < lat ? 1ull : 0ull;
-            if (S.latency) S.latency[x] = lat;
+            if (S.latency) S.lat_s[k] = lat;
         }
         any = 1;
     }
@@ -256,10 +274,17 @@ cudaError_t run_simulate(const SimParams &S, cudaStream_t st, int *launches)
     if (S.n > 0) {
         const uint64_t nch = ceil_div(S.n_cap, kScanBlock);
         const unsigned cblocks = (unsigned)(nch < 296 ? nch : 296);
+        const uint64_t pb = ceil_div(S.n, 256);
+        const unsigned pblocks = (unsigned)(pb < 148 * 16 ? pb : 148 * 16);
+        k_sim_gather<<<pblocks, 256, 0, st>>>(S);
         k_sim_batches<<<cblocks, kScanBlock, 0, st>>>(S);
         k_sim_chunks<<<1, kScanBlock, 0, st>>>(S);
         k_sim_members<<<148 * 8, 256, 0, st>>>(S);
-        l += 3;
+        l += 4;
+        if (S.latency) {
+            k_sim_scatter<<<pblocks, 256, 0, st>>>(S);
+            l += 1;
+        }
     }
     k_sim_totals<<<1, 1, 0, st>>>(S);
     if (launches) *launches = l;

@@ -66,6 +66,16 @@ class SimTotals(C.Structure):
         return d
 
 
+class Predictor(C.Structure):
+    _fields_ = [("variant", C.c_uint32), ("bucket_width", C.c_uint32), ("constant_tokens", C.c_uint32),
+                ("window", C.c_uint32), ("error_rate", C.c_double), ("gamma", C.c_double),
+                ("cap", C.c_double), ("seed", C.c_uint64), ("monitor", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class MonitorState(C.Structure):
+    _fields_ = [("corrections", C.c_uint64), ("inflation_factor", C.c_double), ("scratch", C.c_uint64 * 2)]
+
+
 class Profile(C.Structure):
     _fields_ = [("opaque", C.c_uint64 * 40)]
 
@@ -109,6 +119,8 @@ _lib.uellm_batch_stats.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_vo
                                    C.c_void_p, C.c_void_p, C.c_void_p]
 _lib.uellm_simulate.restype = C.c_int32
 _lib.uellm_simulate.argtypes = [C.POINTER(Profile), C.POINTER(Config)] + [C.c_void_p] * 8
+_lib.uellm_predict_lengths.restype = C.c_int32
+_lib.uellm_predict_lengths.argtypes = [C.c_uint64, C.c_void_p, C.POINTER(Predictor)] + [C.c_void_p] * 4
 _lib.uellm_set_stage_events.restype = C.c_int32
 _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
 _lib.uellm_get_diagnostics.restype = C.c_int32
@@ -121,6 +133,8 @@ assert _lib.uellm_sizeof(2) == C.sizeof(Totals)
 assert _lib.uellm_sizeof(3) == C.sizeof(Profile)
 assert _lib.uellm_sizeof(4) == C.sizeof(Diagnostics)
 assert _lib.uellm_sizeof(5) == C.sizeof(SimTotals)
+assert _lib.uellm_sizeof(6) == C.sizeof(Predictor)
+assert _lib.uellm_sizeof(7) == C.sizeof(MonitorState)
 
 LIBRARY_PATH = _LIB_PATH
 
@@ -197,6 +211,20 @@ def simulate(p: Profile, cfg: Config, arrival_us, order, batch_offsets, num_batc
     _check(_lib.uellm_simulate(C.byref(p), C.byref(cfg), _ptr(arrival_us), _ptr(order), _ptr(batch_offsets),
                                _ptr(num_batches), _ptr(batch_end_us), _ptr(latency_us), _ptr(totals),
                                _stream_handle(stream)), "uellm_simulate")
+
+
+def make_predictor(pc) -> Predictor:
+    """C predictor from any object with the uellm_predictor field names (workloads.PredictorConfig)."""
+    p = Predictor()
+    for name, _ in Predictor._fields_:
+        if name != "pad" and hasattr(pc, name):
+            setattr(p, name, getattr(pc, name))
+    return p
+
+
+def predict_lengths(n: int, true_out_len, pc: Predictor, state, pred_out_len, window_factors=None, stream=None):
+    _check(_lib.uellm_predict_lengths(n, _ptr(true_out_len), C.byref(pc), _ptr(state), _ptr(pred_out_len),
+                                      _ptr(window_factors), _stream_handle(stream)), "uellm_predict_lengths")
 
 
 STAGES = ["sched_begin", "sort_end", "decode_end", "dp_local_end", "dp_fix_end", "dp_cascade_end",

@@ -206,6 +206,33 @@ def random_arrivals(n: int, seed: int, hi: int, stream: int = 12) -> np.ndarray:
     return rng.integers(0, max(hi, 1), size=n).astype(np.uint64)
 
 
+@dataclass
+class PredictorConfig:
+    """Profiler stand-in + monitor configuration (NEXT f4); field names follow include/uellm.h
+    (uellm_predictor).  Defaults: SPEC S:216 (gamma 1.1, cap 2.0); the noisy variant's error
+    rate 0.0049 mimics the paper's 99.51 % bucket precision."""
+    variant: int = 2                # 0 oracle, 1 bucketed, 2 noisy, 3 constant
+    bucket_width: int = 16
+    constant_tokens: int = 256
+    window: int = 0
+    error_rate: float = 0.0049
+    gamma: float = 1.1
+    cap: float = 2.0
+    seed: int = 0
+    monitor: int = 1
+
+    def replace(self, **kw) -> "PredictorConfig":
+        return dataclasses.replace(self, **kw)
+
+
+def true_output_lengths(n: int, seed: int, stream: int = 13) -> np.ndarray:
+    """True (generated) output lengths for the profiler stand-ins: the long-tail shape of c3/c4
+    before bucketing (Pareto(1.2) x 32, <= 4096)."""
+    rng = _rng(seed, stream)
+    x = 32 * (1.0 + rng.pareto(1.2, size=n))
+    return np.minimum(np.ceil(x), 4096).astype(np.uint32)
+
+
 def random_small(seed: int, n: int, pattern: str = "rand"):
     """Tiny brute-force-checkable instances with a random configuration.
     pattern: rand | ties | bucket | identical | descending | classes."""
