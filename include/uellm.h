@@ -270,7 +270,8 @@ typedef struct {
  *                  [host|device] that schedule call's outputs (host pointers: only when that call
  *                  returned them to host memory; the workspace copies are read).
  *   batch_end_us   [device] capacity num_batches x u64 (end_t), or NULL.
- *   latency_us     [device] n x u64 indexed by CALLER index, or NULL.
+ *   latency_us     [device] n x u64 in SCHEDULED order, or NULL: latency_us[k] is the latency
+ *                  of caller query order[k] (coalesced; the caller maps it through `order`).
  *   totals         [host|device] 1 x uellm_sim_totals.
  * Integer results are exact; the doubles are formed once from exact integer sums.  Overflow of
  * the 2^63-us timeline is reported in totals->status (the call itself does not synchronise

@@ -82,6 +82,23 @@ class OrcPredictor(C.Structure):
                 ("cap", C.c_double), ("seed", C.c_uint64), ("monitor", C.c_uint32), ("pad", C.c_uint32)]
 
 
+class OrcHelrCfg(C.Structure):
+    _fields_ = [("num_devices", C.c_uint32), ("num_layers", C.c_uint32), ("model_bytes", C.c_uint64),
+                ("kv_reserve_bytes", C.c_uint64), ("p", C.c_double), ("a1", C.c_double), ("a2", C.c_double)]
+
+
+class OrcDeviceMap(C.Structure):
+    _fields_ = [("count", C.c_uint32), ("feasible", C.c_uint32), ("mask", C.c_uint32), ("pad", C.c_uint32),
+                ("device", C.c_uint32 * 32), ("layer_begin", C.c_uint32 * 32), ("layer_count", C.c_uint32 * 32),
+                ("objective", C.c_double), ("latency_s", C.c_double)]
+
+    def as_dict(self):
+        k = self.count
+        return {"feasible": bool(self.feasible), "mask": self.mask, "devices": list(self.device[:k]),
+                "layer_begin": list(self.layer_begin[:k]), "layer_count": list(self.layer_count[:k]),
+                "objective": self.objective, "latency_s": self.latency_s}
+
+
 _lib = None
 
 
@@ -109,14 +126,18 @@ def lib():
         f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
         _lib.orc_profile_stream.argtypes = [C.c_uint64, u32p, C.POINTER(OrcPredictor), C.c_double, u32p, f64p,
                                             C.POINTER(C.c_uint64)]
+        u64p_ = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+        f64p_ = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        _lib.orc_helr.argtypes = [C.POINTER(OrcHelrCfg), u64p_, f64p_, f64p_, C.POINTER(OrcDeviceMap)]
         for f in ("orc_sizeof_config", "orc_sizeof_batch_stat", "orc_sizeof_totals",
-                  "orc_sizeof_sim_totals", "orc_sizeof_predictor"):
+                  "orc_sizeof_sim_totals", "orc_sizeof_predictor", "orc_sizeof_device_map"):
             getattr(_lib, f).restype = C.c_uint64
         assert _lib.orc_sizeof_config() == C.sizeof(OrcConfig)
         assert _lib.orc_sizeof_batch_stat() == BATCH_STAT_DTYPE.itemsize
         assert _lib.orc_sizeof_totals() == C.sizeof(OrcTotals)
         assert _lib.orc_sizeof_sim_totals() == C.sizeof(OrcSimTotals)
         assert _lib.orc_sizeof_predictor() == C.sizeof(OrcPredictor)
+        assert _lib.orc_sizeof_device_map() == C.sizeof(OrcDeviceMap)
     return _lib
 
 
@@ -189,7 +210,7 @@ def stats(inp, out, slo, cfg, order, offsets):
 
 def simulate(inp, out, slo, cfg, order, offsets, arrival_us):
     """O8 (NEXT f2): sequential execution with arrivals -> (batch_end u64[m], latency u64[n]
-    by caller index, totals dict)."""
+    in scheduled order (latency[k] belongs to query order[k]), totals dict)."""
     inp, out, slo = _arrays(inp, out, slo)
     n = inp.shape[0]
     order = np.ascontiguousarray(order, np.uint32)
@@ -262,3 +283,17 @@ def profile_stream(true_len, pc, factor0: float = 1.0):
     if st:
         raise OracleError(st, "profile_stream")
     return pred[:n], factors, c.value
+
+
+def helr(topo):
+    """O12 (NEXT f3): HELR device map of a workloads.Topology -> dict."""
+    c = OrcHelrCfg(len(topo.memory_bytes), topo.num_layers, topo.model_bytes, topo.kv_reserve_bytes,
+                   topo.p, topo.a1, topo.a2)
+    mem = np.ascontiguousarray(topo.memory_bytes, np.uint64)
+    perf = np.ascontiguousarray(topo.performance, np.float64)
+    lat = np.ascontiguousarray(topo.link_latency_s, np.float64).reshape(-1)
+    out = OrcDeviceMap()
+    st = lib().orc_helr(C.byref(c), mem, perf, lat, C.byref(out))
+    if st:
+        raise OracleError(st, "helr")
+    return out.as_dict()

@@ -27,6 +27,8 @@
  *                            constant predicted output length (NEXT f4)
  *   orc_monitor_observe O10  misprediction monitor, gamma-inflation (NEXT f4)
  *   orc_profile_stream  O11  predict + observe, one monitor epoch per window      R20
+ *   orc_helr            O12  HELR deployer: subsets x bitmask DP over device      P:301-384,
+ *                            visit orders (HE: a1 = 0, LR: a1:a2 = 10:1) (f3)
  *
  * Parity pins (tests/test_oracle_*.py, -m "not gpu"): brute-force enumeration of all
  * 2^(n-1) segmentations (n <= 12), closed forms (identical queries), special cases
@@ -515,6 +517,7 @@ typedef struct {
     double   mean_latency_s, slo_violation_rate, utilization, throughput_tok_s;
 } orc_sim_totals;
 
+/* batch_end_us[t] = end_t; latency_us[k] = latency of query order[k] (scheduled position k). */
 int orc_simulate(uint64_t n, const uint32_t *in, const uint32_t *out, const float *slo_s,
                  const orc_config *cfg, const uint32_t *order, const uint32_t *offsets,
                  uint64_t m, const uint64_t *arrival_us, uint64_t *batch_end_us,
@@ -549,7 +552,7 @@ int orc_simulate(uint64_t n, const uint32_t *in, const uint32_t *out, const floa
             uint32_t x = order[k], su;
             if (orc_slo_us(slo_s[x], &su) != ORC_OK) return ORC_ERR_CONTRACT;
             uint64_t lat = end - arrival_us[x];                             /* S:450 */
-            if (latency_us) latency_us[x] = lat;
+            if (latency_us) latency_us[k] = lat;                           /* scheduled position */
             if (lat > su) tot->viol++;                                      /* S:451 */
             if (lat > tot->latency_max_us) tot->latency_max_us = lat;
             lat_sum += lat;
@@ -692,9 +695,141 @@ int orc_profile_stream(uint64_t n, const uint32_t *true_len, const orc_predictor
     return ORC_OK;
 }
 
+/* ======================================================================== */
+/* O12  HELR deployer (NEXT f3; R21).  PAPER.md Sec. 4.3, Alg. 2,
+ * Eq. 4-6, with SPEC's readings of the garbled passages:
+ *   m = M / Layer(M) bytes per layer (Alg. 2 line 9);
+ *   max_layers(d) = min(L, floor((Memory(d) - T) / m)), 0 when Memory(d) <= T (Alg. 2 line 12,
+ *                   S:354), computed exactly as floor((Memory(d) - T) * L / M);
+ *   compute_cost(d, x) = p * x * m / Performance(d) (Eq. 5 term), evaluated as
+ *                   ((p * x) * m) / perf in doubles;
+ *   layers along a chain are filled greedily in visit order: after the visited set S the
+ *   remaining layers are max(0, L - sum_{d in S} max_layers(d)) and the next device j takes
+ *   min(remaining, max_layers(j));
+ *   dp[{j}][j] = compute_cost(j, min(L, max_layers(j)));
+ *   dp[S][j]   = min over i in S\{j} of (dp[S\{j}][i] + Latency(E[i][j])) + compute_cost(j, x_j)
+ *                (Eq. 5 as a Hamiltonian-path DP over (visited set, last device));
+ *   a subset is feasible iff sum max_layers >= L (Eq. 4 with the sign of Alg. 2 line 5 fixed,
+ *   S:393); its objective is a1 * min_j dp[S][j] + a2 * |S| / |D|;
+ *   the answer minimises (objective, chain latency, subset mask, last device) lexicographically;
+ *   inside the DP the smallest predecessor i wins ties.  HE = (a1 = 0), LR = (a1 : a2 = 10 : 1)
+ *   (P:337).  Device map: the chain decoded through the back-pointers, each device with its
+ *   greedy layer range (devices that receive 0 layers stay on the chain with an empty range). */
+typedef struct {
+    uint32_t num_devices, num_layers;
+    uint64_t model_bytes, kv_reserve_bytes;
+    double p, a1, a2;
+} orc_helr_cfg;
+
+typedef struct {
+    uint32_t count;                       /* devices on the chosen chain, in visit order */
+    uint32_t feasible;                    /* 0: no subset covers the model (Eq. 4)     */
+    uint32_t mask, pad;
+    uint32_t device[32], layer_begin[32], layer_count[32];
+    double objective, latency_s;
+} orc_device_map;
+
+static uint32_t helr_max_layers(const orc_helr_cfg *c, uint64_t mem)
+{
+    if (mem <= c->kv_reserve_bytes) return 0;
+    unsigned __int128 q = (unsigned __int128)(mem - c->kv_reserve_bytes) * c->num_layers / c->model_bytes;
+    return q >= c->num_layers ? c->num_layers : (uint32_t)q;
+}
+
+static double helr_cost(const orc_helr_cfg *c, double m, double perf, uint32_t x)
+{
+    return ((c->p * (double)x) * m) / perf;
+}
+
+int orc_helr(const orc_helr_cfg *c, const uint64_t *memory, const double *perf, const double *lat,
+             orc_device_map *out)
+{
+    if (!c || !memory || !perf || !lat || !out) return ORC_ERR_ARG;
+    const uint32_t D = c->num_devices, L = c->num_layers;
+    if (D < 1 || D > 20 || L < 1 || c->model_bytes == 0) return ORC_ERR_CONFIG;
+    if (!(c->p >= 0.0) || !(c->a1 >= 0.0) || !(c->a2 >= 0.0)) return ORC_ERR_CONFIG;
+    for (uint32_t d = 0; d < D; ++d) if (!(perf[d] > 0.0)) return ORC_ERR_CONFIG;
+    memset(out, 0, sizeof *out);
+    const double m = (double)c->model_bytes / (double)L;
+    uint32_t cap[32];
+    for (uint32_t d = 0; d < D; ++d) cap[d] = helr_max_layers(c, memory[d]);
+    const uint64_t NS = 1ull << D;
+    double *dp = (double *)malloc(sizeof(double) * NS * D);
+    uint8_t *arg = (uint8_t *)malloc(NS * D);
+    uint64_t *capsum = (uint64_t *)malloc(sizeof(uint64_t) * NS);
+    if (!dp || !arg || !capsum) { free(dp); free(arg); free(capsum); return ORC_ERR_ARG; }
+    capsum[0] = 0;
+    for (uint64_t S = 1; S < NS; ++S) {
+        uint32_t low = (uint32_t)__builtin_ctzll(S);
+        capsum[S] = capsum[S & (S - 1)] + cap[low];
+    }
+    for (uint64_t S = 1; S < NS; ++S) {                 /* numeric order: S \ {j} < S */
+        for (uint32_t j = 0; j < D; ++j) {
+            double *cell = &dp[S * D + j];
+            arg[S * D + j] = 0xff;
+            if (!((S >> j) & 1)) { *cell = INFINITY; continue; }
+            uint64_t P = S & ~(1ull << j);
+            uint64_t rem = capsum[P] >= L ? 0 : L - capsum[P];
+            uint32_t x = rem < cap[j] ? (uint32_t)rem : cap[j];
+            double cj = helr_cost(c, m, perf[j], x);
+            if (P == 0) { *cell = cj; continue; }
+            double best = INFINITY;
+            uint32_t bi = 0xff;
+            for (uint32_t i = 0; i < D; ++i) {
+                if (!((P >> i) & 1)) continue;
+                double v = (dp[P * D + i] + lat[i * D + j]) + cj;
+                if (v < best) { best = v; bi = i; }
+            }
+            *cell = best;
+            arg[S * D + j] = (uint8_t)bi;
+        }
+    }
+    /* Alg. 2 lines 3-20: best subset / chain by (objective, latency, mask, last device) */
+    int found = 0;
+    double bobj = 0, blat = 0;
+    uint64_t bS = 0;
+    uint32_t bj = 0;
+    for (uint64_t S = 1; S < NS; ++S) {
+        if (capsum[S] < L) continue;                    /* Eq. 4 */
+        double size = (double)__builtin_popcountll(S) / (double)D;
+        for (uint32_t j = 0; j < D; ++j) {
+            if (!((S >> j) & 1)) continue;
+            double l = dp[S * D + j];
+            double obj = c->a1 * l + c->a2 * size;
+            if (!found || obj < bobj || (obj == bobj && l < blat)) {
+                found = 1; bobj = obj; blat = l; bS = S; bj = j;
+            }
+        }
+    }
+    if (found) {
+        uint32_t chain[32], k = 0;
+        uint64_t S = bS;
+        uint32_t j = bj;
+        while (S) {
+            chain[k++] = j;
+            uint32_t i = arg[S * D + j];
+            S &= ~(1ull << j);
+            j = i;
+        }
+        uint64_t used = 0;
+        for (uint32_t t = 0; t < k; ++t) {            /* visit order = reverse of the walk */
+            uint32_t d = chain[k - 1 - t];
+            uint64_t rem = used >= L ? 0 : L - used;
+            uint32_t x = rem < cap[d] ? (uint32_t)rem : cap[d];
+            out->device[t] = d; out->layer_begin[t] = (uint32_t)(used < L ? used : L); out->layer_count[t] = x;
+            used += x;
+        }
+        out->count = k; out->feasible = 1; out->mask = (uint32_t)bS;
+        out->objective = bobj; out->latency_s = blat;
+    }
+    free(dp); free(arg); free(capsum);
+    return ORC_OK;
+}
+
 /* ABI self-description for the Python side (sizes checked by tests). */
 uint64_t orc_sizeof_config(void) { return sizeof(orc_config); }
 uint64_t orc_sizeof_batch_stat(void) { return sizeof(orc_batch_stat); }
 uint64_t orc_sizeof_totals(void) { return sizeof(orc_totals); }
 uint64_t orc_sizeof_sim_totals(void) { return sizeof(orc_sim_totals); }
 uint64_t orc_sizeof_predictor(void) { return sizeof(orc_predictor); }
+uint64_t orc_sizeof_device_map(void) { return sizeof(orc_device_map); }

@@ -503,7 +503,6 @@ uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, con
     S.chunk_b = S.chunk_a + nch;
     S.carry = S.chunk_b + nch;
     S.arr_s = at<unsigned long long>(w, L.keys0);       // keys0: sort scratch, free after the schedule
-    S.lat_s = at<unsigned long long>(w, L.keys2);       // keys2: read by the gather before it is reused
     S.batch_end = (unsigned long long *)batch_end_us;
     S.latency = (unsigned long long *)latency_us;
     S.acc = at<SimAcc>(w, L.simacc);

@@ -227,7 +227,7 @@ struct SimParams {
     const uint32_t *order, *offsets;
     const unsigned long long *num_batches;
     const unsigned long long *arrival;          // caller index -> arrival time (us)
-    unsigned long long *arr_s, *lat_s;          // arrival / latency in scheduled order (scratch)
+    unsigned long long *arr_s;                  // arrival in scheduled order (scratch)
     unsigned long long *est, *inc_a, *inc_b;    // per batch: est, CTA-local inclusive map
     unsigned long long *chunk_a, *chunk_b, *carry;   // per chunk of kScanBlock batches
     unsigned long long *batch_end, *latency;    // optional outputs (NULL = not requested)

@@ -21,10 +21,9 @@
 //   k_sim_batches  thread per batch (chunks of kScanBlock batches per CTA): s, O, A_t from the
 //                  members, est_t; CTA-wide inclusive scan of the maps; chunk aggregates
 //   k_sim_chunks   one CTA: exclusive scan of the chunk aggregates -> end value entering chunk
-//   k_sim_members  thread per batch: end_t, member latencies (scheduled order) / violations,
-//                  block-aggregated totals (exact 128-bit latency sum)
-//   k_sim_scatter  position-linear (only when per-query latencies are requested):
-//                  latency[order[k]] = lat_s[k]
+//   k_sim_members  thread per batch: end_t, member latencies (scheduled order, written straight
+//                  to the caller's buffer when requested) / violations, block-aggregated totals
+//                  (exact 128-bit latency sum)
 //   k_sim_totals   one thread: uellm_sim_totals
 #include "internal.cuh"
 
@@ -108,13 +107,6 @@ __global__ void __launch_bounds__(256) k_sim_gather(SimParams S)
     const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S.n; k += nt)
         S.arr_s[k] = __ldg(S.arrival + __ldg(S.order + k));
-}
-
-__global__ void __launch_bounds__(256) k_sim_scatter(SimParams S)
-{
-    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S.n; k += nt)
-        S.latency[__ldg(S.order + k)] = S.lat_s[k];
 }
 
 __global__ void __launch_bounds__(kScanBlock) k_sim_batches(SimParams S)
@@ -206,7 +198,7 @@ __global__ void __launch_bounds__(256) k_sim_members(SimParams S)
             lmax = max(lmax, lat);
             llo += lat;
             lhi += llo < lat ? 1ull : 0ull;
-            if (S.latency) S.lat_s[k] = lat;
+            if (S.latency) S.latency[k] = lat;
         }
         any = 1;
     }
@@ -281,10 +273,6 @@ cudaError_t run_simulate(const SimParams &S, cudaStream_t st, int *launches)
         k_sim_chunks<<<1, kScanBlock, 0, st>>>(S);
         k_sim_members<<<148 * 8, 256, 0, st>>>(S);
         l += 4;
-        if (S.latency) {
-            k_sim_scatter<<<pblocks, 256, 0, st>>>(S);
-            l += 1;
-        }
     }
     k_sim_totals<<<1, 1, 0, st>>>(S);
     if (launches) *launches = l;

@@ -47,7 +47,8 @@ class GpuScheduler:
 
     def simulate(self, arrival_us, stream=None, per_batch: bool = True, per_query: bool = True):
         """NEXT f2: sequential execution of the current schedule with arrivals (u64 us by caller
-        index, torch int64/uint64 device tensor or numpy array)."""
+        index, torch int64/uint64 device tensor or numpy array).  Per-query latencies come back in
+        scheduled order (latency[k] belongs to query order[k])."""
         if not hasattr(self, "sim_totals"):
             self.sim_totals = torch.zeros(U.SIM_TOTALS_BYTES, dtype=torch.uint8, device=self.device)
             self.batch_end = torch.empty(max(self.n, 1), dtype=torch.int64, device=self.device)

@@ -233,6 +233,59 @@ def true_output_lengths(n: int, seed: int, stream: int = 13) -> np.ndarray:
     return np.minimum(np.ceil(x), 4096).astype(np.uint32)
 
 
+@dataclass
+class Topology:
+    """HELR deployer input (NEXT f3): devices, links and the model to place."""
+    memory_bytes: np.ndarray            # u64 [D], Memory(d)
+    performance: np.ndarray             # f64 [D], Performance(d) (> 0)
+    link_latency_s: np.ndarray          # f64 [D, D], Latency(E[i][j]), symmetric, zero diagonal
+    num_layers: int = 32                # Layer(M)
+    model_bytes: int = 2 * 6_738_415_616     # M (LLaMA-2-7B fp16 weights)
+    kv_reserve_bytes: int = 0           # T (Alg. 2 line 11)
+    p: float = 1.0
+    a1: float = 1.0
+    a2: float = 1.0
+
+    def replace(self, **kw) -> "Topology":
+        return dataclasses.replace(self, **kw)
+
+
+def b200_cluster(nodes: int = 2, per_node: int = 8, seed: int = 0, model_bytes: int = 2 * 70_553_706_496,
+                 num_layers: int = 80, kv_reserve_bytes: int = 120_000_000_000) -> Topology:
+    """A synthetic multi-node B200 topology for HELR: per-device free memory drawn between 140 and
+    180 GB (other tenants), performance 0.85-1.0 (relative), NVLink 5 / NVSwitch inside a node
+    (~2 us), InfiniBand between nodes (~10 us); default model LLaMA-2-70B fp16 (80 layers) with a
+    120 GB-per-device KV reserve so that several devices are needed."""
+    rng = _rng(seed, 31)
+    D = nodes * per_node
+    mem = rng.integers(140, 181, size=D).astype(np.uint64) * np.uint64(1_000_000_000)
+    perf = rng.uniform(0.85, 1.0, size=D)
+    node = np.arange(D) // per_node
+    lat = np.where(node[:, None] == node[None, :], 2e-6, 10e-6) * rng.uniform(0.9, 1.1, size=(D, D))
+    lat = (lat + lat.T) / 2
+    np.fill_diagonal(lat, 0.0)
+    return Topology(mem, perf, lat, num_layers=num_layers, model_bytes=model_bytes,
+                    kv_reserve_bytes=kv_reserve_bytes, p=1e-12)
+
+
+def random_topology(seed: int, D: int) -> Topology:
+    """Small random topologies for the brute-force pins."""
+    rng = _rng(seed, 32)
+    L = int(rng.integers(1, 40))
+    M = int(rng.integers(1, 100)) * L
+    mem = rng.integers(0, 2 * M, size=D).astype(np.uint64)
+    perf = rng.uniform(0.5, 4.0, size=D)
+    lat = rng.uniform(0.0, 3.0, size=(D, D))
+    if rng.random() < 0.3:
+        lat = np.round(lat)                  # exact ties
+    lat = (lat + lat.T) / 2
+    np.fill_diagonal(lat, 0.0)
+    T = int(rng.integers(0, M // 2 + 1))
+    a1, a2 = [(1.0, 1.0), (0.0, 1.0), (10.0, 1.0), (1.0, 0.0)][int(rng.integers(0, 4))]
+    return Topology(mem, perf, lat, num_layers=L, model_bytes=M, kv_reserve_bytes=T,
+                    p=float(rng.choice([1.0, 0.5, 2.0])), a1=a1, a2=a2)
+
+
 def random_small(seed: int, n: int, pattern: str = "rand"):
     """Tiny brute-force-checkable instances with a random configuration.
     pattern: rand | ties | bucket | identical | descending | classes."""
