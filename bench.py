@@ -393,6 +393,37 @@ def main():
             "launches": (n + (cfg.window or n) - 1) // (cfg.window or n),
             "final_state": {"corrections": fin.corrections, "inflation_factor": fin.inflation_factor}}
 
+    # NEXT f3: HELR deployer on a 20-device B200 topology (3 nodes of 8, truncated to the 20-device
+    # limit; LLaMA-2-70B fp16, 80 layers): 2^20 x 20 DP states, 20 popcount levels
+    if not args.no_sim:
+        import workloads as W
+        t = W.b200_cluster(nodes=3, per_node=8, seed=rank)
+        t = t.replace(memory_bytes=t.memory_bytes[:20], performance=t.performance[:20],
+                      link_latency_s=np.ascontiguousarray(t.link_latency_s[:20, :20]))
+        hb = U.helr_workspace_bytes(20)
+        hws = torch.empty(hb, dtype=torch.uint8, device=dev)
+        hout = torch.zeros(U.C.sizeof(U.DeviceMap), dtype=torch.uint8, device=dev)
+        for _ in range(max(Wm, 1)):
+            U.helr_plan(t, hws, hb, hout, stream)
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(K):
+            U.helr_plan(t, hws, hb, hout, stream)
+        h1.record(stream)
+        torch.cuda.synchronize(dev)
+        hms = h0.elapsed_time(h1) / K
+        dm = U.DeviceMap.from_buffer_copy(hout.cpu().numpy().tobytes()).as_dict()
+        import math
+        relax = sum(math.comb(20, k) * k * (k - 1) for k in range(1, 21))
+        next_rows["f3_helr"] = {
+            "ms": hms, "devices": 20, "dp_states": (1 << 20) * 20, "relaxations": relax,
+            "relaxations_per_s": relax / (hms / 1e3),
+            "roofline": {"bound": "latency", "note": "20 dependent popcount levels; the DP table "
+                         "(168 MB) streams once per level", "dram_table_bytes": (1 << 20) * 20 * 9},
+            "device_map": {"devices": dm["devices"], "layer_count": dm["layer_count"],
+                           "latency_s": dm["latency_s"], "objective": dm["objective"]}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1

@@ -17,6 +17,8 @@
  *                           violations, utilisation, throughput
  *   uellm_predict_lengths   (f4) profiler stand-ins + misprediction monitor that produce the
  *                           predicted output lengths
+ *   uellm_helr_plan         (f3) HELR deployer: layer placement on a device chain (
+ *                           S:341-400)
  *
  * Citations: P:NNN = /root/reference/PAPER.md line; S:NNN = SPEC.md line; Rk = reading k in
  * DESIGN.md.  The C ABI is plain: no exceptions, no C++ or torch types, no global state, no
@@ -185,7 +187,8 @@ typedef struct {
 /* ABI version (UELLM_ABI_VERSION) and struct sizes, for bindings to check their layouts. [host] */
 uint32_t uellm_abi_version(void);
 uint64_t uellm_sizeof(int which);   /* 0 config, 1 batch_stat, 2 totals, 3 profile, 4 diagnostics,
-                                       5 sim_totals, 6 predictor, 7 monitor_state */
+                                       5 sim_totals, 6 predictor, 7 monitor_state,
+                                       8 topology, 9 device_map */
 
 /* Human-readable name of a status code.  [host]  Never NULL; static storage. */
 const char *uellm_status_string(uellm_status s);
@@ -331,6 +334,51 @@ typedef struct {
 uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, const uellm_predictor *pc,
                                    uellm_monitor_state *state, uint32_t *pred_out_len,
                                    double *window_factors, void *stream);
+
+/* HELR deployer (NEXT f3; Sec. 4.3, Alg. 2, Eq. 4-6; SPEC
+ * S:341-400; R21).  Places the model's layers on a chain of devices: the deploy-time
+ * step that fixes the KV reserve T the scheduler's cap comes from. */
+#define UELLM_HELR_MAX_DEVICES 20
+typedef struct {
+    uint32_t num_devices;           /* |D|, 1 .. UELLM_HELR_MAX_DEVICES                            */
+    uint32_t num_layers;            /* Layer(M) >= 1                                               */
+    uint64_t model_bytes;           /* M > 0; m = M / Layer(M) bytes per layer (Alg. 2 line 9)     */
+    uint64_t kv_reserve_bytes;      /* T, memory reserved for the KV cache (Alg. 2 line 11)        */
+    double p;                       /* >= 0, scales compute time (Eq. 5)                           */
+    double a1, a2;                  /* >= 0 objective weights: a1 * latency + a2 * |S| / |D|;
+                                       HE = (0, 1), LR = (10, 1)                            */
+    const uint64_t *memory_bytes;   /* [host] |D| x Memory(d)                                      */
+    const double *performance;      /* [host] |D| x Performance(d) > 0                             */
+    const double *link_latency_s;   /* [host] |D| x |D| row-major Latency(E[i][j]), finite >= 0     */
+} uellm_topology;
+
+/* The chosen chain: device[t] is the t-th device visited, holding layers
+ * [layer_begin[t], layer_begin[t] + layer_count[t]) (greedy fill in visit order). */
+typedef struct {
+    uint32_t count;                 /* devices on the chain                                        */
+    uint32_t feasible;              /* 0: no subset can hold the model (Eq. 4); other fields 0     */
+    uint32_t mask;                  /* the chosen subset S as a bit mask over device ids           */
+    uint32_t pad;
+    uint32_t device[32], layer_begin[32], layer_count[32];
+    double objective;               /* a1 * latency_s + a2 * |S| / |D|                             */
+    double latency_s;               /* chain latency: compute + link terms (Eq. 5)                 */
+} uellm_device_map;
+
+/* Device workspace for uellm_helr_plan with num_devices devices (0 if out of range).  [host] */
+size_t uellm_helr_workspace_bytes(uint32_t num_devices);
+
+/* HELR (Alg. 2) with readings R21: max_layers(d) = min(L, floor((Memory(d) - T) * L / M)) (0 when
+ * Memory(d) <= T); layers filled greedily along the visit order; one bitmask DP over (visited
+ * set, last device) dp[S][j] = min_i (dp[S\{j}][i] + Latency[i][j]) + p*x_j*m/Performance(j)
+ * (smallest i on ties); subsets with sum max_layers < L skipped (Eq. 4); the answer minimises
+ * (objective, latency, mask, last device) lexicographically.
+ *   t    [host] topology + model; UELLM_ERR_CONFIG if out of range.
+ *   ws   [device] workspace of ws_bytes >= uellm_helr_workspace_bytes(t->num_devices), 256-B aligned.
+ *   out  [host|device] 1 x uellm_device_map (host: the call synchronises `stream`).
+ * The host arrays are copied into the workspace on `stream` (pageable copies complete before the
+ * call returns). */
+uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out,
+                             void *stream);
 
 /* Attach (n <= UELLM_STAGE_COUNT) caller-owned cudaEvent_t handles (void*, created with timing
  * enabled; NULL entries are skipped) to the profile; subsequent schedule/stats calls record

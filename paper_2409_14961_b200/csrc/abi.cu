@@ -69,6 +69,29 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     return L;
 }
 
+struct HelrLayout {
+    uint64_t cap, perf, lat, binom, part_obj, part_lat, part_sj, out, capsum, dp, arg, total;
+};
+
+HelrLayout helr_layout(uint32_t D)
+{
+    HelrLayout H;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
+    const uint64_t NS = 1ull << D;
+    H.cap = take(4 * kHelrMaxDevices);
+    H.perf = take(8 * kHelrMaxDevices);
+    H.lat = take(8 * kHelrMaxDevices * kHelrMaxDevices);
+    H.binom = take(8 * (kHelrMaxDevices + 1) * (kHelrMaxDevices + 1));
+    H.part_obj = take(8 * kHelrParts); H.part_lat = take(8 * kHelrParts); H.part_sj = take(8 * kHelrParts);
+    H.out = take(sizeof(uellm_device_map));
+    H.capsum = take(8 * NS);
+    H.dp = take(8 * NS * D);
+    H.arg = take(NS * D);
+    H.total = off;
+    return H;
+}
+
 }  // namespace uellm
 
 namespace {
@@ -136,6 +159,8 @@ uint64_t uellm_sizeof(int which)
     case 5: return sizeof(uellm_sim_totals);
     case 6: return sizeof(uellm_predictor);
     case 7: return sizeof(uellm_monitor_state);
+    case 8: return sizeof(uellm_topology);
+    case 9: return sizeof(uellm_device_map);
     default: return 0;
     }
 }
@@ -542,6 +567,68 @@ uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, con
     P.monitor = pc->monitor; P.error_rate = pc->error_rate; P.gamma = pc->gamma; P.cap = pc->cap;
     P.seed = pc->seed;
     CU(run_predict(P, n, window, (cudaStream_t)stream, nullptr));
+    return UELLM_OK;
+}
+
+size_t uellm_helr_workspace_bytes(uint32_t num_devices)
+{
+    if (num_devices < 1 || num_devices > kHelrMaxDevices) return 0;
+    return (size_t)helr_layout(num_devices).total;
+}
+
+uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream)
+{
+    if (!t || !out) return UELLM_ERR_ARG;
+    const uint32_t D = t->num_devices;
+    if (D < 1 || D > kHelrMaxDevices || t->num_layers < 1 || t->model_bytes == 0) return UELLM_ERR_CONFIG;
+    if (!t->memory_bytes || !t->performance || !t->link_latency_s) return UELLM_ERR_ARG;
+    if (!(t->p >= 0.0) || !(t->a1 >= 0.0) || !(t->a2 >= 0.0) || !(t->p < 1e308) || !(t->a1 < 1e308) || !(t->a2 < 1e308))
+        return UELLM_ERR_CONFIG;
+    for (uint32_t d = 0; d < D; ++d)
+        if (!(t->performance[d] > 0.0) || !(t->performance[d] < 1e308)) return UELLM_ERR_CONFIG;
+    for (uint32_t e = 0; e < D * D; ++e)
+        if (!(t->link_latency_s[e] >= 0.0) || !(t->link_latency_s[e] < 1e308)) return UELLM_ERR_CONFIG;
+    const HelrLayout Lh = helr_layout(D);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255) || ws_bytes < Lh.total) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = (uint8_t *)ws;
+    // host-side tables: caps (exact integer floor((mem - T) * L / M)), binomials
+    uint32_t cap[kHelrMaxDevices];
+    for (uint32_t d = 0; d < D; ++d) {
+        const uint64_t mem = t->memory_bytes[d];
+        if (mem <= t->kv_reserve_bytes) { cap[d] = 0; continue; }
+        const unsigned __int128 q = (unsigned __int128)(mem - t->kv_reserve_bytes) * t->num_layers / t->model_bytes;
+        cap[d] = q >= t->num_layers ? t->num_layers : (uint32_t)q;
+    }
+    static_assert(kHelrMaxDevices <= 20, "binomial table size");
+    unsigned long long binom[(kHelrMaxDevices + 1) * (kHelrMaxDevices + 1)];
+    for (uint32_t a = 0; a <= kHelrMaxDevices; ++a)
+        for (uint32_t b = 0; b <= kHelrMaxDevices; ++b)
+            binom[a * (kHelrMaxDevices + 1) + b] =
+                b > a ? 0ull : (b == 0 || b == a) ? 1ull
+                      : binom[(a - 1) * (kHelrMaxDevices + 1) + b - 1] + binom[(a - 1) * (kHelrMaxDevices + 1) + b];
+    CU(cudaMemcpyAsync(at<uint32_t>(w, Lh.cap), cap, 4 * D, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(at<double>(w, Lh.perf), t->performance, 8 * D, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(at<double>(w, Lh.lat), t->link_latency_s, 8 * D * D, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(at<unsigned long long>(w, Lh.binom), binom, sizeof binom, cudaMemcpyHostToDevice, st));
+    const bool dev_out = is_device_ptr(out);
+    HelrParams H;
+    std::memset(&H, 0, sizeof H);
+    H.D = D; H.L = t->num_layers; H.p = t->p; H.a1 = t->a1; H.a2 = t->a2;
+    H.m = (double)t->model_bytes / (double)t->num_layers;
+    H.cap = at<uint32_t>(w, Lh.cap); H.perf = at<double>(w, Lh.perf); H.lat = at<double>(w, Lh.lat);
+    H.binom = at<unsigned long long>(w, Lh.binom); H.binom_host = binom;
+    H.capsum = at<unsigned long long>(w, Lh.capsum); H.dp = at<double>(w, Lh.dp); H.arg = at<uint8_t>(w, Lh.arg);
+    H.part_obj = at<double>(w, Lh.part_obj); H.part_lat = at<double>(w, Lh.part_lat);
+    H.part_sj = at<unsigned long long>(w, Lh.part_sj);
+    H.out = dev_out ? out : at<uellm_device_map>(w, Lh.out);
+    CU(run_helr(H, st, nullptr));
+    if (!dev_out) {
+        CU(cudaMemcpyAsync(out, H.out, sizeof(uellm_device_map), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    // (pageable host->device copies return once the source has been staged, so the stack tables
+    // above may go out of scope without a synchronisation)
     return UELLM_OK;
 }
 

@@ -250,4 +250,24 @@ struct PredictParams {
 };
 cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cudaStream_t st, int *launches);
 
+constexpr uint32_t kHelrMaxDevices = 20;        // dp table 2^20 x 20 doubles = 168 MB
+constexpr uint32_t kHelrParts = 296;            // CTAs of the feasible-minimum reduction
+struct HelrParams {
+    uint32_t D;
+    unsigned long long L;
+    double p, a1, a2, m;                        // m = M / L
+    const uint32_t *cap;                        // [D] max_layers
+    const double *perf;                         // [D]
+    const double *lat;                          // [D*D]
+    const unsigned long long *binom;            // [(kHelrMaxDevices+1)^2] C(n, k), device copy
+    const unsigned long long *binom_host;       // same table on the host (launch sizing)
+    unsigned long long *capsum;                 // [2^D]
+    double *dp;                                 // [2^D * D]
+    uint8_t *arg;                               // [2^D * D]
+    double *part_obj, *part_lat;                // [kHelrParts]
+    unsigned long long *part_sj;                // [kHelrParts] S << 32 | j
+    uellm_device_map *out;
+};
+cudaError_t run_helr(const HelrParams &H, cudaStream_t st, int *launches);
+
 }  // namespace uellm

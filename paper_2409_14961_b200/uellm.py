@@ -76,6 +76,24 @@ class MonitorState(C.Structure):
     _fields_ = [("corrections", C.c_uint64), ("inflation_factor", C.c_double), ("scratch", C.c_uint64 * 2)]
 
 
+class Topology(C.Structure):
+    _fields_ = [("num_devices", C.c_uint32), ("num_layers", C.c_uint32), ("model_bytes", C.c_uint64),
+                ("kv_reserve_bytes", C.c_uint64), ("p", C.c_double), ("a1", C.c_double), ("a2", C.c_double),
+                ("memory_bytes", C.c_void_p), ("performance", C.c_void_p), ("link_latency_s", C.c_void_p)]
+
+
+class DeviceMap(C.Structure):
+    _fields_ = [("count", C.c_uint32), ("feasible", C.c_uint32), ("mask", C.c_uint32), ("pad", C.c_uint32),
+                ("device", C.c_uint32 * 32), ("layer_begin", C.c_uint32 * 32), ("layer_count", C.c_uint32 * 32),
+                ("objective", C.c_double), ("latency_s", C.c_double)]
+
+    def as_dict(self):
+        k = self.count
+        return {"feasible": bool(self.feasible), "mask": self.mask, "devices": list(self.device[:k]),
+                "layer_begin": list(self.layer_begin[:k]), "layer_count": list(self.layer_count[:k]),
+                "objective": self.objective, "latency_s": self.latency_s}
+
+
 class Profile(C.Structure):
     _fields_ = [("opaque", C.c_uint64 * 40)]
 
@@ -121,6 +139,10 @@ _lib.uellm_simulate.restype = C.c_int32
 _lib.uellm_simulate.argtypes = [C.POINTER(Profile), C.POINTER(Config)] + [C.c_void_p] * 8
 _lib.uellm_predict_lengths.restype = C.c_int32
 _lib.uellm_predict_lengths.argtypes = [C.c_uint64, C.c_void_p, C.POINTER(Predictor)] + [C.c_void_p] * 4
+_lib.uellm_helr_workspace_bytes.restype = C.c_size_t
+_lib.uellm_helr_workspace_bytes.argtypes = [C.c_uint32]
+_lib.uellm_helr_plan.restype = C.c_int32
+_lib.uellm_helr_plan.argtypes = [C.POINTER(Topology), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
 _lib.uellm_set_stage_events.restype = C.c_int32
 _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
 _lib.uellm_get_diagnostics.restype = C.c_int32
@@ -135,6 +157,8 @@ assert _lib.uellm_sizeof(4) == C.sizeof(Diagnostics)
 assert _lib.uellm_sizeof(5) == C.sizeof(SimTotals)
 assert _lib.uellm_sizeof(6) == C.sizeof(Predictor)
 assert _lib.uellm_sizeof(7) == C.sizeof(MonitorState)
+assert _lib.uellm_sizeof(8) == C.sizeof(Topology)
+assert _lib.uellm_sizeof(9) == C.sizeof(DeviceMap)
 
 LIBRARY_PATH = _LIB_PATH
 
@@ -225,6 +249,25 @@ def make_predictor(pc) -> Predictor:
 def predict_lengths(n: int, true_out_len, pc: Predictor, state, pred_out_len, window_factors=None, stream=None):
     _check(_lib.uellm_predict_lengths(n, _ptr(true_out_len), C.byref(pc), _ptr(state), _ptr(pred_out_len),
                                       _ptr(window_factors), _stream_handle(stream)), "uellm_predict_lengths")
+
+
+def helr_workspace_bytes(num_devices: int) -> int:
+    return _lib.uellm_helr_workspace_bytes(num_devices)
+
+
+def helr_plan(topo, ws, ws_bytes: int, out=None, stream=None) -> DeviceMap | None:
+    """topo: any object with the uellm_topology scalar fields + numpy arrays memory_bytes (u64),
+    performance (f64), link_latency_s (f64 [D, D]) (e.g. workloads.Topology).  out=None returns a
+    host DeviceMap (synchronising); otherwise out is a device buffer of sizeof(DeviceMap) bytes."""
+    mem = np.ascontiguousarray(topo.memory_bytes, np.uint64)
+    perf = np.ascontiguousarray(topo.performance, np.float64)
+    lat = np.ascontiguousarray(topo.link_latency_s, np.float64)
+    t = Topology(len(mem), topo.num_layers, topo.model_bytes, topo.kv_reserve_bytes, topo.p, topo.a1, topo.a2,
+                 mem.ctypes.data, perf.ctypes.data, lat.ctypes.data)
+    host = DeviceMap() if out is None else None
+    _check(_lib.uellm_helr_plan(C.byref(t), _ptr(ws), ws_bytes, C.addressof(host) if host is not None else _ptr(out),
+                                _stream_handle(stream)), "uellm_helr_plan")
+    return host
 
 
 STAGES = ["sched_begin", "sort_end", "decode_end", "dp_local_end", "dp_fix_end", "dp_cascade_end",
