@@ -178,6 +178,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200 import distributed as D
     from paper_2409_14961_b200.distributed import GATHER_WORDS, combine_totals
     from paper_2409_14961_b200.scheduler import GpuScheduler
 
@@ -208,8 +209,12 @@ def main():
         for row in ev:
             for e in row:
                 e.record(stream)          # materialise the cudaEvent_t handles
-    gather_buf = torch.zeros(world * GATHER_WORDS, dtype=torch.int64, device=dev)
-    gather_in = torch.zeros(GATHER_WORDS, dtype=torch.int64, device=dev)
+    # a9 exchange buffer: [16 totals words | boundary bitmap of this rank's positions] (every rank
+    # schedules n queries, so the buffers have one size)
+    xw = D.exchange_words(n)
+    gather_buf = torch.zeros(world * xw, dtype=torch.int64, device=dev)
+    gather_in = torch.zeros(xw, dtype=torch.int64, device=dev)
+    bm_view = D.bitmap_view(gather_in)
 
     def step(k=None):
         if k is not None:
@@ -220,7 +225,8 @@ def main():
             U.set_stage_events(g.profile, ev[k])
         g.schedule(stream)
         g.stats(stream)
-        if world > 1:   # a9: one NCCL allgather of the per-rank totals (device-resident)
+        if world > 1:   # a9: ONE NCCL allgather of per-rank totals + batch-boundary bitmap
+            U.boundary_bitmap(g.profile, g.cfg, bm_view, stream)
             with torch.cuda.stream(stream):
                 gather_in[:13].copy_(g.totals.view(torch.int64)[:13])
                 dist.all_gather_into_tensor(gather_buf, gather_in)
@@ -306,6 +312,7 @@ def main():
             U.schedule_batches(p, g.cfg, h_order, h_offs, h_nb, stream)
             U.batch_stats(p, g.cfg, h_offs, h_nb, None, h_tot, stream)
             if world > 1:
+                U.boundary_bitmap(p, g.cfg, bm_view, stream)
                 with torch.cuda.stream(stream):
                     gather_in[:13].copy_(h_tot.view(torch.int64)[:13], non_blocking=True)
                     dist.all_gather_into_tensor(gather_buf, gather_in)
@@ -437,14 +444,15 @@ def main():
             "config": {"workload": desc, "queries_per_rank": n, "window": cfg.window,
                        "max_batch": cfg.max_batch, "lambda_us": cfg.lambda_us,
                        "l2": "inputs 1.2 GB/rank >> 126 MB L2; no flush needed",
-                       "parallelism": f"{world} rank(s), windows independent, one allgather of totals"},
+                       "parallelism": f"{world} rank(s), windows independent, one allgather of totals + boundary bitmaps"},
             "roofline": roof, "step_hbm_roofline": step_hbm, "stage_ms": st_ms,
             # our kernels launched inside the timed region: K steps x (load + schedule + stats)
             "gpu_launches": K * int(diag["sched_launches"] + diag["stats_launches"] + 1),
             "gpu_launches_per_step": int(diag["sched_launches"] + diag["stats_launches"] + 1),
             "diagnostics": diag, "batches": m, "dp_cost": res["totals"]["dp_cost"],
-            "job_totals": ({k: v for k, v in combine_totals(gather_buf.view(world, GATHER_WORDS)).items()
+            "job_totals": ({k: v for k, v in combine_totals(gather_buf.view(world, xw)[:, :GATHER_WORDS]).items()
                             if k in ("n", "batches", "dp_cost", "viol_alone")} if world > 1 else None),
+            "a9_exchange_bytes_per_rank": 8 * xw,
             "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "next_rows": next_rows,
         }
         print(json.dumps(line), flush=True)

@@ -380,6 +380,13 @@ size_t uellm_helr_workspace_bytes(uint32_t num_devices);
 uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out,
                              void *stream);
 
+/* Boundary bitmap of the last uellm_schedule_batches call on p (the a9 exchange format):
+ * bit k of words (k = 0 .. n, word k / 32, bit k % 32) is set iff a batch starts at scheduled
+ * position k, i.e. iff k is one of batch_offsets[0 .. num_batches] (bit n = the end).
+ *   words  [device] capacity (n + 32) / 32 x u32; written stream-ordered, never synchronises. */
+uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *cfg, uint32_t *words,
+                                   void *stream);
+
 /* Attach (n <= UELLM_STAGE_COUNT) caller-owned cudaEvent_t handles (void*, created with timing
  * enabled; NULL entries are skipped) to the profile; subsequent schedule/stats calls record
  * event k at stage boundary k on their stream.  n = 0 detaches.  [host] */

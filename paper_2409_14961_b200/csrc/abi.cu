@@ -570,6 +570,22 @@ uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, con
     return UELLM_OK;
 }
 
+uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *cfg, uint32_t *words, void *stream)
+{
+    if (!p || !cfg || !words) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
+    if (!is_device_ptr(words)) return UELLM_ERR_ARG;
+    const WsLayout L = make_layout(v.n, *cfg);
+    if (v.n == 0) {
+        const uint32_t one = 1u;                       // n = 0: the single boundary 0 (= n)
+        CU(cudaMemcpyAsync(words, &one, 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));   // pageable: staged before return
+        return UELLM_OK;
+    }
+    CU(cudaMemcpyAsync(words, v.ws + L.bitmap, 4 * L.nwords, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return UELLM_OK;
+}
+
 size_t uellm_helr_workspace_bytes(uint32_t num_devices)
 {
     if (num_devices < 1 || num_devices > kHelrMaxDevices) return 0;

@@ -1,7 +1,10 @@
 """Multi-GPU sharding of the scheduling path: windows are independent (no batch
 crosses a window, O1), so rank r owns the contiguous window block
 [floor(N_w*r/P), floor(N_w*(r+1)/P)) and runs the whole path on its own GPU with no data-path
-collective.  The one exchange step (a9) is a single all_gather of fixed-size per-rank totals.
+collective.  The one exchange step (a9) is a single all_gather of a fixed-size per-rank buffer:
+the rank's totals (16 int64 words) followed by its boundary bitmap over its own scheduled
+positions (uellm_boundary_bitmap: bit k set iff a batch starts at local position k, k = 0..n_r),
+padded to the largest rank.  Every rank can then rebuild the whole job's batch_offsets.
 
 torch.distributed is plumbing here (NCCL on GPUs, gloo in the CPU tests); no scheduling
 arithmetic happens in this module.
@@ -64,3 +67,37 @@ def combine_totals(gathered: torch.Tensor) -> dict:
     mk = out["makespan_us"]
     out["throughput_tok_s"] = out["gen_tokens"] / (mk * 1e-6) if mk else 0.0
     return out
+
+
+def exchange_words(n_max: int) -> int:
+    """int64 words of one rank's a9 buffer: totals + bitmap of n_max + 1 bits (u32 words, 2 per int64)."""
+    u32 = (n_max + 1 + 31) // 32
+    return GATHER_WORDS + (u32 + 1) // 2
+
+
+def bitmap_view(buf: torch.Tensor) -> torch.Tensor:
+    """The u32 bitmap region of one rank's int64 exchange buffer (a view: the library writes it in place)."""
+    return buf[GATHER_WORDS:].view(torch.int32)
+
+
+def all_gather_exchange(mine: torch.Tensor, group=None) -> torch.Tensor:
+    """a9: ONE all_gather_into_tensor of the per-rank [totals | bitmap] buffers -> [world, words]."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty(world * mine.numel(), dtype=torch.int64, device=mine.device)
+    dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
+    return out.view(world, mine.numel())
+
+
+def global_offsets(gathered: torch.Tensor, ranges) -> np.ndarray:
+    """Whole-job batch_offsets from the gathered buffers: rank r's set bits k (0 <= k <= n_r) are
+    global positions q0_r + k; consecutive ranks share the boundary q1_r = q0_{r+1}."""
+    g = gathered.cpu().numpy()
+    parts = []
+    for r, (q0, q1) in enumerate(ranges):
+        n_r = q1 - q0
+        words = g[r, GATHER_WORDS:].view(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: n_r + 1]
+        parts.append(np.flatnonzero(bits).astype(np.int64) + q0)
+    allpos = np.concatenate(parts) if parts else np.zeros(1, np.int64)
+    return np.unique(allpos)

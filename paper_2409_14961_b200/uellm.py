@@ -143,6 +143,8 @@ _lib.uellm_helr_workspace_bytes.restype = C.c_size_t
 _lib.uellm_helr_workspace_bytes.argtypes = [C.c_uint32]
 _lib.uellm_helr_plan.restype = C.c_int32
 _lib.uellm_helr_plan.argtypes = [C.POINTER(Topology), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+_lib.uellm_boundary_bitmap.restype = C.c_int32
+_lib.uellm_boundary_bitmap.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p]
 _lib.uellm_set_stage_events.restype = C.c_int32
 _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
 _lib.uellm_get_diagnostics.restype = C.c_int32
@@ -249,6 +251,11 @@ def make_predictor(pc) -> Predictor:
 def predict_lengths(n: int, true_out_len, pc: Predictor, state, pred_out_len, window_factors=None, stream=None):
     _check(_lib.uellm_predict_lengths(n, _ptr(true_out_len), C.byref(pc), _ptr(state), _ptr(pred_out_len),
                                       _ptr(window_factors), _stream_handle(stream)), "uellm_predict_lengths")
+
+
+def boundary_bitmap(p: Profile, cfg: Config, words, stream=None):
+    _check(_lib.uellm_boundary_bitmap(C.byref(p), C.byref(cfg), _ptr(words), _stream_handle(stream)),
+           "uellm_boundary_bitmap")
 
 
 def helr_workspace_bytes(num_devices: int) -> int:

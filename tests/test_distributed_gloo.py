@@ -36,8 +36,20 @@ def _worker(rank, world, port, q):
         _, tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], cfg, order, offs)
         g = D.all_gather_totals(D.pack_totals(tot, "cpu"))
         comb = D.combine_totals(g)
+        # the a9 buffer proper: [totals | boundary bitmap of this rank's positions], padded to the
+        # largest rank (on the GPU the library writes the bitmap, uellm_boundary_bitmap)
+        ranges = [D.query_range(len(inp), cfg.window, world, r) for r in range(world)]
+        n_max = max(b - a_ for a_, b in ranges)
+        buf = torch.zeros(D.exchange_words(n_max), dtype=torch.int64)
+        buf[:D.GATHER_WORDS] = D.pack_totals(tot, "cpu")
+        bits = np.zeros(32 * D.bitmap_view(buf).numel(), np.uint8)
+        bits[offs.astype(np.int64)] = 1
+        D.bitmap_view(buf).copy_(torch.from_numpy(np.packbits(bits, bitorder="little").view(np.int32)))
+        gx = D.all_gather_exchange(buf)
+        offs_all = D.global_offsets(gx, ranges)
+        comb2 = D.combine_totals(gx[:, :D.GATHER_WORDS])
         if rank == 0:
-            q.put((comb, cost))
+            q.put((comb, cost, offs_all, comb2))
     finally:
         dist.destroy_process_group()
 
@@ -69,7 +81,7 @@ def test_allgather_world2_equals_single_process():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    comb, _ = q.get(timeout=300)
+    comb, _, offs_all, comb2 = q.get(timeout=300)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -80,6 +92,8 @@ def test_allgather_world2_equals_single_process():
     for f in D.TOTAL_FIELDS:
         assert comb[f] == tot[f], f
     assert comb["dp_cost"] == cost
+    assert np.array_equal(offs_all, offs.astype(np.int64))      # global batch boundaries
+    assert comb2 == comb
     assert comb["mean_latency_s"] == pytest.approx(tot["mean_latency_s"], rel=1e-12)
     assert comb["throughput_tok_s"] == pytest.approx(tot["throughput_tok_s"], rel=1e-12)
 

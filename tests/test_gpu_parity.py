@@ -265,11 +265,23 @@ def test_sharded_ranks_equal_single_run():
     from paper_2409_14961_b200 import distributed as D
     inp, out, slo, cfg = W.c3(12, n=400_000)
     cfg = cfg.replace(window=30_000)
+    from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.scheduler import GpuScheduler
     full = gpu_run(inp, out, slo, cfg)
-    rows, offs_all = [], []
+    rows, offs_all, bufs = [], [], []
+    ranges = [D.query_range(len(inp), cfg.window, 4, r) for r in range(4)]
+    n_max = max(z - a for a, z in ranges)
     for r in range(4):
-        a, z = D.query_range(len(inp), cfg.window, 4, r)
+        a, z = ranges[r]
         part = gpu_run(inp[a:z], out[a:z], slo[a:z], cfg)
+        # the a9 buffer as bench.py builds it: totals + the library's boundary bitmap
+        g = GpuScheduler(z - a, cfg, device="cuda:0")
+        g.run(torch.from_numpy(inp[a:z].view(np.int32)).cuda(), torch.from_numpy(out[a:z].view(np.int32)).cuda(),
+              torch.from_numpy(slo[a:z]).cuda())
+        buf = torch.zeros(D.exchange_words(n_max), dtype=torch.int64, device="cuda:0")
+        U.boundary_bitmap(g.profile, g.cfg, D.bitmap_view(buf))
+        buf[:13] = g.totals.view(torch.int64)[:13]
+        bufs.append(buf)
         rows.append(D.pack_totals(part["totals"], "cpu"))
         offs_all.append(part["offsets"][:-1].astype(np.int64) + a)
         assert np.array_equal(part["order"].astype(np.int64) + a, full["order"][a:z].astype(np.int64))
@@ -278,6 +290,11 @@ def test_sharded_ranks_equal_single_run():
     comb = D.combine_totals(torch.stack(rows))
     for f in D.TOTAL_FIELDS:
         assert comb[f] == full["totals"][f], f
+    gathered = torch.stack(bufs)
+    assert np.array_equal(D.global_offsets(gathered, ranges), full["offsets"].astype(np.int64))
+    comb2 = D.combine_totals(gathered[:, :D.GATHER_WORDS])
+    for f in D.TOTAL_FIELDS:
+        assert comb2[f] == full["totals"][f], f
 
 
 def test_sort_paths_compressed_and_generic():
