@@ -163,7 +163,8 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override query count (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-sim", action="store_true", help="skip the NEXT f2 simulator timing")
+    ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-row timings (f2, f3, f4)")
+    ap.add_argument("--e2e-groups", type=int, default=0, help="window groups of the pipelined e2e call (0 = 8)")
     ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
     ap.add_argument("--mode", default="seg_dp", choices=["seg_dp", "slo_odbs", "fifo", "sort_only"],
                     help="segmentation mode (default: the SEG-DP hot path)")
@@ -296,25 +297,30 @@ def main():
                 "peak_gbs": hbm_gbs, "frac": comp / (ms_step_max / 1e3) / 1e9 / hbm_gbs,
                 "peak_source": peak_src}
 
-    # e2e: the C-ABI with HOST buffers (pinned), H2D/D2H inside the timed region
+    # e2e: the C-ABI with HOST buffers (pinned), H2D/D2H inside the timed region.  The public
+    # host-buffer entry point uellm_schedule_pipelined cuts the job into window groups and overlaps
+    # group g's compute with the PCIe copies of its neighbours (same results as the three calls).
     e2e = None
     if not args.no_e2e:
+        import ctypes
         p_in = torch.from_numpy(inp.view(np.int32)).pin_memory()
         p_out = torch.from_numpy(out.view(np.int32)).pin_memory()
         p_slo = torch.from_numpy(slo).pin_memory()
         h_order = torch.empty(n, dtype=torch.int32).pin_memory()
         h_offs = torch.empty(n + 1, dtype=torch.int32).pin_memory()
-        h_nb = torch.zeros(1, dtype=torch.int64).pin_memory()
-        h_tot = torch.zeros(U.TOTALS_BYTES, dtype=torch.uint8).pin_memory()
+        h_nb = np.zeros(1, np.uint64)
+        h_tot = U.Totals()
+        groups = args.e2e_groups
+        pwsb = U.pipeline_workspace_bytes(n, g.cfg, groups)
+        pws = torch.empty(pwsb, dtype=torch.uint8, device=dev)
 
         def e2e_step():
-            p = U.profile_load(n, p_in, p_out, p_slo, g.cfg, g.ws, g.ws_bytes, stream)
-            U.schedule_batches(p, g.cfg, h_order, h_offs, h_nb, stream)
-            U.batch_stats(p, g.cfg, h_offs, h_nb, None, h_tot, stream)
+            U.schedule_pipelined(n, p_in, p_out, p_slo, g.cfg, groups, pws, pwsb, h_order, h_offs, h_nb,
+                                 ctypes.addressof(h_tot), stream)
             if world > 1:
-                U.boundary_bitmap(p, g.cfg, bm_view, stream)
                 with torch.cuda.stream(stream):
-                    gather_in[:13].copy_(h_tot.view(torch.int64)[:13], non_blocking=True)
+                    gather_in[:13].copy_(torch.from_numpy(np.frombuffer(bytes(h_tot), np.int64)[:13].copy()),
+                                         non_blocking=False)
                     dist.all_gather_into_tensor(gather_buf, gather_in)
         e2e_step()
         torch.cuda.synchronize(dev)
@@ -330,11 +336,11 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1) / K], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        mh = int(h_nb.item())
+        mh = int(h_nb[0])
         e2e = {"value": world * n / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 4 * n + 4 * (mh + 1) + 8 + U.TOTALS_BYTES,
-               "ms_per_step": float(te.item())}
-        assert mh == m, "host-buffer path disagrees with the device path"
+               "ms_per_step": float(te.item()), "api": f"uellm_schedule_pipelined ({groups or 8} window groups)"}
+        assert mh == m and h_tot.dp_cost == res["totals"]["dp_cost"], "host-buffer path disagrees with the device path"
 
     # NEXT f2: the sequential-execution simulator over this step's schedule, timed on its own
     # (not part of the a1-a9 step): Poisson arrivals resident in HBM, per-batch ends and

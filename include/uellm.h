@@ -11,6 +11,8 @@
  *                           sorted stream into batches (SEG-DP / Alg. 1 / FIFO / sort-only)
  *   uellm_batch_stats       per-batch padding, generated tokens (b x O), KV-cache peak
  *                           bytes (4*b*l*h*(s+n)), estimated latency and SLO violations
+ *   uellm_schedule_pipelined  the three calls for host-resident queries, window groups
+ *                           pipelined against the PCIe copies
  *
  * and the adjacent steps of SURVEY.md section 8(f):
  *   uellm_simulate          (f2) sequential execution of a schedule with arrivals: latency, SLO
@@ -379,6 +381,25 @@ size_t uellm_helr_workspace_bytes(uint32_t num_devices);
  * call returns). */
 uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out,
                              void *stream);
+
+/* End-to-end scheduling of HOST-resident queries with the PCIe copies overlapped with the GPU
+ * work.  Windows are independent (R15), so the job is cut into `groups` groups of whole windows
+ * (0 = 8); group g+1's host->device copy and group g-1's device->host copy run on two internal
+ * copy streams while group g is loaded, scheduled and summarised on `stream` -- the same
+ * results as uellm_profile_load + uellm_schedule_batches + uellm_batch_stats on the whole job
+ * (mean_latency_s is re-weighted from the groups' means: within 1e-12 relative).
+ *   q                       [host] queries with HOST arrays (pinned for overlap; pageable works
+ *                           but serialises the copies).
+ *   ws                      [device] >= uellm_pipeline_workspace_bytes(n, cfg, groups), 256-B aligned.
+ *   order, batch_offsets    [host] n and n+1 x u32 (pinned for overlap), as uellm_schedule_batches.
+ *   num_batches, totals     [host].
+ * Creates and destroys two streams, 3 x groups events and a small pinned host block per call;
+ * synchronises `stream` once per group (each group's load reads its validation record) and at
+ * the end.  On an error the host outputs are unspecified. */
+size_t uellm_pipeline_workspace_bytes(uint64_t n, const uellm_config *cfg, uint32_t groups);
+uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config *cfg, uint32_t groups, void *ws,
+                                      size_t ws_bytes, uint32_t *order, uint32_t *batch_offsets,
+                                      uint64_t *num_batches, uellm_totals *totals, void *stream);
 
 /* Boundary bitmap of the last uellm_schedule_batches call on p (the a9 exchange format):
  * bit k of words (k = 0 .. n, word k / 32, bit k % 32) is set iff a batch starts at scheduled

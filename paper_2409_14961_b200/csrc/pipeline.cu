@@ -1,0 +1,234 @@
+// pipeline.cu -- end-to-end scheduling of HOST-resident queries with the PCIe copies overlapped
+// with the GPU work (uellm_schedule_pipelined).  Windows are independent (R15, O1), so the job
+// is cut into groups of whole windows; group g's host->device copy runs on a copy stream while
+// group g-1 is loaded / scheduled / summarised on the caller's stream, and group g-1's results
+// go back on a second copy stream.  Host code (stream/event orchestration) plus one tiny kernel.
+//
+//   H stream : H2D(g+1) into input staging slot (g+1)%2   [waits: compute of g-1 done]
+//   C stream : load(g) (sync: host decisions need its maxima) -> schedule(g) -> stats(g)
+//              -> rebase order/offsets to global indices      [waits: H2D(g), D2H(g-2) done]
+//   D stream : D2H(g) of order, offsets, totals                [waits: compute of g done]
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace uellm {
+
+__global__ void k_add_base(uint32_t *a, uint64_t n, uint32_t base)
+{
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += nt) a[k] += base;
+}
+
+static cudaError_t add_base(uint32_t *a, uint64_t n, uint32_t base, cudaStream_t st)
+{
+    if (n == 0 || base == 0) return cudaSuccess;
+    const uint64_t nb = ceil_div(n, 256 * 4);
+    k_add_base<<<(unsigned)(nb < 148 * 8 ? nb : 148 * 8), 256, 0, st>>>(a, n, base);
+    return cudaGetLastError();
+}
+
+struct PipeLayout {
+    uint64_t group_q;                 // queries per full group (whole windows)
+    uint64_t groups;
+    uint64_t ws, ws_bytes;            // per-group scheduling workspace (re-used by every group)
+    uint64_t in[2], out[2], slo[2];   // input staging slots
+    uint64_t order[2], offs[2];       // output staging slots
+    uint64_t tot, nb;                 // per-group totals / num_batches (device)
+    uint64_t total;
+};
+
+static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t groups)
+{
+    PipeLayout P;
+    std::memset(&P, 0, sizeof P);
+    const uint64_t wl = cfg.window ? (cfg.window < n ? cfg.window : n) : n;
+    const uint64_t nwin = n ? ceil_div(n, wl ? wl : 1) : 0;
+    uint64_t G = groups ? groups : 8;
+    if (G > nwin) G = nwin ? nwin : 1;
+    const uint64_t wpg = nwin ? ceil_div(nwin, G) : 1;          // windows per group
+    P.group_q = n ? wpg * wl : 0;
+    if (P.group_q > n) P.group_q = n;
+    P.groups = n ? ceil_div(nwin, wpg) : 0;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
+    uellm_config c = cfg;
+    c.window = (uint32_t)wl;
+    P.ws_bytes = make_layout(P.group_q, c).total;
+    P.ws = take(P.ws_bytes);
+    const uint64_t q = P.group_q ? P.group_q : 1;
+    for (int s = 0; s < 2; ++s) {
+        P.in[s] = take(4 * q); P.out[s] = take(4 * q); P.slo[s] = take(4 * q);
+        P.order[s] = take(4 * q); P.offs[s] = take(4 * (q + 1));
+    }
+    P.tot = take(sizeof(uellm_totals) * (P.groups ? P.groups : 1));
+    P.nb = take(8 * (P.groups ? P.groups : 1));
+    P.total = off;
+    return P;
+}
+
+}  // namespace uellm
+
+using namespace uellm;
+
+extern "C" {
+
+size_t uellm_pipeline_workspace_bytes(uint64_t n, const uellm_config *cfg, uint32_t groups)
+{
+    if (!cfg) return 0;
+    return (size_t)pipe_layout(n, *cfg, groups).total;
+}
+
+uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config *cfg, uint32_t groups, void *ws,
+                                      size_t ws_bytes, uint32_t *order, uint32_t *batch_offsets,
+                                      uint64_t *num_batches, uellm_totals *totals, void *stream)
+{
+    if (!q || !cfg || !order || !batch_offsets || !num_batches || !totals) return UELLM_ERR_ARG;
+    const uint64_t n = q->n;
+    if (n >= 0xffffffffull) return UELLM_ERR_ARG;
+    if (n > 0 && (!q->input_len || !q->pred_out_len || !q->slo_s)) return UELLM_ERR_ARG;
+    const PipeLayout PL = pipe_layout(n, *cfg, groups);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255) || ws_bytes < PL.total) return UELLM_ERR_ARG;
+    uint8_t *w = (uint8_t *)ws;
+    cudaStream_t C = (cudaStream_t)stream;
+    if (n == 0) {
+        // the single-call path handles the empty job (no copies to overlap)
+        uellm_profile p;
+        uellm_status s = uellm_profile_load(q, cfg, w + PL.ws, PL.ws_bytes, stream, &p);
+        if (s != UELLM_OK) return s;
+        if ((s = uellm_schedule_batches(&p, cfg, order, batch_offsets, num_batches, stream)) != UELLM_OK) return s;
+        return uellm_batch_stats(&p, cfg, batch_offsets, num_batches, nullptr, totals, stream);
+    }
+    const uint64_t G = PL.groups, gq = PL.group_q;
+    uellm_config gcfg = *cfg;
+    gcfg.window = (uint32_t)(cfg->window ? (cfg->window < n ? cfg->window : n) : n);
+    cudaStream_t H = nullptr, D = nullptr;
+    std::vector<cudaEvent_t> h2d(G, nullptr), done(G, nullptr), d2h(G, nullptr);
+    std::vector<uint64_t> m(G, 0);
+    uint64_t *nb_host = nullptr;
+    uellm_totals *tot_host = nullptr;
+    uellm_status status = UELLM_OK;
+    auto qa = [&](uint64_t g) { return g * gq; };
+    auto qz = [&](uint64_t g) { return (g + 1) * gq < n ? (g + 1) * gq : n; };
+#define PCU(x)                                   \
+    do {                                         \
+        if ((x) != cudaSuccess) {                \
+            cudaGetLastError();                  \
+            return UELLM_ERR_CUDA;               \
+        }                                        \
+    } while (0)
+  auto body = [&]() -> uellm_status {
+    PCU(cudaStreamCreateWithFlags(&H, cudaStreamNonBlocking));
+    PCU(cudaStreamCreateWithFlags(&D, cudaStreamNonBlocking));
+    for (uint64_t g = 0; g < G; ++g) {
+        PCU(cudaEventCreateWithFlags(&h2d[g], cudaEventDisableTiming));
+        PCU(cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming));
+        PCU(cudaEventCreateWithFlags(&d2h[g], cudaEventDisableTiming));
+    }
+    PCU(cudaMallocHost(&nb_host, 8 * G));
+    PCU(cudaMallocHost(&tot_host, sizeof(uellm_totals) * G));
+    {
+        // everything already queued on the caller's stream happens before our copies
+        cudaEvent_t start;
+        PCU(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+        cudaEventRecord(start, C);
+        cudaStreamWaitEvent(H, start, 0);
+        cudaStreamWaitEvent(D, start, 0);
+        cudaEventDestroy(start);
+    }
+    auto enqueue_h2d = [&](uint64_t g) -> cudaError_t {
+        const int s = (int)(g & 1);
+        if (g >= 2) cudaStreamWaitEvent(H, done[g - 2], 0);    // staging slot free again
+        const uint64_t a = qa(g), len = qz(g) - a;
+        cudaError_t e;
+        if ((e = cudaMemcpyAsync(w + PL.in[s], q->input_len + a, 4 * len, cudaMemcpyHostToDevice, H))) return e;
+        if ((e = cudaMemcpyAsync(w + PL.out[s], q->pred_out_len + a, 4 * len, cudaMemcpyHostToDevice, H))) return e;
+        if ((e = cudaMemcpyAsync(w + PL.slo[s], q->slo_s + a, 4 * len, cudaMemcpyHostToDevice, H))) return e;
+        return cudaEventRecord(h2d[g], H);
+    };
+    // D2H of group g's offsets needs m[g] (read after the host has synchronised past schedule(g))
+    auto enqueue_d2h = [&](uint64_t g, uint64_t moff) -> cudaError_t {
+        const int s = (int)(g & 1);
+        const uint64_t a = qa(g), len = qz(g) - a;
+        cudaStreamWaitEvent(D, done[g], 0);
+        cudaError_t e;
+        if ((e = cudaMemcpyAsync(order + a, w + PL.order[s], 4 * len, cudaMemcpyDeviceToHost, D))) return e;
+        // offsets[0 .. m_g) of the group (its closing offset is the next group's first, or n)
+        if ((e = cudaMemcpyAsync(batch_offsets + moff, w + PL.offs[s], 4 * m[g], cudaMemcpyDeviceToHost, D))) return e;
+        return cudaEventRecord(d2h[g], D);
+    };
+    PCU(enqueue_h2d(0));
+    {
+        uint64_t moff = 0;
+        for (uint64_t g = 0; g < G; ++g) {
+            const int s = (int)(g & 1);
+            const uint64_t a = qa(g), len = qz(g) - a;
+            if (g + 1 < G) PCU(enqueue_h2d(g + 1));
+            PCU(cudaStreamWaitEvent(C, h2d[g], 0));
+            if (g >= 2) PCU(cudaStreamWaitEvent(C, d2h[g - 2], 0));     // output slot free again
+            uellm_queries gq_ = {len, (const uint32_t *)(w + PL.in[s]), (const uint32_t *)(w + PL.out[s]),
+                                 (const float *)(w + PL.slo[s])};
+            uellm_profile prof;
+            // synchronises C: by now schedule(g-1) has completed and m[g-1] is on the host
+            uellm_status st = uellm_profile_load(&gq_, &gcfg, w + PL.ws, PL.ws_bytes, stream, &prof);
+            if (st != UELLM_OK) return st;
+            if (g >= 1) {
+                m[g - 1] = nb_host[g - 1];
+                PCU(enqueue_d2h(g - 1, moff));
+                moff += m[g - 1];
+            }
+            uint32_t *d_order = (uint32_t *)(w + PL.order[s]);
+            uint32_t *d_offs = (uint32_t *)(w + PL.offs[s]);
+            uint64_t *d_nb = (uint64_t *)(w + PL.nb) + g;
+            uellm_totals *d_tot = (uellm_totals *)(w + PL.tot) + g;
+            if ((st = uellm_schedule_batches(&prof, &gcfg, d_order, d_offs, d_nb, stream)) != UELLM_OK) return st;
+            if ((st = uellm_batch_stats(&prof, &gcfg, d_offs, d_nb, nullptr, d_tot, stream)) != UELLM_OK) return st;
+            PCU(add_base(d_order, len, (uint32_t)a, C));       // group-local -> caller indices
+            PCU(add_base(d_offs, len + 1, (uint32_t)a, C));    // (only [0, m_g] are copied)
+            PCU(cudaMemcpyAsync(nb_host + g, d_nb, 8, cudaMemcpyDeviceToHost, C));
+            PCU(cudaMemcpyAsync(tot_host + g, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, C));
+            PCU(cudaEventRecord(done[g], C));
+        }
+        PCU(cudaStreamSynchronize(C));
+        m[G - 1] = nb_host[G - 1];
+        PCU(enqueue_d2h(G - 1, moff));
+        moff += m[G - 1];
+        PCU(cudaStreamSynchronize(D));
+        batch_offsets[moff] = (uint32_t)n;
+        *num_batches = moff;
+        // whole-job totals from the per-group integer totals (exact); the latency mean is
+        // re-weighted by the group sizes, the throughput recomputed from the integer sums
+        uellm_totals T;
+        std::memset(&T, 0, sizeof T);
+        double lat = 0.0;
+        for (uint64_t g = 0; g < G; ++g) {
+            const uellm_totals &t = tot_host[g];
+            T.n += t.n; T.batches += t.batches; T.gen_tokens += t.gen_tokens; T.pad_in += t.pad_in;
+            T.pad_out += t.pad_out; T.kv_bytes_max = t.kv_bytes_max > T.kv_bytes_max ? t.kv_bytes_max : T.kv_bytes_max;
+            T.dp_cost += t.dp_cost; T.viol_alone += t.viol_alone; T.viol_seq += t.viol_seq;
+            T.over_cap += t.over_cap; T.makespan_us += t.makespan_us;
+            lat += t.mean_latency_s * (double)t.n;
+        }
+        T.mean_latency_s = T.n ? lat / (double)T.n : 0.0;
+        T.throughput_tok_s = T.makespan_us ? (double)T.gen_tokens / ((double)T.makespan_us * 1e-6) : 0.0;
+        *totals = T;
+    }
+    return UELLM_OK;
+  };
+    status = body();
+    if (status != UELLM_OK) { cudaStreamSynchronize(C); }
+    if (H) { cudaStreamSynchronize(H); cudaStreamDestroy(H); }
+    if (D) { cudaStreamSynchronize(D); cudaStreamDestroy(D); }
+    for (uint64_t g = 0; g < G; ++g) {
+        if (h2d[g]) cudaEventDestroy(h2d[g]);
+        if (done[g]) cudaEventDestroy(done[g]);
+        if (d2h[g]) cudaEventDestroy(d2h[g]);
+    }
+    if (nb_host) cudaFreeHost(nb_host);
+    if (tot_host) cudaFreeHost(tot_host);
+#undef PCU
+    return status;
+}
+
+}  // extern "C"

@@ -145,6 +145,11 @@ _lib.uellm_helr_plan.restype = C.c_int32
 _lib.uellm_helr_plan.argtypes = [C.POINTER(Topology), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
 _lib.uellm_boundary_bitmap.restype = C.c_int32
 _lib.uellm_boundary_bitmap.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p]
+_lib.uellm_pipeline_workspace_bytes.restype = C.c_size_t
+_lib.uellm_pipeline_workspace_bytes.argtypes = [C.c_uint64, C.POINTER(Config), C.c_uint32]
+_lib.uellm_schedule_pipelined.restype = C.c_int32
+_lib.uellm_schedule_pipelined.argtypes = [C.POINTER(Queries), C.POINTER(Config), C.c_uint32, C.c_void_p,
+                                          C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
 _lib.uellm_set_stage_events.restype = C.c_int32
 _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
 _lib.uellm_get_diagnostics.restype = C.c_int32
@@ -251,6 +256,18 @@ def make_predictor(pc) -> Predictor:
 def predict_lengths(n: int, true_out_len, pc: Predictor, state, pred_out_len, window_factors=None, stream=None):
     _check(_lib.uellm_predict_lengths(n, _ptr(true_out_len), C.byref(pc), _ptr(state), _ptr(pred_out_len),
                                       _ptr(window_factors), _stream_handle(stream)), "uellm_predict_lengths")
+
+
+def pipeline_workspace_bytes(n: int, cfg: Config, groups: int = 0) -> int:
+    return _lib.uellm_pipeline_workspace_bytes(n, C.byref(cfg), groups)
+
+
+def schedule_pipelined(n: int, input_len, pred_out_len, slo_s, cfg: Config, groups: int, ws, ws_bytes: int,
+                       order, batch_offsets, num_batches, totals, stream=None):
+    q = Queries(n, _ptr(input_len), _ptr(pred_out_len), _ptr(slo_s))
+    _check(_lib.uellm_schedule_pipelined(C.byref(q), C.byref(cfg), groups, _ptr(ws), ws_bytes, _ptr(order),
+                                         _ptr(batch_offsets), _ptr(num_batches), _ptr(totals),
+                                         _stream_handle(stream)), "uellm_schedule_pipelined")
 
 
 def boundary_bitmap(p: Profile, cfg: Config, words, stream=None):

@@ -24,7 +24,8 @@ def kname(s):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--rep", required=True)
+    ap.add_argument("--rep", default=None, help=".ncu-rep (or pass --raw)")
+    ap.add_argument("--raw", default=None, help="csv of `ncu -i REP --page raw --csv`")
     ap.add_argument("--launches", required=True)
     ap.add_argument("--bench", required=True)
     ap.add_argument("--tag", default="r01")
@@ -52,7 +53,8 @@ def main():
     open(os.path.join(HERE, f"{a.tag}_launch_shares.csv"), "w").write("\n".join(lines) + "\n")
 
     # full capture
-    raw = subprocess.check_output(["ncu", "-i", a.rep, "--page", "raw", "--csv"]).decode()
+    raw = (open(a.raw).read() if a.raw else
+           subprocess.check_output(["ncu", "-i", a.rep, "--page", "raw", "--csv"]).decode())
     rr = list(csv.reader(io.StringIO(raw)))
     h, units, body = rr[0], rr[1], rr[2:]
     ix = {n: h.index(n) for n in h}
@@ -76,7 +78,7 @@ def main():
                   "issue_active_pct": float(r[ix["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                   "warps_active_pct": float(r[ix["sm__warps_active.avg.pct_of_peak_sustained_active"]]),
                   "registers": int(float(r[ix["launch__registers_per_thread"]]))}
-    summ = {"round": a.tag, "source": f"ncu --set full --clock-control none; {os.path.basename(a.rep)}; "
+    summ = {"round": a.tag, "source": f"ncu --set full --clock-control none; {os.path.basename(a.rep or a.raw)}; "
                                      "bench.py c4 (1e8 queries, seed 0), one step",
             "dp_candidate_evals_c4_seed0": evals,
             "dp_warp_inst_per_eval": K["k_dp_tiles"]["inst_executed"] / evals, "kernels": K}

@@ -331,3 +331,54 @@ def test_mode_slo_odbs_single_window_many_tiles():
     inp, out, slo, cfg = W.c2(16, n=250_000)
     cfg = cfg.replace(mode=W.MODE_SLO_ODBS, w1=1.0, w2=0.05, threshold=400.0, window=0)
     assert_parity(inp, out, slo, cfg, nthreads=1)
+
+
+@pytest.mark.parametrize("n,window,groups", [(2_000_000, 100_000, 0), (1_234_567, 100_000, 3),
+                                             (300_000, 0, 0), (250_000, 60_000, 64)])
+def test_pipelined_host_end_to_end(n, window, groups):
+    """uellm_schedule_pipelined (window groups overlapped with the PCIe copies) gives the oracle's
+    whole-job schedule and totals from pinned host buffers."""
+    from paper_2409_14961_b200 import uellm as U
+    inp, out, slo, cfg = W.c3(17, n=n)
+    cfg = cfg.replace(window=window)
+    c = U.make_config(cfg)
+    wsb = U.pipeline_workspace_bytes(n, c, groups)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda:0")
+    p_in = torch.from_numpy(inp.view(np.int32)).pin_memory()
+    p_out = torch.from_numpy(out.view(np.int32)).pin_memory()
+    p_slo = torch.from_numpy(slo).pin_memory()
+    h_order = torch.empty(n, dtype=torch.int32).pin_memory()
+    h_offs = torch.empty(n + 1, dtype=torch.int32).pin_memory()
+    nb = np.zeros(1, np.uint64)
+    tot = U.Totals()
+    import ctypes
+    U.schedule_pipelined(n, p_in, p_out, p_slo, c, groups, ws, wsb, h_order, h_offs, nb, ctypes.addressof(tot))
+    m = int(nb[0])
+    o_order, o_offs, o_m, o_cost = oracle.schedule(inp, out, slo, cfg, nthreads=8)
+    assert m == o_m
+    assert np.array_equal(h_order.numpy().view(np.uint32), o_order)
+    assert np.array_equal(h_offs.numpy().view(np.uint32)[: m + 1], o_offs)
+    _, o_tot = oracle.stats(inp, out, slo, cfg, o_order, o_offs)
+    t = tot.as_dict()
+    for f in TOT_INT:
+        assert t[f] == o_tot[f], f
+    assert t["dp_cost"] == o_cost
+    for f in ("mean_latency_s", "throughput_tok_s"):
+        assert t[f] == pytest.approx(o_tot[f], rel=1e-12), f
+
+
+def test_pipelined_contract_error():
+    from paper_2409_14961_b200 import uellm as U
+    inp, out, slo, cfg = W.c3(18, n=200_000)
+    cfg = cfg.replace(window=50_000)
+    slo = slo.copy()
+    slo[170_000] = 0.0                       # in the last group
+    c = U.make_config(cfg)
+    wsb = U.pipeline_workspace_bytes(len(inp), c, 4)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda:0")
+    tot = U.Totals()
+    with pytest.raises(U.UellmError) as e:
+        U.schedule_pipelined(len(inp), inp, out, slo, c, 4, ws, wsb, np.zeros(len(inp), np.uint32),
+                             np.zeros(len(inp) + 1, np.uint32), np.zeros(1, np.uint64),
+                             __import__("ctypes").addressof(tot))
+    assert e.value.status == U.ERR_CONTRACT
