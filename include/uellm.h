@@ -328,14 +328,19 @@ typedef struct {
  * observation at a time, before window w + 1 is predicted.
  *   true_out_len   [device] n x u32, true (generated) output length of caller query k.
  *   pc             [host] predictor; UELLM_ERR_CONFIG if a field is out of range.
- *   state          [device] 1 x uellm_monitor_state, read and updated on the stream.
+ *   state          [device] 1 x uellm_monitor_state, read and updated on the stream; its
+ *                  inflation_factor must be >= 1.
  *   pred_out_len   [device] n x u32 output (feeds uellm_queries.pred_out_len).
  *   window_factors [device] capacity nwin + 1 x f64 or NULL: factor used by each window, then
  *                  the final factor.
- * One kernel launch per window; never synchronises. */
+ *   ws, ws_bytes   [device] optional scratch (NULL, 0 = none).  With ws_bytes >=
+ *                  uellm_predict_workspace_bytes(n, pc) > 0 the factor levels are evaluated for all
+ *                  windows in one pass (4 launches); otherwise one launch per window.  Same results.
+ * Never synchronises. */
+size_t uellm_predict_workspace_bytes(uint64_t n, const uellm_predictor *pc);
 uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, const uellm_predictor *pc,
                                    uellm_monitor_state *state, uint32_t *pred_out_len,
-                                   double *window_factors, void *stream);
+                                   double *window_factors, void *ws, size_t ws_bytes, void *stream);
 
 /* HELR deployer (NEXT f3; Sec. 4.3, Alg. 2, Eq. 4-6; SPEC
  * S:341-400; R21).  Places the model's layers on a chain of devices: the deploy-time

@@ -1,5 +1,6 @@
 // abi.cu -- the C ABI of include/uellm.h: argument/config validation, workspace carving and
 // stream-ordered orchestration of the kernels (host code only; no allocation, no globals).
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -7,6 +8,15 @@
 using namespace uellm;
 
 namespace uellm {
+
+uint64_t sort_group_windows(uint64_t window, uint64_t nwin)
+{
+    uint64_t q = 4ull << 20;                           // ~4 M queries: 16-48 MB per pass in flight
+    if (const char *e = getenv("UELLM_SORT_GROUP_Q")) q = strtoull(e, nullptr, 10);
+    uint64_t g = window ? q / window : 1;
+    if (g < 1) g = 1;
+    return g < nwin ? g : (nwin ? nwin : 1);
+}
 
 uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_tile)
 {
@@ -311,24 +321,32 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         uint32_t *kc = at<uint32_t>(w, L.keysc);
         uint32_t *vals0 = at<uint32_t>(w, L.vals0);
         CU(launch_slo_table(at<uint32_t>(w, L.slo_set), at<uint32_t>(w, L.slo_table), at<uint32_t>(w, L.slo_rank), st));
+        launches += 1;
         uint32_t mask = 0;
         for (int d = 0; d < 4; ++d) if (8 * d < rb + ob) mask |= 1u << d;
-        CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, L.nwin, at<uint32_t>(w, L.slo_set),
-                              at<uint32_t>(w, L.slo_rank), ob, kc, vals0, at<uint32_t>(w, L.hist), st));
-        launches += 2;
+        // window groups: every pass of a group runs before the next group starts, so the group's
+        // keys / payloads stay in L2 between passes
+        const uint64_t gw = mask ? sort_group_windows(L.window, L.nwin) : L.nwin;
         const uint32_t *k32 = kc;
-        const uint32_t *vals = nullptr;            // identity payload (arrival index = position)
-        (void)vals0;
-        CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
-                                (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                                at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st,
-                                (mask & 1u) != 0, &D));
-        launches += 3 * passes - ((mask & 1u) && passes ? 1 : 0);
-        rec(v, UELLM_STAGE_SORT_END, st);
-        if (passes == 0) {
-            CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
+        for (uint64_t w0 = 0; w0 < L.nwin; w0 += gw) {
+            const uint64_t wn = L.nwin - w0 < gw ? L.nwin - w0 : gw;
+            CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, w0, wn, at<uint32_t>(w, L.slo_set),
+                                  at<uint32_t>(w, L.slo_rank), ob, kc, vals0, at<uint32_t>(w, L.hist), st));
             launches += 1;
+            k32 = kc;
+            const uint32_t *vals = nullptr;            // identity payload (arrival index = position)
+            CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
+                                    (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
+                                    at<uint32_t>(w, L.hist), n, L.window, w0, wn, mask, &passes, st,
+                                    (mask & 1u) != 0, &D));
+            launches += 3 * passes - ((mask & 1u) && passes ? 1 : 0);
+            if (passes == 0) {
+                CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
+                launches += 1;                         // (mask == 0: one group covers every window)
+            }
         }
+        (void)vals0;
+        rec(v, UELLM_STAGE_SORT_END, st);
     } else {
         unsigned long long *k0 = at<unsigned long long>(w, L.keys0);
         uint32_t *v0 = at<uint32_t>(w, L.vals0);
@@ -340,10 +358,17 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
             const unsigned long long vary = v.key_or ^ v.key_and;
             uint32_t mask = 0;
             for (int d = 0; d < 8; ++d) if ((vary >> (8 * d)) & 0xffull) mask |= 1u << d;
-            CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
-                                  at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                                  at<uint32_t>(w, L.hist), n, L.window, L.nwin, mask, &passes, st, &D));
-            launches += 3 * passes;
+            const uint64_t gw = sort_group_windows(L.window, L.nwin);
+            for (uint64_t w0 = 0; w0 < L.nwin; w0 += gw) {
+                const uint64_t wn = L.nwin - w0 < gw ? L.nwin - w0 : gw;
+                keys = k0;
+                vals = v0;
+                CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
+                                      at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
+                                      at<uint32_t>(w, L.hist), n, L.window, w0, wn, mask, &passes, st, &D));
+                launches += 3 * passes;
+                if (passes == 0) break;
+            }
         }
         rec(v, UELLM_STAGE_SORT_END, st);
         if (passes == 0) {
@@ -542,9 +567,37 @@ uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, con
     return UELLM_OK;
 }
 
+// level-path scratch (0 = the level path does not apply: too many windows or factor levels)
+static uint64_t predict_ws_bytes(uint64_t n, const uellm_predictor *pc, uint64_t *nwin_out)
+{
+    const uint64_t window = pc->window ? (pc->window < n ? pc->window : n) : (n ? n : 1);
+    const uint64_t nwin = n ? ceil_div(n, window) : 0;
+    if (nwin_out) *nwin_out = nwin;
+    if (n == 0 || nwin > kPredMaxWindows) return 0;
+    if (pc->monitor) {
+        // the chain from factor 1 is the longest from any factor >= 1 (fl(v*gamma) is monotone)
+        double v = 1.0;
+        uint32_t K = 0;
+        for (;;) {
+            const double h = v * pc->gamma;
+            const double nv = h < pc->cap ? h : pc->cap;
+            if (nv == v) break;
+            v = nv;
+            if (++K >= kPredMaxLevels - 1) return 0;
+        }
+    }
+    return align_up(8 * kPredMaxLevels, 256) + 256 + align_up(8ull * kPredMaxLevels * nwin, 256) + align_up(nwin, 256);
+}
+
+size_t uellm_predict_workspace_bytes(uint64_t n, const uellm_predictor *pc)
+{
+    if (!pc) return 0;
+    return (size_t)predict_ws_bytes(n, pc, nullptr);
+}
+
 uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, const uellm_predictor *pc,
                                    uellm_monitor_state *state, uint32_t *pred_out_len, double *window_factors,
-                                   void *stream)
+                                   void *ws, size_t ws_bytes, void *stream)
 {
     if (!pc || !state || !is_device_ptr(state)) return UELLM_ERR_ARG;
     if (n >= 0xffffffffull) return UELLM_ERR_ARG;
@@ -566,6 +619,15 @@ uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, con
     P.variant = pc->variant; P.bucket_width = pc->bucket_width; P.constant_tokens = pc->constant_tokens;
     P.monitor = pc->monitor; P.error_rate = pc->error_rate; P.gamma = pc->gamma; P.cap = pc->cap;
     P.seed = pc->seed;
+    uint64_t nwin_l = 0;
+    const uint64_t need = predict_ws_bytes(n, pc, &nwin_l);
+    if (ws && need && ws_bytes >= need && is_device_ptr(ws) && !(reinterpret_cast<uintptr_t>(ws) & 255)) {
+        uint8_t *b = (uint8_t *)ws;
+        P.levels = (double *)b;
+        P.nlevels = (uint32_t *)(b + align_up(8 * kPredMaxLevels, 256));
+        P.hist = (unsigned long long *)(b + align_up(8 * kPredMaxLevels, 256) + 256);
+        P.wlevel = b + align_up(8 * kPredMaxLevels, 256) + 256 + align_up(8ull * kPredMaxLevels * nwin_l, 256);
+    }
     CU(run_predict(P, n, window, (cudaStream_t)stream, nullptr));
     return UELLM_OK;
 }

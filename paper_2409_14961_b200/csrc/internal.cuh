@@ -138,13 +138,17 @@ struct DecodeArgs {
 };
 // compressed path: rank table, then pack key32 = rank << ob | out with the digit-0 histogram
 cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, uint32_t *rank_of_slot, cudaStream_t st);
-cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t nwin,
-                               const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob, uint32_t *keys32,
-                               uint32_t *vals, uint32_t *hist0, cudaStream_t st);
+// [w_first, w_first + nwin): the windows processed by this call (window groups keep a group's
+// intermediate arrays resident in L2 across the passes)
+cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t w_first,
+                               uint64_t nwin, const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob,
+                               uint32_t *keys32, uint32_t *vals, uint32_t *hist0, cudaStream_t st);
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
-                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st,
-                                 bool hist0_ready = false, const DecodeArgs *dec = nullptr);
+                                 uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
+                                 cudaStream_t st, bool hist0_ready = false, const DecodeArgs *dec = nullptr);
+// windows per sort group: about kSortGroupQueries queries (env UELLM_SORT_GROUP_Q overrides, tuning)
+uint64_t sort_group_windows(uint64_t window, uint64_t nwin);
 cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const uint32_t *in, uint64_t n,
                             const uint32_t *table, int ob, uint32_t *rin, uint32_t *rout, uint32_t *rslo,
                             uint32_t *order, cudaStream_t st);
@@ -156,7 +160,7 @@ cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const ui
 cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
                                unsigned long long *keys_a, uint32_t *vals_a,
                                unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
-                               uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
+                               uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
                                int *passes, cudaStream_t st, const struct DecodeArgs *dec = nullptr);
 
 // Decode sorted keys into records: slo = key >> 32, out = key & 0xffffffff, idx = val.
@@ -238,7 +242,13 @@ struct SimParams {
 };
 cudaError_t run_simulate(const SimParams &S, cudaStream_t st, int *launches);
 
+constexpr uint32_t kPredMaxLevels = 32;         // factor levels of the level path (chain v_0 .. v_K)
+constexpr uint64_t kPredMaxWindows = 1ull << 20; // windows of the level path (histogram rows)
 struct PredictParams {
+    double *levels;                             // level path: [kPredMaxLevels] chain, NULL = window path
+    uint32_t *nlevels;                          // K (last level index)
+    unsigned long long *hist;                   // [nwin][kPredMaxLevels] under-predictions per level
+    uint8_t *wlevel;                            // [nwin] level of each window
     const uint32_t *true_len;
     uint32_t *pred;
     uellm_monitor_state *state;

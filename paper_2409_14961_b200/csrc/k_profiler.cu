@@ -11,10 +11,17 @@
 //   and rounded up").  Monitor: every under-prediction (true > pred) counts one
 //   correction and factor <- min(factor * gamma, cap).
 //
-// k_predict_window (one launch per window, position-linear): predictions with the factor in
-// force at the window's start, under-prediction count reduced per CTA; the last CTA to finish
-// (threadfence + arrival counter) applies the monitor update for the window's corrections and
-// publishes the next window's factor in the device-resident monitor state.
+// Two schedules of the same computation:
+//  * level path (a workspace is given, <= kPredMaxLevels factor levels, <= kPredMaxWindows
+//    windows): the factor only ever moves along the chain v_0 = factor, v_{i+1} = min(v_i*gamma,
+//    cap) (one step per correction), so every window's under-prediction count is computed for
+//    EVERY level at once (k_pred_count, one position-linear pass over all windows), a single
+//    thread walks the windows through the chain (k_pred_chain: level l_{w+1} = min(l_w + c_w(l_w),
+//    K)), and k_pred_write writes each window's predictions with its level's factor -- 4 launches
+//    in total instead of one per window;
+//  * window path: k_predict_window, one launch per window: predictions with the factor in
+//    force, under-prediction count reduced per CTA; the last CTA to finish (threadfence +
+//    arrival counter) applies the monitor update and publishes the next window's factor.
 #include "internal.cuh"
 
 namespace uellm {
@@ -107,6 +114,82 @@ __global__ void __launch_bounds__(256) k_predict_window(PredictParams P, uint64_
     cnt[1] = 0;
 }
 
+// ---- level path
+__global__ void k_pred_levels(PredictParams P)
+{
+    if (threadIdx.x != 0) return;
+    double v = P.state->inflation_factor;
+    uint32_t K = 0;
+    P.levels[0] = v;
+    if (P.monitor) {
+        while (K < kPredMaxLevels - 1) {
+            const double h = __dmul_rn(v, P.gamma);
+            const double nv = h < P.cap ? h : P.cap;
+            if (nv == v) break;                 // fixpoint: cap reached (or gamma == 1)
+            v = nv;
+            P.levels[++K] = v;
+        }
+    }
+    *P.nlevels = K;
+}
+
+__global__ void __launch_bounds__(256) k_pred_count(PredictParams P, uint64_t n, uint64_t window)
+{
+    __shared__ double V[kPredMaxLevels];
+    const uint32_t K = *P.nlevels;
+    if (threadIdx.x <= K) V[threadIdx.x] = P.levels[threadIdx.x];
+    __syncthreads();
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t n_pad = ceil_div(n, 32) * 32;             // whole warps stay in the loop
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_pad; k += nt) {
+        uint32_t under = 0;
+        uint32_t w = 0xffffffffu;
+        if (k < n) {
+            const uint32_t t = __ldg(P.true_len + k);
+            w = (uint32_t)(k / window);
+            for (uint32_t i = 0; i <= K; ++i) under |= (uint32_t)(t > predict_one(P, k, t, V[i])) << i;
+        }
+        const uint32_t grp = __match_any_sync(0xffffffffu, w);
+        const uint32_t lane = threadIdx.x & 31;
+        const bool leader = (__ffs(grp) - 1) == (int)lane;
+        for (uint32_t i = 0; i <= K; ++i) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (under >> i) & 1u) & grp;
+            if (leader && b && w != 0xffffffffu)
+                atomicAdd(P.hist + (uint64_t)w * kPredMaxLevels + i, (unsigned long long)__popc(b));
+        }
+    }
+}
+
+__global__ void k_pred_chain(PredictParams P, uint64_t nwin)
+{
+    if (threadIdx.x != 0) return;
+    const uint32_t K = *P.nlevels;
+    uint32_t l = 0;
+    unsigned long long corr = 0;
+    for (uint64_t w = 0; w < nwin; ++w) {
+        P.wlevel[w] = (uint8_t)l;
+        if (P.factors) P.factors[w] = P.levels[l];
+        const unsigned long long c = P.hist[w * kPredMaxLevels + l];
+        corr += c;
+        const unsigned long long nl = (unsigned long long)l + c;
+        l = nl < K ? (uint32_t)nl : K;
+    }
+    if (P.factors) P.factors[nwin] = P.levels[l];
+    if (P.monitor) {
+        P.state->corrections += corr;
+        P.state->inflation_factor = P.levels[l];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pred_write(PredictParams P, uint64_t n, uint64_t window)
+{
+    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += nt) {
+        const uint32_t t = __ldg(P.true_len + k);
+        P.pred[k] = predict_one(P, k, t, P.levels[P.wlevel[k / window]]);
+    }
+}
+
 __global__ void k_predict_empty(PredictParams P)
 {
     if (P.factors) P.factors[0] = P.state->inflation_factor;
@@ -118,6 +201,17 @@ cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cud
     if (n == 0) {
         k_predict_empty<<<1, 1, 0, st>>>(P);
         l = 1;
+    } else if (P.levels) {
+        const uint64_t nwin = ceil_div(n, window);
+        cudaError_t e;
+        if ((e = cudaMemsetAsync(P.hist, 0, 8 * kPredMaxLevels * nwin, st))) return e;
+        k_pred_levels<<<1, 32, 0, st>>>(P);
+        const uint64_t nb = ceil_div(n, 256 * 4);
+        const unsigned blocks = (unsigned)(nb < 148 * 8 ? nb : 148 * 8);
+        k_pred_count<<<blocks, 256, 0, st>>>(P, n, window);
+        k_pred_chain<<<1, 32, 0, st>>>(P, nwin);
+        k_pred_write<<<blocks, 256, 0, st>>>(P, n, window);
+        l = 4;
     } else {
         for (uint64_t w = 0, a = 0; a < n; a += window, ++w) {
             const uint64_t z = a + window < n ? a + window : n;

@@ -38,14 +38,16 @@ __device__ __forceinline__ void tile_range(uint64_t t, uint64_t n, uint64_t wind
 
 template <class K>
 __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ kin, uint32_t *__restrict__ hist,
-                                                          uint64_t n, uint64_t window, uint64_t tpw, int shift)
+                                                          uint64_t n, uint64_t window, uint64_t tpw, int shift,
+                                                          uint64_t t0)
 {
     __shared__ uint32_t h[256];
     const int tid = threadIdx.x;
     if (tid < 256) h[tid] = 0;
     __syncthreads();
     uint64_t start, end;
-    tile_range(blockIdx.x, n, window, tpw, start, end);
+    const uint64_t tile = t0 + blockIdx.x;
+    tile_range(tile, n, window, tpw, start, end);
 #pragma unroll 4
     for (uint32_t i = 0; i < kSortItems; ++i) {
         uint64_t p = start + (uint64_t)i * kSortThreads + tid;
@@ -58,18 +60,18 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ 
         }
     }
     __syncthreads();
-    if (tid < 256) hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
+    if (tid < 256) hist[tile * 256 + tid] = h[tid];
 }
 
 // 1024 threads per window: thread (g, d) owns digit d of the g-th quarter of the window's tiles.
 // Column loads are issued 8 at a time (independent), so the pass is bandwidth- not latency-bound.
 constexpr int kScanGroups = 4;
 __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__restrict__ hist, uint64_t n,
-                                                                 uint64_t window, uint64_t tpw)
+                                                                 uint64_t window, uint64_t tpw, uint64_t w_first)
 {
     __shared__ uint32_t gs[kScanGroups][256];
     __shared__ uint32_t s[256];
-    const uint64_t w = blockIdx.x;
+    const uint64_t w = w_first + blockIdx.x;
     const int d = threadIdx.x & 255, g = threadIdx.x >> 8;
     const uint64_t w0 = w * window;
     const uint64_t L = min(window, n - w0);
@@ -119,7 +121,8 @@ template <class K, bool DECODE>
 __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                             K *__restrict__ kout, uint32_t *__restrict__ vout,
                                                             const uint32_t *__restrict__ hist, uint64_t n,
-                                                            uint64_t window, uint64_t tpw, int shift, DecodeArgs D)
+                                                            uint64_t window, uint64_t tpw, int shift, DecodeArgs D,
+                                                            uint64_t t0)
 {
     constexpr int kWarps = kSortThreads / 32;
     constexpr int kPerWarpIters = kSortTile / kWarps / 32;     // 16
@@ -128,11 +131,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
     __shared__ uint32_t stab[DECODE && sizeof(K) == 4 ? kSloRankMax : 1];
     extern __shared__ __align__(16) unsigned char dyn[];      // staging: K[kSortTile] + u32[kSortTile]
     uint64_t start, end;
-    tile_range(blockIdx.x, n, window, tpw, start, end);
+    const uint64_t tile = t0 + blockIdx.x;
+    tile_range(tile, n, window, tpw, start, end);
     if (start >= end) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < kWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
-    if (tid < 256) tbase[tid] = hist[(uint64_t)blockIdx.x * 256 + tid];
+    if (tid < 256) tbase[tid] = hist[tile * 256 + tid];
     if (DECODE && sizeof(K) == 4)
         for (int i = tid; i < (int)kSloRankMax; i += kSortThreads) stab[i] = D.table[i];
     __syncthreads();
@@ -223,13 +227,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict_
 template <class K>
 static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, K *keys_a, uint32_t *vals_a,
                                    K *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n, uint64_t window,
-                                   uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st,
-                                   bool hist0_ready, const DecodeArgs *dec)
+                                   uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
+                                   cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
 {
     *passes = 0;
     if (n == 0) return cudaSuccess;
     const uint64_t tpw = ceil_div(window, kSortTile);
-    const uint64_t tiles = tpw * nwin;
+    const uint64_t tiles = tpw * nwin, t0 = tpw * w_first;
     const K *kin = *keys_io;
     const uint32_t *vin = *vals_io;
     int last = -1;
@@ -240,17 +244,17 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
         if (!(hist0_ready && *passes == 0))
-            k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d);
-        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hist, n, window, tpw);
+            k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d, t0);
+        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hist, n, window, tpw, w_first);
         const size_t stage = kSortTile * (sizeof(K) + sizeof(uint32_t));
         if (dec && d == last) {
             cudaFuncSetAttribute(k_sort_down<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
             k_sort_down<K, true><<<(unsigned)tiles, kSortThreads, stage, st>>>(kin, vin, kout, vout, hist, n, window,
-                                                                              tpw, 8 * d, D0);
+                                                                              tpw, 8 * d, D0, t0);
         } else {
             cudaFuncSetAttribute(k_sort_down<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
             k_sort_down<K, false><<<(unsigned)tiles, kSortThreads, stage, st>>>(kin, vin, kout, vout, hist, n, window,
-                                                                               tpw, 8 * d, D0);
+                                                                               tpw, 8 * d, D0, t0);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -266,20 +270,20 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
 cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
                                unsigned long long *keys_a, uint32_t *vals_a,
                                unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
-                               uint64_t n, uint64_t window, uint64_t nwin, uint32_t digit_mask,
+                               uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
                                int *passes, cudaStream_t st, const DecodeArgs *dec)
 {
     return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window,
-                                               nwin, digit_mask, passes, st, false, dec);
+                                               w_first, nwin, digit_mask, passes, st, false, dec);
 }
 
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
-                                 uint64_t window, uint64_t nwin, uint32_t digit_mask, int *passes, cudaStream_t st,
-                                 bool hist0_ready, const DecodeArgs *dec)
+                                 uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
+                                 cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
 {
-    return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window, nwin,
-                                     digit_mask, passes, st, hist0_ready, dec);
+    return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window, w_first,
+                                     nwin, digit_mask, passes, st, hist0_ready, dec);
 }
 
 // a2 (compressed key) fused with the digit-0 histogram of the first radix pass:
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
                                                               const uint32_t *__restrict__ slo_set,
                                                               const uint32_t *__restrict__ rank_of_slot, int ob,
                                                               uint32_t *__restrict__ keys32, uint32_t *__restrict__ vals,
-                                                              uint32_t *__restrict__ hist)
+                                                              uint32_t *__restrict__ hist, uint64_t t0)
 {
     __shared__ uint32_t sset[kSloSetSize], srank[kSloSetSize];
     __shared__ uint32_t h[256];
@@ -299,7 +303,8 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
     if (tid < 256) h[tid] = 0;
     __syncthreads();
     uint64_t start, end;
-    tile_range(blockIdx.x, n, window, tpw, start, end);
+    const uint64_t tile = t0 + blockIdx.x;
+    tile_range(tile, n, window, tpw, start, end);
 #pragma unroll 4
     for (uint32_t i = 0; i < kSortItems; ++i) {
         const uint64_t p = start + (uint64_t)i * kSortThreads + tid;
@@ -318,17 +323,17 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
         }
     }
     __syncthreads();
-    if (tid < 256) hist[(uint64_t)blockIdx.x * 256 + tid] = h[tid];
+    if (tid < 256) hist[tile * 256 + tid] = h[tid];
 }
 
-cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t nwin,
-                               const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob, uint32_t *keys32,
-                               uint32_t *vals, uint32_t *hist0, cudaStream_t st)
+cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t w_first,
+                               uint64_t nwin, const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob,
+                               uint32_t *keys32, uint32_t *vals, uint32_t *hist0, cudaStream_t st)
 {
     if (n == 0) return cudaSuccess;
     const uint64_t tpw = ceil_div(window, kSortTile);
     k_pack32_hist<<<(unsigned)(tpw * nwin), kSortThreads, 0, st>>>(out, slo, n, window, tpw, slo_set, rank_of_slot,
-                                                                  ob, keys32, vals, hist0);
+                                                                  ob, keys32, vals, hist0, tpw * w_first);
     return cudaGetLastError();
 }
 

@@ -138,7 +138,10 @@ _lib.uellm_batch_stats.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_vo
 _lib.uellm_simulate.restype = C.c_int32
 _lib.uellm_simulate.argtypes = [C.POINTER(Profile), C.POINTER(Config)] + [C.c_void_p] * 8
 _lib.uellm_predict_lengths.restype = C.c_int32
-_lib.uellm_predict_lengths.argtypes = [C.c_uint64, C.c_void_p, C.POINTER(Predictor)] + [C.c_void_p] * 4
+_lib.uellm_predict_lengths.argtypes = [C.c_uint64, C.c_void_p, C.POINTER(Predictor)] + [C.c_void_p] * 4 + \
+    [C.c_void_p, C.c_size_t, C.c_void_p]
+_lib.uellm_predict_workspace_bytes.restype = C.c_size_t
+_lib.uellm_predict_workspace_bytes.argtypes = [C.c_uint64, C.POINTER(Predictor)]
 _lib.uellm_helr_workspace_bytes.restype = C.c_size_t
 _lib.uellm_helr_workspace_bytes.argtypes = [C.c_uint32]
 _lib.uellm_helr_plan.restype = C.c_int32
@@ -253,9 +256,15 @@ def make_predictor(pc) -> Predictor:
     return p
 
 
-def predict_lengths(n: int, true_out_len, pc: Predictor, state, pred_out_len, window_factors=None, stream=None):
+def predict_workspace_bytes(n: int, pc: Predictor) -> int:
+    return _lib.uellm_predict_workspace_bytes(n, C.byref(pc))
+
+
+def predict_lengths(n: int, true_out_len, pc: Predictor, state, pred_out_len, window_factors=None, stream=None,
+                    ws=None, ws_bytes: int = 0):
     _check(_lib.uellm_predict_lengths(n, _ptr(true_out_len), C.byref(pc), _ptr(state), _ptr(pred_out_len),
-                                      _ptr(window_factors), _stream_handle(stream)), "uellm_predict_lengths")
+                                      _ptr(window_factors), _ptr(ws), ws_bytes, _stream_handle(stream)),
+           "uellm_predict_lengths")
 
 
 def pipeline_workspace_bytes(n: int, cfg: Config, groups: int = 0) -> int:

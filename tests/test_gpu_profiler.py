@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 P = W.PredictorConfig
 
 
-def gpu_predict(t, pc, factor0=1.0):
+def gpu_predict(t, pc, factor0=1.0, levels=True):
     from paper_2409_14961_b200 import uellm as U
     dev = torch.device("cuda:0")
     n = len(t)
@@ -26,7 +26,11 @@ def gpu_predict(t, pc, factor0=1.0):
     wl = pc.window or max(n, 1)
     nwin = (n + wl - 1) // wl
     d_f = torch.zeros(nwin + 1, dtype=torch.float64, device=dev)
-    U.predict_lengths(n, d_t if n else None, U.make_predictor(pc), d_state, d_p if n else None, d_f)
+    cp = U.make_predictor(pc)
+    wsb = U.predict_workspace_bytes(n, cp) if levels else 0
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    U.predict_lengths(n, d_t if n else None, cp, d_state, d_p if n else None, d_f, ws=ws if wsb else None,
+                      ws_bytes=wsb)
     torch.cuda.synchronize()
     s = U.MonitorState.from_buffer_copy(d_state.cpu().numpy().tobytes())
     return d_p[:n].cpu().numpy().view(np.uint32), d_f.cpu().numpy(), s
@@ -38,9 +42,10 @@ def gpu_predict(t, pc, factor0=1.0):
                                 P(variant=2, error_rate=1.0, bucket_width=8, window=0, seed=5),
                                 P(variant=3, constant_tokens=64, window=2048, gamma=1.01, cap=3.0),
                                 P(variant=3, constant_tokens=1, window=100, monitor=0)])
-def test_predict_parity(pc):
+@pytest.mark.parametrize("levels", [True, False])
+def test_predict_parity(pc, levels):
     t = W.true_output_lengths(60_000, 7)
-    pred, factors, st = gpu_predict(t, pc)
+    pred, factors, st = gpu_predict(t, pc, levels=levels)
     o_pred, o_factors, o_corr = oracle.profile_stream(t, pc)
     assert np.array_equal(pred, o_pred)
     assert np.array_equal(factors, o_factors)            # bit-identical doubles (same operation order)
@@ -48,20 +53,37 @@ def test_predict_parity(pc):
     assert list(st.scratch) == [0, 0]
 
 
-def test_predict_factor0_and_saturation():
+@pytest.mark.parametrize("levels", [True, False])
+def test_predict_factor0_and_saturation(levels):
     t = np.full(5000, 4_000_000_000, np.uint32)
     pc = P(variant=0, window=1000)
-    pred, factors, st = gpu_predict(t, pc, factor0=1.5)
+    pred, factors, st = gpu_predict(t, pc, factor0=1.5, levels=levels)
     o_pred, o_factors, o_corr = oracle.profile_stream(t, pc, factor0=1.5)
     assert np.array_equal(pred, o_pred) and np.all(pred == 2**32 - 1)
     assert np.array_equal(factors, o_factors) and st.corrections == o_corr
 
 
-def test_predict_full_size_stream():
+def test_predict_level_path_applicability():
+    from paper_2409_14961_b200 import uellm as U
+    assert U.predict_workspace_bytes(10**6, U.make_predictor(P(window=1000))) > 0
+    assert U.predict_workspace_bytes(10**6, U.make_predictor(P(window=1000, gamma=1.0001))) == 0   # too many levels
+    assert U.predict_workspace_bytes(10**6, U.make_predictor(P(window=1000, monitor=0, gamma=1.0001))) > 0
+
+
+def test_predict_many_levels_window_path():
+    t = W.true_output_lengths(30_000, 9)
+    pc = P(variant=3, constant_tokens=20, window=300, gamma=1.001, cap=4.0)
+    pred, factors, st = gpu_predict(t, pc)          # no level workspace available: window path
+    o_pred, o_factors, o_corr = oracle.profile_stream(t, pc)
+    assert np.array_equal(pred, o_pred) and np.array_equal(factors, o_factors) and st.corrections == o_corr
+
+
+@pytest.mark.parametrize("levels", [True, False])
+def test_predict_full_size_stream(levels):
     """c4's shape: 10^8 true lengths, one monitor epoch per 10^6-query window."""
     t = W.true_output_lengths(100_000_000, 0)
     pc = P(variant=2, error_rate=0.0049, bucket_width=16, window=1_000_000, seed=0)
-    pred, factors, st = gpu_predict(t, pc)
+    pred, factors, st = gpu_predict(t, pc, levels=levels)
     o_pred, o_factors, o_corr = oracle.profile_stream(t, pc)
     assert np.array_equal(pred, o_pred) and np.array_equal(factors, o_factors) and st.corrections == o_corr
 
