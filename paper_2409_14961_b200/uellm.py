@@ -138,7 +138,7 @@ _lib.uellm_batch_stats.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_vo
 _lib.uellm_simulate.restype = C.c_int32
 _lib.uellm_simulate.argtypes = [C.POINTER(Profile), C.POINTER(Config)] + [C.c_void_p] * 8
 _lib.uellm_predict_lengths.restype = C.c_int32
-_lib.uellm_predict_lengths.argtypes = [C.c_uint64, C.c_void_p, C.POINTER(Predictor)] + [C.c_void_p] * 4 + \
+_lib.uellm_predict_lengths.argtypes = [C.c_uint64, C.c_void_p, C.POINTER(Predictor)] + [C.c_void_p] * 3 + \
     [C.c_void_p, C.c_size_t, C.c_void_p]
 _lib.uellm_predict_workspace_bytes.restype = C.c_size_t
 _lib.uellm_predict_workspace_bytes.argtypes = [C.c_uint64, C.POINTER(Predictor)]

@@ -382,3 +382,14 @@ def test_pipelined_contract_error():
                              np.zeros(len(inp) + 1, np.uint32), np.zeros(1, np.uint64),
                              __import__("ctypes").addressof(tot))
     assert e.value.status == U.ERR_CONTRACT
+
+
+@pytest.mark.parametrize("uniform_slo", [False, True])
+def test_sort_window_groups(uniform_slo, monkeypatch):
+    """The sort's window-group path (a tuning knob, UELLM_SORT_GROUP_Q) gives the same order on
+    both key layouts."""
+    inp, out, slo, cfg = W.c3(19, n=400_000)
+    if uniform_slo:
+        slo = W.gen_uniform_slo(400_000, 19)
+    monkeypatch.setenv("UELLM_SORT_GROUP_Q", "90000")
+    assert_parity(inp, out, slo, cfg.replace(window=30_000))
