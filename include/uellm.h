@@ -398,9 +398,9 @@ uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes,
  *   ws                      [device] >= uellm_pipeline_workspace_bytes(n, cfg, groups), 256-B aligned.
  *   order, batch_offsets    [host] n and n+1 x u32 (pinned for overlap), as uellm_schedule_batches.
  *   num_batches, totals     [host].
- * Creates and destroys two streams, 3 x groups events and a small pinned host block per call;
- * synchronises `stream` once per group (each group's load reads its validation record) and at
- * the end.  On an error the host outputs are unspecified. */
+ * Creates and destroys two streams and 3 x groups events per call (no host or device
+ * allocation); synchronises `stream` once per group (each group's load reads its validation
+ * record) and at the end.  On an error the host outputs are unspecified. */
 size_t uellm_pipeline_workspace_bytes(uint64_t n, const uellm_config *cfg, uint32_t groups);
 uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config *cfg, uint32_t groups, void *ws,
                                       size_t ws_bytes, uint32_t *order, uint32_t *batch_offsets,

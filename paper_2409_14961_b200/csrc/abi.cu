@@ -291,17 +291,16 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         std::memset(&hd, 0, sizeof hd);
         hd.tiles = cfg->mode == UELLM_MODE_SEG_DP ? L.ntiles : 0;
         hd.tile_len = L.tile_len;
-        CU(cudaMemcpyAsync(diag, &hd, sizeof hd, cudaMemcpyHostToDevice, st));
+        CU(launch_set_u64s(st, {{reinterpret_cast<unsigned long long *>(diag), 0ull}}, true));
+        CU(launch_set_u64s(st, {{&diag->tiles, hd.tiles}, {&diag->tile_len, hd.tile_len}}));
         CU(cudaMemsetAsync(at<unsigned long long>(w, L.wincost), 0, 8 * (L.nwin ? L.nwin : 1), st));
     }
     rec(v, UELLM_STAGE_SCHED_BEGIN, st);
-    int launches = 0;
+    int launches = 4;     // small-store kernels: diag clear, tile sizes, sort record, launch count
     if (n == 0) {
-        const uint32_t zero32 = 0;
-        const uint64_t zero64 = 0;
-        if (dev_offs) { CU(cudaMemcpyAsync(batch_offsets, &zero32, 4, cudaMemcpyHostToDevice, st)); }
+        if (dev_offs) { CU(cudaMemsetAsync(batch_offsets, 0, 4, st)); }
         else batch_offsets[0] = 0;
-        if (dev_nb) { CU(cudaMemcpyAsync(num_batches, &zero64, 8, cudaMemcpyHostToDevice, st)); }
+        if (dev_nb) { CU(cudaMemsetAsync(num_batches, 0, 8, st)); }
         else *num_batches = 0;
         if (!dev_offs || !dev_nb) CU(cudaStreamSynchronize(st));
         return UELLM_OK;
@@ -382,8 +381,7 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
     rec(v, UELLM_STAGE_DECODE_END, st);
     {
         unsigned long long sp[2] = {(unsigned long long)passes, compressed ? (unsigned long long)(rb + ob) : 64ull};
-        CU(cudaMemcpyAsync(&diag->sort_passes, &sp[0], 8, cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(&diag->sort_key_bits, &sp[1], 8, cudaMemcpyHostToDevice, st));
+        CU(launch_set_u64s(st, {{&diag->sort_passes, sp[0]}, {&diag->sort_key_bits, sp[1]}}));
     }
     // a6/a7: segmentation -> boundary bitmap
     uint32_t *bm = at<uint32_t>(w, L.bitmap);
@@ -447,7 +445,7 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
     rec(v, UELLM_STAGE_SCHED_END, st);
     {
         unsigned long long lc = (unsigned long long)launches;
-        CU(cudaMemcpyAsync(&diag->sched_launches, &lc, 8, cudaMemcpyHostToDevice, st));
+        CU(launch_set_u64s(st, {{&diag->sched_launches, lc}}));
     }
     if (!dev_order || !dev_offs || !dev_nb) {
         uint64_t m = 0;
@@ -501,8 +499,8 @@ uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg, 
     CU(run_stats(S, st));
     rec(v, UELLM_STAGE_STATS_END, st);
     {
-        unsigned long long lc = n ? 6ull : 1ull;
-        CU(cudaMemcpyAsync(&at<Diag>(w, L.diag)->stats_launches, &lc, 8, cudaMemcpyHostToDevice, st));
+        unsigned long long lc = n ? 7ull : 2ull;       // + this small-store kernel
+        CU(launch_set_u64s(st, {{&at<Diag>(w, L.diag)->stats_launches, lc}}));
     }
     if (!dev_tot) {
         CU(cudaMemcpyAsync(totals, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, st));
@@ -643,8 +641,8 @@ uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *c
     if (!is_device_ptr(words)) return UELLM_ERR_ARG;
     const WsLayout L = make_layout(v.n, *cfg);
     if (v.n == 0) {
-        const uint32_t one = 1u;                       // n = 0: the single boundary 0 (= n)
-        CU(cudaMemcpyAsync(words, &one, 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));   // pageable: staged before return
+        CU(cudaMemsetAsync(words, 0, 4, (cudaStream_t)stream));   // n = 0: the single boundary 0 (= n)
+        CU(cudaMemsetAsync(words, 1, 1, (cudaStream_t)stream));
         return UELLM_OK;
     }
     CU(cudaMemcpyAsync(words, v.ws + L.bitmap, 4 * L.nwords, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));

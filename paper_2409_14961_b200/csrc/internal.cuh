@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <initializer_list>
 #include <cuda_runtime.h>
 
 #include "../../include/uellm.h"
@@ -120,6 +121,15 @@ struct ProfileView {
 static_assert(sizeof(ProfileView) <= sizeof(uellm_profile), "ProfileView fits uellm_profile");
 
 WsLayout make_layout(uint64_t n, const uellm_config &cfg);
+
+// Stream-ordered stores of small host values into device memory without a pageable copy (a
+// pageable cudaMemcpyAsync synchronises the stream first).  zero_diag: the first pair's pointer is
+// a Diag to clear before the stores.
+struct U64Store {
+    unsigned long long *dst;
+    unsigned long long val;
+};
+cudaError_t launch_set_u64s(cudaStream_t st, std::initializer_list<U64Store> stores, bool zero_diag = false);
 uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_tile);
 
 // --------------------------------------------------------------------------------------

@@ -270,3 +270,37 @@ cudaError_t launch_mark_fifo(uint32_t *bitmap, uint64_t n, uint64_t window, uint
 }
 
 }  // namespace uellm
+
+namespace uellm {
+
+struct U64Stores4 {
+    unsigned long long *dst[4];
+    unsigned long long val[4];
+    int n, zero_diag;
+};
+
+__global__ void k_set_u64s(U64Stores4 S)
+{
+    if (S.zero_diag) {
+        unsigned long long *d = S.dst[0];
+        for (unsigned i = threadIdx.x; i < sizeof(Diag) / 8; i += blockDim.x) d[i] = 0ull;
+        return;
+    }
+    if ((int)threadIdx.x < S.n) *S.dst[threadIdx.x] = S.val[threadIdx.x];
+}
+
+cudaError_t launch_set_u64s(cudaStream_t st, std::initializer_list<U64Store> stores, bool zero_diag)
+{
+    U64Stores4 S = {};
+    for (const U64Store &u : stores) {
+        if (S.n == 4) return cudaErrorInvalidValue;
+        S.dst[S.n] = u.dst;
+        S.val[S.n] = u.val;
+        ++S.n;
+    }
+    S.zero_diag = zero_diag ? 1 : 0;
+    k_set_u64s<<<1, 32, 0, st>>>(S);
+    return cudaGetLastError();
+}
+
+}  // namespace uellm

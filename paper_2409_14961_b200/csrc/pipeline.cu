@@ -8,6 +8,9 @@
 //   C stream : load(g) (sync: host decisions need its maxima) -> schedule(g) -> stats(g)
 //              -> rebase order/offsets to global indices      [waits: H2D(g), D2H(g-2) done]
 //   D stream : D2H(g) of order, offsets, totals                [waits: compute of g done]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -106,8 +109,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     cudaStream_t H = nullptr, D = nullptr;
     std::vector<cudaEvent_t> h2d(G, nullptr), done(G, nullptr), d2h(G, nullptr);
     std::vector<uint64_t> m(G, 0);
-    uint64_t *nb_host = nullptr;
-    uellm_totals *tot_host = nullptr;
+    std::vector<uellm_totals> tot_host(G);
     uellm_status status = UELLM_OK;
     auto qa = [&](uint64_t g) { return g * gq; };
     auto qz = [&](uint64_t g) { return (g + 1) * gq < n ? (g + 1) * gq : n; };
@@ -118,6 +120,12 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
             return UELLM_ERR_CUDA;               \
         }                                        \
     } while (0)
+    // UELLM_PIPE_TRACE=1: host-side timestamps per group on stderr (diagnosis only)
+    const bool trace = getenv("UELLM_PIPE_TRACE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto ms = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    };
   auto body = [&]() -> uellm_status {
     PCU(cudaStreamCreateWithFlags(&H, cudaStreamNonBlocking));
     PCU(cudaStreamCreateWithFlags(&D, cudaStreamNonBlocking));
@@ -126,8 +134,6 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         PCU(cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming));
         PCU(cudaEventCreateWithFlags(&d2h[g], cudaEventDisableTiming));
     }
-    PCU(cudaMallocHost(&nb_host, 8 * G));
-    PCU(cudaMallocHost(&tot_host, sizeof(uellm_totals) * G));
     {
         // everything already queued on the caller's stream happens before our copies
         cudaEvent_t start;
@@ -171,10 +177,15 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
                                  (const float *)(w + PL.slo[s])};
             uellm_profile prof;
             // synchronises C: by now schedule(g-1) has completed and m[g-1] is on the host
+            const double t0 = ms();
             uellm_status st = uellm_profile_load(&gq_, &gcfg, w + PL.ws, PL.ws_bytes, stream, &prof);
             if (st != UELLM_OK) return st;
+            const double t1 = ms();
             if (g >= 1) {
-                m[g - 1] = nb_host[g - 1];
+                // schedule(g-1) is complete (the load synchronised C and nothing is queued after
+                // it yet): an 8-byte read of its batch count, no pinned host block needed
+                PCU(cudaMemcpyAsync(&m[g - 1], (uint64_t *)(w + PL.nb) + (g - 1), 8, cudaMemcpyDeviceToHost, C));
+                PCU(cudaStreamSynchronize(C));
                 PCU(enqueue_d2h(g - 1, moff));
                 moff += m[g - 1];
             }
@@ -183,18 +194,22 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
             uint64_t *d_nb = (uint64_t *)(w + PL.nb) + g;
             uellm_totals *d_tot = (uellm_totals *)(w + PL.tot) + g;
             if ((st = uellm_schedule_batches(&prof, &gcfg, d_order, d_offs, d_nb, stream)) != UELLM_OK) return st;
+            const double t2 = ms();
             if ((st = uellm_batch_stats(&prof, &gcfg, d_offs, d_nb, nullptr, d_tot, stream)) != UELLM_OK) return st;
+            if (trace)
+                fprintf(stderr, "[pipe] g=%llu load_in %.3f load_out %.3f sched_out %.3f stats_out %.3f ms\n",
+                        (unsigned long long)g, t0, t1, t2, ms());
             PCU(add_base(d_order, len, (uint32_t)a, C));       // group-local -> caller indices
             PCU(add_base(d_offs, len + 1, (uint32_t)a, C));    // (only [0, m_g] are copied)
-            PCU(cudaMemcpyAsync(nb_host + g, d_nb, 8, cudaMemcpyDeviceToHost, C));
-            PCU(cudaMemcpyAsync(tot_host + g, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, C));
             PCU(cudaEventRecord(done[g], C));
         }
         PCU(cudaStreamSynchronize(C));
-        m[G - 1] = nb_host[G - 1];
+        PCU(cudaMemcpy(&m[G - 1], (uint64_t *)(w + PL.nb) + (G - 1), 8, cudaMemcpyDeviceToHost));
+        PCU(cudaMemcpy(tot_host.data(), w + PL.tot, sizeof(uellm_totals) * G, cudaMemcpyDeviceToHost));
         PCU(enqueue_d2h(G - 1, moff));
         moff += m[G - 1];
         PCU(cudaStreamSynchronize(D));
+        if (trace) fprintf(stderr, "[pipe] end %.3f ms (%llu groups)\n", ms(), (unsigned long long)G);
         batch_offsets[moff] = (uint32_t)n;
         *num_batches = moff;
         // whole-job totals from the per-group integer totals (exact); the latency mean is
@@ -225,8 +240,6 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         if (done[g]) cudaEventDestroy(done[g]);
         if (d2h[g]) cudaEventDestroy(d2h[g]);
     }
-    if (nb_host) cudaFreeHost(nb_host);
-    if (tot_host) cudaFreeHost(tot_host);
 #undef PCU
     return status;
 }
