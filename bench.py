@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-row timings (f2, f3, f4)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo only for multi-rank tests on one GPU)")
     ap.add_argument("--e2e-groups", type=int, default=0, help="window groups of the pipelined e2e call (0 = 8)")
     ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
     ap.add_argument("--mode", default="seg_dp", choices=["seg_dp", "slo_odbs", "fifo", "sort_only"],
@@ -183,10 +185,21 @@ def main():
     from paper_2409_14961_b200.distributed import GATHER_WORDS, combine_totals
     from paper_2409_14961_b200.scheduler import GpuScheduler
 
+    local = local % max(torch.cuda.device_count(), 1)   # (test runs may put several ranks on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
+
+    def allgather(out_buf, in_buf):
+        """a9: one collective; NCCL's allgather into one tensor (gloo, for tests: list form)."""
+        if args.dist_backend == "nccl":
+            dist.all_gather_into_tensor(out_buf, in_buf)
+        else:
+            dist.all_gather(list(out_buf.view(world, -1).unbind(0)), in_buf)
     desc, inp, out, slo, cfg = workload(args.config, rank, args.n)
     if args.dp_tile:
         cfg = cfg.replace(dp_tile=args.dp_tile)
@@ -230,7 +243,7 @@ def main():
             U.boundary_bitmap(g.profile, g.cfg, bm_view, stream)
             with torch.cuda.stream(stream):
                 gather_in[:13].copy_(g.totals.view(torch.int64)[:13])
-                dist.all_gather_into_tensor(gather_buf, gather_in)
+                allgather(gather_buf, gather_in)
 
     for _ in range(Wm):
         step()
@@ -321,7 +334,7 @@ def main():
                 with torch.cuda.stream(stream):
                     gather_in[:13].copy_(torch.from_numpy(np.frombuffer(bytes(h_tot), np.int64)[:13].copy()),
                                          non_blocking=False)
-                    dist.all_gather_into_tensor(gather_buf, gather_in)
+                    allgather(gather_buf, gather_in)
         e2e_step()
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -339,7 +352,8 @@ def main():
         mh = int(h_nb[0])
         e2e = {"value": world * n / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 4 * n + 4 * (mh + 1) + 8 + U.TOTALS_BYTES,
-               "ms_per_step": float(te.item()), "api": f"uellm_schedule_pipelined ({groups or 8} window groups)"}
+               "ms_per_step": float(te.item()), "api": f"uellm_schedule_pipelined ({groups or 8} window groups)",
+               "exchange": "N > 1: allgather of the per-rank totals (the boundaries are already in each rank's host buffers)"}
         assert mh == m and h_tot.dp_cost == res["totals"]["dp_cost"], "host-buffer path disagrees with the device path"
 
     # NEXT f2: the sequential-execution simulator over this step's schedule, timed on its own

@@ -33,8 +33,9 @@ static cudaError_t add_base(uint32_t *a, uint64_t n, uint32_t base, cudaStream_t
 }
 
 struct PipeLayout {
-    uint64_t group_q;                 // queries per full group (whole windows)
+    uint64_t group_q;                 // queries of the largest group (whole windows)
     uint64_t groups;
+    uint64_t wl, nwin, tail, per, rem; // group g = windows [gwin(g), gwin(g+1)) (see gwin)
     uint64_t ws, ws_bytes;            // per-group scheduling workspace (re-used by every group)
     uint64_t in[2], out[2], slo[2];   // input staging slots
     uint64_t order[2], offs[2];       // output staging slots
@@ -50,10 +51,18 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     const uint64_t nwin = n ? ceil_div(n, wl ? wl : 1) : 0;
     uint64_t G = groups ? groups : 8;
     if (G > nwin) G = nwin ? nwin : 1;
-    const uint64_t wpg = nwin ? ceil_div(nwin, G) : 1;          // windows per group
-    P.group_q = n ? wpg * wl : 0;
+    // The pipeline is bound by the host->device copies; once the last group's copy lands, its
+    // load / schedule / stats and device->host copy are exposed.  So the last group is small
+    // (about 1/4 of an even share, at least one window) and the rest split evenly.
+    P.wl = wl; P.nwin = nwin;
+    P.tail = G > 1 ? (nwin / (4 * G) > 1 ? nwin / (4 * G) : 1) : nwin;
+    const uint64_t body = nwin - P.tail;
+    P.per = G > 1 ? body / (G - 1) : 0;
+    P.rem = G > 1 ? body % (G - 1) : 0;
+    const uint64_t maxw = G > 1 ? (P.per + (P.rem ? 1 : 0) > P.tail ? P.per + (P.rem ? 1 : 0) : P.tail) : nwin;
+    P.group_q = n ? maxw * wl : 0;
     if (P.group_q > n) P.group_q = n;
-    P.groups = n ? ceil_div(nwin, wpg) : 0;
+    P.groups = n ? G : 0;
     uint64_t off = 0;
     auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
     uellm_config c = cfg;
@@ -69,6 +78,15 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     P.nb = take(8 * (P.groups ? P.groups : 1));
     P.total = off;
     return P;
+}
+
+// first window of group g (g = groups gives nwin)
+static uint64_t gwin(const PipeLayout &P, uint64_t g)
+{
+    if (P.groups <= 1) return g ? P.nwin : 0;
+    if (g >= P.groups) return P.nwin;
+    const uint64_t gg = g < P.groups - 1 ? g : P.groups - 1;
+    return gg * P.per + (gg < P.rem ? gg : P.rem);
 }
 
 }  // namespace uellm
@@ -103,7 +121,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         if ((s = uellm_schedule_batches(&p, cfg, order, batch_offsets, num_batches, stream)) != UELLM_OK) return s;
         return uellm_batch_stats(&p, cfg, batch_offsets, num_batches, nullptr, totals, stream);
     }
-    const uint64_t G = PL.groups, gq = PL.group_q;
+    const uint64_t G = PL.groups;
     uellm_config gcfg = *cfg;
     gcfg.window = (uint32_t)(cfg->window ? (cfg->window < n ? cfg->window : n) : n);
     cudaStream_t H = nullptr, D = nullptr;
@@ -111,8 +129,8 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     std::vector<uint64_t> m(G, 0);
     std::vector<uellm_totals> tot_host(G);
     uellm_status status = UELLM_OK;
-    auto qa = [&](uint64_t g) { return g * gq; };
-    auto qz = [&](uint64_t g) { return (g + 1) * gq < n ? (g + 1) * gq : n; };
+    auto qa = [&](uint64_t g) { const uint64_t q = gwin(PL, g) * PL.wl; return q < n ? q : n; };
+    auto qz = [&](uint64_t g) { return qa(g + 1); };
 #define PCU(x)                                   \
     do {                                         \
         if ((x) != cudaSuccess) {                \

@@ -393,3 +393,30 @@ def test_sort_window_groups(uniform_slo, monkeypatch):
         slo = W.gen_uniform_slo(400_000, 19)
     monkeypatch.setenv("UELLM_SORT_GROUP_Q", "90000")
     assert_parity(inp, out, slo, cfg.replace(window=30_000))
+
+
+def test_bench_two_ranks_one_gpu_gloo(tmp_path):
+    """bench.py's N > 1 path (a9 exchange of totals + boundary bitmaps, max-over-ranks timing) with
+    two ranks sharing the one GPU over gloo: the job totals are the two ranks' oracle totals."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = 2_000_000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--n", str(n), "--no-cpu-baseline", "--no-sim",
+           "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["e2e"] is not None
+    jt = line["job_totals"]
+    want_cost = want_b = 0
+    for rank in range(2):
+        inp, out, slo, cfg = W.c4(seed=rank, n=n)
+        o = oracle.schedule(inp, out, slo, cfg, nthreads=8)
+        want_cost += o[3]
+        want_b += o[2]
+    assert jt["n"] == 2 * n and jt["dp_cost"] == want_cost and jt["batches"] == want_b
