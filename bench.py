@@ -160,7 +160,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="uellm", choices=["uellm", "reference"])
     ap.add_argument("--config", default="c4")
-    ap.add_argument("--n", type=int, default=None, help="override query count (testing only)")
+    ap.add_argument("--queries", dest="n", type=int, default=None, help="override query count (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-row timings (f2, f3, f4)")

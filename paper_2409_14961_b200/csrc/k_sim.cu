@@ -18,10 +18,11 @@
 //   k_sim_gather   position-linear: arrival in scheduled order, arr_s[k] = arrival[order[k]]
 //                  (the random gather stays inside the window the resident CTAs work on, so it
 //                  is served from L2; everything after it streams coalesced)
-//   k_sim_batches  thread per batch (chunks of kScanBlock batches per CTA): s, O, A_t from the
-//                  members, est_t; CTA-wide inclusive scan of the maps; chunk aggregates
+//   k_sim_batches  chunks of kScanBlock batches per CTA: groups of 8 lanes stream each batch's
+//                  members (s, O, A_t, est_t), then thread = batch for the CTA-wide inclusive
+//                  scan of the maps; chunk aggregates
 //   k_sim_chunks   one CTA: exclusive scan of the chunk aggregates -> end value entering chunk
-//   k_sim_members  thread per batch: end_t, member latencies (scheduled order, written straight
+//   k_sim_members  8 lanes per batch: end_t, member latencies (scheduled order, written straight
 //                  to the caller's buffer when requested) / violations, block-aggregated totals
 //                  (exact 128-bit latency sum)
 //   k_sim_totals   one thread: uellm_sim_totals
@@ -109,33 +110,57 @@ __global__ void __launch_bounds__(256) k_sim_gather(SimParams S)
         S.arr_s[k] = __ldg(S.arrival + __ldg(S.order + k));
 }
 
+constexpr uint32_t kSimGroup = 8;     // lanes per batch in the member-streaming loops
+
 __global__ void __launch_bounds__(kScanBlock) k_sim_batches(SimParams S)
 {
+    // phase 1: groups of kSimGroup lanes stream each batch's members (consecutive lanes on
+    // consecutive positions); phase 2: thread = batch, CTA-wide scan of the maps
+    __shared__ unsigned long long s_est[kScanBlock], s_A[kScanBlock];
     const uint64_t m = *S.num_batches;
     const uint64_t nch = ceil_div(m, kScanBlock);
+    const uint32_t sub = threadIdx.x % kSimGroup;
     unsigned long long busy = 0, gen = 0;
     for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+        for (uint32_t loc = threadIdx.x / kSimGroup; loc < kScanBlock; loc += blockDim.x / kSimGroup) {
+            const uint64_t t = c * kScanBlock + loc;
+            const bool act = t < m;
+            uint32_t s = 0, O = 0, a = 0, z = 0;
+            unsigned long long A = 0;
+            if (act) {
+                a = S.offsets[t];
+                z = S.offsets[t + 1];
+                for (uint32_t k = a + sub; k < z; k += kSimGroup) {
+                    s = max(s, __ldg(S.rin + k));
+                    O = max(O, __ldg(S.rout + k));
+                    A = max(A, __ldg(S.arr_s + k));
+                }
+            }
+#pragma unroll
+            for (int d = kSimGroup / 2; d; d >>= 1) {
+                s = max(s, __shfl_xor_sync(0xffffffffu, s, d));
+                O = max(O, __shfl_xor_sync(0xffffffffu, O, d));
+                A = max(A, __shfl_xor_sync(0xffffffffu, A, d));
+            }
+            if (act && sub == 0) {
+                const unsigned long long b = z - a;
+                const unsigned long long est = S.t_batch + S.t_iter * O + S.t_tok * b * O + S.t_pre * b * s;
+                S.est[t] = est;
+                s_est[loc] = est;
+                s_A[loc] = A;
+                busy += est;
+                gen += b * O;
+            }
+        }
+        __syncthreads();
         const uint64_t t = c * kScanBlock + threadIdx.x;
         MaxPlus f = {0ull, 0ull};
         if (t < m) {
-            const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
-            uint32_t s = 0, O = 0;
-            unsigned long long A = 0;
-            for (uint32_t k = a; k < z; ++k) {
-                s = max(s, __ldg(S.rin + k));
-                O = max(O, __ldg(S.rout + k));
-                A = max(A, __ldg(S.arr_s + k));
-            }
-            const unsigned long long b = z - a;
-            const unsigned long long est = S.t_batch + S.t_iter * O + S.t_tok * b * O + S.t_pre * b * s;
-            S.est[t] = est;
-            f.a = est;
-            f.b = sat_add(A, est);
-            busy += est;
-            gen += b * O;
+            f.a = s_est[threadIdx.x];
+            f.b = sat_add(s_A[threadIdx.x], f.a);
         }
         MaxPlus agg;
-        const MaxPlus inc = block_scan_maps(f, &agg);
+        const MaxPlus inc = block_scan_maps(f, &agg);        // ends with a barrier: smem reusable
         if (t < m) { S.inc_a[t] = inc.a; S.inc_b[t] = inc.b; }
         if (threadIdx.x == 0) { S.chunk_a[c] = agg.a; S.chunk_b[c] = agg.b; }
     }
@@ -181,17 +206,21 @@ __global__ void __launch_bounds__(kScanBlock) k_sim_chunks(SimParams S)
 __global__ void __launch_bounds__(256) k_sim_members(SimParams S)
 {
     __shared__ unsigned long long red[8][5];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane % kSimGroup;
     const uint64_t m = *S.num_batches;
-    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t ng = (uint64_t)gridDim.x * (blockDim.x / kSimGroup);
+    const uint64_t mpad = ceil_div(m, 32 / kSimGroup) * (32 / kSimGroup);   // whole warps iterate together
     unsigned long long viol = 0, lmax = 0, llo = 0, lhi = 0, any = 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += nt) {
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / kSimGroup; t < mpad; t += ng) {
+        if (t >= m) continue;
         const unsigned long long e_in = S.carry[t / kScanBlock];
         const unsigned long long end = max(sat_add(e_in, S.inc_a[t]), S.inc_b[t]);
-        if (S.batch_end) S.batch_end[t] = end;
-        if (t == m - 1) S.acc->makespan = end;
+        if (sub == 0) {
+            if (S.batch_end) S.batch_end[t] = end;
+            if (t == m - 1) S.acc->makespan = end;
+        }
         const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
-        for (uint32_t k = a; k < z; ++k) {
+        for (uint32_t k = a + sub; k < z; k += kSimGroup) {
             const unsigned long long arr = __ldg(S.arr_s + k);
             const unsigned long long lat = end > arr ? end - arr : 0ull;
             viol += lat > (unsigned long long)__ldg(S.rslo + k);

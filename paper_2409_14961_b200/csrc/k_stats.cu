@@ -15,6 +15,8 @@
 
 namespace uellm {
 
+constexpr uint32_t kStatsGroup = 8;   // lanes per batch in the member-streaming passes
+
 __device__ __forceinline__ uint32_t warp_max(uint32_t v)
 {
     return __reduce_max_sync(0xffffffffu, v);
@@ -57,23 +59,38 @@ __device__ __forceinline__ BatchCore batch_core(const StatsParams &S, uint64_t t
 
 __global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
 {
-    // thread per batch: members are contiguous, each thread streams its own range
+    // kStatsGroup lanes per batch: the group streams the batch's contiguous members with
+    // consecutive lanes on consecutive positions (one 32-byte sector per load instruction and
+    // group), then reduces across the group with shuffles
     const uint64_t m = *S.num_batches;
-    const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += nt) {
+    const uint32_t lane = threadIdx.x & 31, sub = lane % kStatsGroup;
+    const uint64_t ng = (uint64_t)gridDim.x * (blockDim.x / kStatsGroup);
+    for (uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / kStatsGroup; t0 < ceil_div(m, 32 / kStatsGroup) * (32 / kStatsGroup);
+         t0 += ng) {
+        const bool act = t0 < m;
+        const uint64_t t = act ? t0 : m - 1;
         const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
         uint32_t s = 0, O = 0;
-        unsigned long long si = 0, so = 0;
-        for (uint32_t k = a; k < z; ++k) {
+        unsigned long long si64 = 0, so64 = 0;
+        for (uint32_t k = a + sub; k < z; k += kStatsGroup) {
             const uint32_t vi = __ldg(S.rin + k), vo = __ldg(S.rout + k);
             s = max(s, vi); O = max(O, vo);
-            si += vi; so += vo;
+            si64 += vi; so64 += vo;
         }
-        const unsigned long long b = z - a;
-        S.est[t] = S.t_batch + S.t_iter * O + S.t_tok * b * O + S.t_pre * b * s;
-        S.so[t] = (unsigned long long)s | ((unsigned long long)O << 32);
-        S.pin[t] = b * s - si;
-        S.pout[t] = b * O - so;
+#pragma unroll
+        for (int d = kStatsGroup / 2; d; d >>= 1) {
+            s = max(s, __shfl_xor_sync(0xffffffffu, s, d));
+            O = max(O, __shfl_xor_sync(0xffffffffu, O, d));
+            si64 += __shfl_xor_sync(0xffffffffu, si64, d);
+            so64 += __shfl_xor_sync(0xffffffffu, so64, d);
+        }
+        if (act && sub == 0) {
+            const unsigned long long b = z - a;
+            S.est[t] = S.t_batch + S.t_iter * O + S.t_tok * b * O + S.t_pre * b * s;
+            S.so[t] = (unsigned long long)s | ((unsigned long long)O << 32);
+            S.pin[t] = b * s - si64;
+            S.pout[t] = b * O - so64;
+        }
     }
 }
 

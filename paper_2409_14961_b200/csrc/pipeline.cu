@@ -147,19 +147,19 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
   auto body = [&]() -> uellm_status {
     PCU(cudaStreamCreateWithFlags(&H, cudaStreamNonBlocking));
     PCU(cudaStreamCreateWithFlags(&D, cudaStreamNonBlocking));
+    const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
     for (uint64_t g = 0; g < G; ++g) {
-        PCU(cudaEventCreateWithFlags(&h2d[g], cudaEventDisableTiming));
-        PCU(cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming));
-        PCU(cudaEventCreateWithFlags(&d2h[g], cudaEventDisableTiming));
+        PCU(cudaEventCreateWithFlags(&h2d[g], evflags));
+        PCU(cudaEventCreateWithFlags(&done[g], evflags));
+        PCU(cudaEventCreateWithFlags(&d2h[g], evflags));
     }
+    cudaEvent_t start = nullptr;
     {
         // everything already queued on the caller's stream happens before our copies
-        cudaEvent_t start;
-        PCU(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+        PCU(cudaEventCreateWithFlags(&start, evflags));
         cudaEventRecord(start, C);
         cudaStreamWaitEvent(H, start, 0);
         cudaStreamWaitEvent(D, start, 0);
-        cudaEventDestroy(start);
     }
     auto enqueue_h2d = [&](uint64_t g) -> cudaError_t {
         const int s = (int)(g & 1);
@@ -227,7 +227,18 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         PCU(enqueue_d2h(G - 1, moff));
         moff += m[G - 1];
         PCU(cudaStreamSynchronize(D));
-        if (trace) fprintf(stderr, "[pipe] end %.3f ms (%llu groups)\n", ms(), (unsigned long long)G);
+        if (trace) {
+            fprintf(stderr, "[pipe] end %.3f ms (%llu groups)\n", ms(), (unsigned long long)G);
+            for (uint64_t g = 0; g < G; ++g) {
+                float a = 0, b = 0, c = 0;
+                cudaEventElapsedTime(&a, start, h2d[g]);
+                cudaEventElapsedTime(&b, start, done[g]);
+                cudaEventElapsedTime(&c, start, d2h[g]);
+                fprintf(stderr, "[pipe]   g=%llu q=%llu  h2d_done %.3f  compute_done %.3f  d2h_done %.3f ms\n",
+                        (unsigned long long)g, (unsigned long long)(qz(g) - qa(g)), a, b, c);
+            }
+        }
+        cudaEventDestroy(start);
         batch_offsets[moff] = (uint32_t)n;
         *num_batches = moff;
         // whole-job totals from the per-group integer totals (exact); the latency mean is

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json():
     out = subprocess.check_output([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                                   "--config", "c4", "--n", "2000000", "--steps", "1", "--warmup", "0"],
+                                   "--config", "c4", "--queries", "2000000", "--steps", "1", "--warmup", "0"],
                                   cwd=ROOT, timeout=600).decode().strip().splitlines()
     assert len(out) == 1
     d = json.loads(out[0])

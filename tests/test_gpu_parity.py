@@ -406,7 +406,7 @@ def test_bench_two_ranks_one_gpu_gloo(tmp_path):
     n = 2_000_000
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "1", "--n", str(n), "--no-cpu-baseline", "--no-sim",
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--queries", str(n), "--no-cpu-baseline", "--no-sim",
            "--dist-backend", "gloo"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
