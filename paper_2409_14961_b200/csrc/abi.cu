@@ -29,16 +29,12 @@ uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_ti
     } else {
         // ~3 waves of 32 resident DP warps per SM: short tiles balance the data-dependent
         // per-tile work (measured on c4: 7 K-query tiles beat 28 K by 1.37x; fix-ups cost ~5 %).
-        // Small jobs (a window group of the pipelined call, a single 10^6 window) would get fewer
-        // tiles than warps at the 16 W floor, and a tile's sequential walk (~1.5 ms for 4096
-        // positions) would set the latency: there the tiles are sized for about one wave, down to
-        // 4 W (fix-ups then cost more, the cascade keeps it exact).
-        const uint64_t N = n ? n : 1;
-        T = ceil_div(N, 148ull * 96);
-        if (T < 16ull * W) {
-            T = ceil_div(N, 148ull * 32);
-            T = T < 4ull * W ? 4ull * W : (T > 16ull * W ? 16ull * W : T);
-        }
+        // The 16 W floor stays for small jobs too: one-wave tiles of 4 W .. 16 W were measured
+        // slower on 6-7 M-query window groups (3.5-7 ms against 2.7 ms per group: more fix-ups
+        // and cascade re-runs than the extra parallelism gains).
+        const uint64_t target_tiles = 148ull * 96;
+        T = ceil_div(n ? n : 1, target_tiles);
+        T = T < 16ull * W ? 16ull * W : T;
         T = align_up(T, W);
     }
     if (T < 2ull * W) T = 2ull * W;

@@ -37,30 +37,36 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long seed, uns
     return z ^ (z >> 31);
 }
 
+// the variant's prediction before the inflation factor (R20)
+__device__ __forceinline__ unsigned long long base_of(const PredictParams &P, unsigned long long index, uint32_t t)
+{
+    if (P.variant == UELLM_PREDICT_ORACLE) return t;
+    if (P.variant == UELLM_PREDICT_CONSTANT) return P.constant_tokens;
+    const unsigned long long w = P.bucket_width;
+    unsigned long long k = ((unsigned long long)t + w - 1) / w;
+    k = k < 1 ? 1 : k;
+    if (P.variant == UELLM_PREDICT_NOISY) {
+        const unsigned long long z = mix64(P.seed, index);
+        const double u = (double)(z >> 11) * 0x1.0p-53;
+        if (u < P.error_rate) {
+            if (z & 1ull) k += 1;
+            else if (k > 1) k -= 1;
+        }
+    }
+    return k * w;
+}
+
+// "multiplied by monitor.inflation_factor and rounded up", saturating (R20)
+__device__ __forceinline__ uint32_t inflate(unsigned long long base, double factor)
+{
+    const double x = ceil(__dmul_rn((double)base, factor));
+    return x >= 4294967295.0 ? 4294967295u : (uint32_t)x;
+}
+
 __device__ __forceinline__ uint32_t predict_one(const PredictParams &P, unsigned long long index, uint32_t t,
                                                 double factor)
 {
-    unsigned long long base;
-    if (P.variant == UELLM_PREDICT_ORACLE) {
-        base = t;
-    } else if (P.variant == UELLM_PREDICT_CONSTANT) {
-        base = P.constant_tokens;
-    } else {
-        const unsigned long long w = P.bucket_width;
-        unsigned long long k = ((unsigned long long)t + w - 1) / w;
-        k = k < 1 ? 1 : k;
-        if (P.variant == UELLM_PREDICT_NOISY) {
-            const unsigned long long z = mix64(P.seed, index);
-            const double u = (double)(z >> 11) * 0x1.0p-53;
-            if (u < P.error_rate) {
-                if (z & 1ull) k += 1;
-                else if (k > 1) k -= 1;
-            }
-        }
-        base = k * w;
-    }
-    const double x = ceil(__dmul_rn((double)base, factor));
-    return x >= 4294967295.0 ? 4294967295u : (uint32_t)x;
+    return inflate(base_of(P, index, t), factor);
 }
 
 }  // namespace
@@ -147,7 +153,8 @@ __global__ void __launch_bounds__(256) k_pred_count(PredictParams P, uint64_t n,
         if (k < n) {
             const uint32_t t = __ldg(P.true_len + k);
             w = (uint32_t)(k / window);
-            for (uint32_t i = 0; i <= K; ++i) under |= (uint32_t)(t > predict_one(P, k, t, V[i])) << i;
+            const unsigned long long base = base_of(P, k, t);
+            for (uint32_t i = 0; i <= K; ++i) under |= (uint32_t)(t > inflate(base, V[i])) << i;
         }
         const uint32_t grp = __match_any_sync(0xffffffffu, w);
         const uint32_t lane = threadIdx.x & 31;

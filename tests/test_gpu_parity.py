@@ -420,3 +420,18 @@ def test_bench_two_ranks_one_gpu_gloo(tmp_path):
         want_cost += o[3]
         want_b += o[2]
     assert jt["n"] == 2 * n and jt["dp_cost"] == want_cost and jt["batches"] == want_b
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer(tool):
+    """T6: compute-sanitizer finds no error in a small run of every entry point."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = ["/usr/local/cuda/bin/compute-sanitizer", "--tool", tool, "--error-exitcode", "9",
+           sys.executable, os.path.join(root, "tools", "sanitize_run.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=root)
+    tail = (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0 and "SANITIZE_RUN_OK" in r.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
