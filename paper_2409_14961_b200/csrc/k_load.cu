@@ -28,29 +28,40 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
     __syncthreads();
     uint32_t bad = 0, mx_in = 0, mx_out = 0, mx_slo = 0;
     unsigned long long kor = 0, kand = ~0ull;
-    // distinct-SLO collection: a read-only probe first (class-valued SLOs hit at once), the CAS
-    // insert only on a miss; stops once the CTA saw more than kCtaMax values
-    auto consume = [&](uint32_t a, uint32_t o, float sf, bool cv) {
-        bool ok;
-        const uint32_t su = slo_to_us(sf, ok);
-        if (a == 0) bad |= 1u;
-        if (o == 0) bad |= 2u;
-        if (!ok) bad |= 4u;
-        const unsigned long long key = ((unsigned long long)su << 32) | o;
-        mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
-        kor |= key; kand &= key;
-        if (cv || su == 0) return;
+    // distinct-SLO collection, warp-synchronous and race-free: the warp's SLO values are grouped
+    // with match.any and only one lane per distinct value touches the CTA set (atomicCAS only:
+    // present -> old == su); stops once the CTA saw more than kCtaMax values (cover).
+    const uint32_t lane = threadIdx.x & 31;
+    auto consume = [&](uint32_t a, uint32_t o, float sf, bool valid, bool cv) {
+        bool ok = true;
+        const uint32_t su = valid ? slo_to_us(sf, ok) : 0u;
+        if (valid) {
+            if (a == 0) bad |= 1u;
+            if (o == 0) bad |= 2u;
+            if (!ok) bad |= 4u;
+            const unsigned long long key = ((unsigned long long)su << 32) | o;
+            mx_in = max(mx_in, a); mx_out = max(mx_out, o); mx_slo = max(mx_slo, su);
+            kor |= key; kand &= key;
+        }
+        if (cv) return;                                        // warp-uniform
+        const uint32_t k = valid ? su : 0u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, k);
+        if (k == 0u || lane != (uint32_t)(__ffs(peers) - 1)) return;
         uint32_t h = slo_hash(su, kCtaBits);
-        if (((volatile uint32_t *)cset)[h] == su) return;
         for (uint32_t probe = 0; probe < kCtaSlots; ++probe) {
             const uint32_t old = atomicCAS(&cset[h], 0u, su);
             if (old == 0u) {
-                if (atomicAdd(&ccount, 1u) + 1 > kCtaMax) cover = 1;
+                if (atomicAdd(&ccount, 1u) + 1 > kCtaMax) atomicExch(&cover, 1u);
                 break;
             }
             if (old == su) break;
             h = (h + 1) & (kCtaSlots - 1);
         }
+    };
+    auto cover_now = [&]() -> bool {                           // one shared atomic read per warp
+        uint32_t c = 0;
+        if (lane == 0) c = atomicOr(&cover, 0u);
+        return __shfl_sync(0xffffffffu, c, 0) != 0u;
     };
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -59,19 +70,25 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
         const uint64_t n4 = n / 4;
         const uint4 *in4 = reinterpret_cast<const uint4 *>(in), *out4 = reinterpret_cast<const uint4 *>(out);
         const float4 *slo4 = reinterpret_cast<const float4 *>(slo);
-        for (uint64_t g = tid; g < n4; g += stride) {
-            const uint4 a = __ldg(in4 + g), o = __ldg(out4 + g);
-            const float4 f = __ldg(slo4 + g);
-            const bool cv = *(volatile uint32_t *)&cover;
-            consume(a.x, o.x, f.x, cv);
-            consume(a.y, o.y, f.y, cv);
-            consume(a.z, o.z, f.z, cv);
-            consume(a.w, o.w, f.w, cv);
+        for (uint64_t g0 = tid - lane; g0 < n4; g0 += stride) {    // whole warps iterate together
+            const uint64_t g = g0 + lane;
+            const bool v = g < n4;
+            uint4 a = make_uint4(0, 0, 0, 0), o = make_uint4(0, 0, 0, 0);
+            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (v) { a = __ldg(in4 + g); o = __ldg(out4 + g); f = __ldg(slo4 + g); }
+            const bool cv = cover_now();
+            consume(a.x, o.x, f.x, v, cv);
+            consume(a.y, o.y, f.y, v, cv);
+            consume(a.z, o.z, f.z, v, cv);
+            consume(a.w, o.w, f.w, v, cv);
         }
         head = n4 * 4;
     }
-    for (uint64_t k = head + tid; k < n; k += stride)
-        consume(__ldg(in + k), __ldg(out + k), __ldg(slo + k), *(volatile uint32_t *)&cover);
+    for (uint64_t k0 = head + tid - lane; k0 < n; k0 += stride) {
+        const uint64_t k = k0 + lane;
+        const bool v = k < n;
+        consume(v ? __ldg(in + k) : 0u, v ? __ldg(out + k) : 0u, v ? __ldg(slo + k) : 0.f, v, cover_now());
+    }
     // warp reductions, one atomic per warp
     for (int d = 16; d; d >>= 1) {
         bad |= __shfl_xor_sync(0xffffffffu, bad, d);
@@ -91,7 +108,7 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
     }
     __syncthreads();
     // merge the CTA's distinct SLO values into the global set
-    if (cover) {
+    if (*(volatile uint32_t *)&cover) {
         if (threadIdx.x == 0) atomicExch(&meta->slo_overflow, 1u);
         return;
     }

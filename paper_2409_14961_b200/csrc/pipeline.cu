@@ -36,9 +36,9 @@ struct PipeLayout {
     uint64_t group_q;                 // queries of the largest group (whole windows)
     uint64_t groups;
     uint64_t wl, nwin, tail, per, rem; // group g = windows [gwin(g), gwin(g+1)) (see gwin)
-    uint64_t ws, ws_bytes;            // per-group scheduling workspace (re-used by every group)
-    uint64_t in[2], out[2], slo[2];   // input staging slots
-    uint64_t order[2], offs[2];       // output staging slots
+    uint64_t ws[2], ws_bytes;         // scheduling workspaces of the two compute lanes
+    uint64_t in[2], out[2], slo[2];   // input staging slots (one per compute lane)
+    uint64_t order[3], offs[3];       // output staging slots (g % 3)
     uint64_t tot, nb;                 // per-group totals / num_batches (device)
     uint64_t total;
 };
@@ -68,12 +68,11 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     uellm_config c = cfg;
     c.window = (uint32_t)wl;
     P.ws_bytes = make_layout(P.group_q, c).total;
-    P.ws = take(P.ws_bytes);
+    P.ws[0] = take(P.ws_bytes);
+    P.ws[1] = take(P.ws_bytes);
     const uint64_t q = P.group_q ? P.group_q : 1;
-    for (int s = 0; s < 2; ++s) {
-        P.in[s] = take(4 * q); P.out[s] = take(4 * q); P.slo[s] = take(4 * q);
-        P.order[s] = take(4 * q); P.offs[s] = take(4 * (q + 1));
-    }
+    for (int s = 0; s < 2; ++s) { P.in[s] = take(4 * q); P.out[s] = take(4 * q); P.slo[s] = take(4 * q); }
+    for (int s = 0; s < 3; ++s) { P.order[s] = take(4 * q); P.offs[s] = take(4 * (q + 1)); }
     P.tot = take(sizeof(uellm_totals) * (P.groups ? P.groups : 1));
     P.nb = take(8 * (P.groups ? P.groups : 1));
     P.total = off;
@@ -116,7 +115,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     if (n == 0) {
         // the single-call path handles the empty job (no copies to overlap)
         uellm_profile p;
-        uellm_status s = uellm_profile_load(q, cfg, w + PL.ws, PL.ws_bytes, stream, &p);
+        uellm_status s = uellm_profile_load(q, cfg, w + PL.ws[0], PL.ws_bytes, stream, &p);
         if (s != UELLM_OK) return s;
         if ((s = uellm_schedule_batches(&p, cfg, order, batch_offsets, num_batches, stream)) != UELLM_OK) return s;
         return uellm_batch_stats(&p, cfg, batch_offsets, num_batches, nullptr, totals, stream);
@@ -124,7 +123,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     const uint64_t G = PL.groups;
     uellm_config gcfg = *cfg;
     gcfg.window = (uint32_t)(cfg->window ? (cfg->window < n ? cfg->window : n) : n);
-    cudaStream_t H = nullptr, D = nullptr;
+    cudaStream_t H = nullptr, D = nullptr, C2 = nullptr;
     std::vector<cudaEvent_t> h2d(G, nullptr), done(G, nullptr), d2h(G, nullptr);
     std::vector<uint64_t> m(G, 0);
     std::vector<uellm_totals> tot_host(G);
@@ -147,6 +146,8 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
   auto body = [&]() -> uellm_status {
     PCU(cudaStreamCreateWithFlags(&H, cudaStreamNonBlocking));
     PCU(cudaStreamCreateWithFlags(&D, cudaStreamNonBlocking));
+    PCU(cudaStreamCreateWithFlags(&C2, cudaStreamNonBlocking));
+    cudaStream_t CS[2] = {C, C2};       // compute lanes: group g runs on lane g % 2
     const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
     for (uint64_t g = 0; g < G; ++g) {
         PCU(cudaEventCreateWithFlags(&h2d[g], evflags));
@@ -160,6 +161,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         cudaEventRecord(start, C);
         cudaStreamWaitEvent(H, start, 0);
         cudaStreamWaitEvent(D, start, 0);
+        cudaStreamWaitEvent(C2, start, 0);
     }
     auto enqueue_h2d = [&](uint64_t g) -> cudaError_t {
         const int s = (int)(g & 1);
@@ -173,7 +175,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     };
     // D2H of group g's offsets needs m[g] (read after the host has synchronised past schedule(g))
     auto enqueue_d2h = [&](uint64_t g, uint64_t moff) -> cudaError_t {
-        const int s = (int)(g & 1);
+        const int s = (int)(g % 3);
         const uint64_t a = qa(g), len = qz(g) - a;
         cudaStreamWaitEvent(D, done[g], 0);
         cudaError_t e;
@@ -184,48 +186,52 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     };
     PCU(enqueue_h2d(0));
     {
+        // Two compute lanes: group g loads / schedules / summarises on lane g % 2 with its own
+        // workspace, so one group's latency-bound tail (the DP's last tiles, the traceback)
+        // overlaps the next group's sort.  Group g's load synchronises its lane, i.e. group g-2 is
+        // complete: its batch count is read and its results go back on the D stream then.
         uint64_t moff = 0;
+        auto flush_group = [&](uint64_t gd, cudaStream_t lane) -> cudaError_t {
+            cudaError_t e;
+            if ((e = cudaMemcpyAsync(&m[gd], (uint64_t *)(w + PL.nb) + gd, 8, cudaMemcpyDeviceToHost, lane))) return e;
+            if ((e = cudaStreamSynchronize(lane))) return e;
+            if ((e = enqueue_d2h(gd, moff))) return e;
+            moff += m[gd];
+            return cudaSuccess;
+        };
         for (uint64_t g = 0; g < G; ++g) {
-            const int s = (int)(g & 1);
+            const int s = (int)(g & 1), o = (int)(g % 3);
+            cudaStream_t L = CS[s];
             const uint64_t a = qa(g), len = qz(g) - a;
             if (g + 1 < G) PCU(enqueue_h2d(g + 1));
-            PCU(cudaStreamWaitEvent(C, h2d[g], 0));
-            if (g >= 2) PCU(cudaStreamWaitEvent(C, d2h[g - 2], 0));     // output slot free again
+            PCU(cudaStreamWaitEvent(L, h2d[g], 0));
             uellm_queries gq_ = {len, (const uint32_t *)(w + PL.in[s]), (const uint32_t *)(w + PL.out[s]),
                                  (const float *)(w + PL.slo[s])};
             uellm_profile prof;
-            // synchronises C: by now schedule(g-1) has completed and m[g-1] is on the host
             const double t0 = ms();
-            uellm_status st = uellm_profile_load(&gq_, &gcfg, w + PL.ws, PL.ws_bytes, stream, &prof);
+            uellm_status st = uellm_profile_load(&gq_, &gcfg, w + PL.ws[s], PL.ws_bytes, L, &prof);
             if (st != UELLM_OK) return st;
             const double t1 = ms();
-            if (g >= 1) {
-                // schedule(g-1) is complete (the load synchronised C and nothing is queued after
-                // it yet): an 8-byte read of its batch count, no pinned host block needed
-                PCU(cudaMemcpyAsync(&m[g - 1], (uint64_t *)(w + PL.nb) + (g - 1), 8, cudaMemcpyDeviceToHost, C));
-                PCU(cudaStreamSynchronize(C));
-                PCU(enqueue_d2h(g - 1, moff));
-                moff += m[g - 1];
-            }
-            uint32_t *d_order = (uint32_t *)(w + PL.order[s]);
-            uint32_t *d_offs = (uint32_t *)(w + PL.offs[s]);
+            if (g >= 2) PCU(flush_group(g - 2, L));
+            if (g >= 3) PCU(cudaStreamWaitEvent(L, d2h[g - 3], 0));     // output slot g % 3 free again
+            uint32_t *d_order = (uint32_t *)(w + PL.order[o]);
+            uint32_t *d_offs = (uint32_t *)(w + PL.offs[o]);
             uint64_t *d_nb = (uint64_t *)(w + PL.nb) + g;
             uellm_totals *d_tot = (uellm_totals *)(w + PL.tot) + g;
-            if ((st = uellm_schedule_batches(&prof, &gcfg, d_order, d_offs, d_nb, stream)) != UELLM_OK) return st;
+            if ((st = uellm_schedule_batches(&prof, &gcfg, d_order, d_offs, d_nb, L)) != UELLM_OK) return st;
             const double t2 = ms();
-            if ((st = uellm_batch_stats(&prof, &gcfg, d_offs, d_nb, nullptr, d_tot, stream)) != UELLM_OK) return st;
+            if ((st = uellm_batch_stats(&prof, &gcfg, d_offs, d_nb, nullptr, d_tot, L)) != UELLM_OK) return st;
             if (trace)
                 fprintf(stderr, "[pipe] g=%llu load_in %.3f load_out %.3f sched_out %.3f stats_out %.3f ms\n",
                         (unsigned long long)g, t0, t1, t2, ms());
-            PCU(add_base(d_order, len, (uint32_t)a, C));       // group-local -> caller indices
-            PCU(add_base(d_offs, len + 1, (uint32_t)a, C));    // (only [0, m_g] are copied)
-            PCU(cudaEventRecord(done[g], C));
+            PCU(add_base(d_order, len, (uint32_t)a, L));       // group-local -> caller indices
+            PCU(add_base(d_offs, len + 1, (uint32_t)a, L));    // (only [0, m_g] are copied)
+            PCU(cudaEventRecord(done[g], L));
         }
-        PCU(cudaStreamSynchronize(C));
-        PCU(cudaMemcpy(&m[G - 1], (uint64_t *)(w + PL.nb) + (G - 1), 8, cudaMemcpyDeviceToHost));
+        for (uint64_t gd = G >= 2 ? G - 2 : 0; gd < G; ++gd) PCU(flush_group(gd, CS[gd & 1]));
+        PCU(cudaStreamSynchronize(CS[0]));
+        PCU(cudaStreamSynchronize(CS[1]));
         PCU(cudaMemcpy(tot_host.data(), w + PL.tot, sizeof(uellm_totals) * G, cudaMemcpyDeviceToHost));
-        PCU(enqueue_d2h(G - 1, moff));
-        moff += m[G - 1];
         PCU(cudaStreamSynchronize(D));
         if (trace) {
             fprintf(stderr, "[pipe] end %.3f ms (%llu groups)\n", ms(), (unsigned long long)G);
@@ -264,6 +270,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     if (status != UELLM_OK) { cudaStreamSynchronize(C); }
     if (H) { cudaStreamSynchronize(H); cudaStreamDestroy(H); }
     if (D) { cudaStreamSynchronize(D); cudaStreamDestroy(D); }
+    if (C2) { cudaStreamSynchronize(C2); cudaStreamDestroy(C2); }
     for (uint64_t g = 0; g < G; ++g) {
         if (h2d[g]) cudaEventDestroy(h2d[g]);
         if (done[g]) cudaEventDestroy(done[g]);

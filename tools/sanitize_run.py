@@ -46,5 +46,14 @@ for levels in (True, False):
 topo = W.random_topology(3, 6)
 wsb = U.helr_workspace_bytes(6)
 U.helr_plan(topo, torch.zeros(wsb, dtype=torch.uint8, device=dev), wsb)
+# host-buffer pipelined call (two compute lanes, copy streams)
+inp, out, slo, cfg = W.c3(4, n=30_000)
+cfg = cfg.replace(window=5000)
+c = U.make_config(cfg)
+wsb = U.pipeline_workspace_bytes(30_000, c, 3)
+ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+tot = U.Totals()
+U.schedule_pipelined(30_000, inp, out, slo, c, 3, ws, wsb, np.zeros(30_000, np.uint32), np.zeros(30_001, np.uint32),
+                     np.zeros(1, np.uint64), ctypes.addressof(tot))
 torch.cuda.synchronize()
 print("SANITIZE_RUN_OK")
