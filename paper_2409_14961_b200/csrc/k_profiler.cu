@@ -152,9 +152,13 @@ __global__ void __launch_bounds__(256) k_pred_count(PredictParams P, uint64_t n,
         uint32_t w = 0xffffffffu;
         if (k < n) {
             const uint32_t t = __ldg(P.true_len + k);
-            w = (uint32_t)(k / window);
+            w = (uint32_t)k / (uint32_t)window;             // 32-bit: n < 2^32 (a 64-bit divide is ~10x)
             const unsigned long long base = base_of(P, k, t);
-            for (uint32_t i = 0; i <= K; ++i) under |= (uint32_t)(t > inflate(base, V[i])) << i;
+            // every level factor is >= 1, so inflate(base, v) >= base: only a base below the true
+            // length can be an under-prediction at some level (the noisy variant's downward moves,
+            // a small constant) -- the common case needs no double arithmetic
+            if (base < t)
+                for (uint32_t i = 0; i <= K; ++i) under |= (uint32_t)(t > inflate(base, V[i])) << i;
         }
         const uint32_t grp = __match_any_sync(0xffffffffu, w);
         const uint32_t lane = threadIdx.x & 31;
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(256) k_pred_write(PredictParams P, uint64_t n,
     const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += nt) {
         const uint32_t t = __ldg(P.true_len + k);
-        P.pred[k] = predict_one(P, k, t, P.levels[P.wlevel[k / window]]);
+        P.pred[k] = predict_one(P, k, t, P.levels[P.wlevel[(uint32_t)k / (uint32_t)window]]);
     }
 }
 

@@ -37,7 +37,7 @@ struct PipeLayout {
     uint64_t groups;
     uint64_t wl, nwin, tail, per, rem; // group g = windows [gwin(g), gwin(g+1)) (see gwin)
     uint64_t ws[2], ws_bytes;         // scheduling workspaces of the two compute lanes
-    uint64_t in[2], out[2], slo[2];   // input staging slots (one per compute lane)
+    uint64_t in[3], out[3], slo[3];   // input staging slots (g % 3)
     uint64_t order[3], offs[3];       // output staging slots (g % 3)
     uint64_t tot, nb;                 // per-group totals / num_batches (device)
     uint64_t total;
@@ -71,7 +71,7 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     P.ws[0] = take(P.ws_bytes);
     P.ws[1] = take(P.ws_bytes);
     const uint64_t q = P.group_q ? P.group_q : 1;
-    for (int s = 0; s < 2; ++s) { P.in[s] = take(4 * q); P.out[s] = take(4 * q); P.slo[s] = take(4 * q); }
+    for (int s = 0; s < 3; ++s) { P.in[s] = take(4 * q); P.out[s] = take(4 * q); P.slo[s] = take(4 * q); }
     for (int s = 0; s < 3; ++s) { P.order[s] = take(4 * q); P.offs[s] = take(4 * (q + 1)); }
     P.tot = take(sizeof(uellm_totals) * (P.groups ? P.groups : 1));
     P.nb = take(8 * (P.groups ? P.groups : 1));
@@ -164,8 +164,8 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         cudaStreamWaitEvent(C2, start, 0);
     }
     auto enqueue_h2d = [&](uint64_t g) -> cudaError_t {
-        const int s = (int)(g & 1);
-        if (g >= 2) cudaStreamWaitEvent(H, done[g - 2], 0);    // staging slot free again
+        const int s = (int)(g % 3);
+        if (g >= 3) cudaStreamWaitEvent(H, done[g - 3], 0);    // staging slot free again
         const uint64_t a = qa(g), len = qz(g) - a;
         cudaError_t e;
         if ((e = cudaMemcpyAsync(w + PL.in[s], q->input_len + a, 4 * len, cudaMemcpyHostToDevice, H))) return e;
@@ -203,10 +203,12 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
             const int s = (int)(g & 1), o = (int)(g % 3);
             cudaStream_t L = CS[s];
             const uint64_t a = qa(g), len = qz(g) - a;
-            if (g + 1 < G) PCU(enqueue_h2d(g + 1));
+            if (g == 0 && G > 1) PCU(enqueue_h2d(1));
+            if (g + 2 < G) PCU(enqueue_h2d(g + 2));           // copies run up to two groups ahead
             PCU(cudaStreamWaitEvent(L, h2d[g], 0));
-            uellm_queries gq_ = {len, (const uint32_t *)(w + PL.in[s]), (const uint32_t *)(w + PL.out[s]),
-                                 (const float *)(w + PL.slo[s])};
+            const int si = (int)(g % 3);
+            uellm_queries gq_ = {len, (const uint32_t *)(w + PL.in[si]), (const uint32_t *)(w + PL.out[si]),
+                                 (const float *)(w + PL.slo[si])};
             uellm_profile prof;
             const double t0 = ms();
             uellm_status st = uellm_profile_load(&gq_, &gcfg, w + PL.ws[s], PL.ws_bytes, L, &prof);
