@@ -110,8 +110,19 @@ def ncu_traffic(kernel: str):
     return k.get("dram_bytes_per_launch") if k else None
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(inp, out, slo, cfg, windows: int):
-    """The oracle as it stands on the host cores, on a bounded sample (first `windows` windows)."""
+    """The oracle as it stands on the host cores, on a bounded sample (first `windows` windows),
+    plus one window on one thread (core count, CPU model, single-thread run)."""
     import oracle
     cores = os.cpu_count() or 1
     nq = min(len(inp), windows * cfg.window)
@@ -119,7 +130,14 @@ def cpu_baseline(inp, out, slo, cfg, windows: int):
     o = oracle.schedule(inp[:nq], out[:nq], slo[:nq], cfg, nthreads=cores)
     oracle.stats(inp[:nq], out[:nq], slo[:nq], cfg, o[0], o[1])
     dt = time.perf_counter() - t
+    n1 = min(len(inp), cfg.window or len(inp))
+    t = time.perf_counter()
+    o = oracle.schedule(inp[:n1], out[:n1], slo[:n1], cfg, nthreads=1)
+    oracle.stats(inp[:n1], out[:n1], slo[:n1], cfg, o[0], o[1])
+    dt1 = time.perf_counter() - t
     return {"value": nq / dt, "unit": UNIT, "cores": min(cores, windows), "kind": "oracle",
+            "cpu_model": cpu_model(), "host_cores": cores,
+            "single_thread": {"value": n1 / dt1, "unit": UNIT, "sample": f"first window ({n1} queries), {dt1:.2f} s"},
             "sample": f"first {windows} windows ({nq} queries) of the same workload, schedule + stats, "
                       f"{min(cores, windows)} threads (one window per thread), {dt:.1f} s"}
 
@@ -148,6 +166,7 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": desc, "sample_queries": nq, "windows": nwin},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, nwin), "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"{nwin} windows x {wl} queries per step, one window per thread"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -177,9 +177,10 @@ __global__ void __launch_bounds__(1024) k_slo_table(const uint32_t *__restrict__
     }
     __syncthreads();
     const uint32_t K = min(cnt, kSloRankMax);
+    for (uint32_t r = K + threadIdx.x; r < kSloRankMax; r += blockDim.x) table[r] = 0;   // unused ranks
     for (uint32_t h = threadIdx.x; h < kSloSetSize; h += blockDim.x) {
         const uint32_t v = slo_set[h];
-        if (!v) continue;
+        if (!v) { rank_of_slot[h] = 0; continue; }     // empty slots are copied too (initcheck-clean)
         uint32_t r = 0;
         for (uint32_t f = 0; f < K; ++f) r += vals[f] < v;
         rank_of_slot[h] = r;
