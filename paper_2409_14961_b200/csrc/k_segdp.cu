@@ -600,14 +600,30 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 const bool dead = (lane <= q) | (b > W) | ((single_ok | (b > 1)) & (b * (pmo + mi) > cap32));
                 if (!dead && tot < r32) { r32 = tot; ri = j0 + 1 + q; }
             }
+            if (Qd == 0 && B == 32) {
+                // the common case, fully unrolled: q is a compile-time constant, so the table
+                // entry of (q, lane) is M[lane + tri_off(q) - q - 1] -- an immediate offset from
+                // the lane's base, no address arithmetic per step
+                const uint32_t *Ml = M + (int)lane;
+                const uint32_t j0p1 = j0 + 1;
+#pragma unroll
+                for (int q = 0; q < 31; ++q) {
+                    const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
+                    const uint32_t b = lane - (uint32_t)q;
+                    const uint32_t mi = Ml[(int)tri_off(q) - q - 1] & 0xffffu;
+                    const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
+                    if (lane > (uint32_t)q && tot < r32) { r32 = tot; ri = j0p1 + (uint32_t)q; }
+                }
+            } else {
 #pragma unroll 4
-            for (uint32_t q = Qd; q + 1 < B; ++q) {
-                const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
-                const uint32_t b = lane - q;
-                const uint32_t mi = M[off] & 0xffffu;
-                off += 30 - (int)q;
-                const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
-                if (lane > q && tot < r32) { r32 = tot; ri = j0 + 1 + q; }
+                for (uint32_t q = Qd; q + 1 < B; ++q) {
+                    const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
+                    const uint32_t b = lane - q;
+                    const uint32_t mi = M[off] & 0xffffu;
+                    off += 30 - (int)q;
+                    const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
+                    if (lane > q && tot < r32) { r32 = tot; ri = j0 + 1 + q; }
+                }
             }
             lb = (unsigned long long)base + r32;
             lbi = ri;
