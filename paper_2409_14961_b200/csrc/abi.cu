@@ -27,12 +27,14 @@ uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_ti
     if (dp_tile) {
         T = align_up(dp_tile, W);
     } else {
-        // ~3 waves of 32 resident DP warps per SM: short tiles balance the data-dependent
-        // per-tile work (measured on c4: 7 K-query tiles beat 28 K by 1.37x; fix-ups cost ~5 %).
+        // ~4.6 tiles per resident DP warp (32 per SM): short tiles balance the data-dependent
+        // per-tile work against the fix-ups (tools/sweep_tile.sh on c4, DP ms by tile length:
+        // 3584: 7.10, 4608: 7.05, 5120: 7.36, 7168: 7.38, 8192: 7.79; fix-ups re-evaluate 7.4 %
+        // of the positions at 4608).
         // The 16 W floor stays for small jobs too: one-wave tiles of 4 W .. 16 W were measured
         // slower on 6-7 M-query window groups (3.5-7 ms against 2.7 ms per group: more fix-ups
         // and cascade re-runs than the extra parallelism gains).
-        const uint64_t target_tiles = 148ull * 96;
+        const uint64_t target_tiles = 148ull * 148;
         T = ceil_div(n ? n : 1, target_tiles);
         T = T < 16ull * W ? 16ull * W : T;
         T = align_up(T, W);

@@ -34,6 +34,15 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// relaxed (gpu scope) poll: unlike ld.acquire it does not invalidate the SM's L1 on every
+// iteration (CCTL.IVALL), which would evict the records other warps on the SM are streaming; the
+// acquire is a single fence once the flag is seen
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(uint32_t *p, uint32_t v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -833,8 +842,9 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_tiles(DPParams P,
         tile_bounds(P, t, s, e, k, w, valid);
         if (!valid || k == 0) continue;
         if (lane == 0) {
-            while (ld_acquire(P.tflags + t - 1) == 0u) __nanosleep(64);
-            while (ld_acquire(P.tflags + t) == 0u) __nanosleep(64);
+            while (ld_relaxed(P.tflags + t - 1) == 0u) __nanosleep(128);
+            while (ld_relaxed(P.tflags + t) == 0u) __nanosleep(128);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");     // acquire: pairs with st.release
         }
         __syncwarp();
         __threadfence();
