@@ -379,7 +379,10 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     // Prune slots [0, Lt) at the state of boundary jend: slots below Lold first fold the block
     // maxima (bmo, bmi).  Drops the dead prefix (b > W, KV cap, SLO split) and every candidate
     // dominated (D1) by its successor; survivors are compacted in order.
-    auto prune = [&](uint32_t Lt, uint32_t Lold, uint32_t bmo, uint32_t bmi, uint32_t jend) {
+    // onerun: every candidate and every element up to jend lie in one SLO run of value slo_run
+    // (enables the penalty-aware D1, see dominated_by)
+    auto prune = [&](uint32_t Lt, uint32_t Lold, uint32_t bmo, uint32_t bmi, uint32_t jend, bool onerun,
+                     uint32_t slo_run) {
         uint32_t wr = 0;
         for (uint32_t r = 0; r * 32 < Lt; ++r) {
             const uint32_t k = r * 32 + lane;
@@ -396,13 +399,24 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             // D1 against the successors at list distance 1, 8 and 32 (any later candidate is a valid
             // dominator: strict dominance is transitive and a later candidate outlives an earlier
             // one, so dropping i needs no dominator to be kept).  (n_i - i) * S < W * S <= E < 2^32.
+            // Penalty-aware D1 (exact): when the later candidate i' already violates at this state
+            // inside one SLO run (slo_run < est(i', jend)), every member of [i, i') violates under
+            // est(i', j) <= est(i, j) for every later j -- est only grows and the members' SLOs are
+            // slo_run -- so viol(i, j) >= viol(i', j) + (i' - i) and the dominance slope gains
+            // lambda per position: i is dead once C[i'] - C[i] < (i' - i) * (S(i', j) + lambda).
             auto dominated_by = [&](uint32_t k2) -> bool {
                 const longlong2 nv = S.sl[k2];
                 const unsigned long long np = (unsigned long long)nv.y;
                 uint32_t nmo = (uint32_t)(np >> 32) & 0xffffu, nmi = (uint32_t)(np >> 48);
                 if (k2 < Lold) { nmo = max(nmo, bmo); nmi = max(nmi, bmi); }
                 const uint32_t nS = t_tok * nmo + t_pre * nmi;
-                return nv.x - cC < (long long)(unsigned long long)(((uint32_t)np - ci) * nS);
+                const uint32_t gap = (uint32_t)np - ci;
+                long long rhs = (long long)(unsigned long long)(gap * nS);
+                if (LAM && onerun) {
+                    const uint32_t nest = t_b + t_it * nmo + (jend - (uint32_t)np) * nS;
+                    if (slo_run < nest) rhs += (long long)penalty(gap);
+                }
+                return nv.x - cC < rhs;
             };
             bool dominated = false;
             if (!dead) {
@@ -422,7 +436,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         }
         L = wr;
     };
-    if (FIX) prune(L, L, 0, 0, s);      // the W fix-up candidates, pruned before the first block
+    if (FIX) prune(L, L, 0, 0, s, false, 0u);   // the W fix-up candidates, pruned before the first block
     uint32_t evals = 0;
     bool stop = false;
     uint32_t done = s;
@@ -743,7 +757,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         if (vl) SW.put(S, L + lane, iC, j0 + 1 + lane, imo, imi);
         evals += B * (B - 1) / 2;
         __syncwarp();
-        prune(L + B, L, bmo, bmi, jend);
+        prune(L + B, L, bmo, bmi, jend, one_run_ext && one_run_intra, prev_slo);
     }
     R.positions = done - s;
     R.evals = evals;
