@@ -185,7 +185,7 @@ def main():
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-row timings (f2, f3, f4)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo only for multi-rank tests on one GPU)")
-    ap.add_argument("--e2e-groups", type=int, default=0, help="window groups of the pipelined e2e call (0 = 8)")
+    ap.add_argument("--e2e-groups", type=int, default=0, help="window groups of the pipelined e2e call (0 = 12)")
     ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
     ap.add_argument("--mode", default="seg_dp", choices=["seg_dp", "slo_odbs", "fifo", "sort_only"],
                     help="segmentation mode (default: the SEG-DP hot path)")
@@ -371,7 +371,7 @@ def main():
         mh = int(h_nb[0])
         e2e = {"value": world * n / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 4 * n + 4 * (mh + 1) + 8 + U.TOTALS_BYTES,
-               "ms_per_step": float(te.item()), "api": f"uellm_schedule_pipelined ({groups or 8} window groups)",
+               "ms_per_step": float(te.item()), "api": f"uellm_schedule_pipelined ({groups or 12} window groups)",
                "exchange": "N > 1: allgather of the per-rank totals (the boundaries are already in each rank's host buffers)"}
         assert mh == m and h_tot.dp_cost == res["totals"]["dp_cost"], "host-buffer path disagrees with the device path"
 

@@ -389,7 +389,7 @@ uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes,
 
 /* End-to-end scheduling of HOST-resident queries with the PCIe copies overlapped with the GPU
  * work.  Windows are independent (R15), so the job is cut into `groups` groups of whole windows
- * (0 = 8); group g+1's host->device copy and group g-1's device->host copy run on two internal
+ * (0 = 12); group g+1's host->device copy and group g-1's device->host copy run on two internal
  * copy streams while group g is loaded, scheduled and summarised on `stream` -- the same
  * results as uellm_profile_load + uellm_schedule_batches + uellm_batch_stats on the whole job
  * (mean_latency_s is re-weighted from the groups' means: within 1e-12 relative).

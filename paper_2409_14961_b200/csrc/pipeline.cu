@@ -49,7 +49,7 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     std::memset(&P, 0, sizeof P);
     const uint64_t wl = cfg.window ? (cfg.window < n ? cfg.window : n) : n;
     const uint64_t nwin = n ? ceil_div(n, wl ? wl : 1) : 0;
-    uint64_t G = groups ? groups : 8;
+    uint64_t G = groups ? groups : 12;
     if (G > nwin) G = nwin ? nwin : 1;
     // The pipeline is bound by the host->device copies; once the last group's copy lands, its
     // load / schedule / stats and device->host copy are exposed.  So the last group is small
