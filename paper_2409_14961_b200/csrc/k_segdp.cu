@@ -882,9 +882,45 @@ __global__ void k_dp_cascade(DPParams P)
     const uint32_t w = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t t0 = (uint64_t)w * P.tpw;
+    // valid tiles form a prefix of the window's tpw slots: count them 32 at a time, and check
+    // whether every fix-up converged (the common case: then the frame offsets are a prefix sum
+    // of the deltas, computed warp-parallel instead of walking the tiles one by one)
     uint32_t K = 0;
-    while (K < P.tpw && P.tiles[t0 + K].valid) ++K;
+    bool allconv = true;
+    for (uint32_t k0 = 0; k0 < P.tpw; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool v = k < P.tpw && P.tiles[t0 + k].valid;
+        const uint32_t bv = __ballot_sync(0xffffffffu, v);
+        K += __popc(bv);
+        const bool nc = v && k >= 1 && !P.tiles[t0 + k].conv;
+        if (__any_sync(0xffffffffu, nc)) allconv = false;
+        if (bv != 0xffffffffu) break;
+    }
     if (K == 0) return;
+    if (allconv) {
+        long long carry = 0;                                    // off_local of the previous tile
+        for (uint32_t k0 = 0; k0 < K; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            const long long d = (k >= 1 && k < K) ? P.tiles[t0 + k].delta : 0ll;
+            long long inc = d;                                  // inclusive warp scan of deltas
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+                if ((int)lane >= o) inc += y;
+            }
+            if (k < K) {
+                P.tiles[t0 + k].off_fix = k ? carry + inc - d : 0ll;
+                P.tiles[t0 + k].off_local = k ? carry + inc : 0ll;
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const TileRec &r = P.tiles[t0 + K - 1];
+            P.wincost[w] = (unsigned long long)(P.Cx[r.e - 1] + (K == 1 ? 0ll : r.off_local));
+        }
+        return;
+    }
     // tile 0 is exact in its local frame
     long long tail_off = 0;          // offset of the frame holding tile (k-1)'s tail values
     bool tail_local = true;          // tail in Cx (local frame) vs CFx (fix-up frame)

@@ -102,13 +102,27 @@ __global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uin
 __global__ void k_trace_c(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t tpw, uint64_t nwin,
                           uint64_t window, uint32_t *bm, Diag *diag)
 {
-    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per window: count the valid tiles (a prefix) and check 32 tiles at a time whether
+    // every B-walk merged (exitB == exitA for tiles 1 .. K-1) -- then every tile's entry was right
+    // and nothing needs re-walking; otherwise lane 0 walks the tiles in order (rare)
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     if (w >= nwin) return;
     const uint64_t t0 = w * tpw;
     uint32_t K = 0;
-    while (K < tpw && tiles[t0 + K].valid) ++K;
-    if (K == 0) return;
+    bool allm = true;
+    for (uint32_t k0 = 0; k0 < tpw; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool v = k < tpw && tiles[t0 + k].valid;
+        const uint32_t bv = __ballot_sync(0xffffffffu, v);
+        K += __popc(bv);
+        const bool bad = v && k >= 1 && tiles[t0 + k].exitB != tiles[t0 + k].exitA;
+        if (__any_sync(0xffffffffu, bad)) allm = false;
+        if (bv != 0xffffffffu) break;
+    }
+    if (K == 0 || lane != 0) return;
     bm_set(bm, (uint32_t)(w * window));                 // every window starts a batch
+    if (allm) return;
     uint32_t exit_true = tiles[t0 + K - 1].exitB;
     for (int k = (int)K - 2; k >= 0; --k) {
         const TileRec r = tiles[t0 + k];
@@ -144,7 +158,7 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
         k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
     }
     k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag);
-    k_trace_c<<<(unsigned)ceil_div(P.nwin, 64), 64, 0, st>>>(P.argx, P.tiles, P.tpw, P.nwin, P.window, bitmap,
+    k_trace_c<<<(unsigned)ceil_div(P.nwin * 32, 128), 128, 0, st>>>(P.argx, P.tiles, P.tpw, P.nwin, P.window, bitmap,
                                                            P.diag);
     return cudaGetLastError();
 }

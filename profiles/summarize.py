@@ -75,6 +75,7 @@ def main():
         K[key] = {"duration_ms": dur, "dram_read_bytes": rd, "dram_write_bytes": wr,
                   "dram_bytes_per_launch": rd + wr, "dram_gbs": (rd + wr) / dur / 1e6,
                   "inst_executed": float(r[ix["smsp__inst_executed.sum"]]),
+                  "l2_bytes": float(r[ix["lts__t_sectors.sum"]]) * 32.0,
                   "issue_active_pct": float(r[ix["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                   "warps_active_pct": float(r[ix["sm__warps_active.avg.pct_of_peak_sustained_active"]]),
                   "registers": int(float(r[ix["launch__registers_per_thread"]]))}
@@ -86,11 +87,12 @@ def main():
     md = [f"# {a.tag} ncu summary (B200, c4 = 10^8 queries, one step)", "",
           f"Bench line of the same code: {bench['value']:.3e} q/s, {bench['ms_per_step']:.2f} ms/step "
           f"(stage ms: " + ", ".join(f"{k} {v:.2f}" for k, v in bench["stage_ms"].items()) + ").", "",
-          "| kernel | ms (ncu) | DRAM read GB | DRAM write GB | DRAM GB/s | issue active % | warps active % | regs |",
-          "|---|---|---|---|---|---|---|---|"]
+          "| kernel | ms (ncu) | DRAM read GB | DRAM write GB | DRAM GB/s | L2 GB/s | issue active % | warps active % | regs |",
+          "|---|---|---|---|---|---|---|---|---|"]
     for k, v in K.items():
         md.append(f"| {k} | {v['duration_ms']:.3f} | {v['dram_read_bytes'] / 1e9:.3f} | "
-                  f"{v['dram_write_bytes'] / 1e9:.3f} | {v['dram_gbs']:.0f} | {v['issue_active_pct']:.1f} | "
+                  f"{v['dram_write_bytes'] / 1e9:.3f} | {v['dram_gbs']:.0f} | {v['l2_bytes'] / v['duration_ms'] / 1e6:.0f} | "
+                  f"{v['issue_active_pct']:.1f} | "
                   f"{v['warps_active_pct']:.1f} | {v['registers']} |")
     md += ["", f"SEG-DP: {K['k_dp_tiles']['inst_executed'] / 1e8:.1f} warp instructions per query, "
                f"{summ['dp_warp_inst_per_eval']:.3f} per candidate evaluation ({evals / 1e8:.1f} evaluations per query)."]
