@@ -226,10 +226,10 @@ cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cud
     } else {
         for (uint64_t w = 0, a = 0; a < n; a += window, ++w) {
             const uint64_t z = a + window < n ? a + window : n;
-            // two CTAs per SM: every CTA ends with two atomics on the window's counters (same
-            // address), so fewer, fatter CTAs keep that serialised tail short
-            const uint64_t nb = ceil_div(z - a, 256 * 8);
-            const unsigned blocks = (unsigned)(nb < 148 * 2 ? nb : 148 * 2);
+            // (measured: 2 CTAs per SM, to shorten the same-address atomic tail, is slower --
+            // 1.65 vs 1.03 ms per 10^8 -- the window is too small to hide latency with fewer CTAs)
+            const uint64_t nb = ceil_div(z - a, 256 * 4);
+            const unsigned blocks = (unsigned)(nb < 148 * 8 ? nb : 148 * 8);
             k_predict_window<<<blocks, 256, 0, st>>>(P, a, z, w);
             ++l;
         }

@@ -436,3 +436,4 @@ def test_compute_sanitizer(tool):
     assert r.returncode == 0 and "SANITIZE_RUN_OK" in r.stdout, tail
     out = r.stdout + r.stderr
     assert "ERROR SUMMARY: 0 errors" in out or "(0 errors, 0 warnings)" in out, tail
+

@@ -9,7 +9,7 @@ n = len(inp); c = U.make_config(cfg)
 p_in = torch.from_numpy(inp.view(np.int32)).pin_memory(); p_out = torch.from_numpy(out.view(np.int32)).pin_memory(); p_slo = torch.from_numpy(slo).pin_memory()
 h_order = torch.empty(n, dtype=torch.int32).pin_memory(); h_offs = torch.empty(n + 1, dtype=torch.int32).pin_memory()
 nb = np.zeros(1, np.uint64); tot = U.Totals(); st = torch.cuda.Stream()
-for groups in (8, 16):
+for groups in (12,):
     wsb = U.pipeline_workspace_bytes(n, c, groups); ws = torch.empty(wsb, dtype=torch.uint8, device="cuda:0")
     for it in range(2):
         t = time.perf_counter()
