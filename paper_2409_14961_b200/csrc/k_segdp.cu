@@ -396,7 +396,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             if (k < Lold) { mo = max(mo, bmo); mi = max(mi, bmi); }
             const uint32_t b = jend - ci;
             const bool dead = !valid | (b > W) | ((b > 1) & (b * (mo + mi) > cap32)) | (split & (ci < run_start));
-            // D1 against the successors at list distance 1, 8 and 32 (any later candidate is a valid
+            // D1 against the successors at list distance 1 and 32 (any later candidate is a valid
             // dominator: strict dominance is transitive and a later candidate outlives an earlier
             // one, so dropping i needs no dominator to be kept).  (n_i - i) * S < W * S <= E < 2^32.
             // Penalty-aware D1 (exact): when the later candidate i' already violates at this state
@@ -420,9 +420,17 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             };
             bool dominated = false;
             if (!dead) {
+// successors tested besides the next one (tools/variant_run.sh on c4, DP ms: {8, 32}: 6.74,
+// {32}: 6.57, {16}: 6.59, {64}: 6.67, {8}: 6.69, {}: 6.82, {4, 16}: 6.84, {16, 64}: 6.68)
+#ifndef UELLM_D1_D2
+#define UELLM_D1_D2 0
+#endif
+#ifndef UELLM_D1_D3
+#define UELLM_D1_D3 32
+#endif
                 if (k + 1 < Lt) dominated = dominated_by(k + 1);
-                if (!dominated && k + 8 < Lt) dominated = dominated_by(k + 8);
-                if (!dominated && k + 32 < Lt) dominated = dominated_by(k + 32);
+                if (UELLM_D1_D2 && !dominated && k + UELLM_D1_D2 < Lt) dominated = dominated_by(k + UELLM_D1_D2);
+                if (UELLM_D1_D3 && !dominated && k + UELLM_D1_D3 < Lt) dominated = dominated_by(k + UELLM_D1_D3);
             }
             const bool keep = !dead && !dominated;
             __syncwarp();
