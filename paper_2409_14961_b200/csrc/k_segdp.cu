@@ -28,6 +28,11 @@
 
 namespace uellm {
 
+#ifndef UELLM_EXT_UNROLL
+#define UELLM_EXT_UNROLL 4
+#endif
+constexpr int kExtUnroll = UELLM_EXT_UNROLL;   // unroll of the fast block's external-candidate loop
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
 {
     uint32_t v;
@@ -603,7 +608,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             if (Vs > Pd) ext_lean(Pd, Vs);             // may violate: 64-bit with the penalty
             const uint32_t base_lo = (uint32_t)base;
             uint32_t r32 = 0xffffffffu, ri = 0xffffffffu;
-#pragma unroll 4
+#pragma unroll (kExtUnroll)
             for (uint32_t c = Vs; c < L; ++c) {
                 const longlong2 sv = S.sl[c];
                 const uint32_t ci = (uint32_t)sv.y;
@@ -822,7 +827,10 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
 // local run belongs to a running warp that sets its flag before claiming anything else, so the
 // waits always end; the fix-ups fill the SMs as the local runs drain instead of a second,
 // tail-bound launch.
-__global__ void __launch_bounds__(kDpWarpsPerCta * 32, 4) k_dp_tiles(DPParams P, uint64_t ntiles)
+#ifndef UELLM_DP_MINB
+#define UELLM_DP_MINB 3     // 78 registers, no spills, 24 warps per SM (DP 6.53 vs 6.57 ms at 4)
+#endif
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_tiles(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
     const uint32_t lane = threadIdx.x & 31;
