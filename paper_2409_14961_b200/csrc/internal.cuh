@@ -11,8 +11,16 @@
 namespace uellm {
 
 constexpr uint32_t kMaxBatchLimit = 4096;      // W limit of this build (UELLM_ERR_UNSUPPORTED)
-constexpr uint32_t kSortTile = 4096;           // keys per radix-sort CTA (512 threads x 8)
-constexpr uint32_t kSortThreads = 512;
+// radix-sort CTA shape (tools/variant_run.sh on c4, sort ms: 2048 x 256: 2.51, 4096 x 512: 2.54,
+// 2048 x 512: 2.64, 4096 x 256: 2.70, 8192 x 1024: 2.87, 1024 x 256: 3.10)
+#ifndef UELLM_SORT_TILE
+#define UELLM_SORT_TILE 2048
+#endif
+#ifndef UELLM_SORT_THREADS
+#define UELLM_SORT_THREADS 256
+#endif
+constexpr uint32_t kSortTile = UELLM_SORT_TILE;         // keys per radix-sort CTA (256 threads x 8)
+constexpr uint32_t kSortThreads = UELLM_SORT_THREADS;
 constexpr uint32_t kSortItems = kSortTile / kSortThreads;
 constexpr uint32_t kDpWarpsPerCta = 8;
 constexpr uint32_t kScanBlock = 1024;          // elements per CTA in the scan kernels
