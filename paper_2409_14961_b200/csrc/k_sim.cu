@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(256) k_sim_gather(SimParams S)
         S.arr_s[k] = __ldg(S.arrival + __ldg(S.order + k));
 }
 
-constexpr uint32_t kSimGroup = 8;     // lanes per batch in the member-streaming loops
+#ifndef UELLM_GROUP_LANES
+#define UELLM_GROUP_LANES 8
+#endif
+constexpr uint32_t kSimGroup = UELLM_GROUP_LANES;   // lanes per batch in the member-streaming loops
 
 __global__ void __launch_bounds__(kScanBlock) k_sim_batches(SimParams S)
 {

@@ -15,7 +15,10 @@
 
 namespace uellm {
 
-constexpr uint32_t kStatsGroup = 8;   // lanes per batch in the member-streaming passes
+#ifndef UELLM_GROUP_LANES
+#define UELLM_GROUP_LANES 8
+#endif
+constexpr uint32_t kStatsGroup = UELLM_GROUP_LANES;   // lanes per batch in the member-streaming loops
 
 __device__ __forceinline__ uint32_t warp_max(uint32_t v)
 {

@@ -49,7 +49,7 @@ __global__ void k_trace_a(const uint16_t *__restrict__ argx, TileRec *tiles, uin
 
 // Walk A with the tile's args staged in shared memory (one CTA per tile): the pointer chase
 // then costs a shared-memory latency per hop instead of a DRAM one.
-__global__ void __launch_bounds__(256) k_trace_a_smem(const uint16_t *__restrict__ argx, TileRec *tiles, uint32_t *bm)
+__global__ void __launch_bounds__(1024) k_trace_a_smem(const uint16_t *__restrict__ argx, TileRec *tiles, uint32_t *bm)
 {
     extern __shared__ uint16_t sa[];
     const uint64_t t = blockIdx.x;
@@ -150,10 +150,16 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
     if (P.n == 0) return cudaSuccess;
     const unsigned tb = 128;
     const size_t stage = (size_t)P.tile_len * sizeof(uint16_t);
-    if (stage <= 160 * 1024) {
+// walk A: thread per tile through L1/L2 (0) or one CTA per tile with the tile's args staged in
+// shared memory (threads per CTA).  Measured on c4 (traceback ms): 0: 0.292, 256: 0.316,
+// 64: 0.374, 32: 0.475 -- with 21,800 tiles every walk runs at once and hides its own latency.
+#ifndef UELLM_TRACE_A
+#define UELLM_TRACE_A 0
+#endif
+    if (UELLM_TRACE_A && stage <= 160 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_trace_a_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
         if (e != cudaSuccess) return e;
-        k_trace_a_smem<<<(unsigned)ntiles, 256, stage, st>>>(P.argx, P.tiles, bitmap);
+        k_trace_a_smem<<<(unsigned)ntiles, UELLM_TRACE_A, stage, st>>>(P.argx, P.tiles, bitmap);
     } else {
         k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
     }
