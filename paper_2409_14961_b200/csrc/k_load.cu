@@ -130,8 +130,11 @@ cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *sl
                         LoadMeta *meta, uint32_t *slo_set, cudaStream_t st)
 {
     if (n == 0) return cudaSuccess;
+#ifndef UELLM_LOAD_CTAS_PER_SM
+#define UELLM_LOAD_CTAS_PER_SM 16
+#endif
     uint64_t blocks = ceil_div(n, 256ull * 8);      // ~8 queries per thread
-    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    if (blocks > 148ull * UELLM_LOAD_CTAS_PER_SM) blocks = 148ull * UELLM_LOAD_CTAS_PER_SM;
     if (blocks < 1) blocks = 1;
     k_load<<<(unsigned)blocks, 256, 0, st>>>(in, out, slo, n, meta, slo_set);
     return cudaGetLastError();
