@@ -471,6 +471,7 @@ def main():
         torch.cuda.synchronize(dev)
         hms = h0.elapsed_time(h1) / K
         dm = U.DeviceMap.from_buffer_copy(hout.cpu().numpy().tobytes()).as_dict()
+        bg = U.bgs_plan(t, hws, hb).as_dict()           # the paper's baseline deployer, for context
         import math
         relax = sum(math.comb(20, k) * k * (k - 1) for k in range(1, 21))
         next_rows["f3_helr"] = {
@@ -479,7 +480,8 @@ def main():
             "roofline": {"bound": "latency", "note": "20 dependent popcount levels; the DP table "
                          "(168 MB) streams once per level", "dram_table_bytes": (1 << 20) * 20 * 9},
             "device_map": {"devices": dm["devices"], "layer_count": dm["layer_count"],
-                           "latency_s": dm["latency_s"], "objective": dm["objective"]}}
+                           "latency_s": dm["latency_s"], "objective": dm["objective"]},
+            "bgs_baseline": {"devices": bg["devices"], "latency_s": bg["latency_s"], "objective": bg["objective"]}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -413,6 +413,15 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
 uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *cfg, uint32_t *words,
                                    void *stream);
 
+/* BGS, the paper's baseline deployer ("Greedy Scheduling Algorithm"):
+ * devices in descending order of Memory(d) (ties: smaller id first) each take max_layers(d)
+ * (as in uellm_helr_plan) until the layers are exhausted; that prefix is the chain.  latency_s and
+ * objective use uellm_helr_plan's chain formula, so the two are directly comparable (HELR's
+ * objective is never larger: BGS's chain is one of the chains it searches).  Same arguments and
+ * workspace as uellm_helr_plan; feasible = 0 if all devices together cannot hold the model. */
+uellm_status uellm_bgs_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out,
+                            void *stream);
+
 /* Attach (n <= UELLM_STAGE_COUNT) caller-owned cudaEvent_t handles (void*, created with timing
  * enabled; NULL entries are skipped) to the profile; subsequent schedule/stats calls record
  * event k at stage boundary k on their stream.  n = 0 detaches.  [host] */

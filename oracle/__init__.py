@@ -129,6 +129,7 @@ def lib():
         u64p_ = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
         f64p_ = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
         _lib.orc_helr.argtypes = [C.POINTER(OrcHelrCfg), u64p_, f64p_, f64p_, C.POINTER(OrcDeviceMap)]
+        _lib.orc_bgs.argtypes = [C.POINTER(OrcHelrCfg), u64p_, f64p_, f64p_, C.POINTER(OrcDeviceMap)]
         for f in ("orc_sizeof_config", "orc_sizeof_batch_stat", "orc_sizeof_totals",
                   "orc_sizeof_sim_totals", "orc_sizeof_predictor", "orc_sizeof_device_map"):
             getattr(_lib, f).restype = C.c_uint64
@@ -296,4 +297,18 @@ def helr(topo):
     st = lib().orc_helr(C.byref(c), mem, perf, lat, C.byref(out))
     if st:
         raise OracleError(st, "helr")
+    return out.as_dict()
+
+
+def bgs(topo):
+    """O13 (NEXT f3): the BGS baseline deployer's device map of a workloads.Topology -> dict."""
+    c = OrcHelrCfg(len(topo.memory_bytes), topo.num_layers, topo.model_bytes, topo.kv_reserve_bytes,
+                   topo.p, topo.a1, topo.a2)
+    mem = np.ascontiguousarray(topo.memory_bytes, np.uint64)
+    perf = np.ascontiguousarray(topo.performance, np.float64)
+    lat = np.ascontiguousarray(topo.link_latency_s, np.float64).reshape(-1)
+    out = OrcDeviceMap()
+    st = lib().orc_bgs(C.byref(c), mem, perf, lat, C.byref(out))
+    if st:
+        raise OracleError(st, "bgs")
     return out.as_dict()

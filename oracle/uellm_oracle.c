@@ -29,6 +29,7 @@
  *   orc_profile_stream  O11  predict + observe, one monitor epoch per window      R20
  *   orc_helr            O12  HELR deployer: subsets x bitmask DP over device      P:301-384,
  *                            visit orders (HE: a1 = 0, LR: a1:a2 = 10:1) (f3)
+ *   orc_bgs             O13  BGS baseline deployer: greedy by memory (f3)
  *
  * Parity pins (tests/test_oracle_*.py, -m "not gpu"): brute-force enumeration of all
  * 2^(n-1) segmentations (n <= 12), closed forms (identical queries), special cases
@@ -823,6 +824,49 @@ int orc_helr(const orc_helr_cfg *c, const uint64_t *memory, const double *perf, 
         out->objective = bobj; out->latency_s = blat;
     }
     free(dp); free(arg); free(capsum);
+    return ORC_OK;
+}
+
+/* O13  BGS, the paper's baseline deployer ("Greedy Scheduling Algorithm (BGS)"), as SPEC
+ * S:385-393 reads it: devices in descending order of memory (ties: smaller id first), each takes
+ * max_layers(d) until the layers are exhausted; that prefix is the chain.  Its latency and
+ * objective are evaluated with O12's chain formula (same operation order) for comparison. */
+int orc_bgs(const orc_helr_cfg *c, const uint64_t *memory, const double *perf, const double *lat,
+            orc_device_map *out)
+{
+    if (!c || !memory || !perf || !lat || !out) return ORC_ERR_ARG;
+    const uint32_t D = c->num_devices, L = c->num_layers;
+    if (D < 1 || D > 20 || L < 1 || c->model_bytes == 0) return ORC_ERR_CONFIG;
+    if (!(c->p >= 0.0) || !(c->a1 >= 0.0) || !(c->a2 >= 0.0)) return ORC_ERR_CONFIG;
+    for (uint32_t d = 0; d < D; ++d) if (!(perf[d] > 0.0)) return ORC_ERR_CONFIG;
+    memset(out, 0, sizeof *out);
+    uint32_t ord[32];
+    for (uint32_t d = 0; d < D; ++d) ord[d] = d;
+    for (uint32_t a = 1; a < D; ++a) {                  /* insertion sort: memory desc, id asc */
+        uint32_t x = ord[a], b = a;
+        while (b > 0 && memory[ord[b - 1]] < memory[x]) { ord[b] = ord[b - 1]; --b; }
+        ord[b] = x;
+    }
+    const double m = (double)c->model_bytes / (double)L;
+    uint64_t used = 0;
+    uint32_t k = 0, mask = 0;
+    double l = 0.0;
+    while (used < L && k < D) {
+        uint32_t d = ord[k];
+        uint32_t cap = helr_max_layers(c, memory[d]);
+        uint64_t rem = L - used;
+        uint32_t x = rem < cap ? (uint32_t)rem : cap;
+        double cst = helr_cost(c, m, perf[d], x);
+        l = k == 0 ? cst : (l + lat[ord[k - 1] * D + d]) + cst;
+        out->device[k] = d; out->layer_begin[k] = (uint32_t)used; out->layer_count[k] = x;
+        used += cap;
+        mask |= 1u << d;
+        ++k;
+    }
+    if (used < L) { memset(out, 0, sizeof *out); return ORC_OK; }   /* infeasible */
+    out->count = k; out->feasible = 1; out->mask = mask;
+    out->latency_s = l;
+    out->objective = c->a1 * l + c->a2 * ((double)k / (double)D);
     return ORC_OK;
 }
 

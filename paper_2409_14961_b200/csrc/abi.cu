@@ -88,7 +88,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
 }
 
 struct HelrLayout {
-    uint64_t cap, perf, lat, binom, part_obj, part_lat, part_sj, out, capsum, dp, arg, total;
+    uint64_t cap, mem, perf, lat, binom, part_obj, part_lat, part_sj, out, capsum, dp, arg, total;
 };
 
 HelrLayout helr_layout(uint32_t D)
@@ -98,6 +98,7 @@ HelrLayout helr_layout(uint32_t D)
     auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
     const uint64_t NS = 1ull << D;
     H.cap = take(4 * kHelrMaxDevices);
+    H.mem = take(8 * kHelrMaxDevices);
     H.perf = take(8 * kHelrMaxDevices);
     H.lat = take(8 * kHelrMaxDevices * kHelrMaxDevices);
     H.binom = take(8 * (kHelrMaxDevices + 1) * (kHelrMaxDevices + 1));
@@ -660,7 +661,8 @@ size_t uellm_helr_workspace_bytes(uint32_t num_devices)
     return (size_t)helr_layout(num_devices).total;
 }
 
-uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream)
+static uellm_status deploy_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream,
+                                bool bgs)
 {
     if (!t || !out) return UELLM_ERR_ARG;
     const uint32_t D = t->num_devices;
@@ -692,6 +694,7 @@ uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes,
                 b > a ? 0ull : (b == 0 || b == a) ? 1ull
                       : binom[(a - 1) * (kHelrMaxDevices + 1) + b - 1] + binom[(a - 1) * (kHelrMaxDevices + 1) + b];
     CU(cudaMemcpyAsync(at<uint32_t>(w, Lh.cap), cap, 4 * D, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(at<unsigned long long>(w, Lh.mem), t->memory_bytes, 8 * D, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(at<double>(w, Lh.perf), t->performance, 8 * D, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(at<double>(w, Lh.lat), t->link_latency_s, 8 * D * D, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(at<unsigned long long>(w, Lh.binom), binom, sizeof binom, cudaMemcpyHostToDevice, st));
@@ -700,13 +703,14 @@ uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes,
     std::memset(&H, 0, sizeof H);
     H.D = D; H.L = t->num_layers; H.p = t->p; H.a1 = t->a1; H.a2 = t->a2;
     H.m = (double)t->model_bytes / (double)t->num_layers;
-    H.cap = at<uint32_t>(w, Lh.cap); H.perf = at<double>(w, Lh.perf); H.lat = at<double>(w, Lh.lat);
+    H.cap = at<uint32_t>(w, Lh.cap); H.mem = at<unsigned long long>(w, Lh.mem); H.perf = at<double>(w, Lh.perf); H.lat = at<double>(w, Lh.lat);
     H.binom = at<unsigned long long>(w, Lh.binom); H.binom_host = binom;
     H.capsum = at<unsigned long long>(w, Lh.capsum); H.dp = at<double>(w, Lh.dp); H.arg = at<uint8_t>(w, Lh.arg);
     H.part_obj = at<double>(w, Lh.part_obj); H.part_lat = at<double>(w, Lh.part_lat);
     H.part_sj = at<unsigned long long>(w, Lh.part_sj);
     H.out = dev_out ? out : at<uellm_device_map>(w, Lh.out);
-    CU(run_helr(H, st, nullptr));
+    if (bgs) CU(run_bgs(H, st));
+    else CU(run_helr(H, st, nullptr));
     if (!dev_out) {
         CU(cudaMemcpyAsync(out, H.out, sizeof(uellm_device_map), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -714,6 +718,16 @@ uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes,
     // (pageable host->device copies return once the source has been staged, so the stack tables
     // above may go out of scope without a synchronisation)
     return UELLM_OK;
+}
+
+uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream)
+{
+    return deploy_plan(t, ws, ws_bytes, out, stream, false);
+}
+
+uellm_status uellm_bgs_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream)
+{
+    return deploy_plan(t, ws, ws_bytes, out, stream, true);
 }
 
 uellm_status uellm_set_stage_events(uellm_profile *p, void *const *events, uint32_t n)

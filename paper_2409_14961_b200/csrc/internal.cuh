@@ -285,6 +285,7 @@ struct HelrParams {
     unsigned long long L;
     double p, a1, a2, m;                        // m = M / L
     const uint32_t *cap;                        // [D] max_layers
+    const unsigned long long *mem;              // [D] Memory(d) (BGS order)
     const double *perf;                         // [D]
     const double *lat;                          // [D*D]
     const unsigned long long *binom;            // [(kHelrMaxDevices+1)^2] C(n, k), device copy
@@ -297,5 +298,6 @@ struct HelrParams {
     uellm_device_map *out;
 };
 cudaError_t run_helr(const HelrParams &H, cudaStream_t st, int *launches);
+cudaError_t run_bgs(const HelrParams &H, cudaStream_t st);
 
 }  // namespace uellm

@@ -185,6 +185,53 @@ __global__ void __launch_bounds__(256) k_helr_final(HelrParams H, uint32_t npart
     *H.out = M;
 }
 
+// BGS, the paper's baseline deployer: devices by descending memory (ties:
+// smaller id), each takes max_layers until the layers are exhausted.  One thread: |D| <= 20.
+__global__ void k_bgs(HelrParams H)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t D = H.D;
+    uint32_t ord[kHelrMaxDevices];
+    for (uint32_t d = 0; d < D; ++d) ord[d] = d;
+    for (uint32_t a = 1; a < D; ++a) {
+        const uint32_t x = ord[a];
+        uint32_t b = a;
+        while (b > 0 && H.mem[ord[b - 1]] < H.mem[x]) { ord[b] = ord[b - 1]; --b; }
+        ord[b] = x;
+    }
+    uellm_device_map M;
+    for (int t = 0; t < 32; ++t) { M.device[t] = 0; M.layer_begin[t] = 0; M.layer_count[t] = 0; }
+    M.count = 0; M.feasible = 0; M.mask = 0; M.pad = 0; M.objective = 0.0; M.latency_s = 0.0;
+    unsigned long long used = 0;
+    uint32_t k = 0, mask = 0;
+    double l = 0.0;
+    while (used < H.L && k < D) {
+        const uint32_t d = ord[k];
+        const uint32_t cap = H.cap[d];
+        const unsigned long long rem = H.L - used;
+        const uint32_t x = rem < cap ? (uint32_t)rem : cap;
+        const double c = cost_of(H, d, x);
+        l = k == 0 ? c : __dadd_rn(__dadd_rn(l, H.lat[ord[k - 1] * D + d]), c);
+        M.device[k] = d; M.layer_begin[k] = (uint32_t)used; M.layer_count[k] = x;
+        used += cap;
+        mask |= 1u << d;
+        ++k;
+    }
+    if (used >= H.L) {
+        M.count = k; M.feasible = 1; M.mask = mask; M.latency_s = l;
+        M.objective = __dadd_rn(__dmul_rn(H.a1, l), __dmul_rn(H.a2, __ddiv_rn((double)k, (double)D)));
+    } else {
+        for (int t = 0; t < 32; ++t) { M.device[t] = 0; M.layer_begin[t] = 0; M.layer_count[t] = 0; }
+    }
+    *H.out = M;
+}
+
+cudaError_t run_bgs(const HelrParams &H, cudaStream_t st)
+{
+    k_bgs<<<1, 32, 0, st>>>(H);
+    return cudaGetLastError();
+}
+
 cudaError_t run_helr(const HelrParams &H, cudaStream_t st, int *launches)
 {
     const uint64_t NS = 1ull << H.D;

@@ -146,6 +146,8 @@ _lib.uellm_helr_workspace_bytes.restype = C.c_size_t
 _lib.uellm_helr_workspace_bytes.argtypes = [C.c_uint32]
 _lib.uellm_helr_plan.restype = C.c_int32
 _lib.uellm_helr_plan.argtypes = [C.POINTER(Topology), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+_lib.uellm_bgs_plan.restype = C.c_int32
+_lib.uellm_bgs_plan.argtypes = [C.POINTER(Topology), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
 _lib.uellm_boundary_bitmap.restype = C.c_int32
 _lib.uellm_boundary_bitmap.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p]
 _lib.uellm_pipeline_workspace_bytes.restype = C.c_size_t
@@ -286,6 +288,25 @@ def boundary_bitmap(p: Profile, cfg: Config, words, stream=None):
 
 def helr_workspace_bytes(num_devices: int) -> int:
     return _lib.uellm_helr_workspace_bytes(num_devices)
+
+
+def _topology(topo):
+    mem = np.ascontiguousarray(topo.memory_bytes, np.uint64)
+    perf = np.ascontiguousarray(topo.performance, np.float64)
+    lat = np.ascontiguousarray(topo.link_latency_s, np.float64)
+    t = Topology(len(mem), topo.num_layers, topo.model_bytes, topo.kv_reserve_bytes, topo.p, topo.a1, topo.a2,
+                 mem.ctypes.data, perf.ctypes.data, lat.ctypes.data)
+    return t, (mem, perf, lat)
+
+
+def bgs_plan(topo, ws, ws_bytes: int, out=None, stream=None) -> DeviceMap | None:
+    """The BGS baseline deployer (same arguments as helr_plan)."""
+    t, keep = _topology(topo)
+    host = DeviceMap() if out is None else None
+    _check(_lib.uellm_bgs_plan(C.byref(t), _ptr(ws), ws_bytes, C.addressof(host) if host is not None else _ptr(out),
+                               _stream_handle(stream)), "uellm_bgs_plan")
+    del keep
+    return host
 
 
 def helr_plan(topo, ws, ws_bytes: int, out=None, stream=None) -> DeviceMap | None:

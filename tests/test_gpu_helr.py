@@ -58,3 +58,24 @@ def test_helr_infeasible_and_config_errors():
         with pytest.raises(U.UellmError) as e:
             U.helr_plan(bad, ws, ws.numel())
         assert e.value.status == U.ERR_CONFIG
+
+
+def gpu_bgs(t):
+    from paper_2409_14961_b200 import uellm as U
+    D = len(t.memory_bytes)
+    wsb = U.helr_workspace_bytes(D)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda:0")
+    return U.bgs_plan(t, ws, wsb).as_dict()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_bgs_small_random(seed):
+    t = W.random_topology(seed, 1 + seed % 8)
+    assert gpu_bgs(t) == oracle.bgs(t)
+
+
+def test_bgs_b200_cluster_vs_helr():
+    t = W.b200_cluster(nodes=2, per_node=8, seed=5)
+    b = gpu_bgs(t)
+    assert b == oracle.bgs(t)
+    assert gpu_helr(t)["objective"] <= b["objective"]

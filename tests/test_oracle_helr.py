@@ -129,3 +129,34 @@ def test_he_minimal_subset_and_monotone(seed):
 def test_cluster_topology_runs():
     r = oracle.helr(W.b200_cluster(nodes=1, per_node=8))
     assert r["feasible"] and sum(r["layer_count"]) == 80
+
+
+# ---------------------------------------------------------------------------- BGS (O13)
+def test_spec_s391_s393_bgs():
+    # memories {20, 10} layer-units for 25 layers -> [(d0, 0..19), (d1, 20..24)]
+    t = W.Topology(np.array([20, 10], np.uint64), np.array([1.0, 1.0]), np.array([[0, 1.0], [1.0, 0]]),
+                   num_layers=25, model_bytes=25)
+    r = oracle.bgs(t)
+    assert r["devices"] == [0, 1] and r["layer_begin"] == [0, 20] and r["layer_count"] == [20, 5]
+    # all layers fit on the largest device -> singleton
+    r = oracle.bgs(t.replace(memory_bytes=np.array([10, 30], np.uint64)))
+    assert r["devices"] == [1] and r["layer_count"] == [25]
+    # equal memories -> tie broken by device id
+    r = oracle.bgs(t.replace(memory_bytes=np.array([15, 15], np.uint64)))
+    assert r["devices"] == [0, 1] and r["layer_count"] == [15, 10]
+    # infeasible
+    assert not oracle.bgs(t.replace(memory_bytes=np.array([5, 5], np.uint64)))["feasible"]
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_bgs_never_beats_helr(seed):
+    # BGS's chain is one of the chains HELR searches (same greedy fill, same cost arithmetic)
+    t = W.random_topology(seed, 1 + seed % 7)
+    b, h = oracle.bgs(t), oracle.helr(t)
+    assert b["feasible"] == h["feasible"]
+    if b["feasible"]:
+        assert h["objective"] <= b["objective"]
+        assert chain_latency(t, b["devices"]) == b["latency_s"]
+        assert sum(b["layer_count"]) == t.num_layers
+        mem = [int(t.memory_bytes[d]) for d in b["devices"]]
+        assert mem == sorted(mem, reverse=True)
