@@ -450,6 +450,34 @@ def main():
             "launches": 4 if best == "level" else (n + (cfg.window or n) - 1) // (cfg.window or n),
             "final_state": {"corrections": fin.corrections, "inflation_factor": fin.inflation_factor}}
 
+    # NEXT f1: the paper's own Alg. 1 (SLO-ODBS, parallel greedy) on the same resident stream
+    if not args.no_sim and args.mode == "seg_dp":
+        import workloads as W
+        c1 = cfg.replace(mode=W.MODE_SLO_ODBS, w1=1.0, w2=0.02, threshold=900.0)
+        g1 = GpuScheduler(n, c1, device=dev, per_batch=False)
+
+        def f1_step():
+            g1.load(d_in, d_out, d_slo, stream)
+            g1.schedule(stream)
+            g1.stats(stream)
+        for _ in range(max(Wm, 1)):
+            f1_step()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(K):
+            f1_step()
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        f1_ms = a0.elapsed_time(a1) / K
+        r1 = g1.results()
+        next_rows["f1_slo_odbs"] = {
+            "ms": f1_ms, "queries_per_s": n / (f1_ms / 1e3),
+            "algorithm": "Alg. 1 literal (w1=1, w2=0.02, threshold=900), load + schedule + stats",
+            "batches": r1["m"], "dp_objective_of_its_schedule": r1["totals"]["dp_cost"]}
+        del g1
+        torch.cuda.empty_cache()
+
     # NEXT f3: HELR deployer on a 20-device B200 topology (3 nodes of 8, truncated to the 20-device
     # limit; LLaMA-2-70B fp16, 80 layers): 2^20 x 20 DP states, 20 popcount levels
     if not args.no_sim:
