@@ -466,22 +466,11 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         uint32_t sprev = __shfl_up_sync(0xffffffffu, slo_l, 1);
         if (lane == 0) sprev = prev_slo;
         uint32_t rsv = (vl && slo_l != sprev) ? x : 0u;
-        if (__ballot_sync(0xffffffffu, rsv != 0u)) {
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t a = __shfl_up_sync(0xffffffffu, pmo, d), b = __shfl_up_sync(0xffffffffu, pmi, d);
-                const uint32_t c = __shfl_up_sync(0xffffffffu, rsv, d);
-                if ((int)lane >= d) { pmo = max(pmo, a); pmi = max(pmi, b); rsv = max(rsv, c); }
-            }
-        } else {
-            // no run starts in the block: every element continues the previous SLO run, whose keys
-            // ascend in predicted length, so the prefix maximum of out is the lane's own out
-            // (idle lanes past B are never read); only the input maxima need the scan
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t b = __shfl_up_sync(0xffffffffu, pmi, d);
-                if ((int)lane >= d) pmi = max(pmi, b);
-            }
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, pmo, d), b = __shfl_up_sync(0xffffffffu, pmi, d);
+            const uint32_t c = __shfl_up_sync(0xffffffffu, rsv, d);
+            if ((int)lane >= d) { pmo = max(pmo, a); pmi = max(pmi, b); rsv = max(rsv, c); }
         }
         const uint32_t rs_l = max(run_start, rsv);
         const uint32_t rs_last = __shfl_sync(0xffffffffu, rs_l, B - 1);
