@@ -60,28 +60,28 @@ __device__ __forceinline__ BatchCore batch_core(const StatsParams &S, uint64_t t
     return c;
 }
 
-__global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
+template <uint32_t G>
+__device__ __forceinline__ void stats_est_body(const StatsParams &S, uint64_t m)
 {
-    // kStatsGroup lanes per batch: the group streams the batch's contiguous members with
-    // consecutive lanes on consecutive positions (one 32-byte sector per load instruction and
-    // group), then reduces across the group with shuffles
-    const uint64_t m = *S.num_batches;
-    const uint32_t lane = threadIdx.x & 31, sub = lane % kStatsGroup;
-    const uint64_t ng = (uint64_t)gridDim.x * (blockDim.x / kStatsGroup);
-    for (uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / kStatsGroup; t0 < ceil_div(m, 32 / kStatsGroup) * (32 / kStatsGroup);
+    // G lanes per batch: the group streams the batch's contiguous members with consecutive lanes
+    // on consecutive positions (one 32-byte sector per load instruction and group), then reduces
+    // across the group with shuffles
+    const uint32_t lane = threadIdx.x & 31, sub = lane % G;
+    const uint64_t ng = (uint64_t)gridDim.x * (blockDim.x / G);
+    for (uint64_t t0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; t0 < ceil_div(m, 32 / G) * (32 / G);
          t0 += ng) {
         const bool act = t0 < m;
         const uint64_t t = act ? t0 : m - 1;
         const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
         uint32_t s = 0, O = 0;
         unsigned long long si64 = 0, so64 = 0;
-        for (uint32_t k = a + sub; k < z; k += kStatsGroup) {
+        for (uint32_t k = a + sub; k < z; k += G) {
             const uint32_t vi = __ldg(S.rin + k), vo = __ldg(S.rout + k);
             s = max(s, vi); O = max(O, vo);
             si64 += vi; so64 += vo;
         }
 #pragma unroll
-        for (int d = kStatsGroup / 2; d; d >>= 1) {
+        for (int d = G / 2; d; d >>= 1) {
             s = max(s, __shfl_xor_sync(0xffffffffu, s, d));
             O = max(O, __shfl_xor_sync(0xffffffffu, O, d));
             si64 += __shfl_xor_sync(0xffffffffu, si64, d);
@@ -95,6 +95,18 @@ __global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
             S.pout[t] = b * O - so64;
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
+{
+    // lanes per batch from the mean batch size (uniform over the grid): 8 for SEG-DP-sized batches
+    // (c4: 38 queries), 2 or 1 for the many small batches of Alg. 1 / sort-only schedules
+    const uint64_t m = *S.num_batches;
+    if (m == 0) return;
+    const uint64_t mean = S.n / m;
+    if (mean >= 24) stats_est_body<kStatsGroup>(S, m);
+    else if (mean >= 6) stats_est_body<2>(S, m);
+    else stats_est_body<1>(S, m);
 }
 
 // #{k in [a, z) : rslo[k] < x} -- members ascend in slo_us when S.sorted (a contiguous range of

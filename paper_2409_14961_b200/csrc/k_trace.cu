@@ -188,10 +188,16 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
         uint64_t bsize = 0, MI = 0;
         double L_CM = 0.0, O_CM = 0.0, CM = 0.0;
         uint64_t p = x, next = w1;
+        // the two double divisions are cached (exactly): slo_s only changes with the SLO value
+        // (sorted runs), the line-20 cap only with CM
+        uint32_t last_su = 0;
+        double slo = 0.0;
+        uint64_t cap = 0;
+        bool cap_valid = false;
         for (; p < w1; ++p) {
             const uint32_t su = A.rslo[p];
             if (A.split && bsize > 0 && su != A.rslo[p - 1]) { next = p; break; }
-            const double slo = __ddiv_rn((double)su, 1e6);
+            if (su != last_su || p == x) { slo = __ddiv_rn((double)su, 1e6); last_su = su; }
             const double len = (double)A.rout[p];
             const uint32_t inx = A.rin[p];
             const double nb1 = (double)(bsize + 1);
@@ -210,11 +216,14 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
             bsize += 1;
             if (slo > L_CM) L_CM = slo;
             if (len > O_CM) O_CM = len;
-            if (cmq > CM) CM = cmq;
+            if (cmq > CM) { CM = cmq; cap_valid = false; }
             if (inx > MI) MI = inx;
-            const double den = CM > A.eps ? CM : A.eps;
-            const double capd = floor(__ddiv_rn(A.threshold, den));
-            const uint64_t cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
+            if (!cap_valid) {
+                const double den = CM > A.eps ? CM : A.eps;
+                const double capd = floor(__ddiv_rn(A.threshold, den));
+                cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
+                cap_valid = true;
+            }
             if (bsize >= cap) { next = p + 1; break; }       // line 20: flush after q
         }
         nd[x] = (uint16_t)(next - x);                          // in [1, W]
