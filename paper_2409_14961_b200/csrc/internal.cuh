@@ -22,7 +22,10 @@ constexpr uint32_t kMaxBatchLimit = 4096;      // W limit of this build (UELLM_E
 constexpr uint32_t kSortTile = UELLM_SORT_TILE;         // keys per radix-sort CTA (256 threads x 8)
 constexpr uint32_t kSortThreads = UELLM_SORT_THREADS;
 constexpr uint32_t kSortItems = kSortTile / kSortThreads;
-constexpr uint32_t kDpWarpsPerCta = 8;
+#ifndef UELLM_DP_WARPS
+#define UELLM_DP_WARPS 8
+#endif
+constexpr uint32_t kDpWarpsPerCta = UELLM_DP_WARPS;
 constexpr uint32_t kScanBlock = 1024;          // elements per CTA in the scan kernels
 constexpr uint64_t kProfileMagic = 0x55454c4c4d763031ull;  // "UELLMv01"
 constexpr uint32_t kSloSetSize = 4096;         // global hash set of distinct slo_us values
