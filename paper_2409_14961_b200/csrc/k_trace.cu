@@ -233,15 +233,14 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
 // Chain marking w0 -> next(w0) -> ... without a serial walk.  Greedy chains started at
 // different positions phase-lock on the dynamic cap and rarely re-merge, so the walk is split
 // by binary lifting instead, per sub-tile of T positions (T a power of two >= W):
-//   k_a1_lift<false>  lift tables L[k][x] = next^(2^k)(x) inside the sub-tile (EXIT once it
+//   k_a1_lift         lift tables L[k][x] = next^(2^k)(x) inside the sub-tile (EXIT once it
 //                     leaves), then for each possible entry x < W the exit offset into the next
 //                     sub-tile;
 //   k_a1_entries      per window, sub-tile entries in order (one table lookup per sub-tile);
-//   k_a1_lift<true>   rebuild the tables; x is on the chain from entry e iff it has the same
-//                     exit, is no deeper, and lift(e, depth(e) - depth(x)) == x.
+//   k_a1_mark         with the entries known, walk each sub-tile's part of the chain from its
+//                     entry (one thread per sub-tile).
 constexpr uint16_t kExit = 0xffff;
 
-template <bool MARK>
 __global__ void __launch_bounds__(256) k_a1_lift(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t T, uint32_t K,
                                                  uint64_t spw, uint16_t *__restrict__ exit_first,
                                                  const uint32_t *__restrict__ entries, uint32_t *bm)
@@ -276,33 +275,12 @@ __global__ void __launch_bounds__(256) k_a1_lift(Alg1Params A, const uint16_t *_
         ex = E0[y];
     };
     const uint32_t Wf = min(A.W, len);
-    if (!MARK) {
-        for (uint32_t x = threadIdx.x; x < Wf; x += blockDim.x) {
-            uint32_t d, ex;
-            climb(x, d, ex);
-            exit_first[t * A.W + x] = (uint16_t)ex;
-        }
-        return;
+    for (uint32_t x = threadIdx.x; x < Wf; x += blockDim.x) {
+        uint32_t d, ex;
+        climb(x, d, ex);
+        exit_first[t * A.W + x] = (uint16_t)ex;
     }
-    const uint32_t e = (uint32_t)(entries[t] - s);
-    uint32_t De, Ee;
-    climb(e, De, Ee);
-    for (uint32_t x0 = 0; x0 < len; x0 += blockDim.x) {
-        const uint32_t x = x0 + threadIdx.x;
-        bool on = false;
-        if (x < len && x >= e) {
-            uint32_t Dx, Ex;
-            climb(x, Dx, Ex);
-            if (Ex == Ee && Dx <= De) {
-                uint32_t y = e, h = De - Dx;
-                for (uint32_t lv = 0; h; ++lv, h >>= 1)
-                    if (h & 1u) y = sl[lv * T + y];
-                on = (y == x);
-            }
-        }
-        if (on) bm_set(bm, (uint32_t)(s + x));
-    }
-    if (s + len == A.n && threadIdx.x == 0) bm_set(bm, A.n);
+
 }
 
 __global__ void k_a1_entries(Alg1Params A, uint32_t T, uint64_t spw, const uint16_t *__restrict__ exit_first,
@@ -320,6 +298,23 @@ __global__ void k_a1_entries(Alg1Params A, uint32_t T, uint64_t spw, const uint1
         const uint64_t len = min((uint64_t)T, w1 - s);
         e = s + len + exit_first[t * A.W + (e - s)];
     }
+}
+
+// With every sub-tile's entry known (k_a1_entries), marking its part of the chain is a plain walk
+// e -> next(e) -> ... inside the sub-tile: one thread per sub-tile, all walks in flight at once
+// (replaces the table rebuild + per-position climb of k_a1_lift<true>: same marks).
+__global__ void __launch_bounds__(128) k_a1_mark(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t T,
+                                                 uint64_t spw, const uint32_t *__restrict__ entries, uint32_t *bm)
+{
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= spw * A.nwin) return;
+    const uint64_t w = t / spw, kk = t % spw;
+    const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
+    const uint64_t s = w0 + kk * T;
+    if (s >= w1) return;
+    const uint64_t z = min(s + (uint64_t)T, w1);
+    for (uint64_t x = entries[t]; x < z; x += __ldg(nd + x)) bm_set(bm, (uint32_t)x);
+    if (z == A.n) bm_set(bm, A.n);
 }
 
 static uint32_t a1_sub(uint32_t W)
@@ -346,11 +341,10 @@ cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_de
     uint16_t *exit_first = reinterpret_cast<uint16_t *>(entries + nt + 1);
     const size_t smem = ((size_t)K + 1) * T * sizeof(uint16_t);
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_a1_lift<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_a1_lift<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    k_a1_lift<false><<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
+    if ((e = cudaFuncSetAttribute(k_a1_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    k_a1_lift<<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
     k_a1_entries<<<(unsigned)ceil_div(A.nwin, 64), 64, 0, st>>>(A, T, spw, exit_first, entries);
-    k_a1_lift<true><<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
+    k_a1_mark<<<(unsigned)ceil_div(nt, 128), 128, 0, st>>>(A, next_delta, T, spw, entries, bitmap);
     return cudaGetLastError();
 }
 
