@@ -283,38 +283,124 @@ __global__ void __launch_bounds__(256) k_a1_lift(Alg1Params A, const uint16_t *_
 
 }
 
-__global__ void k_a1_entries(Alg1Params A, uint32_t T, uint64_t spw, const uint16_t *__restrict__ exit_first,
-                             uint32_t *entries)
+// One warp per window: the exit rows of the next CH sub-tiles (contiguous in exit_first) are
+// staged in shared memory by the whole warp, then lane 0 follows the chain through them with
+// shared-memory lookups only -- one global-memory latency per CH sub-tiles instead of per sub-tile.
+constexpr uint32_t kA1EntWarps = 4, kA1EntElems = 4096;          // u16 staged per warp
+__global__ void __launch_bounds__(kA1EntWarps * 32) k_a1_entries(Alg1Params A, uint32_t T, uint64_t spw,
+                                                                 const uint16_t *__restrict__ exit_first,
+                                                                 uint32_t *entries)
 {
-    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ __align__(16) uint16_t buf[kA1EntWarps][kA1EntElems];
+    const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const uint64_t w = (uint64_t)blockIdx.x * kA1EntWarps + wi;
     if (w >= A.nwin) return;
     const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
+    const uint64_t nsub = ceil_div(w1 - w0, (uint64_t)T);
+    const uint32_t CH = max(1u, kA1EntElems / A.W);
+    uint16_t *b = buf[wi];
     uint64_t e = w0;
-    for (uint64_t k = 0; k < spw; ++k) {
-        const uint64_t s = w0 + k * T;
-        if (s >= w1) break;
-        const uint64_t t = w * spw + k;
-        entries[t] = (uint32_t)e;
-        const uint64_t len = min((uint64_t)T, w1 - s);
-        e = s + len + exit_first[t * A.W + (e - s)];
+    for (uint64_t k0 = 0; k0 < nsub; k0 += CH) {
+        const uint32_t c = (uint32_t)min((uint64_t)CH, nsub - k0);
+        const uint16_t *src = exit_first + (w * spw + k0) * A.W;
+        // only a window's last sub-tile can be shorter than W (its exit row holds len entries)
+        const uint64_t last_len = min((uint64_t)T, w1 - (w0 + (k0 + c - 1) * T));
+        const uint32_t m = (uint32_t)min((uint64_t)(c - 1) * A.W + min((uint64_t)A.W, last_len),
+                                         (uint64_t)kA1EntElems);   // W > kA1EntElems: first part only
+        if (A.W % 8 == 0) {                                    // rows 16-byte aligned: uint4 loads, all in flight
+            const uint32_t m8 = m >> 3;
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+            uint4 *b4 = reinterpret_cast<uint4 *>(b);
+            uint4 r[kA1EntElems / 8 / 32];
+#pragma unroll
+            for (uint32_t u = 0; u < kA1EntElems / 8 / 32; ++u)
+                if (lane + 32 * u < m8) r[u] = s4[lane + 32 * u];
+#pragma unroll
+            for (uint32_t u = 0; u < kA1EntElems / 8 / 32; ++u)
+                if (lane + 32 * u < m8) b4[lane + 32 * u] = r[u];
+            for (uint32_t i = 8 * m8 + lane; i < m; i += 32) b[i] = src[i];
+        } else {
+            for (uint32_t i = lane; i < m; i += 32) b[i] = src[i];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (uint32_t j = 0; j < c; ++j) {
+                const uint64_t s = w0 + (k0 + j) * T;
+                entries[w * spw + k0 + j] = (uint32_t)e;
+                const uint64_t len = min((uint64_t)T, w1 - s), off = e - s;
+                const uint64_t idx = (uint64_t)j * A.W + off;
+                e = s + len + (idx < m ? b[idx] : src[idx]);
+            }
+        }
+        e = __shfl_sync(0xffffffffu, e, 0);
+        __syncwarp();
     }
 }
 
 // With every sub-tile's entry known (k_a1_entries), marking its part of the chain is a plain walk
-// e -> next(e) -> ... inside the sub-tile: one thread per sub-tile, all walks in flight at once
-// (replaces the table rebuild + per-position climb of k_a1_lift<true>: same marks).
-__global__ void __launch_bounds__(128) k_a1_mark(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t T,
-                                                 uint64_t spw, const uint32_t *__restrict__ entries, uint32_t *bm)
+// e -> next(e) -> ... inside the sub-tile (same marks as climbing the lift tables).  One warp per
+// sub-tile: the warp stages next_delta of the sub-tile in shared memory with 16-byte loads, lane 0
+// walks it there and sets the bits in a shared-memory copy of the sub-tile's bitmap words, which
+// the warp then ORs into the global bitmap (neighbouring sub-tiles may share a boundary word).
+constexpr uint32_t kA1MarkWarps = 8, kA1MarkElems = 2048 + 32, kA1MarkWords = kA1MarkElems / 32;
+constexpr uint32_t kA1MarkVec = (kA1MarkElems / 8 + 31) / 32;      // uint4 loads per lane
+__global__ void __launch_bounds__(kA1MarkWarps * 32) k_a1_mark(Alg1Params A, const uint16_t *__restrict__ nd,
+                                                               uint32_t T, uint64_t spw,
+                                                               const uint32_t *__restrict__ entries, uint32_t *bm)
 {
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ __align__(16) uint16_t snd[kA1MarkWarps][kA1MarkElems];
+    __shared__ uint32_t sbits[kA1MarkWarps][kA1MarkWords];
+    const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const uint64_t t = (uint64_t)blockIdx.x * kA1MarkWarps + wi;
     if (t >= spw * A.nwin) return;
     const uint64_t w = t / spw, kk = t % spw;
     const uint64_t w0 = w * A.window, w1 = min(w0 + A.window, (uint64_t)A.n);
     const uint64_t s = w0 + kk * T;
     if (s >= w1) return;
     const uint64_t z = min(s + (uint64_t)T, w1);
-    for (uint64_t x = entries[t]; x < z; x += __ldg(nd + x)) bm_set(bm, (uint32_t)x);
-    if (z == A.n) bm_set(bm, A.n);
+    const uint64_t bb = s & ~31ull;                       // staging and bitmap base (word aligned)
+    const uint64_t nwords = (z - 1 - bb) / 32 + 1;
+    if (nwords > kA1MarkWords) {                          // T > 2048 (W > 2048): walk global memory
+        if (lane == 0) {
+            for (uint64_t x = entries[t]; x < z; x += nd[x]) bm_set(bm, (uint32_t)x);
+            if (z == A.n) bm_set(bm, A.n);
+        }
+        return;
+    }
+    const uint32_t L = (uint32_t)(z - bb);                // <= kA1MarkElems
+    uint16_t *b = snd[wi];
+    uint32_t *sw = sbits[wi];
+    {
+        const uint32_t L8 = L >> 3;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(nd + bb);
+        uint4 *b4 = reinterpret_cast<uint4 *>(b);
+        uint4 r[kA1MarkVec];
+#pragma unroll
+        for (uint32_t u = 0; u < kA1MarkVec; ++u)
+            if (lane + 32 * u < L8) r[u] = s4[lane + 32 * u];
+#pragma unroll
+        for (uint32_t u = 0; u < kA1MarkVec; ++u)
+            if (lane + 32 * u < L8) b4[lane + 32 * u] = r[u];
+        for (uint32_t i = 8 * L8 + lane; i < L; i += 32) b[i] = nd[bb + i];
+        for (uint32_t i = lane; i < nwords; i += 32) sw[i] = 0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        // offsets are monotone along the chain, so each bitmap word is visited in one run:
+        // accumulate it in a register and store it once (no shared-memory read-modify-write)
+        uint32_t o = (uint32_t)(entries[t] - bb), cw = o >> 5, acc = 0;
+        while (o < L) {
+            const uint32_t wd = o >> 5;
+            if (wd != cw) { sw[cw] = acc; acc = 0; cw = wd; }
+            acc |= 1u << (o & 31);
+            o += b[o];
+        }
+        if (acc) sw[cw] = acc;
+        if (z == A.n) bm_set(bm, A.n);
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < nwords; i += 32)
+        if (sw[i]) atomicOr(bm + (bb >> 5) + i, sw[i]);
 }
 
 static uint32_t a1_sub(uint32_t W)
@@ -338,13 +424,13 @@ cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_de
     const uint64_t spw = ceil_div(A.window, T), nt = spw * A.nwin;
     // scratch inside the Alg. 1 tile area: entries (u32 per sub-tile), exit_first (u16 x W per sub-tile)
     uint32_t *entries = reinterpret_cast<uint32_t *>(tile_exits);
-    uint16_t *exit_first = reinterpret_cast<uint16_t *>(entries + nt + 1);
+    uint16_t *exit_first = reinterpret_cast<uint16_t *>(entries + ((nt + 1 + 3) & ~3ull));   // 16-byte aligned rows
     const size_t smem = ((size_t)K + 1) * T * sizeof(uint16_t);
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_a1_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     k_a1_lift<<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
-    k_a1_entries<<<(unsigned)ceil_div(A.nwin, 64), 64, 0, st>>>(A, T, spw, exit_first, entries);
-    k_a1_mark<<<(unsigned)ceil_div(nt, 128), 128, 0, st>>>(A, next_delta, T, spw, entries, bitmap);
+    k_a1_entries<<<(unsigned)ceil_div(A.nwin, kA1EntWarps), kA1EntWarps * 32, 0, st>>>(A, T, spw, exit_first, entries);
+    k_a1_mark<<<(unsigned)ceil_div(nt, kA1MarkWarps), kA1MarkWarps * 32, 0, st>>>(A, next_delta, T, spw, entries, bitmap);
     return cudaGetLastError();
 }
 
