@@ -180,20 +180,34 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 //   k_a1_*        mark the chain w0 -> next(w0) -> ... by binary lifting (below).
 // Doubles with explicit round-to-nearest intrinsics (no FMA contraction): every decision is
 // bit-identical to the CPU oracle's sequential scan.
+// Line-20 flush test without the division (exact): with den = max(CM, eps) > 0 and finite,
+// q = RN(threshold / den) and k = bsize + 1 <= W, "bsize >= cap" is "q < k".  The sign of
+// fma(-k, den, threshold) is the sign of threshold - k*den exactly, so q >= k when it is >= 0;
+// when the same test against km (the double below k) is < 0, q <= km < k.  Only a quotient in
+// [km, k) -- where rounding decides -- takes the division.
+__device__ __forceinline__ bool a1_cap_flush(double threshold, double den, uint32_t bsize, uint32_t W)
+{
+    if (bsize >= W) return true;                               // cap <= W
+    const double k = (double)(bsize + 1);
+    if (__fma_rn(-k, den, threshold) >= 0.0) return false;
+    const double km = __longlong_as_double(__double_as_longlong(k) - 1);
+    if (__fma_rn(-km, den, threshold) < 0.0) return true;
+    return !(__ddiv_rn(threshold, den) >= k);
+}
+
 __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__restrict__ nd)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < A.n; x += stride) {
-        const uint64_t w1 = min((x / A.window + 1) * A.window, (uint64_t)A.n);
-        uint64_t bsize = 0, MI = 0;
+    const bool thr_finite = isfinite(A.threshold);
+    for (uint64_t xx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; xx < A.n; xx += stride) {
+        const uint32_t x = (uint32_t)xx;
+        const uint32_t w1 = min((x / A.window + 1) * A.window, A.n);
+        uint32_t bsize = 0, MI = 0;
         double L_CM = 0.0, O_CM = 0.0, CM = 0.0;
-        uint64_t p = x, next = w1;
-        // the two double divisions are cached (exactly): slo_s only changes with the SLO value
-        // (sorted runs), the line-20 cap only with CM
+        uint32_t p = x, next = w1;
+        // the slo division is cached (exactly): slo_s only changes with the SLO value (sorted runs)
         uint32_t last_su = 0;
         double slo = 0.0;
-        uint64_t cap = 0;
-        bool cap_valid = false;
         for (; p < w1; ++p) {
             const uint32_t su = A.rslo[p];
             if (A.split && bsize > 0 && su != A.rslo[p - 1]) { next = p; break; }
@@ -207,24 +221,27 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
             const double Total = __dadd_rn(__dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
             bool admit = (bsize == 0);
             if (!admit && Total <= A.threshold) {
-                const uint64_t s = max((uint64_t)inx, MI);
+                const uint64_t s = max(inx, MI);
                 const uint64_t O = (uint64_t)(len > O_CM ? len : O_CM);
-                admit = (bsize + 1) * (s + O) <= A.cap_tok;
+                admit = (uint64_t)(bsize + 1) * (s + O) <= A.cap_tok;
             }
             if (!admit) { next = p; break; }                  // q seeds the next batch
             const double cmq = __dadd_rn(__dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
             bsize += 1;
             if (slo > L_CM) L_CM = slo;
             if (len > O_CM) O_CM = len;
-            if (cmq > CM) { CM = cmq; cap_valid = false; }
+            if (cmq > CM) CM = cmq;
             if (inx > MI) MI = inx;
-            if (!cap_valid) {
-                const double den = CM > A.eps ? CM : A.eps;
+            const double den = CM > A.eps ? CM : A.eps;
+            bool flush;
+            if (thr_finite && den > 0.0 && isfinite(den)) {
+                flush = a1_cap_flush(A.threshold, den, bsize, A.W);
+            } else {                                           // the literal form
                 const double capd = floor(__ddiv_rn(A.threshold, den));
-                cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
-                cap_valid = true;
+                const uint64_t cap = capd < 1.0 ? 1 : (capd > (double)A.W ? (uint64_t)A.W : (uint64_t)capd);
+                flush = bsize >= cap;
             }
-            if (bsize >= cap) { next = p + 1; break; }       // line 20: flush after q
+            if (flush) { next = p + 1; break; }                // line 20: flush after q
         }
         nd[x] = (uint16_t)(next - x);                          // in [1, W]
     }

@@ -123,6 +123,20 @@ def test_mode_slo_odbs(w1, w2, thr, split):
     assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_SLO_ODBS, w1=w1, w2=w2, threshold=thr, window=3000))
 
 
+@pytest.mark.parametrize("w1,w2,thr,eps", [(0.1, 0.0, 90.0, 1e-9), (0.3, 0.0, 270.0, 1e-9), (1.0, 0.0, 4096.0, 1e-9),
+                                           (0.0, 1e-9, 5.0, 0.7), (1.0, 0.02, float("inf"), 1e-9)])
+def test_mode_slo_odbs_cap_edges(w1, w2, thr, eps):
+    """Line-20 cap = floor(threshold / max(CM, eps)) near integer quotients (w1 = 0.1, 0.3 with
+    threshold = 900 w1: RN(w1 len) makes threshold/den land within an ulp of 900/len whenever len
+    divides 900), exact integer quotients, den = eps, infinite threshold (threshold, eps > 0 by contract):
+    the kernel's division-free flush test must decide exactly like the division."""
+    inp, out, slo, cfg = W.c2(21, n=6000)
+    out = out.copy()
+    out[::7] = np.array([100, 150, 180, 225, 300, 450, 900, 60, 75, 90], np.uint32)[np.arange(len(out[::7])) % 10]
+    assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_SLO_ODBS, w1=w1, w2=w2, threshold=thr, eps=eps,
+                                             window=2500))
+
+
 # ------------------------------------------------------------------ edges and errors
 def test_edges():
     for n in (1, 2, 3, 31, 32, 33):
