@@ -305,17 +305,26 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
     uint64_t start, end;
     const uint64_t tile = t0 + blockIdx.x;
     tile_range(tile, n, window, tpw, start, end);
-#pragma unroll 4
+    // all loads first (independent, in flight together), then probe / pack / count
+    float fr[kSortItems];
+    uint32_t orr[kSortItems];
+#pragma unroll
+    for (uint32_t i = 0; i < kSortItems; ++i) {
+        const uint64_t p = start + (uint64_t)i * kSortThreads + tid;
+        fr[i] = p < end ? __ldg(slo + p) : 0.0f;
+        orr[i] = p < end ? __ldg(out + p) : 0u;
+    }
+#pragma unroll
     for (uint32_t i = 0; i < kSortItems; ++i) {
         const uint64_t p = start + (uint64_t)i * kSortThreads + tid;
         const bool valid = p < end;
         const uint32_t act = __ballot_sync(0xffffffffu, valid);
         if (valid) {
             bool ok;
-            const uint32_t su = slo_to_us(__ldg(slo + p), ok);
+            const uint32_t su = slo_to_us(fr[i], ok);
             uint32_t hh = slo_hash(su, kSloSetBits);
             while (sset[hh] != su) hh = (hh + 1) & (kSloSetSize - 1);
-            const uint32_t key = (srank[hh] << ob) | __ldg(out + p);
+            const uint32_t key = (srank[hh] << ob) | orr[i];
             keys32[p] = key;                       // payload = arrival index p: implicit (NULL vals)
             const uint32_t d = key & 0xffu;
             const uint32_t peers = __match_any_sync(act, d);

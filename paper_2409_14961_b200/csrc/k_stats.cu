@@ -126,6 +126,32 @@ __device__ __forceinline__ uint32_t count_below(const StatsParams &S, uint32_t a
     return c;
 }
 
+// both violation counts of a batch: the two binary searches run in lockstep so their
+// dependent loads overlap
+__device__ __forceinline__ void count_below2(const StatsParams &S, uint32_t a, uint32_t z, unsigned long long x1,
+                                             unsigned long long x2, uint32_t &c1, uint32_t &c2)
+{
+    if (S.sorted) {
+        uint32_t lo1 = a, hi1 = z, lo2 = a, hi2 = z;
+        while (lo1 < hi1 || lo2 < hi2) {
+            const uint32_t m1 = lo1 + (hi1 - lo1) / 2, m2 = lo2 + (hi2 - lo2) / 2;
+            const bool g1 = lo1 < hi1, g2 = lo2 < hi2;
+            const unsigned long long v1 = g1 ? __ldg(S.rslo + m1) : 0, v2 = g2 ? __ldg(S.rslo + m2) : 0;
+            if (g1) { if (v1 < x1) lo1 = m1 + 1; else hi1 = m1; }
+            if (g2) { if (v2 < x2) lo2 = m2 + 1; else hi2 = m2; }
+        }
+        c1 = lo1 - a;
+        c2 = lo2 - a;
+        return;
+    }
+    c1 = c2 = 0;
+    for (uint32_t k = a; k < z; ++k) {
+        const unsigned long long v = __ldg(S.rslo + k);
+        c1 += v < x1;
+        c2 += v < x2;
+    }
+}
+
 // ---- segmented inclusive scan of est by window (head flag = first batch of a window) ----
 __device__ __forceinline__ bool head_flag(const StatsParams &S, uint64_t t)
 {
@@ -231,6 +257,7 @@ __global__ void __launch_bounds__(kScanBlock) k_seg_scan_apply(StatsParams S)
     }
 }
 
+static_assert(sizeof(uellm_batch_stat) % 16 == 0, "record copied as uint4");
 // ---- all fields + totals ----
 __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
 {
@@ -241,29 +268,51 @@ __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
     const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
     unsigned long long a_gen = 0, a_pin = 0, a_pout = 0, a_kv = 0, a_obj = 0, a_v1 = 0, a_v2 = 0, a_oc = 0,
                        a_mk = 0, a_llo = 0, a_lhi = 0, a_nb = 0;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += nt) {
-        const uint32_t a = S.offsets[t], z = S.offsets[t + 1], b = z - a;
-        const unsigned long long so = S.so[t], est = S.est[t], compl_us = S.compl_[t];
-        const uint32_t s = (uint32_t)so, O = (uint32_t)(so >> 32);
-        const unsigned long long pin = S.pin[t], pout = S.pout[t];
-        const uint32_t v1 = count_below(S, a, z, est);
-        const uint32_t v2 = count_below(S, a, z, compl_us);
-        const unsigned long long kv = S.kv_unit * (unsigned long long)b * ((unsigned long long)s + O);
-        const uint32_t oc = (S.kv_cap != 0 && kv > S.kv_cap) ? 1u : 0u;
-        const unsigned long long gen = (unsigned long long)b * O;
-        if (S.per_batch) {
-            uellm_batch_stat r;
-            r.start = a; r.size = b; r.max_in = s; r.max_out = O;
-            r.gen_tokens = gen; r.pad_in = pin; r.pad_out = pout; r.kv_bytes = kv;
-            r.est_us = est; r.completion_us = compl_us;
-            r.viol_alone = v1; r.viol_seq = v2; r.over_cap = oc; r.window = a / S.window;
-            S.per_batch[t] = r;
+    // block-uniform loop: the 80-byte records go through shared memory and leave as coalesced
+    // 16-byte stores (a record per thread would be ten 8-byte stores at an 80-byte lane stride)
+    __shared__ __align__(16) uellm_batch_stat rec[256];
+    const bool vec = ((uintptr_t)S.per_batch & 15) == 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < m; base += nt) {
+        const uint64_t t = base + threadIdx.x;
+        if (t < m) {
+            const uint32_t a = S.offsets[t], z = S.offsets[t + 1], b = z - a;
+            const unsigned long long so = S.so[t], est = S.est[t], compl_us = S.compl_[t];
+            const uint32_t s = (uint32_t)so, O = (uint32_t)(so >> 32);
+            const unsigned long long pin = S.pin[t], pout = S.pout[t];
+            uint32_t v1, v2;
+            count_below2(S, a, z, est, compl_us, v1, v2);
+            const unsigned long long kv = S.kv_unit * (unsigned long long)b * ((unsigned long long)s + O);
+            const uint32_t oc = (S.kv_cap != 0 && kv > S.kv_cap) ? 1u : 0u;
+            const unsigned long long gen = (unsigned long long)b * O;
+            if (S.per_batch) {
+                uellm_batch_stat &r = rec[threadIdx.x];
+                r.start = a; r.size = b; r.max_in = s; r.max_out = O;
+                r.gen_tokens = gen; r.pad_in = pin; r.pad_out = pout; r.kv_bytes = kv;
+                r.est_us = est; r.completion_us = compl_us;
+                r.viol_alone = v1; r.viol_seq = v2; r.over_cap = oc; r.window = a / S.window;
+            }
+            a_gen += gen; a_pin += pin; a_pout += pout; a_kv = max(a_kv, kv);
+            a_obj += est + S.lambda * v1; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += est; a_nb += 1;
+            const unsigned long long lo = (unsigned long long)b * compl_us;
+            const unsigned long long hi = __umul64hi((unsigned long long)b, compl_us);
+            a_llo += lo; a_lhi += hi + (a_llo < lo ? 1ull : 0ull);
         }
-        a_gen += gen; a_pin += pin; a_pout += pout; a_kv = max(a_kv, kv);
-        a_obj += est + S.lambda * v1; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += est; a_nb += 1;
-        const unsigned long long lo = (unsigned long long)b * compl_us;
-        const unsigned long long hi = __umul64hi((unsigned long long)b, compl_us);
-        a_llo += lo; a_lhi += hi + (a_llo < lo ? 1ull : 0ull);
+        if (S.per_batch) {
+            __syncthreads();
+            const uint32_t cnt = (uint32_t)min((uint64_t)blockDim.x, m - base);
+            if (vec) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(rec);
+                uint4 *dst = reinterpret_cast<uint4 *>(S.per_batch + base);
+                for (uint32_t i = threadIdx.x; i < cnt * (uint32_t)(sizeof(uellm_batch_stat) / 16); i += blockDim.x)
+                    dst[i] = src[i];
+            } else {
+                const unsigned long long *src = reinterpret_cast<const unsigned long long *>(rec);
+                unsigned long long *dst = reinterpret_cast<unsigned long long *>(S.per_batch + base);
+                for (uint32_t i = threadIdx.x; i < cnt * (uint32_t)(sizeof(uellm_batch_stat) / 8); i += blockDim.x)
+                    dst[i] = src[i];
+            }
+            __syncthreads();
+        }
     }
     // warp reduction (128-bit carry for the latency sum)
 #pragma unroll
