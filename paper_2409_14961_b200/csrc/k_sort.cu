@@ -117,8 +117,11 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__res
     for (; k < k1; ++k) { const uint32_t v = col[(uint64_t)k * 256]; col[(uint64_t)k * 256] = run; run += v; }
 }
 
+#ifndef UELLM_SORT_DOWN_MINB
+#define UELLM_SORT_DOWN_MINB 5
+#endif
 template <class K, bool DECODE>
-__global__ void __launch_bounds__(kSortThreads) k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
+__global__ void __launch_bounds__(kSortThreads, UELLM_SORT_DOWN_MINB) k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                             K *__restrict__ kout, uint32_t *__restrict__ vout,
                                                             const uint32_t *__restrict__ hist, uint64_t n,
                                                             uint64_t window, uint64_t tpw, int shift, DecodeArgs D,
