@@ -32,6 +32,10 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
     // with match.any and only one lane per distinct value touches the CTA set (atomicCAS only:
     // present -> old == su); stops once the CTA saw more than kCtaMax values (cover).
     const uint32_t lane = threadIdx.x & 31;
+    constexpr int kLaneCache = 8;
+    uint32_t cache[kLaneCache];
+#pragma unroll
+    for (int c = 0; c < kLaneCache; ++c) cache[c] = 0u;       // 0 is never a member (su >= 1)
     auto consume = [&](uint32_t a, uint32_t o, float sf, bool valid, bool cv) {
         bool ok = true;
         const uint32_t su = valid ? slo_to_us(sf, ok) : 0u;
@@ -44,7 +48,19 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
             kor |= key; kand &= key;
         }
         if (cv) return;                                        // warp-uniform
-        const uint32_t k = valid ? su : 0u;
+        // per-lane cache of the last 8 values this lane already put through the CTA set: class-
+        // valued SLOs hit it almost always, and a warp with no new value skips the match + CAS
+        bool known = false;
+#pragma unroll
+        for (int c = 0; c < kLaneCache; ++c) known |= (cache[c] == su);
+        const bool need = valid && su != 0u && !known;
+        if (!__any_sync(0xffffffffu, need)) return;            // warp-uniform
+        if (need) {
+#pragma unroll
+            for (int c = kLaneCache - 1; c > 0; --c) cache[c] = cache[c - 1];
+            cache[0] = su;
+        }
+        const uint32_t k = need ? su : 0u;
         const uint32_t peers = __match_any_sync(0xffffffffu, k);
         if (k == 0u || lane != (uint32_t)(__ffs(peers) - 1)) return;
         uint32_t h = slo_hash(su, kCtaBits);
