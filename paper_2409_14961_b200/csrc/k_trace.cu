@@ -195,41 +195,48 @@ __device__ __forceinline__ bool a1_cap_flush(double threshold, double den, uint3
     return !(__ddiv_rn(threshold, den) >= k);
 }
 
+// SPLIT: split_on_slo_change; UNIT: l1 == l2 == 1 (x * 1.0 == x exactly, so the two
+// multiplications are skipped without changing a bit).  O (the batch's max predicted length) is
+// kept as an integer beside its double copy (outputs are u32, exact in a double).
+template <bool SPLIT, bool UNIT>
 __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__restrict__ nd)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const bool thr_finite = isfinite(A.threshold);
     for (uint64_t xx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; xx < A.n; xx += stride) {
         const uint32_t x = (uint32_t)xx;
-        const uint32_t w1 = min((x / A.window + 1) * A.window, A.n);
-        uint32_t bsize = 0, MI = 0;
-        double L_CM = 0.0, O_CM = 0.0, CM = 0.0;
+        const uint32_t w1 = (uint32_t)min(((uint64_t)(x / A.window) + 1) * A.window, (uint64_t)A.n);
+        uint32_t bsize = 0, MI = 0, Oi = 0;
+        double L_CM = 0.0, O_CM = 0.0, CM = 0.0, nb1 = 1.0;
         uint32_t p = x, next = w1;
         // the slo division is cached (exactly): slo_s only changes with the SLO value (sorted runs)
-        uint32_t last_su = 0;
-        double slo = 0.0;
+        uint32_t last_su = A.rslo[x];
+        double slo = __ddiv_rn((double)last_su, 1e6);
         for (; p < w1; ++p) {
             const uint32_t su = A.rslo[p];
-            if (A.split && bsize > 0 && su != A.rslo[p - 1]) { next = p; break; }
-            if (su != last_su || p == x) { slo = __ddiv_rn((double)su, 1e6); last_su = su; }
-            const double len = (double)A.rout[p];
+            if (SPLIT && bsize > 0 && su != last_su) { next = p; break; }
+            if (su != last_su) { slo = __ddiv_rn((double)su, 1e6); last_su = su; }
+            const uint32_t outp = A.rout[p];
+            const double len = (double)outp;
             const uint32_t inx = A.rin[p];
-            const double nb1 = (double)(bsize + 1);
-            const double T_l = __dmul_rn(__dmul_rn(__dadd_rn(slo, L_CM), nb1), A.l1);
+            double T_l = __dmul_rn(__dadd_rn(slo, L_CM), nb1);
+            if (!UNIT) T_l = __dmul_rn(T_l, A.l1);
             double T_o = A.eq2_additive ? __dadd_rn(len, O_CM) : __dsub_rn(len, O_CM);
-            T_o = __dmul_rn(__dmul_rn(T_o, nb1), A.l2);
+            T_o = __dmul_rn(T_o, nb1);
+            if (!UNIT) T_o = __dmul_rn(T_o, A.l2);
             const double Total = __dadd_rn(__dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
             bool admit = (bsize == 0);
             if (!admit && Total <= A.threshold) {
                 const uint64_t s = max(inx, MI);
-                const uint64_t O = (uint64_t)(len > O_CM ? len : O_CM);
+                const uint64_t O = max(outp, Oi);
                 admit = (uint64_t)(bsize + 1) * (s + O) <= A.cap_tok;
             }
             if (!admit) { next = p; break; }                  // q seeds the next batch
             const double cmq = __dadd_rn(__dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
             bsize += 1;
+            nb1 = __dadd_rn(nb1, 1.0);                         // = bsize + 1, exact
             if (slo > L_CM) L_CM = slo;
-            if (len > O_CM) O_CM = len;
+            if (outp > Oi) { Oi = outp; O_CM = len; }
             if (cmq > CM) CM = cmq;
             if (inx > MI) MI = inx;
             const double den = CM > A.eps ? CM : A.eps;
@@ -434,7 +441,14 @@ cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_de
     if (A.n == 0) return cudaSuccess;
     uint64_t blocks = ceil_div(A.n, 256);
     if (blocks > 148ull * 64) blocks = 148ull * 64;
-    k_alg1_next<<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
+    const bool unit = A.l1 == 1.0 && A.l2 == 1.0;
+    if (A.split) {
+        if (unit) k_alg1_next<true, true><<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
+        else k_alg1_next<true, false><<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
+    } else {
+        if (unit) k_alg1_next<false, true><<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
+        else k_alg1_next<false, false><<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
+    }
     const uint32_t T = a1_sub(A.W);
     uint32_t K = 0;
     while ((1u << K) < T) ++K;

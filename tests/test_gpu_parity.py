@@ -137,6 +137,15 @@ def test_mode_slo_odbs_cap_edges(w1, w2, thr, eps):
                                              window=2500))
 
 
+@pytest.mark.parametrize("l1,l2,additive,split", [(1.0, 1.0, 1, 0), (0.5, 2.0, 0, 1), (1.3, 0.7, 1, 1), (2.0, 1.0, 0, 0)])
+def test_mode_slo_odbs_eq_variants(l1, l2, additive, split):
+    """Alg. 1 with the Eq. 1/2 scale factors l1, l2 != 1 (the kernel skips the multiplications
+    only when both are 1), the additive Eq. 2 reading and the SLO-change split."""
+    inp, out, slo, cfg = W.c2(23, n=7000, split=split)
+    assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_SLO_ODBS, w1=1.0, w2=0.02, threshold=900.0, l1=l1, l2=l2,
+                                             eq2_additive=additive, window=3000))
+
+
 # ------------------------------------------------------------------ edges and errors
 def test_edges():
     for n in (1, 2, 3, 31, 32, 33):
