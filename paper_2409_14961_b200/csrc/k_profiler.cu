@@ -42,8 +42,9 @@ __device__ __forceinline__ unsigned long long base_of(const PredictParams &P, un
 {
     if (P.variant == UELLM_PREDICT_ORACLE) return t;
     if (P.variant == UELLM_PREDICT_CONSTANT) return P.constant_tokens;
-    const unsigned long long w = P.bucket_width;
-    unsigned long long k = ((unsigned long long)t + w - 1) / w;
+    const uint32_t w = P.bucket_width;
+    const uint32_t q = t / w;                                 // ceil(t / w) in 32-bit arithmetic
+    unsigned long long k = q + (q * w != t ? 1u : 0u);
     k = k < 1 ? 1 : k;
     if (P.variant == UELLM_PREDICT_NOISY) {
         const unsigned long long z = mix64(P.seed, index);
@@ -53,7 +54,7 @@ __device__ __forceinline__ unsigned long long base_of(const PredictParams &P, un
             else if (k > 1) k -= 1;
         }
     }
-    return k * w;
+    return k * (unsigned long long)w;
 }
 
 // "multiplied by monitor.inflation_factor and rounded up", saturating (R20)
