@@ -427,9 +427,12 @@ __global__ void __launch_bounds__(kA1MarkWarps * 32) k_a1_mark(Alg1Params A, con
         if (sw[i]) atomicOr(bm + (bb >> 5) + i, sw[i]);
 }
 
+#ifndef UELLM_A1_SUB
+#define UELLM_A1_SUB 1024
+#endif
 static uint32_t a1_sub(uint32_t W)
 {
-    uint32_t T = 2048;
+    uint32_t T = UELLM_A1_SUB;
     while (T < W) T <<= 1;
     return T;
 }
