@@ -366,7 +366,12 @@ __global__ void __launch_bounds__(kA1EntWarps * 32) k_a1_entries(Alg1Params A, u
 // sub-tile: the warp stages next_delta of the sub-tile in shared memory with 16-byte loads, lane 0
 // walks it there and sets the bits in a shared-memory copy of the sub-tile's bitmap words, which
 // the warp then ORs into the global bitmap (neighbouring sub-tiles may share a boundary word).
-constexpr uint32_t kA1MarkWarps = 8, kA1MarkElems = 2048 + 32, kA1MarkWords = kA1MarkElems / 32;
+#ifndef UELLM_A1_SUB
+#define UELLM_A1_SUB 1024
+#endif
+// staged deltas per warp: one minimum-size sub-tile plus the word-alignment slack (larger T,
+// i.e. W > UELLM_A1_SUB, walks global memory)
+constexpr uint32_t kA1MarkWarps = 8, kA1MarkElems = UELLM_A1_SUB + 32, kA1MarkWords = kA1MarkElems / 32;
 constexpr uint32_t kA1MarkVec = (kA1MarkElems / 8 + 31) / 32;      // uint4 loads per lane
 __global__ void __launch_bounds__(kA1MarkWarps * 32) k_a1_mark(Alg1Params A, const uint16_t *__restrict__ nd,
                                                                uint32_t T, uint64_t spw,
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(kA1MarkWarps * 32) k_a1_mark(Alg1Params A, con
     const uint64_t z = min(s + (uint64_t)T, w1);
     const uint64_t bb = s & ~31ull;                       // staging and bitmap base (word aligned)
     const uint64_t nwords = (z - 1 - bb) / 32 + 1;
-    if (nwords > kA1MarkWords) {                          // T > 2048 (W > 2048): walk global memory
+    if (nwords > kA1MarkWords) {                          // T > UELLM_A1_SUB (large W): walk global memory
         if (lane == 0) {
             for (uint64_t x = entries[t]; x < z; x += nd[x]) bm_set(bm, (uint32_t)x);
             if (z == A.n) bm_set(bm, A.n);
@@ -427,9 +432,6 @@ __global__ void __launch_bounds__(kA1MarkWarps * 32) k_a1_mark(Alg1Params A, con
         if (sw[i]) atomicOr(bm + (bb >> 5) + i, sw[i]);
 }
 
-#ifndef UELLM_A1_SUB
-#define UELLM_A1_SUB 1024
-#endif
 static uint32_t a1_sub(uint32_t W)
 {
     uint32_t T = UELLM_A1_SUB;

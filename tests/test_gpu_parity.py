@@ -146,6 +146,15 @@ def test_mode_slo_odbs_eq_variants(l1, l2, additive, split):
                                              eq2_additive=additive, window=3000))
 
 
+@pytest.mark.parametrize("W_", [1024, 2048, 4096])
+def test_mode_slo_odbs_large_max_batch(W_):
+    """Alg. 1 with W at and above the chain sub-tile (sub-tile = next power of two >= W: the
+    shared-memory staging of the marking kernel no longer fits and it walks global memory)."""
+    inp, out, slo, cfg = W.c2(24, n=12_000)
+    assert_parity(inp, out, slo, cfg.replace(mode=W.MODE_SLO_ODBS, w1=0.001, w2=0.0001, threshold=1e5,
+                                             max_batch=W_, window=7000))
+
+
 # ------------------------------------------------------------------ edges and errors
 def test_edges():
     for n in (1, 2, 3, 31, 32, 33):
