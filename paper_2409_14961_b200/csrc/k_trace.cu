@@ -195,7 +195,7 @@ __device__ __forceinline__ bool a1_cap_flush(double threshold, double den, uint3
     return !(__ddiv_rn(threshold, den) >= k);
 }
 
-// SPLIT: split_on_slo_change; UNIT: l1 == l2 == 1 (x * 1.0 == x exactly, so the two
+// SPLIT: split_on_slo_change; UNIT: w1 == l1 == l2 == 1 (x * 1.0 == x exactly, so those four
 // multiplications are skipped without changing a bit).  O (the batch's max predicted length) is
 // kept as an integer beside its double copy (outputs are u32, exact in a double).
 template <bool SPLIT, bool UNIT>
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
             double T_o = A.eq2_additive ? __dadd_rn(len, O_CM) : __dsub_rn(len, O_CM);
             T_o = __dmul_rn(T_o, nb1);
             if (!UNIT) T_o = __dmul_rn(T_o, A.l2);
-            const double Total = __dadd_rn(__dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
+            const double Total = __dadd_rn(UNIT ? T_l : __dmul_rn(A.w1, T_l), __dmul_rn(A.w2, T_o));
             bool admit = (bsize == 0);
             if (!admit && Total <= A.threshold) {
                 const uint64_t s = max(inx, MI);
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
                 admit = (uint64_t)(bsize + 1) * (s + O) <= A.cap_tok;
             }
             if (!admit) { next = p; break; }                  // q seeds the next batch
-            const double cmq = __dadd_rn(__dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
+            const double cmq = __dadd_rn(UNIT ? len : __dmul_rn(A.w1, len), __dmul_rn(A.w2, slo));
             bsize += 1;
             nb1 = __dadd_rn(nb1, 1.0);                         // = bsize + 1, exact
             if (slo > L_CM) L_CM = slo;
@@ -446,7 +446,7 @@ cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_de
     if (A.n == 0) return cudaSuccess;
     uint64_t blocks = ceil_div(A.n, 256);
     if (blocks > 148ull * 64) blocks = 148ull * 64;
-    const bool unit = A.l1 == 1.0 && A.l2 == 1.0;
+    const bool unit = A.w1 == 1.0 && A.l1 == 1.0 && A.l2 == 1.0;
     if (A.split) {
         if (unit) k_alg1_next<true, true><<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
         else k_alg1_next<true, false><<<(unsigned)blocks, 256, 0, st>>>(A, next_delta);
