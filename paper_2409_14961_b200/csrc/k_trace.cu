@@ -323,26 +323,48 @@ __global__ void __launch_bounds__(kA1EntWarps * 32) k_a1_entries(Alg1Params A, u
     const uint64_t nsub = ceil_div(w1 - w0, (uint64_t)T);
     const uint32_t CH = max(1u, kA1EntElems / A.W);
     uint16_t *b = buf[wi];
-    uint64_t e = w0;
-    for (uint64_t k0 = 0; k0 < nsub; k0 += CH) {
-        const uint32_t c = (uint32_t)min((uint64_t)CH, nsub - k0);
-        const uint16_t *src = exit_first + (w * spw + k0) * A.W;
+    // chunk k0: sub-tiles [k0, k0 + c), their exit rows at src, m staged u16
+    auto chunk = [&](uint64_t k0, uint32_t &c, const uint16_t *&src, uint32_t &m) {
+        c = (uint32_t)min((uint64_t)CH, nsub - k0);
+        src = exit_first + (w * spw + k0) * A.W;
         // only a window's last sub-tile can be shorter than W (its exit row holds len entries)
         const uint64_t last_len = min((uint64_t)T, w1 - (w0 + (k0 + c - 1) * T));
-        const uint32_t m = (uint32_t)min((uint64_t)(c - 1) * A.W + min((uint64_t)A.W, last_len),
-                                         (uint64_t)kA1EntElems);   // W > kA1EntElems: first part only
-        if (A.W % 8 == 0) {                                    // rows 16-byte aligned: uint4 loads, all in flight
+        m = (uint32_t)min((uint64_t)(c - 1) * A.W + min((uint64_t)A.W, last_len),
+                          (uint64_t)kA1EntElems);              // W > kA1EntElems: first part only
+    };
+    constexpr uint32_t kV = kA1EntElems / 8 / 32;
+    const bool vec = A.W % 8 == 0;                             // rows 16-byte aligned: uint4 loads
+    uint4 r[kV];                                               // next chunk, in flight during the walk
+    auto issue = [&](const uint16_t *src, uint32_t m) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+#pragma unroll
+        for (uint32_t u = 0; u < kV; ++u)
+            if (lane + 32 * u < (m >> 3)) r[u] = s4[lane + 32 * u];
+    };
+    uint64_t e = w0;
+    if (vec && nsub > 0) {
+        uint32_t c0, m0;
+        const uint16_t *s0;
+        chunk(0, c0, s0, m0);
+        issue(s0, m0);
+    }
+    for (uint64_t k0 = 0; k0 < nsub; k0 += CH) {
+        uint32_t c, m;
+        const uint16_t *src;
+        chunk(k0, c, src, m);
+        if (vec) {
             const uint32_t m8 = m >> 3;
-            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
             uint4 *b4 = reinterpret_cast<uint4 *>(b);
-            uint4 r[kA1EntElems / 8 / 32];
 #pragma unroll
-            for (uint32_t u = 0; u < kA1EntElems / 8 / 32; ++u)
-                if (lane + 32 * u < m8) r[u] = s4[lane + 32 * u];
-#pragma unroll
-            for (uint32_t u = 0; u < kA1EntElems / 8 / 32; ++u)
+            for (uint32_t u = 0; u < kV; ++u)
                 if (lane + 32 * u < m8) b4[lane + 32 * u] = r[u];
             for (uint32_t i = 8 * m8 + lane; i < m; i += 32) b[i] = src[i];
+            if (k0 + CH < nsub) {
+                uint32_t c1, m1;
+                const uint16_t *s1;
+                chunk(k0 + CH, c1, s1, m1);
+                issue(s1, m1);
+            }
         } else {
             for (uint32_t i = lane; i < m; i += 32) b[i] = src[i];
         }
