@@ -265,7 +265,10 @@ __global__ void __launch_bounds__(256) k_alg1_next(Alg1Params A, uint16_t *__res
 //                     entry (one thread per sub-tile).
 constexpr uint16_t kExit = 0xffff;
 
-__global__ void __launch_bounds__(256) k_a1_lift(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t T, uint32_t K,
+#ifndef UELLM_A1_LIFT_THREADS
+#define UELLM_A1_LIFT_THREADS 256
+#endif
+__global__ void __launch_bounds__(UELLM_A1_LIFT_THREADS) k_a1_lift(Alg1Params A, const uint16_t *__restrict__ nd, uint32_t T, uint32_t K,
                                                  uint64_t spw, uint16_t *__restrict__ exit_first,
                                                  const uint32_t *__restrict__ entries, uint32_t *bm)
 {
@@ -486,7 +489,7 @@ cudaError_t launch_alg1(const Alg1Params &A, uint32_t *bitmap, uint16_t *next_de
     const size_t smem = ((size_t)K + 1) * T * sizeof(uint16_t);
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_a1_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    k_a1_lift<<<(unsigned)nt, 256, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
+    k_a1_lift<<<(unsigned)nt, UELLM_A1_LIFT_THREADS, smem, st>>>(A, next_delta, T, K, spw, exit_first, entries, bitmap);
     k_a1_entries<<<(unsigned)ceil_div(A.nwin, kA1EntWarps), kA1EntWarps * 32, 0, st>>>(A, T, spw, exit_first, entries);
     k_a1_mark<<<(unsigned)ceil_div(nt, kA1MarkWarps), kA1MarkWarps * 32, 0, st>>>(A, next_delta, T, spw, entries, bitmap);
     return cudaGetLastError();
