@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define UELLM_ABI_VERSION 1u
+#define UELLM_ABI_VERSION 2u
 
 typedef int32_t uellm_status;
 enum {
@@ -144,7 +144,13 @@ typedef struct {
     uint64_t makespan_us;           /* sum of est_us                                        */
     double mean_latency_s;          /* sum over queries of completion_us(batch) / n * 1e-6          */
     double throughput_tok_s;        /* gen_tokens / (makespan_us * 1e-6)                            */
-} uellm_totals;
+    uint64_t latency_sum_lo;        /* exact 128-bit sum over queries of completion_us(batch), the  */
+    uint64_t latency_sum_hi;        /*   numerator of mean_latency_s (lets totals combine exactly) */
+    uint64_t overflow;              /* bit i set iff the i-th u64 field above (n = bit 0 ...
+                                       makespan_us = bit 10) did not fit 64 bits and saturated at
+                                       2^64 - 1 (only dp_cost and makespan_us can: the load bounds
+                                       one window, not the whole job); 0 normally                 */
+} uellm_totals;                     /* 128 bytes: also the head of the a9 exchange record          */
 
 /* Diagnostics of the last uellm_schedule_batches call on a profile (SEG-DP internals). */
 typedef struct {
@@ -196,7 +202,9 @@ uint64_t uellm_sizeof(int which);   /* 0 config, 1 batch_stat, 2 totals, 3 profi
 const char *uellm_status_string(uellm_status s);
 
 /* Device workspace bytes needed to load and schedule n queries with cfg (a pure function of
- * n, cfg->window, cfg->max_batch, cfg->dp_tile).  [host]  Returns 0 if cfg is NULL. */
+ * n, cfg->window, cfg->max_batch, cfg->dp_tile).  [host]  Returns 0 if cfg is NULL.
+ * A profile is bound to the cfg it was loaded with: every later call on it must pass a cfg equal
+ * in every field (compared through a hash of all fields), else UELLM_ERR_ARG. */
 size_t uellm_workspace_bytes(uint64_t n, const uellm_config *cfg);
 
 /* Validate and load n profiled queries (Sec. 4.1 output).
@@ -231,13 +239,17 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
 /* Per-batch statistics of the schedule produced by the
  * last uellm_schedule_batches call on p.
  *   batch_offsets, num_batches  [host|device] that call's outputs.  Device pointers may hold
- *                  a caller-modified segmentation of the same order.  Host pointers are accepted
+ *                  a caller-modified segmentation of the same order (a batch that crosses a
+ *                  window boundary is counted with a linear scan and attributed to the window of
+ *                  its first member).  Host pointers are accepted
  *                  only when that schedule call also returned its results to host memory; the
  *                  library then reads the workspace copy it staged them through.
  *   per_batch      [device] capacity num_batches x uellm_batch_stat, or NULL.
  *   totals         [host|device] 1 x uellm_totals.
  * Integer statistics are exact; mean_latency_s and throughput_tok_s are doubles computed from
- * exact 128-bit / 64-bit integer sums. */
+ * exact 128-bit / 64-bit integer sums.  A job total that does not fit 64 bits (dp_cost or
+ * makespan_us of a huge job) saturates and is flagged in totals->overflow; with a HOST totals
+ * pointer the call then returns UELLM_ERR_OVERFLOW (the totals are still written). */
 uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg,
                                const uint32_t *batch_offsets, const uint64_t *num_batches,
                                uellm_batch_stat *per_batch, uellm_totals *totals, void *stream);
@@ -412,6 +424,54 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
  *   words  [device] capacity (n + 32) / 32 x u32; written stream-ordered, never synchronises. */
 uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *cfg, uint32_t *words,
                                    void *stream);
+
+/* a9 -- the one exchange step of the multi-GPU path (BASELINE.json north_star "one
+ * NCCL allgather of batch boundaries and statistics").  Windows never share a batch (R15), so
+ * rank r schedules the contiguous window block [q_r, q_{r+1}) of the job on its own GPU; each
+ * rank then contributes ONE fixed-size record to an allgather:
+ *     record = [ uellm_totals of the rank (128 B) | boundary bitmap of the rank's n_r + 1
+ *                positions (bit k set iff a batch starts at local position k; bit n_r = end) ]
+ * padded to uellm_exchange_bytes(n_max) with n_max the largest rank's query count.  From the
+ * gathered records every rank rebuilds the whole job's batch_offsets and exact totals.
+ * The collective itself is the caller's (torch.distributed / NCCL all_gather_into_tensor). */
+
+/* Bytes of one rank's exchange record for ranks of at most n_max queries (multiple of 16). */
+size_t uellm_exchange_bytes(uint64_t n_max);
+
+/* Write this rank's record.  [stream-ordered, never synchronises]
+ *   p, cfg     the rank's loaded profile; the schedule of its last uellm_schedule_batches call.
+ *   totals     [device] the rank's uellm_totals (uellm_batch_stats output on the same stream).
+ *   record     [device] uellm_exchange_bytes(n_max) bytes, 16-B aligned; n_max >= the rank's n. */
+uellm_status uellm_exchange_pack(const uellm_profile *p, const uellm_config *cfg, const uellm_totals *totals,
+                                 void *record, uint64_t n_max, void *stream);
+
+/* Job totals from `count` partial uellm_totals (window groups, ranks) laid out `stride_bytes` apart
+ * in device memory -- e.g. the heads of gathered exchange records (stride uellm_exchange_bytes).
+ * Same combination as uellm_exchange_combine's totals.  parts [device]; out [host|device] (host:
+ * the call synchronises `stream` and returns UELLM_ERR_OVERFLOW if out->overflow != 0). */
+uellm_status uellm_totals_combine(const void *parts, uint32_t count, uint64_t stride_bytes, uellm_totals *out,
+                                  void *ws, size_t ws_bytes, void *stream);
+
+/* Workspace of uellm_exchange_combine for a job of n_total queries (device bytes). */
+size_t uellm_exchange_workspace_bytes(uint64_t n_total, uint32_t world);
+
+/* Rebuild the whole job from the gathered records (record r = rank r, contiguous).
+ *   gathered        [device] world x uellm_exchange_bytes(n_max) bytes.
+ *   query_begin     [host] world + 1 entries: rank r owns global positions
+ *                   [query_begin[r], query_begin[r+1]); query_begin[world] = n_total < 2^32 - 1.
+ *   ws              [device] >= uellm_exchange_workspace_bytes(n_total, world), 256-B aligned.
+ *   batch_offsets   [device] capacity n_total + 1 x u32: the job's offsets (rank r's local
+ *                   boundary k is global position query_begin[r] + k).
+ *   num_batches     [device] 1 x u64.
+ *   totals          [host|device] 1 x uellm_totals: sums of the ranks' integer totals (kv_bytes_max:
+ *                   max), exact 128-bit latency numerator, doubles re-formed from the sums as
+ *                   uellm_batch_stats forms them; overflow flags OR-ed plus any saturation here.
+ * Host totals: the call synchronises `stream`.  Identical to a single-GPU run of the whole job
+ * (tests/test_gpu_parity.py, tests/test_distributed_gloo.py). */
+uellm_status uellm_exchange_combine(const void *gathered, uint32_t world, uint64_t n_max,
+                                    const uint64_t *query_begin, void *ws, size_t ws_bytes,
+                                    uint32_t *batch_offsets, uint64_t *num_batches, uellm_totals *totals,
+                                    void *stream);
 
 /* BGS, the paper's baseline deployer ("Greedy Scheduling Algorithm"):
  * devices in descending order of Memory(d) (ties: smaller id first) each take max_layers(d)

@@ -143,9 +143,21 @@ uellm_status check_config(const uellm_config *c)
 
 inline const ProfileView *view_of(const uellm_profile *p) { return reinterpret_cast<const ProfileView *>(p); }
 
+// FNV-1a over every field of the config: a profile is bound to the exact cfg it was loaded with
+// (the overflow bounds, the narrow DP path and the stats' sortedness are decided from it).
 uint64_t layout_key(const uellm_config *c)
 {
-    return ((uint64_t)c->window << 32) ^ ((uint64_t)c->max_batch << 8) ^ ((uint64_t)c->dp_tile * 0x9E3779B97F4A7C15ull);
+    uint64_t h = 0xcbf29ce484222325ull;
+    auto mix = [&](uint64_t v) {
+        for (int b = 0; b < 8; ++b) { h ^= (v >> (8 * b)) & 0xff; h *= 0x100000001b3ull; }
+    };
+    auto dbl = [](double d) { uint64_t u; std::memcpy(&u, &d, 8); return u; };
+    mix(c->mode); mix(c->window); mix(c->max_batch); mix(c->split_on_slo_change);
+    mix(c->kv_bytes_per_elem); mix(c->n_layers); mix(c->hidden); mix(c->dp_tile); mix(c->kv_cap_bytes);
+    mix(c->t_batch_us); mix(c->t_iter_us); mix(c->t_tok_us); mix(c->t_prefill_us); mix(c->lambda_us);
+    mix(dbl(c->w1)); mix(dbl(c->w2)); mix(dbl(c->l1)); mix(dbl(c->l2)); mix(dbl(c->threshold)); mix(dbl(c->eps));
+    mix(c->eq2_additive); mix(c->flags);
+    return h;
 }
 
 inline void rec(const ProfileView &v, int k, cudaStream_t st)
@@ -511,6 +523,7 @@ uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg, 
     if (!dev_tot) {
         CU(cudaMemcpyAsync(totals, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
+        if (totals->overflow) return UELLM_ERR_OVERFLOW;
     }
     return UELLM_OK;
 }
@@ -652,6 +665,107 @@ uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *c
         return UELLM_OK;
     }
     CU(cudaMemcpyAsync(words, v.ws + L.bitmap, 4 * L.nwords, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return UELLM_OK;
+}
+
+size_t uellm_exchange_bytes(uint64_t n_max) { return (size_t)exchange_record_bytes(n_max); }
+
+uellm_status uellm_exchange_pack(const uellm_profile *p, const uellm_config *cfg, const uellm_totals *totals,
+                                 void *record, uint64_t n_max, void *stream)
+{
+    if (!p || !cfg || !totals || !record) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
+    if (v.n > n_max || !is_device_ptr(record) || !is_device_ptr(totals) ||
+        (reinterpret_cast<uintptr_t>(record) & 15))
+        return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t rb = exchange_record_bytes(n_max);
+    uint8_t *r = (uint8_t *)record;
+    const uint64_t bm_bytes = 4 * ((v.n + 1 + 31) / 32);
+    CU(cudaMemcpyAsync(r, totals, sizeof(uellm_totals), cudaMemcpyDeviceToDevice, st));
+    if (v.n == 0) {
+        CU(cudaMemsetAsync(r + sizeof(uellm_totals), 0, rb - sizeof(uellm_totals), st));
+        CU(cudaMemsetAsync(r + sizeof(uellm_totals), 1, 1, st));           // the single boundary 0 (= n)
+        return UELLM_OK;
+    }
+    const WsLayout L = make_layout(v.n, *cfg);
+    CU(cudaMemcpyAsync(r + sizeof(uellm_totals), v.ws + L.bitmap, bm_bytes, cudaMemcpyDeviceToDevice, st));
+    const uint64_t used = sizeof(uellm_totals) + bm_bytes;
+    if (rb > used) CU(cudaMemsetAsync(r + used, 0, rb - used, st));      // padding (initialised)
+    return UELLM_OK;
+}
+
+namespace {
+struct XcLayout { uint64_t qb, bitmap, wscan, blocksum, totals, total; };
+XcLayout xc_layout(uint64_t n_total, uint32_t world)
+{
+    XcLayout X;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
+    const uint64_t nwords = (n_total + 1 + 31) / 32;
+    X.qb = take(8ull * ((uint64_t)world + 1));
+    X.bitmap = take(4 * nwords);
+    X.wscan = take(4 * nwords);
+    X.blocksum = take(4 * (ceil_div(nwords, kScanBlock) + 2));
+    X.totals = take(sizeof(uellm_totals));
+    X.total = off;
+    return X;
+}
+}  // namespace
+
+uellm_status uellm_totals_combine(const void *parts, uint32_t count, uint64_t stride_bytes, uellm_totals *out,
+                                  void *ws, size_t ws_bytes, void *stream)
+{
+    if (!parts || count < 1 || stride_bytes < sizeof(uellm_totals) || (stride_bytes & 7) || !out) return UELLM_ERR_ARG;
+    if (!is_device_ptr(parts)) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool dev_out = is_device_ptr(out);
+    if (!dev_out && (!ws || ws_bytes < sizeof(uellm_totals) || !is_device_ptr(ws))) return UELLM_ERR_ARG;
+    uellm_totals *d_out = dev_out ? out : (uellm_totals *)ws;
+    CU(launch_totals_combine((const uint8_t *)parts, count, stride_bytes, d_out, st));
+    if (!dev_out) {
+        CU(cudaMemcpyAsync(out, d_out, sizeof(uellm_totals), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (out->overflow) return UELLM_ERR_OVERFLOW;
+    }
+    return UELLM_OK;
+}
+
+size_t uellm_exchange_workspace_bytes(uint64_t n_total, uint32_t world)
+{
+    if (world < 1) return 0;
+    return (size_t)xc_layout(n_total, world).total;
+}
+
+uellm_status uellm_exchange_combine(const void *gathered, uint32_t world, uint64_t n_max, const uint64_t *query_begin,
+                                    void *ws, size_t ws_bytes, uint32_t *batch_offsets, uint64_t *num_batches,
+                                    uellm_totals *totals, void *stream)
+{
+    if (!gathered || world < 1 || !query_begin || !batch_offsets || !num_batches || !totals) return UELLM_ERR_ARG;
+    if (query_begin[0] != 0) return UELLM_ERR_ARG;
+    for (uint32_t r = 0; r < world; ++r)
+        if (query_begin[r + 1] < query_begin[r] || query_begin[r + 1] - query_begin[r] > n_max) return UELLM_ERR_ARG;
+    const uint64_t n_total = query_begin[world];
+    if (n_total >= 0xffffffffull) return UELLM_ERR_ARG;
+    const XcLayout X = xc_layout(n_total, world);
+    if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255) || ws_bytes < X.total) return UELLM_ERR_ARG;
+    if (!is_device_ptr(gathered) || !is_device_ptr(batch_offsets) || !is_device_ptr(num_batches)) return UELLM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = (uint8_t *)ws;
+    const bool dev_tot = is_device_ptr(totals);
+    uellm_totals *d_tot = dev_tot ? totals : at<uellm_totals>(w, X.totals);
+    // (a pageable host->device copy returns once the source has been staged)
+    CU(cudaMemcpyAsync(at<unsigned long long>(w, X.qb), query_begin, 8ull * (world + 1), cudaMemcpyHostToDevice, st));
+    CU(run_exchange_combine((const uint8_t *)gathered, world, exchange_record_bytes(n_max),
+                            at<unsigned long long>(w, X.qb), n_total, at<uint32_t>(w, X.bitmap),
+                            at<uint32_t>(w, X.wscan), at<uint32_t>(w, X.blocksum), batch_offsets,
+                            (unsigned long long *)num_batches, d_tot, st));
+    if (!dev_tot) {
+        CU(cudaMemcpyAsync(totals, d_tot, sizeof(uellm_totals), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (totals->overflow) return UELLM_ERR_OVERFLOW;
+    }
     return UELLM_OK;
 }
 

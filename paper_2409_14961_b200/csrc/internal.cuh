@@ -78,10 +78,39 @@ struct Diag {                // device counters, see uellm_diagnostics
         trace_unmerged, trace_rewalks, sort_passes, dp_evals, sched_launches, stats_launches, sort_key_bits;
 };
 
+// Whole-job totals from partial totals (window groups of the pipelined call, ranks of the a9
+// exchange): integer sums (kv_bytes_max: max) saturating at 2^64 - 1 with the overflow bit of the
+// field (uellm_totals.overflow), exact 128-bit latency numerator; finish_totals re-forms the two
+// doubles exactly as k_totals forms them.
+__host__ __device__ inline void sat_add_u64(uint64_t &a, uint64_t b, uint64_t &of, int bit)
+{
+    const uint64_t s = a + b;
+    if (s < a) { a = ~0ull; of |= 1ull << bit; } else a = s;
+}
+__host__ __device__ inline void combine_totals_into(uellm_totals &T, const uellm_totals &t)
+{
+    uint64_t *dst = &T.n;
+    const uint64_t *src = &t.n;
+    for (int f = 0; f < 11; ++f) {            // n .. makespan_us (struct order)
+        if (f == 5) dst[f] = src[f] > dst[f] ? src[f] : dst[f];
+        else sat_add_u64(dst[f], src[f], T.overflow, f);
+    }
+    const uint64_t lo = T.latency_sum_lo + t.latency_sum_lo;
+    T.latency_sum_hi += t.latency_sum_hi + (lo < T.latency_sum_lo ? 1ull : 0ull);
+    T.latency_sum_lo = lo;
+    T.overflow |= t.overflow;
+}
+__host__ __device__ inline void finish_totals(uellm_totals &T)
+{
+    const double lat = (double)T.latency_sum_hi * 18446744073709551616.0 + (double)T.latency_sum_lo;
+    T.mean_latency_s = T.n ? lat / (double)T.n * 1e-6 : 0.0;
+    T.throughput_tok_s = T.makespan_us ? (double)T.gen_tokens / ((double)T.makespan_us * 1e-6) : 0.0;
+}
+
 // Exact 128-bit accumulator of sum(b * completion_us) for mean_latency_s.
 struct StatAcc {
     unsigned long long gen, pad_in, pad_out, kv_max, dp_cost, viol_alone, viol_seq, over_cap,
-        makespan, lat_lo, lat_hi, batches;
+        makespan, lat_lo, lat_hi, batches, overflow;
 };
 
 // Accumulators of uellm_simulate (exact 128-bit latency sum).
@@ -225,6 +254,20 @@ uint64_t alg1_scratch_bytes(uint64_t window, uint64_t nwin, uint32_t W);
 // Compaction of the boundary bitmap (n+1 bits) into batch_offsets, num_batches.
 cudaError_t run_compact(const uint32_t *bitmap, uint64_t n, uint32_t *wscan, uint32_t *blocksum,
                         uint32_t *offsets, unsigned long long *num_batches, cudaStream_t st);
+
+// a9: job bitmap + offsets + totals from the gathered exchange records (k_exchange.cu)
+cudaError_t run_exchange_combine(const uint8_t *gathered, uint32_t world, uint64_t rec_bytes,
+                                 const unsigned long long *d_qb, uint64_t n_total, uint32_t *bitmap, uint32_t *wscan,
+                                 uint32_t *blocksum, uint32_t *offsets, unsigned long long *num_batches,
+                                 uellm_totals *d_tot, cudaStream_t st);
+cudaError_t launch_totals_combine(const uint8_t *parts, uint32_t count, uint64_t stride, uellm_totals *out,
+                                  cudaStream_t st);
+// bytes of one exchange record for ranks of <= n_max queries: totals + (n_max + 1)-bit bitmap
+// + one spare word (the combine reads a word pair), 16-B multiple
+inline uint64_t exchange_record_bytes(uint64_t n_max)
+{
+    return align_up(sizeof(uellm_totals) + 4 * ((n_max + 1 + 31) / 32 + 1), 16);
+}
 
 struct StatsParams {
     const uint32_t *rin, *rout, *rslo;

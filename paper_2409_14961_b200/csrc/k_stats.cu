@@ -109,29 +109,14 @@ __global__ void __launch_bounds__(256) k_stats_est(StatsParams S)
     else stats_est_body<1>(S, m);
 }
 
-// #{k in [a, z) : rslo[k] < x} -- members ascend in slo_us when S.sorted (a contiguous range of
-// the (slo, out, index)-sorted window), else a plain count (FIFO batches keep arrival order).
-__device__ __forceinline__ uint32_t count_below(const StatsParams &S, uint32_t a, uint32_t z, unsigned long long x)
-{
-    if (S.sorted) {
-        uint32_t lo = a, hi = z;
-        while (lo < hi) {
-            const uint32_t mid = lo + (hi - lo) / 2;
-            if ((unsigned long long)__ldg(S.rslo + mid) < x) lo = mid + 1; else hi = mid;
-        }
-        return lo - a;
-    }
-    uint32_t c = 0;
-    for (uint32_t k = a; k < z; ++k) c += (unsigned long long)__ldg(S.rslo + k) < x;
-    return c;
-}
-
 // both violation counts of a batch: the two binary searches run in lockstep so their
 // dependent loads overlap
 __device__ __forceinline__ void count_below2(const StatsParams &S, uint32_t a, uint32_t z, unsigned long long x1,
                                              unsigned long long x2, uint32_t &c1, uint32_t &c2)
 {
-    if (S.sorted) {
+    // members ascend in slo_us only inside one window (a caller-modified segmentation may cross a
+    // window boundary: then the plain count)
+    if (S.sorted && a / S.window == (z - 1) / S.window) {
         uint32_t lo1 = a, hi1 = z, lo2 = a, hi2 = z;
         while (lo1 < hi1 || lo2 < hi2) {
             const uint32_t m1 = lo1 + (hi1 - lo1) / 2, m2 = lo2 + (hi2 - lo2) / 2;
@@ -262,12 +247,15 @@ static_assert(sizeof(uellm_batch_stat) % 16 == 0, "record copied as uint4");
 __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
 {
     // thread per batch: reads the pass-1 record, two binary searches for the violation counts
-    __shared__ unsigned long long red[8][12];
+    __shared__ unsigned long long red[8][13];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t m = *S.num_batches;
     const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
     unsigned long long a_gen = 0, a_pin = 0, a_pout = 0, a_kv = 0, a_obj = 0, a_v1 = 0, a_v2 = 0, a_oc = 0,
                        a_mk = 0, a_llo = 0, a_lhi = 0, a_nb = 0;
+    // dp_cost and makespan are the only sums the load's per-window bound does not cover: carry a
+    // sticky overflow flag per field (bit 6 dp_cost, bit 10 makespan_us, as in uellm_totals)
+    unsigned long long of = 0;
     // block-uniform loop: the 80-byte records go through shared memory and leave as coalesced
     // 16-byte stores (a record per thread would be ten 8-byte stores at an 80-byte lane stride)
     __shared__ __align__(16) uellm_batch_stat rec[256];
@@ -292,7 +280,9 @@ __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
                 r.viol_alone = v1; r.viol_seq = v2; r.over_cap = oc; r.window = a / S.window;
             }
             a_gen += gen; a_pin += pin; a_pout += pout; a_kv = max(a_kv, kv);
-            a_obj += est + S.lambda * v1; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += est; a_nb += 1;
+            const unsigned long long obj = est + S.lambda * v1;     // <= E + lambda*W (load bound)
+            a_obj += obj; a_v1 += v1; a_v2 += v2; a_oc += oc; a_mk += est; a_nb += 1;
+            of |= (a_obj < obj ? (1ull << 6) : 0ull) | (a_mk < est ? (1ull << 10) : 0ull);
             const unsigned long long lo = (unsigned long long)b * compl_us;
             const unsigned long long hi = __umul64hi((unsigned long long)b, compl_us);
             a_llo += lo; a_lhi += hi + (a_llo < lo ? 1ull : 0ull);
@@ -319,9 +309,16 @@ __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
     for (int d = 16; d; d >>= 1) {
         a_gen += __shfl_xor_sync(0xffffffffu, a_gen, d); a_pin += __shfl_xor_sync(0xffffffffu, a_pin, d);
         a_pout += __shfl_xor_sync(0xffffffffu, a_pout, d); a_kv = max(a_kv, __shfl_xor_sync(0xffffffffu, a_kv, d));
-        a_obj += __shfl_xor_sync(0xffffffffu, a_obj, d); a_v1 += __shfl_xor_sync(0xffffffffu, a_v1, d);
+        {
+            const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, a_obj, d);
+            const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, a_mk, d);
+            of |= __shfl_xor_sync(0xffffffffu, of, d);
+            a_obj += o2; a_mk += m2;
+            of |= (a_obj < o2 ? (1ull << 6) : 0ull) | (a_mk < m2 ? (1ull << 10) : 0ull);
+        }
+        a_v1 += __shfl_xor_sync(0xffffffffu, a_v1, d);
         a_v2 += __shfl_xor_sync(0xffffffffu, a_v2, d); a_oc += __shfl_xor_sync(0xffffffffu, a_oc, d);
-        a_mk += __shfl_xor_sync(0xffffffffu, a_mk, d); a_nb += __shfl_xor_sync(0xffffffffu, a_nb, d);
+        a_nb += __shfl_xor_sync(0xffffffffu, a_nb, d);
         const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, a_llo, d), hi2 = __shfl_xor_sync(0xffffffffu, a_lhi, d);
         const unsigned long long lo = a_llo + lo2;
         a_lhi += hi2 + (lo < a_llo ? 1ull : 0ull);
@@ -330,24 +327,37 @@ __global__ void __launch_bounds__(256) k_stats_final(StatsParams S)
     if (lane == 0) {
         unsigned long long *r = red[warp];
         r[0] = a_gen; r[1] = a_pin; r[2] = a_pout; r[3] = a_kv; r[4] = a_obj; r[5] = a_v1;
-        r[6] = a_v2; r[7] = a_oc; r[8] = a_mk; r[9] = a_llo; r[10] = a_lhi; r[11] = a_nb;
+        r[6] = a_v2; r[7] = a_oc; r[8] = a_mk; r[9] = a_llo; r[10] = a_lhi; r[11] = a_nb; r[12] = of;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long s[12] = {};
+        unsigned long long s[13] = {};
         const int nwarps = blockDim.x >> 5;
         for (int w = 0; w < nwarps; ++w) {
-            for (int f = 0; f < 12; ++f) {
+            for (int f = 0; f < 13; ++f) {
                 if (f == 3) s[3] = max(s[3], red[w][3]);
                 else if (f == 9) { unsigned long long lo = red[w][9]; s[9] += lo; if (s[9] < lo) s[10] += 1; }
-                else s[f] += red[w][f];
+                else if (f == 12) s[12] |= red[w][12];
+                else {
+                    const unsigned long long x = red[w][f];
+                    s[f] += x;
+                    if (f == 4 && s[4] < x) s[12] |= 1ull << 6;
+                    if (f == 8 && s[8] < x) s[12] |= 1ull << 10;
+                }
             }
         }
         StatAcc *A = S.acc;
         if (s[11] == 0) return;
         atomicAdd(&A->gen, s[0]); atomicAdd(&A->pad_in, s[1]); atomicAdd(&A->pad_out, s[2]);
-        atomicMax(&A->kv_max, s[3]); atomicAdd(&A->dp_cost, s[4]); atomicAdd(&A->viol_alone, s[5]);
-        atomicAdd(&A->viol_seq, s[6]); atomicAdd(&A->over_cap, s[7]); atomicAdd(&A->makespan, s[8]);
+        atomicMax(&A->kv_max, s[3]); atomicAdd(&A->viol_alone, s[5]);
+        atomicAdd(&A->viol_seq, s[6]); atomicAdd(&A->over_cap, s[7]);
+        {
+            const unsigned long long o4 = atomicAdd(&A->dp_cost, s[4]);
+            const unsigned long long o8 = atomicAdd(&A->makespan, s[8]);
+            if (o4 + s[4] < o4) s[12] |= 1ull << 6;
+            if (o8 + s[8] < o8) s[12] |= 1ull << 10;
+            if (s[12]) atomicOr(&A->overflow, s[12]);
+        }
         const unsigned long long old = atomicAdd(&A->lat_lo, s[9]);
         atomicAdd(&A->lat_hi, s[10] + (old + s[9] < old ? 1ull : 0ull));
         atomicAdd(&A->batches, s[11]);
@@ -363,9 +373,12 @@ __global__ void k_totals(StatsParams S)
     T.gen_tokens = A.gen; T.pad_in = A.pad_in; T.pad_out = A.pad_out; T.kv_bytes_max = A.kv_max;
     T.dp_cost = A.dp_cost; T.viol_alone = A.viol_alone; T.viol_seq = A.viol_seq; T.over_cap = A.over_cap;
     T.makespan_us = A.makespan;
-    const double lat = (double)A.lat_hi * 18446744073709551616.0 + (double)A.lat_lo;
-    T.mean_latency_s = S.n ? lat / (double)S.n * 1e-6 : 0.0;
-    T.throughput_tok_s = A.makespan ? (double)A.gen / ((double)A.makespan * 1e-6) : 0.0;
+    T.overflow = A.overflow;
+    if (T.overflow & (1ull << 6)) T.dp_cost = ~0ull;          // saturate (flagged)
+    if (T.overflow & (1ull << 10)) T.makespan_us = ~0ull;
+    T.latency_sum_lo = A.lat_lo;
+    T.latency_sum_hi = A.lat_hi;
+    finish_totals(T);
     *S.totals = T;
 }
 

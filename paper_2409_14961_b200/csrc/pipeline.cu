@@ -253,18 +253,10 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         // re-weighted by the group sizes, the throughput recomputed from the integer sums
         uellm_totals T;
         std::memset(&T, 0, sizeof T);
-        double lat = 0.0;
-        for (uint64_t g = 0; g < G; ++g) {
-            const uellm_totals &t = tot_host[g];
-            T.n += t.n; T.batches += t.batches; T.gen_tokens += t.gen_tokens; T.pad_in += t.pad_in;
-            T.pad_out += t.pad_out; T.kv_bytes_max = t.kv_bytes_max > T.kv_bytes_max ? t.kv_bytes_max : T.kv_bytes_max;
-            T.dp_cost += t.dp_cost; T.viol_alone += t.viol_alone; T.viol_seq += t.viol_seq;
-            T.over_cap += t.over_cap; T.makespan_us += t.makespan_us;
-            lat += t.mean_latency_s * (double)t.n;
-        }
-        T.mean_latency_s = T.n ? lat / (double)T.n : 0.0;
-        T.throughput_tok_s = T.makespan_us ? (double)T.gen_tokens / ((double)T.makespan_us * 1e-6) : 0.0;
+        for (uint64_t g = 0; g < G; ++g) combine_totals_into(T, tot_host[g]);
+        finish_totals(T);
         *totals = T;
+        if (T.overflow) return UELLM_ERR_OVERFLOW;
     }
     return UELLM_OK;
   };

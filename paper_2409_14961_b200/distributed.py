@@ -1,22 +1,20 @@
 """Multi-GPU sharding of the scheduling path: windows are independent (no batch
-crosses a window, O1), so rank r owns the contiguous window block
-[floor(N_w*r/P), floor(N_w*(r+1)/P)) and runs the whole path on its own GPU with no data-path
-collective.  The one exchange step (a9) is a single all_gather of a fixed-size per-rank buffer:
-the rank's totals (16 int64 words) followed by its boundary bitmap over its own scheduled
-positions (uellm_boundary_bitmap: bit k set iff a batch starts at local position k, k = 0..n_r),
-padded to the largest rank.  Every rank can then rebuild the whole job's batch_offsets.
+crosses a window, O1/R15), so rank r owns the contiguous window block
+[floor(N_w*r/P), floor(N_w*(r+1)/P)) of ONE job and runs the whole path on its own GPU with no
+data-path collective.  The one exchange step (a9) is a single all_gather of fixed-size per-rank
+records written by the library (uellm_exchange_pack: the rank's uellm_totals followed by its
+boundary bitmap); every rank then rebuilds the whole job's batch_offsets and exact totals on its
+GPU (uellm_exchange_combine).
 
-torch.distributed is plumbing here (NCCL on GPUs, gloo in the CPU tests); no scheduling
-arithmetic happens in this module.
+torch.distributed is plumbing here (NCCL over NVLink on B200 boxes, gloo in the CPU tests); this
+module does no scheduling arithmetic: rank -> window-block bookkeeping and buffer marshalling only.
 """
 from __future__ import annotations
 
 import numpy as np
 import torch
 
-TOTAL_FIELDS = ["n", "batches", "gen_tokens", "pad_in", "pad_out", "kv_bytes_max", "dp_cost",
-                "viol_alone", "viol_seq", "over_cap", "makespan_us"]
-GATHER_WORDS = 16          # 11 integer totals + 2 doubles (as raw bits) + 3 pad
+from . import uellm as U
 
 
 def window_block(n_windows: int, world: int, rank: int) -> tuple[int, int]:
@@ -32,72 +30,47 @@ def query_range(n: int, window: int, world: int, rank: int) -> tuple[int, int]:
     return min(n, w0 * wl), min(n, w1 * wl)
 
 
-def pack_totals(totals: dict, device) -> torch.Tensor:
-    """Per-rank totals -> fixed-size int64 vector (doubles carried bit-exactly)."""
-    v = np.zeros(GATHER_WORDS, np.int64)
-    for k, f in enumerate(TOTAL_FIELDS):
-        v[k] = np.int64(np.uint64(totals[f]).view(np.int64))
-    v[11] = np.array([totals["mean_latency_s"]], np.float64).view(np.int64)[0]
-    v[12] = np.array([totals["throughput_tok_s"]], np.float64).view(np.int64)[0]
-    return torch.from_numpy(v).to(device)
+def query_begins(n: int, window: int, world: int) -> list[int]:
+    """query_begin of uellm_exchange_combine: world + 1 entries, rank r owns [qb[r], qb[r+1])."""
+    return [query_range(n, window, world, r)[0] for r in range(world)] + [n]
 
 
-def all_gather_totals(mine: torch.Tensor, group=None) -> torch.Tensor:
-    """a9: one all_gather_into_tensor of the fixed-size per-rank buffers -> [world, 16]."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    out = torch.empty(world * GATHER_WORDS, dtype=torch.int64, device=mine.device)
-    dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
-    return out.view(world, GATHER_WORDS)
+class Exchange:
+    """a9 buffers of one rank: its record, the gathered records and the combine outputs."""
 
+    def __init__(self, n_total: int, window: int, world: int, rank: int, device):
+        self.world, self.rank = world, rank
+        self.qb = query_begins(n_total, window, world)
+        self.q0, self.q1 = self.qb[rank], self.qb[rank + 1]
+        self.n_total = n_total
+        self.n_max = max(b - a for a, b in zip(self.qb[:-1], self.qb[1:])) if world else 0
+        self.rec_bytes = U.exchange_bytes(self.n_max)
+        dev = torch.device(device)
+        self.record = torch.zeros(self.rec_bytes, dtype=torch.uint8, device=dev)
+        self.gathered = torch.zeros(world * self.rec_bytes, dtype=torch.uint8, device=dev)
+        self.ws_bytes = U.exchange_workspace_bytes(n_total, world)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.offsets = torch.empty(n_total + 1, dtype=torch.int32, device=dev)
+        self.num_batches = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.totals = torch.zeros(U.TOTALS_BYTES, dtype=torch.uint8, device=dev)
 
-def combine_totals(gathered: torch.Tensor) -> dict:
-    """Whole-job totals from the per-rank rows (sums; max for kv_bytes_max; the two means are
-    re-weighted exactly from their integer numerators where possible)."""
-    g = gathered.cpu().numpy()
-    u = g[:, :11].view(np.uint64)
-    out = {}
-    for k, f in enumerate(TOTAL_FIELDS):
-        col = [int(x) for x in u[:, k]]
-        out[f] = max(col) if f == "kv_bytes_max" else sum(col)
-    lat = g[:, 11].view(np.float64)
-    ns = [int(x) for x in u[:, 0]]
-    n = sum(ns)
-    out["mean_latency_s"] = float(sum(l * m for l, m in zip(lat, ns)) / n) if n else 0.0
-    mk = out["makespan_us"]
-    out["throughput_tok_s"] = out["gen_tokens"] / (mk * 1e-6) if mk else 0.0
-    return out
+    def pack(self, profile, cfg, totals_dev, stream=None):
+        U.exchange_pack(profile, cfg, totals_dev, self.record, self.n_max, stream)
 
+    def all_gather(self, group=None, backend: str = "nccl"):
+        """ONE collective: all_gather_into_tensor (NCCL); gloo (CPU / test runs) takes the list form."""
+        import torch.distributed as dist
+        if backend == "nccl":
+            dist.all_gather_into_tensor(self.gathered, self.record, group=group)
+        else:
+            dist.all_gather(list(self.gathered.view(self.world, -1).unbind(0)), self.record, group=group)
 
-def exchange_words(n_max: int) -> int:
-    """int64 words of one rank's a9 buffer: totals + bitmap of n_max + 1 bits (u32 words, 2 per int64)."""
-    u32 = (n_max + 1 + 31) // 32
-    return GATHER_WORDS + (u32 + 1) // 2
+    def combine(self, stream=None):
+        U.exchange_combine(self.gathered, self.world, self.n_max, self.qb, self.ws, self.ws_bytes, self.offsets,
+                           self.num_batches, self.totals, stream)
 
-
-def bitmap_view(buf: torch.Tensor) -> torch.Tensor:
-    """The u32 bitmap region of one rank's int64 exchange buffer (a view: the library writes it in place)."""
-    return buf[GATHER_WORDS:].view(torch.int32)
-
-
-def all_gather_exchange(mine: torch.Tensor, group=None) -> torch.Tensor:
-    """a9: ONE all_gather_into_tensor of the per-rank [totals | bitmap] buffers -> [world, words]."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    out = torch.empty(world * mine.numel(), dtype=torch.int64, device=mine.device)
-    dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
-    return out.view(world, mine.numel())
-
-
-def global_offsets(gathered: torch.Tensor, ranges) -> np.ndarray:
-    """Whole-job batch_offsets from the gathered buffers: rank r's set bits k (0 <= k <= n_r) are
-    global positions q0_r + k; consecutive ranks share the boundary q1_r = q0_{r+1}."""
-    g = gathered.cpu().numpy()
-    parts = []
-    for r, (q0, q1) in enumerate(ranges):
-        n_r = q1 - q0
-        words = g[r, GATHER_WORDS:].view(np.uint32)
-        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: n_r + 1]
-        parts.append(np.flatnonzero(bits).astype(np.int64) + q0)
-    allpos = np.concatenate(parts) if parts else np.zeros(1, np.int64)
-    return np.unique(allpos)
+    def results(self) -> dict:
+        torch.cuda.synchronize(self.offsets.device)
+        m = int(self.num_batches.item())
+        tot = U.Totals.from_buffer_copy(self.totals.cpu().numpy().tobytes())
+        return {"offsets": self.offsets[: m + 1].cpu().numpy().view(np.uint32), "m": m, "totals": tot.as_dict()}

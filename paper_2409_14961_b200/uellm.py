@@ -46,10 +46,13 @@ class Totals(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("n", "batches", "gen_tokens", "pad_in", "pad_out",
                                           "kv_bytes_max", "dp_cost", "viol_alone", "viol_seq",
                                           "over_cap", "makespan_us")] + \
-               [("mean_latency_s", C.c_double), ("throughput_tok_s", C.c_double)]
+               [("mean_latency_s", C.c_double), ("throughput_tok_s", C.c_double),
+                ("latency_sum_lo", C.c_uint64), ("latency_sum_hi", C.c_uint64), ("overflow", C.c_uint64)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["latency_sum_us"] = d["latency_sum_lo"] + (d["latency_sum_hi"] << 64)
+        return d
 
 
 class SimTotals(C.Structure):
@@ -155,12 +158,25 @@ _lib.uellm_pipeline_workspace_bytes.argtypes = [C.c_uint64, C.POINTER(Config), C
 _lib.uellm_schedule_pipelined.restype = C.c_int32
 _lib.uellm_schedule_pipelined.argtypes = [C.POINTER(Queries), C.POINTER(Config), C.c_uint32, C.c_void_p,
                                           C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+_lib.uellm_exchange_bytes.restype = C.c_size_t
+_lib.uellm_exchange_bytes.argtypes = [C.c_uint64]
+_lib.uellm_exchange_pack.restype = C.c_int32
+_lib.uellm_exchange_pack.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_uint64,
+                                     C.c_void_p]
+_lib.uellm_exchange_workspace_bytes.restype = C.c_size_t
+_lib.uellm_exchange_workspace_bytes.argtypes = [C.c_uint64, C.c_uint32]
+_lib.uellm_exchange_combine.restype = C.c_int32
+_lib.uellm_exchange_combine.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_size_t,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+_lib.uellm_totals_combine.restype = C.c_int32
+_lib.uellm_totals_combine.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_size_t,
+                                      C.c_void_p]
 _lib.uellm_set_stage_events.restype = C.c_int32
 _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p), C.c_uint32]
 _lib.uellm_get_diagnostics.restype = C.c_int32
 _lib.uellm_get_diagnostics.argtypes = [C.POINTER(Profile), C.POINTER(Diagnostics), C.c_void_p]
 
-assert _lib.uellm_abi_version() == 1
+assert _lib.uellm_abi_version() == 2
 assert _lib.uellm_sizeof(0) == C.sizeof(Config)
 assert _lib.uellm_sizeof(1) == BATCH_STAT_DTYPE.itemsize == 80
 assert _lib.uellm_sizeof(2) == C.sizeof(Totals)
@@ -284,6 +300,34 @@ def schedule_pipelined(n: int, input_len, pred_out_len, slo_s, cfg: Config, grou
 def boundary_bitmap(p: Profile, cfg: Config, words, stream=None):
     _check(_lib.uellm_boundary_bitmap(C.byref(p), C.byref(cfg), _ptr(words), _stream_handle(stream)),
            "uellm_boundary_bitmap")
+
+
+def exchange_bytes(n_max: int) -> int:
+    return _lib.uellm_exchange_bytes(n_max)
+
+
+def exchange_pack(p: Profile, cfg: Config, totals, record, n_max: int, stream=None):
+    _check(_lib.uellm_exchange_pack(C.byref(p), C.byref(cfg), _ptr(totals), _ptr(record), n_max,
+                                    _stream_handle(stream)), "uellm_exchange_pack")
+
+
+def totals_combine(parts, count: int, stride_bytes: int, out, ws=None, ws_bytes: int = 0, stream=None):
+    _check(_lib.uellm_totals_combine(_ptr(parts), count, stride_bytes, _ptr(out), _ptr(ws), ws_bytes,
+                                     _stream_handle(stream)), "uellm_totals_combine")
+
+
+def exchange_workspace_bytes(n_total: int, world: int) -> int:
+    return _lib.uellm_exchange_workspace_bytes(n_total, world)
+
+
+def exchange_combine(gathered, world: int, n_max: int, query_begin, ws, ws_bytes: int, batch_offsets, num_batches,
+                     totals, stream=None):
+    qb = np.ascontiguousarray(query_begin, np.uint64)
+    if qb.shape != (world + 1,):
+        raise ValueError("query_begin needs world + 1 entries")
+    _check(_lib.uellm_exchange_combine(_ptr(gathered), world, n_max, qb.ctypes.data, _ptr(ws), ws_bytes,
+                                       _ptr(batch_offsets), _ptr(num_batches), _ptr(totals), _stream_handle(stream)),
+           "uellm_exchange_combine")
 
 
 def helr_workspace_bytes(num_devices: int) -> int:

@@ -42,7 +42,9 @@ def test_sm100a_cubin(lib):
 
 
 def test_host_only_calls(lib):
-    assert lib._lib.uellm_abi_version() == 1
+    assert lib._lib.uellm_abi_version() == 2
+    assert lib.exchange_bytes(0) == 144 and lib.exchange_bytes(32) == 144 and lib.exchange_bytes(95) == 144
+    assert lib.exchange_workspace_bytes(1000, 0) == 0 and lib.exchange_workspace_bytes(1000, 4) > 0
     assert lib.status_string(0) == "UELLM_OK" and lib.status_string(2) == "UELLM_ERR_CONTRACT"
     import workloads as W
     cfg = lib.make_config(W.SchedConfig(max_batch=256))
@@ -66,6 +68,11 @@ def test_argument_errors_without_device(lib):
     assert lib._lib.uellm_profile_load(C.byref(q0), C.byref(big), None, 0, None, C.byref(p)) == lib.ERR_UNSUPPORTED
     # schedule on an unloaded profile
     assert lib._lib.uellm_schedule_batches(C.byref(p), C.byref(cfg), None, None, None, None) == lib.ERR_ARG
+    # a9 combine: NULL / inconsistent query ranges are argument errors (checked before any device call)
+    qb = (C.c_uint64 * 3)(0, 10, 5)
+    assert lib._lib.uellm_exchange_combine(None, 2, 10, qb, None, 0, None, None, None, None) == lib.ERR_ARG
+    assert lib._lib.uellm_exchange_pack(C.byref(p), C.byref(cfg), None, None, 0, None) == lib.ERR_ARG
+    assert lib._lib.uellm_totals_combine(None, 1, 128, None, None, 0, None) == lib.ERR_ARG
 
 
 def test_product_does_not_import_oracle():

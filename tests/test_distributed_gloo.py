@@ -1,5 +1,6 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the sharding host logic and of the a9
-allgather: the combined per-rank totals equal the single-process result.  The per-rank compute
+allgather: the per-rank records (header format, tests/xchg_ref.py) gathered in ONE collective give
+the single-process batch boundaries and totals.  The per-rank compute
 is the CPU oracle here (no GPU in this container); on a B200 box the same host path wraps the
 CUDA library (bench.py)."""
 import os
@@ -12,6 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2409_14961_b200 import distributed as D
+from tests import xchg_ref as X
 
 
 def _free_port():
@@ -31,25 +33,19 @@ def _worker(rank, world, port, q):
         import workloads as W
         inp, out, slo, cfg = W.c3(5, n=60_000)
         cfg = cfg.replace(window=7_000)
-        a, z = D.query_range(len(inp), cfg.window, world, rank)
+        qb = D.query_begins(len(inp), cfg.window, world)
+        a, z = qb[rank], qb[rank + 1]
         order, offs, m, cost = oracle.schedule(inp[a:z], out[a:z], slo[a:z], cfg)
-        _, tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], cfg, order, offs)
-        g = D.all_gather_totals(D.pack_totals(tot, "cpu"))
-        comb = D.combine_totals(g)
-        # the a9 buffer proper: [totals | boundary bitmap of this rank's positions], padded to the
-        # largest rank (on the GPU the library writes the bitmap, uellm_boundary_bitmap)
-        ranges = [D.query_range(len(inp), cfg.window, world, r) for r in range(world)]
-        n_max = max(b - a_ for a_, b in ranges)
-        buf = torch.zeros(D.exchange_words(n_max), dtype=torch.int64)
-        buf[:D.GATHER_WORDS] = D.pack_totals(tot, "cpu")
-        bits = np.zeros(32 * D.bitmap_view(buf).numel(), np.uint8)
-        bits[offs.astype(np.int64)] = 1
-        D.bitmap_view(buf).copy_(torch.from_numpy(np.packbits(bits, bitorder="little").view(np.int32)))
-        gx = D.all_gather_exchange(buf)
-        offs_all = D.global_offsets(gx, ranges)
-        comb2 = D.combine_totals(gx[:, :D.GATHER_WORDS])
+        pb, tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], cfg, order, offs)
+        lat = int((pb["size"].astype(object) * pb["completion_us"].astype(object)).sum()) if len(pb) else 0
+        # the a9 record in the header's format (on the GPU the library writes it: uellm_exchange_pack)
+        n_max = max(y - x for x, y in zip(qb[:-1], qb[1:]))
+        rec = torch.from_numpy(X.make_record(tot, lat, offs, z - a, n_max))
+        gathered = torch.zeros(world * rec.numel(), dtype=torch.uint8)
+        dist.all_gather(list(gathered.view(world, -1).unbind(0)), rec)      # ONE collective
+        offs_all, comb = X.combine(gathered.view(world, -1).numpy(), qb)
         if rank == 0:
-            q.put((comb, cost, offs_all, comb2))
+            q.put((comb, offs_all))
     finally:
         dist.destroy_process_group()
 
@@ -81,7 +77,7 @@ def test_allgather_world2_equals_single_process():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    comb, _, offs_all, comb2 = q.get(timeout=300)
+    comb, offs_all = q.get(timeout=300)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -89,21 +85,24 @@ def test_allgather_world2_equals_single_process():
     cfg = cfg.replace(window=7_000)
     order, offs, m, cost = oracle.schedule(inp, out, slo, cfg)
     _, tot = oracle.stats(inp, out, slo, cfg, order, offs)
-    for f in D.TOTAL_FIELDS:
+    for f in X.TOTAL_FIELDS:
         assert comb[f] == tot[f], f
     assert comb["dp_cost"] == cost
     assert np.array_equal(offs_all, offs.astype(np.int64))      # global batch boundaries
-    assert comb2 == comb
     assert comb["mean_latency_s"] == pytest.approx(tot["mean_latency_s"], rel=1e-12)
     assert comb["throughput_tok_s"] == pytest.approx(tot["throughput_tok_s"], rel=1e-12)
 
 
-def test_pack_roundtrip():
-    tot = {f: (i + 1) * 1234567 for i, f in enumerate(D.TOTAL_FIELDS)}
-    tot["dp_cost"] = 2**63 + 5
-    tot["mean_latency_s"] = 3.25
-    tot["throughput_tok_s"] = 1e9 / 3
-    v = D.pack_totals(tot, "cpu").view(1, -1)
-    c = D.combine_totals(v)
-    assert c["dp_cost"] == 2**63 + 5
-    assert c["mean_latency_s"] == 3.25
+def test_record_size_matches_library():
+    """The library's record size (uellm_exchange_bytes, a host function) is the header's layout."""
+    from paper_2409_14961_b200 import uellm as U
+    for n_max in (0, 1, 31, 32, 33, 1000, 12_500_000):
+        assert U.exchange_bytes(n_max) == X.record_bytes(n_max)
+    assert U.TOTALS_BYTES == 128
+
+
+def test_query_begins():
+    qb = D.query_begins(1_000_003, 100_000, 8)
+    assert qb[0] == 0 and qb[-1] == 1_000_003 and len(qb) == 9
+    assert all(x <= y for x, y in zip(qb, qb[1:]))
+    assert D.query_begins(5, 10, 4) == [0, 0, 0, 0, 5]          # one window, three empty ranks

@@ -47,6 +47,9 @@ def assert_parity(inp, out, slo, cfg, stats=True, nthreads=8):
             assert r["totals"][f] == pytest.approx(tot[f], rel=REL, abs=0), f
         if cfg.mode == W.MODE_SEG_DP:
             assert r["totals"]["dp_cost"] == o_cost
+        # the exact latency numerator the totals carry (sum over batches of b * completion_us)
+        want = int((pb["size"].astype(object) * pb["completion_us"].astype(object)).sum()) if len(pb) else 0
+        assert r["totals"]["latency_sum_us"] == want and r["totals"]["overflow"] == 0
     return r
 
 
@@ -238,7 +241,18 @@ def _window_sample_parity(inp, out, slo, cfg, r, windows):
         assert np.array_equal(sel, o_offs.astype(np.int64) + a), w
         pb = r["per_batch"]
         mine = pb[(pb["start"] >= a) & (pb["start"] < z)]
-        _, o_tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], c, o_order, o_offs)
+        o_pb, o_tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], c, o_order, o_offs)
+        # every per-batch record element by element; the window-local oracle run differs only in
+        # the position base (start + a) and the window index (+ w); completion_us restarts at
+        # every window in both (R17)
+        assert len(mine) == len(o_pb), w
+        for f in INT_FIELDS:
+            want = o_pb[f].astype(np.int64)
+            if f == "start":
+                want = want + a
+            if f == "window":
+                want = want + w
+            assert np.array_equal(mine[f].astype(np.int64), want), (w, f)
         assert int(mine["est_us"].sum()) == o_tot["makespan_us"]
         assert int((mine["est_us"] + cfg.lambda_us * mine["viol_alone"].astype(np.uint64)).sum()) == o_cost
 
@@ -291,42 +305,55 @@ def test_wide_values_take_generic_path():
     assert_parity(inp, out, slo, cfg.replace(kv_cap_bytes=0, lambda_us=0))
 
 
-def test_sharded_ranks_equal_single_run():
-    """T5 on one GPU: the window blocks of 4 emulated ranks, scheduled separately, give exactly
-    the single-run batches and (combined via the a9 packing) the single-run totals."""
+@pytest.mark.parametrize("world,n,window", [(4, 400_000, 30_000), (3, 100_003, 7_000), (8, 50_000, 20_000)])
+def test_sharded_ranks_equal_single_run(world, n, window):
+    """T5 on one GPU: the window blocks of `world` emulated ranks, each scheduled alone and packed by
+    uellm_exchange_pack, combined by uellm_exchange_combine after the (emulated) allgather, give
+    exactly the single-run batch_offsets and totals -- and agree with the test-side reference of
+    the record format (tests/xchg_ref.py).  (8, 50_000, 20_000): ranks with empty ranges."""
     from paper_2409_14961_b200 import distributed as D
-    inp, out, slo, cfg = W.c3(12, n=400_000)
-    cfg = cfg.replace(window=30_000)
     from paper_2409_14961_b200 import uellm as U
     from paper_2409_14961_b200.scheduler import GpuScheduler
+    from tests import xchg_ref as X
+    inp, out, slo, cfg = W.c3(12, n=n)
+    cfg = cfg.replace(window=window)
     full = gpu_run(inp, out, slo, cfg)
-    rows, offs_all, bufs = [], [], []
-    ranges = [D.query_range(len(inp), cfg.window, 4, r) for r in range(4)]
-    n_max = max(z - a for a, z in ranges)
-    for r in range(4):
-        a, z = ranges[r]
-        part = gpu_run(inp[a:z], out[a:z], slo[a:z], cfg)
-        # the a9 buffer as bench.py builds it: totals + the library's boundary bitmap
+    xs = [D.Exchange(n, window, world, r, "cuda:0") for r in range(world)]
+    recs = []
+    for r in range(world):
+        a, z = xs[r].q0, xs[r].q1
         g = GpuScheduler(z - a, cfg, device="cuda:0")
         g.run(torch.from_numpy(inp[a:z].view(np.int32)).cuda(), torch.from_numpy(out[a:z].view(np.int32)).cuda(),
               torch.from_numpy(slo[a:z]).cuda())
-        buf = torch.zeros(D.exchange_words(n_max), dtype=torch.int64, device="cuda:0")
-        U.boundary_bitmap(g.profile, g.cfg, D.bitmap_view(buf))
-        buf[:13] = g.totals.view(torch.int64)[:13]
-        bufs.append(buf)
-        rows.append(D.pack_totals(part["totals"], "cpu"))
-        offs_all.append(part["offsets"][:-1].astype(np.int64) + a)
-        assert np.array_equal(part["order"].astype(np.int64) + a, full["order"][a:z].astype(np.int64))
-    offs = np.concatenate(offs_all + [np.array([len(inp)])])
-    assert np.array_equal(offs, full["offsets"].astype(np.int64))
-    comb = D.combine_totals(torch.stack(rows))
-    for f in D.TOTAL_FIELDS:
-        assert comb[f] == full["totals"][f], f
-    gathered = torch.stack(bufs)
-    assert np.array_equal(D.global_offsets(gathered, ranges), full["offsets"].astype(np.int64))
-    comb2 = D.combine_totals(gathered[:, :D.GATHER_WORDS])
-    for f in D.TOTAL_FIELDS:
-        assert comb2[f] == full["totals"][f], f
+        xs[r].pack(g.profile, g.cfg, g.totals)
+        recs.append(xs[r].record.clone())
+        if z > a:
+            part = g.results()
+            assert np.array_equal(part["order"].astype(np.int64) + a, full["order"][a:z].astype(np.int64))
+    gathered = torch.cat(recs)                          # what all_gather_into_tensor delivers
+    x0 = xs[0]
+    x0.gathered.copy_(gathered)
+    x0.combine()
+    res = x0.results()
+    assert res["m"] == full["m"]
+    assert np.array_equal(res["offsets"], full["offsets"])
+    for f in TOT_INT:
+        assert res["totals"][f] == full["totals"][f], f
+    assert res["totals"]["latency_sum_us"] == full["totals"]["latency_sum_us"]
+    assert res["totals"]["overflow"] == 0
+    for f in ("mean_latency_s", "throughput_tok_s"):
+        assert res["totals"][f] == pytest.approx(full["totals"][f], rel=1e-15), f
+    # the records are in the header's format: the independent numpy reading agrees
+    offs_ref, tot_ref = X.combine(gathered.view(world, -1).cpu().numpy(), x0.qb)
+    assert np.array_equal(offs_ref, full["offsets"].astype(np.int64))
+    for f in X.TOTAL_FIELDS:
+        assert tot_ref[f] == full["totals"][f], f
+    # host totals variant of the combine (synchronising)
+    tot_h = U.Totals()
+    import ctypes
+    U.exchange_combine(x0.gathered, world, x0.n_max, x0.qb, x0.ws, x0.ws_bytes, x0.offsets, x0.num_batches,
+                       ctypes.addressof(tot_h))
+    assert tot_h.dp_cost == full["totals"]["dp_cost"]
 
 
 def test_sort_paths_compressed_and_generic():
@@ -427,31 +454,39 @@ def test_sort_window_groups(uniform_slo, monkeypatch):
     assert_parity(inp, out, slo, cfg.replace(window=30_000))
 
 
-def test_bench_two_ranks_one_gpu_gloo(tmp_path):
-    """bench.py's N > 1 path (a9 exchange of totals + boundary bitmaps, max-over-ranks timing) with
-    two ranks sharing the one GPU over gloo: the job totals are the two ranks' oracle totals."""
+def _bench_line(root, args, world=1, port=29517):
     import json
     import os
     import subprocess
     import sys
+    if world > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py")]
+    else:
+        cmd = [sys.executable, os.path.join(root, "bench.py")]
+    r = subprocess.run(cmd + args, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_ranks_one_gpu_gloo_equal_single_rank(world):
+    """bench.py's N > 1 path (one job sharded by window blocks, a9 exchange through the library,
+    max-over-ranks timing) with `world` ranks sharing the one GPU over gloo: the rebuilt job's
+    batch_offsets + totals hash equals the single-rank run's, and the job cost is the oracle's."""
+    import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     n = 2_000_000
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "1", "--queries", str(n), "--no-cpu-baseline", "--no-sim",
-           "--dist-backend", "gloo"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
-    assert r.returncode == 0, r.stderr[-3000:]
-    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["e2e"] is not None
-    jt = line["job_totals"]
-    want_cost = want_b = 0
-    for rank in range(2):
-        inp, out, slo, cfg = W.c4(seed=rank, n=n)
-        o = oracle.schedule(inp, out, slo, cfg, nthreads=8)
-        want_cost += o[3]
-        want_b += o[2]
-    assert jt["n"] == 2 * n and jt["dp_cost"] == want_cost and jt["batches"] == want_b
+    common = ["--steps", "2", "--warmup", "1", "--queries", str(n), "--no-cpu-baseline", "--no-sim", "--no-configs"]
+    one = _bench_line(root, ["--gpus", "1"] + common)
+    many = _bench_line(root, ["--gpus", str(world), "--dist-backend", "gloo"] + common, world=world, port=29517 + world)
+    assert many["n_gpus"] == world and many["scaling"] == "strong" and many["e2e"] is not None
+    assert many["config"]["queries"] == n and many["weak_scaling"] is not None
+    assert many["job_offsets_sha256"] == one["job_offsets_sha256"]
+    assert many["dp_cost"] == one["dp_cost"] and many["batches"] == one["batches"]
+    inp, out, slo, cfg = W.c4(seed=0, n=n)
+    o = oracle.schedule(inp, out, slo, cfg, nthreads=8)
+    assert one["dp_cost"] == o[3] and one["batches"] == o[2]
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])

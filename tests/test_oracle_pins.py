@@ -96,14 +96,14 @@ def test_stats_completion_and_violations():
     # sequential execution; completion = prefix sum of est; viol_seq >= viol_alone
     cfg = W.SchedConfig(mode=W.MODE_FIFO, max_batch=2, t_batch_us=10, t_iter_us=1,
                         t_tok_us=1, t_prefill_us=1)
-    inp, out, slo = [1, 2, 3], [4, 5, 6], [25e-6, 60e-6, 1.0]
+    inp, out, slo = [1, 2, 3], [4, 5, 6], [25e-6, 60e-6, 40e-6]
     pb, tot = _stats_of(inp, out, slo, [[0, 1], [2]], cfg)
     e0 = 10 + 1 * 5 + 1 * 2 * 5 + 1 * 2 * 2       # 29
     e1 = 10 + 6 + 6 + 3                           # 25
     assert list(pb["est_us"]) == [e0, e1]
     assert list(pb["completion_us"]) == [e0, e0 + e1]
-    assert list(pb["viol_alone"]) == [1, 0]       # 25 < 29 ; 60 >= 29
-    assert list(pb["viol_seq"]) == [1, 0]
+    assert list(pb["viol_alone"]) == [1, 0]       # 25 < 29, 60 >= 29 ; 40 >= 25
+    assert list(pb["viol_seq"]) == [1, 1]         # completion 29 ; 40 < 54 = 29 + 25
     assert tot["makespan_us"] == e0 + e1
     assert tot["mean_latency_s"] == pytest.approx((2 * e0 + (e0 + e1)) / 3 * 1e-6, rel=1e-15)
     assert tot["throughput_tok_s"] == pytest.approx((2 * 5 + 6) / ((e0 + e1) * 1e-6), rel=1e-15)
@@ -289,6 +289,77 @@ def test_alg1_length_example():
     # Eq. 2's additive form (R2): T_o = (25+30)*2 = 110 > 50 -> split
     _, b = _alg1([1, 1], [30, 25], [5.0, 6.0], w1=0.0, w2=1.0, threshold=50.0, eq2_additive=1)
     assert b == [[0], [1]]
+
+
+@pytest.mark.parametrize("l1,expect", [(1.0, [[0, 1], [2]]), (2.0, [[0], [1], [2]]),
+                                       (0.25, [[0, 1, 2]])])
+def test_alg1_l1_scale(l1, expect):
+    """Alg. 1 line 6: T_l = (q.SLO + L_CM) x (len(batch_c) + 1) x L1, worked by hand.
+    w1 = 1, w2 = 0, Threshold = 100, (SLO, length) = (10, 30), (20, 30), (90, 30); the line-20 cap
+    is floor(100 / CM) = floor(100 / 30) = 3 (R5):
+      L1 = 1   : x=1 (20+10)*2*1 = 60 <= 100 admit; x=2 (90+20)*3*1 = 330 > 100 split
+      L1 = 2   : x=1 (20+10)*2*2 = 120 > 100 split; x=2 (90+20)*2*2 = 440 > 100 split
+      L1 = 0.25: x=1 15 <= 100 admit; x=2 (90+20)*3*0.25 = 82.5 <= 100 admit, |batch| = 3 = cap
+    A misplaced L1 ((q.SLO*L1 + L_CM)*2 = 100 at L1 = 2 admits) or a dropped L1 fails."""
+    _, b = _alg1([1, 1, 1], [30, 30, 30], [10.0, 20.0, 90.0], w1=1.0, w2=0.0, l1=l1,
+                 threshold=100.0, max_batch=8)
+    assert b == expect
+
+
+@pytest.mark.parametrize("l2,lens,thr,expect", [
+    (2.0, [10, 13, 13], 10.0, [[0], [1, 2]]),      # x=1: (13-10)*2*2 = 12 > 10 split
+    (1.0, [10, 13, 13], 10.0, [[0, 1, 2]]),        # x=1: 6 <= 10; x=2: (13-13)*3 = 0
+    (0.5, [10, 13, 13], 2.0, [[0], [1, 2]]),       # x=1: 3*2*0.5 = 3 > 2 split
+    (0.1, [10, 10, 13], 0.9, [[0, 1, 2]]),         # x=2: ((13-10)*3)*0.1 = 0.9 <= 0.9 (binary64)
+])
+def test_alg1_l2_scale(l2, lens, thr, expect):
+    """Alg. 1 line 7: T_o = (q.length - O_CM) x (len(batch_c) + 1) x L2, evaluated left to
+    right as printed.  w1 = 0, w2 = 1 (SLO-DBS weights), SLO 0.1 s for all, so CM = 0.1 and
+    the line-20 cap is floor(thr / 0.1) >= 3.  The last case pins the printed evaluation order:
+    in binary64 (3*3)*0.1 == 0.9 but (3*0.1)*3 == 0.9000000000000001 > 0.9, so applying L2 before
+    the (len(batch_c) + 1) factor splits the batch."""
+    assert (3 * 3) * 0.1 == 0.9 and (3 * 0.1) * 3 > 0.9        # the arithmetic the case relies on
+    _, b = _alg1([1, 1, 1], lens, [0.1, 0.1, 0.1], w1=0.0, w2=1.0, l2=l2, threshold=thr, max_batch=8)
+    assert b == expect
+
+
+@pytest.mark.parametrize("inp,cap,expect", [
+    ([10, 10, 10, 10, 10], 160, [[0, 1], [2, 3], [4]]),   # kv(b) = 4*b*1*1*(10+10) = 80 b <= 160
+    ([10, 10, 10, 10, 10], 159, [[0], [1], [2], [3], [4]]),
+    ([10, 10, 10, 10, 10], 40, [[0], [1], [2], [3], [4]]),  # a query alone over the cap (R10)
+    ([10, 50, 10], 400, [[0], [1], [2]]),                 # {0,1}: 4*2*(50+10) = 480 > 400;
+                                                          # {1,2}: 4*2*(max(50,10)+10) = 480 > 400
+    ([10, 50, 10], 480, [[0, 1], [2]]),                   # {0,1}: 480 <= 480 admit;
+                                                          # {0,1,2}: 4*3*(50+10) = 720 > 480
+])
+def test_alg1_kv_cap_admission(inp, cap, expect):
+    """R18: Alg. 1 has no memory test; a non-empty batch admits q only if its KV bytes
+    4*b*l*h*(s + O) (s = max input, O = max output incl. q) stay <= the reserve.
+    l = h = 1, kv_bytes_per_elem = 4, every output 10, SLO 1 s, w1 = 0, w2 = 1, threshold 1000
+    (line-20 cap min(floor(1000/1), W = 8) = 8, T_o = 0): only the KV test splits."""
+    _, b = _alg1(inp, [10] * len(inp), [1.0] * len(inp), w1=0.0, w2=1.0, threshold=1000.0,
+                 max_batch=8, kv_bytes_per_elem=4, n_layers=1, hidden=1, kv_cap_bytes=cap)
+    assert b == expect
+
+
+def test_stats_pad_out_kv_over_cap_hand_values():
+    """O7 hand values (S:144-146 extended to the output side and the KV cap):
+    batch {(in 10, out 5), (in 30, out 50)}: pad_out = 2*50 - (5+50) = 45, pad_in = 2*30 - 40 = 20,
+    kv = 4 * 2 * 32 * 4096 * (30 + 50) = 83,886,080 B; over_cap is strict (kv > cap)."""
+    kv = 83_886_080
+    for cap, oc in ((kv, 0), (kv - 1, 1), (0, 0)):
+        cfg = W.SchedConfig(mode=W.MODE_FIFO, max_batch=64, kv_cap_bytes=cap)
+        pb, tot = _stats_of([10, 30], [5, 50], [1.0, 1.0], [[0, 1]], cfg)
+        assert (pb["pad_out"][0], pb["pad_in"][0], pb["kv_bytes"][0]) == (45, 20, kv)
+        assert pb["over_cap"][0] == oc and tot["over_cap"] == oc
+        assert (tot["pad_out"], tot["kv_bytes_max"]) == (45, kv)
+    # two singletons: kv = 4*32*4096*30 = 15,728,640 and 4*32*4096*80 = 41,943,040 -> max; a single
+    # query over the cap is admitted but counted (R10)
+    cfg = W.SchedConfig(mode=W.MODE_FIFO, max_batch=64, kv_cap_bytes=20_000_000)
+    pb, tot = _stats_of([10, 30], [20, 50], [1.0, 1.0], [[0], [1]], cfg)
+    assert list(pb["kv_bytes"]) == [15_728_640, 41_943_040] and tot["kv_bytes_max"] == 41_943_040
+    assert list(pb["over_cap"]) == [0, 1] and tot["over_cap"] == 1
+    assert list(pb["pad_out"]) == [0, 0] and tot["pad_out"] == 0
 
 
 def test_alg1_identical_requests_dynamic_cap():
