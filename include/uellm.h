@@ -168,6 +168,8 @@ typedef struct {
     uint64_t stats_launches;        /* kernels launched by the last uellm_batch_stats               */
     uint64_t sort_key_bits;         /* sort key width: bits(rank) + bits(max_out) when the distinct
                                        SLO values (<= 1024) were rank-compressed, else 64          */
+    uint64_t dp_filled_positions;   /* SEG-DP: boundaries written by the periodic fill of uniform
+                                       stretches (identical records; all passes)                   */
 } uellm_diagnostics;
 
 /* Optional per-stage timing.  Stage boundaries at which uellm_schedule_batches /

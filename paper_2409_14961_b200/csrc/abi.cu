@@ -883,6 +883,7 @@ uellm_status uellm_get_diagnostics(const uellm_profile *p, uellm_diagnostics *ou
     out->sort_passes = hd.sort_passes; out->dp_cost = cost;
     out->dp_candidate_evals = hd.dp_evals; out->sched_launches = hd.sched_launches;
     out->stats_launches = hd.stats_launches; out->sort_key_bits = hd.sort_key_bits;
+    out->dp_filled_positions = hd.dp_filled;
     return UELLM_OK;
 }
 

@@ -70,12 +70,14 @@ struct TileRec {
     int64_t off_local;       // true C = Cx + off_local for boundaries > conv_pos   (cascade)
     int64_t off_fix;         // true C = CFx + off_fix for boundaries <= fix_end       (cascade)
     uint32_t exitA, exitB;   // traceback: exit of the walk from e / from the true entry
-    uint32_t merged, pad;
+    uint32_t merged;
+    uint32_t uni;            // local run: every record of the tile is the same (periodic fill)
 };
 
 struct Diag {                // device counters, see uellm_diagnostics
     unsigned long long tiles, tile_len, fixups_unconverged, cascade_reruns, fixup_positions,
-        trace_unmerged, trace_rewalks, sort_passes, dp_evals, sched_launches, stats_launches, sort_key_bits;
+        trace_unmerged, trace_rewalks, sort_passes, dp_evals, sched_launches, stats_launches, sort_key_bits,
+        dp_filled;
 };
 
 // Whole-job totals from partial totals (window groups of the pipelined call, ranks of the a9

@@ -96,6 +96,8 @@ struct DpResult {
     long long delta;
     uint64_t positions;
     uint64_t evals;
+    uint64_t filled;            // boundaries written by the periodic fill of a uniform stretch
+    uint32_t uni;               // local run: every record of the tile equals its first one
 };
 
 // Runs the DP for boundaries j = s+1 .. e on one warp.
@@ -112,7 +114,7 @@ __device__ DpResult dp_warp(const DPParams &P, const WarpSlots &S, uint32_t s, u
     const uint32_t lt = lane_lt();
     const uint32_t W = P.W;
     DpResult R;
-    R.conv = 0; R.conv_pos = e; R.fix_end = e; R.delta = 0; R.positions = 0; R.evals = 0;
+    R.conv = 0; R.conv_pos = e; R.fix_end = e; R.delta = 0; R.positions = 0; R.evals = 0; R.filled = 0;
     uint32_t L;
     uint32_t run_start;
     uint32_t prev_slo;
@@ -302,6 +304,109 @@ struct SlotWriter {            // writes a candidate slot with its derived cost 
 };
 
 // -------------------------------------------------------------------------------------
+// Periodic fill of a uniform stretch (exact, step 8).  Inside a run of
+// identical records (in, out, slo) the cost of a batch [i, j) depends on j - i only, so the
+// recurrence is shift-equivariant: if C[i] = C[i-P] + F for the W boundaries i = j0-W+1 .. j0
+// and the elements [j0-W-P+1, j) are identical, then by induction C[j] = C[j-P] + F and
+// arg[j] = arg[j-P] + P for every later j up to the end of the stretch (each boundary's W
+// candidates and their costs map one to one onto those of j-P, the tie rule is shift-invariant).
+// Identical keys never converge in a fix-up (the optimal batch period, e.g. 42 under a KV cap,
+// is not a divisor of the tile stride), so without this the cascade re-ran such windows
+// sequentially (BJ configs[4], c5).  P is the last batch length (j0 - arg[j0]); any P for which
+// the check passes is valid.  Returns the last boundary written (j0 if the check failed).
+// Reference args for boundaries at or below s come from the source frame's argx when the
+// caller vouches for them (cascade), else from a direct scan of the boundary's W candidates.
+template <bool FIX>
+__device__ __forceinline__ uint32_t periodic_fill(const DPParams &P, const NarrowSlots &S, uint32_t s, uint32_t e,
+                                               const long long *__restrict__ src, bool src_args_ok, uint32_t j0,
+                                               uint32_t kin, uint32_t kout, uint32_t kslo, bool known_uniform)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t W = P.W;
+    const uint32_t lowb = FIX ? s + 1 - 2 * W : s;          // lowest boundary readable through fval
+    long long *const outC = FIX ? P.CFx : P.Cx;
+    const uint32_t *__restrict__ rin = P.rin;
+    const uint32_t *__restrict__ rout = P.rout;
+    const uint32_t *__restrict__ rslo = P.rslo;
+    // C at boundary b in this run's frame (as in dp_warp_blocked)
+    auto fval = [&](uint32_t b) -> long long {
+        if (b > s) return __ldcg(outC + b - 1);
+        if (FIX) return __ldcg(src + b - 1);
+        return 0ll;
+    };
+    const uint32_t Pp = (uint32_t)__ldcg(reinterpret_cast<const unsigned short *>(P.argx) + j0 - 1);
+    if (Pp < 1 || Pp > W || j0 < lowb + W + Pp - 1) return j0;
+    const uint32_t lo1 = j0 + 1 - W - Pp;                // boundaries / elements from lo1 on are read
+    // elements [lo1, j0) identical to the key (known_uniform: the caller knows [lo1, e) is)
+    bool ok = true;
+    if (!known_uniform) {
+        for (uint32_t q = lo1 + lane; q < j0; q += 32)
+            ok &= (__ldg(rin + q) == kin) & (__ldg(rout + q) == kout) & (__ldg(rslo + q) == kslo);
+        if (!__all_sync(0xffffffffu, ok)) return j0;
+    }
+    // C[i] - C[i-P] == F on the W boundaries i = j0-W+1 .. j0
+    const long long F = fval(j0) - fval(j0 - Pp);
+    for (uint32_t i = j0 + 1 - W + lane; i <= j0; i += 32) ok &= (fval(i) - fval(i - Pp)) == F;
+    if (!__all_sync(0xffffffffu, ok)) return j0;
+    // reference boundaries r = j0-P+1 .. j0 (slot r - (j0-P) - 1): C and the distance r - arg[r]
+    const uint32_t rb = j0 - Pp;
+    const unsigned long long cap = P.cap_tok;
+    const unsigned long long T_ = P.t_tok * kout + P.t_pre * kin;
+    const unsigned long long A_ = P.t_batch + P.t_iter * kout;
+    for (uint32_t q = lane; q < Pp; q += 32) {
+        const uint32_t r = rb + 1 + q;
+        uint32_t dist = 0;
+        if (r > s || src_args_ok) dist = (uint32_t)__ldcg(reinterpret_cast<const unsigned short *>(P.argx) + r - 1);
+        S.sl[q] = make_longlong2(fval(r), (long long)dist);
+    }
+    __syncwarp();
+    if (!(rb + 1 > s || src_args_ok)) {
+        // boundaries r <= s with untrusted args: scan the W candidates i = r-W .. r-1 (ascending,
+        // strict '<': the smallest minimising i, R9); the batch [i, r) lies in the stretch
+        for (uint32_t r = rb + 1; r <= min(j0, s); ++r) {
+            unsigned long long best_hi = ~0ull;
+            uint32_t bi = 0xffffffffu;
+            for (uint32_t c = lane; c < W; c += 32) {
+                const uint32_t b = W - c, i = r - b;          // c ascending -> i ascending
+                const bool feas = b == 1 || (unsigned long long)b * ((unsigned long long)kin + kout) <= cap;
+                const unsigned long long est = A_ + (unsigned long long)b * T_;
+                const unsigned long long pen = ((unsigned long long)kslo < est) ? P.lambda * b : 0ull;
+                const unsigned long long tot = (unsigned long long)(fval(i) + (long long)est) + pen;
+                if (feas && tot < best_hi) { best_hi = tot; bi = i; }
+            }
+            const uint32_t h = (uint32_t)(best_hi >> 32);
+            const uint32_t mh = __reduce_min_sync(0xffffffffu, h);
+            const uint32_t lo = (h == mh) ? (uint32_t)best_hi : 0xffffffffu;
+            const uint32_t ml = __reduce_min_sync(0xffffffffu, lo);
+            const uint32_t ii = (h == mh && (uint32_t)best_hi == ml) ? bi : 0xffffffffu;
+            const uint32_t arg = __reduce_min_sync(0xffffffffu, ii);
+            if (lane == 0) S.sl[r - rb - 1].y = (long long)(r - arg);
+        }
+        __syncwarp();
+    }
+    // fill j = j0+1 .. while the element j-1 is identical to the key (and j <= e)
+    uint32_t j1 = j0;
+    for (uint32_t jb = j0; jb < e; jb += 32) {
+        const uint32_t j = jb + lane + 1;
+        const bool in_t = j <= e;
+        const bool uni = in_t && (known_uniform || (__ldg(rin + j - 1) == kin && __ldg(rout + j - 1) == kout &&
+                                                    __ldg(rslo + j - 1) == kslo));
+        const uint32_t bad = __ballot_sync(0xffffffffu, !uni);
+        const uint32_t lim = bad ? jb + (uint32_t)__ffs(bad) - 1 : jb + 32;   // boundaries <= lim
+        if (j <= lim) {
+            const uint32_t k = (j - j0 + Pp - 1) / Pp;   // j - k*P in (j0-P, j0]
+            const longlong2 rv = S.sl[j - k * Pp - rb - 1];
+            outC[j - 1] = rv.x + (long long)k * F;
+            P.argx[j - 1] = (uint16_t)rv.y;
+        }
+        j1 = lim;
+        if (bad) break;
+    }
+    __syncwarp();
+    return min(j1, e);
+}
+
+// -------------------------------------------------------------------------------------
 // Blocked fast path (narrow arithmetic).  Positions are processed in blocks of 32 boundaries
 // (lane l <-> boundary j0+l+1, element j0+l):
 //  1. external candidates (C known before the block, i <= j0): every lane evaluates every live
@@ -317,7 +422,8 @@ struct SlotWriter {            // writes a candidate slot with its derived cost 
 // LAMK: 0 = no SLO penalty, 1 = lambda < 2^32 (32x32 -> 64-bit product), 2 = 64-bit lambda.
 template <bool FIX, int LAMK, bool SPLIT>
 __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uint32_t s, uint32_t e,
-                                    const long long *__restrict__ src, uint32_t stop_min)
+                                    const long long *__restrict__ src, uint32_t stop_min, bool src_args_ok,
+                                    bool entry_uni)
 {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t lt = lane_lt();
@@ -343,22 +449,35 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     const uint32_t *__restrict__ rout = P.rout;
     const uint32_t *__restrict__ rslo = P.rslo;
     DpResult R;
-    R.conv = 0; R.conv_pos = e; R.fix_end = e; R.delta = 0; R.positions = 0; R.evals = 0;
+    R.conv = 0; R.conv_pos = e; R.fix_end = e; R.delta = 0; R.positions = 0; R.evals = 0; R.filled = 0; R.uni = 0;
+    if (FIX && entry_uni) {
+        // this tile and its predecessor hold one identical record: if the entry state is already
+        // periodic the whole tile is a periodic fill (no candidate list at all)
+        const uint32_t j1 = periodic_fill<FIX>(P, S, s, e, src, src_args_ok, s, __ldg(P.rin + s), __ldg(P.rout + s),
+                                               __ldg(P.rslo + s), true);
+        if (j1 >= e) { R.positions = R.filled = e - s; return R; }
+    }
     uint32_t L, run_start, prev_slo;
     long long d_run = 0;
     uint32_t run = 0;
-    if (!FIX) {
-        if (lane == 0) SW.put(S, 0, 0, s, 0, 0);
-        L = 1;
-        run_start = s;
-        prev_slo = __ldg(rslo + s);
-    } else {
-        const uint32_t i0 = s - W + 1;
+    long long *const outC = FIX ? P.CFx : P.Cx;
+    // C at boundary b in this run's frame: this run's own output above s; at or below s the source
+    // frame (fix-up) or the local start C[s] = 0 (local run).  Boundary b is stored at index b-1.
+    auto fval = [&](uint32_t b) -> long long {
+        if (b > s) return __ldcg(outC + b - 1);
+        if (FIX) return __ldcg(src + b - 1);
+        return 0ll;
+    };
+    // The W candidates i = jb-W+1 .. jb (maxima over elements [i, jb) by suffix max, C from the
+    // frame) -- the fix-up's initial list, and the list after a periodic fill.  Returns the run
+    // start (largest SLO change position in [jb-W+1, jb)).
+    auto init_window = [&](uint32_t jb) -> uint32_t {
+        const uint32_t i0 = jb - W + 1;
         uint32_t cmo = 0, cmi = 0, rs = i0;
         for (uint32_t r = 0; r * 32 < W; ++r) {
             const uint32_t off = r * 32 + lane + 1;
             const bool valid = off <= W - 1;
-            const uint32_t p = s - off;
+            const uint32_t p = jb - off;
             uint32_t vo = valid ? __ldg(rout + p) : 0, vi = valid ? __ldg(rin + p) : 0;
             const uint32_t vs = valid ? __ldg(rslo + p) : 0;
             const uint32_t vsp = (valid && p > i0) ? __ldg(rslo + p - 1) : vs;
@@ -369,13 +488,21 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if ((int)lane >= d) { vo = max(vo, to); vi = max(vi, ti); }
             }
             vo = max(vo, cmo); vi = max(vi, cmi);
-            if (valid) SW.put(S, p - i0, __ldcg(src + p - 1), p, vo, vi);
+            if (valid) SW.put(S, p - i0, fval(p), p, vo, vi);
             cmo = __shfl_sync(0xffffffffu, vo, 31);
             cmi = __shfl_sync(0xffffffffu, vi, 31);
         }
-        if (lane == 0) SW.put(S, W - 1, __ldcg(src + s - 1), s, 0, 0);
+        if (lane == 0) SW.put(S, W - 1, fval(jb), jb, 0, 0);
+        return __reduce_max_sync(0xffffffffu, rs);
+    };
+    if (!FIX) {
+        if (lane == 0) SW.put(S, 0, 0, s, 0, 0);
+        L = 1;
+        run_start = s;
+        prev_slo = __ldg(rslo + s);
+    } else {
+        run_start = init_window(s);
         L = W;
-        run_start = __reduce_max_sync(0xffffffffu, rs);
         prev_slo = __ldg(rslo + s - 1);
         d_run = __ldcg(src + s - 1);  // local C at boundary s is 0
         run = 1;
@@ -450,15 +577,44 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         L = wr;
     };
     if (FIX) prune(L, L, 0, 0, s, false, 0u);   // the W fix-up candidates, pruned before the first block
+
     uint32_t evals = 0;
     bool stop = false;
     uint32_t done = s;
+    uint64_t filled = 0;
+    // local runs: the tile's first record is the uniform key; blocks equal to it may start a fill
+    uint32_t next_try = s + W + 1;                           // earliest block of a fill attempt
+    uint32_t kin = 0, kout = 0, kslo = 0;
+    bool tile_uni = !FIX;
+    if (!FIX) { kin = __ldg(rin + s); kout = __ldg(rout + s); kslo = prev_slo; }
     for (uint32_t j0 = s; j0 < e && !stop; j0 += 32) {
         const uint32_t B = min(32u, e - j0);
         const bool vl = lane < B;
         const uint32_t x = j0 + lane, jl = x + 1;
         const uint32_t in_l = vl ? __ldg(rin + x) : 0, out_l = vl ? __ldg(rout + x) : 0;
         const uint32_t slo_l = vl ? __ldg(rslo + x) : 0;
+        if (!FIX && tile_uni) {
+            tile_uni = __all_sync(0xffffffffu, !vl || (in_l == kin && out_l == kout && slo_l == kslo));
+            if (tile_uni && B == 32 && j0 >= next_try) {
+                const uint32_t j1 = periodic_fill<FIX>(P, S, s, e, src, src_args_ok, j0, kin, kout, kslo, false);
+                next_try = j0 + 96;                            // (a failed check is retried later)
+                if (j1 > j0) {
+                    filled += j1 - j0;
+                    done = j1;
+                    if (j1 >= e) break;
+                    // continue the DP at boundary j1 with its W candidates (the fill passed them)
+                    run_start = init_window(j1);
+                    L = W;
+                    prev_slo = kslo;
+                    __syncwarp();
+                    prune(L, L, 0, 0, j1, false, 0u);
+                    if (FIX) { run = 0; d_run = 0; }           // convergence counts restart
+                    next_try = j1 + 96;
+                    j0 = j1 - 32;                              // (the loop adds 32)
+                    continue;
+                }
+            }
+        }
         long long cl_l = 0;
         if (FIX) cl_l = vl ? P.Cx[x] : 0;
         // block prefix maxima of the elements j0..j0+lane and run starts
@@ -774,6 +930,8 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     }
     R.positions = done - s;
     R.evals = evals;
+    R.filled = filled;
+    R.uni = tile_uni && done >= e ? 1u : 0u;
     if (!R.conv) { R.conv_pos = e; R.fix_end = e; }
     return R;
 }
@@ -798,26 +956,43 @@ static __host__ __device__ __forceinline__ uint32_t warp_smem_bytes(const DPPara
     return P.narrow ? P.cap_slots * 16 + kRmqBytes : P.cap_slots * 20;
 }
 
-template <bool FIX>
+// Variant V of the SEG-DP kernels, fixed on the host (one instantiation per kernel keeps the code
+// the SMs fetch small: with every variant behind a runtime switch the kernel was 60 K SASS
+// instructions and 10 % of the warp samples were "no instruction"):
+//   V = 0: generic 64-bit path;  V = 1 + LK + 3 * SPLIT: narrow blocked path (LK: lambda kind).
+template <bool FIX, int V>
 __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, uint32_t e,
-                           const long long *src, uint32_t stop_min)
+                           const long long *src, uint32_t stop_min, bool src_args_ok, bool entry_uni = false)
 {
-    if (P.narrow) {
+    if constexpr (V == 0) {
+        DpResult R = dp_warp<FIX>(P, slots_for(smem, P.cap_slots, warp), s, e, src, stop_min);
+        R.filled = 0; R.uni = 0;
+        return R;
+    } else {
+        constexpr int LK = (V - 1) % 3;
+        constexpr bool SPLIT = (V - 1) / 3 != 0;
         char *p = smem + (size_t)warp * warp_smem_bytes(P);
         NarrowSlots S;
         S.sl = (longlong2 *)p;
         S.tri = (uint32_t *)(p + (size_t)P.cap_slots * 16);
-        const int lk = P.lambda == 0 ? 0 : (P.lambda < (1ull << 32) ? 1 : 2);
-        if (P.split) {
-            if (lk == 0) return dp_warp_blocked<FIX, 0, true>(P, S, s, e, src, stop_min);
-            if (lk == 1) return dp_warp_blocked<FIX, 1, true>(P, S, s, e, src, stop_min);
-            return dp_warp_blocked<FIX, 2, true>(P, S, s, e, src, stop_min);
-        }
-        if (lk == 0) return dp_warp_blocked<FIX, 0, false>(P, S, s, e, src, stop_min);
-        if (lk == 1) return dp_warp_blocked<FIX, 1, false>(P, S, s, e, src, stop_min);
-        return dp_warp_blocked<FIX, 2, false>(P, S, s, e, src, stop_min);
+        return dp_warp_blocked<FIX, LK, SPLIT>(P, S, s, e, src, stop_min, src_args_ok, entry_uni);
     }
-    return dp_warp<FIX>(P, slots_for(smem, P.cap_slots, warp), s, e, src, stop_min);
+}
+
+static int dp_variant(const DPParams &P)
+{
+    if (!P.narrow) return 0;
+    const int lk = P.lambda == 0 ? 0 : (P.lambda < (1ull << 32) ? 1 : 2);
+    return 1 + lk + 3 * (P.split ? 1 : 0);
+}
+
+// Tile t (> first of its window) and its predecessor each hold one repeated record and the two
+// records agree: [s_{t-1}, e_t) is one uniform stretch (enables the fix-up's entry fill).
+__device__ __forceinline__ bool entry_uniform(const DPParams &P, uint64_t t, uint32_t s)
+{
+    const TileRec &a = P.tiles[t], &b = P.tiles[t - 1];
+    return a.uni && b.uni && __ldg(P.rin + s - 1) == __ldg(P.rin + s) && __ldg(P.rout + s - 1) == __ldg(P.rout + s) &&
+           __ldg(P.rslo + s - 1) == __ldg(P.rslo + s);
 }
 
 // Local run and fix-up fused in one persistent kernel.  Warps first claim local runs in tile
@@ -830,6 +1005,7 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
 #ifndef UELLM_DP_MINB
 #define UELLM_DP_MINB 3     // 78 registers, no spills, 24 warps per SM (DP 6.53 vs 6.57 ms at 4)
 #endif
+template <int V>
 __global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_tiles(DPParams P, uint64_t ntiles)
 {
     extern __shared__ __align__(16) char smem[];
@@ -851,12 +1027,14 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_tiles
             if (lane == 0) st_release(P.tflags + t, 1u);
             continue;
         }
-        DpResult R = dp_run<false>(P, smem, warp, s, e, nullptr, 0);
+        DpResult R = dp_run<false, V>(P, smem, warp, s, e, nullptr, 0, false);
         evals += R.evals;
+        if (lane == 0 && R.filled) atomicAdd(&P.diag->dp_filled, (unsigned long long)R.filled);
         if (lane == 0) {
             TileRec r = {};
             r.s = s; r.e = e; r.valid = 1;
             r.conv = (k == 0); r.conv_pos = s; r.fix_end = s;
+            r.uni = R.uni;
             P.tiles[t] = r;
         }
         __syncwarp();
@@ -878,8 +1056,10 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_tiles
         }
         __syncwarp();
         __threadfence();
-        DpResult F = dp_run<true>(P, smem, warp, s, e, P.Cx, 0);
+        const bool eu = entry_uniform(P, t, s);
+        DpResult F = dp_run<true, V>(P, smem, warp, s, e, P.Cx, 0, false, eu);
         evals += F.evals;
+        if (lane == 0 && F.filled) atomicAdd(&P.diag->dp_filled, (unsigned long long)F.filled);
         if (lane == 0) {
             TileRec &r = P.tiles[t];
             r.conv = F.conv; r.conv_pos = F.conv_pos; r.fix_end = F.fix_end; r.delta = F.delta;
@@ -892,6 +1072,7 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_tiles
 
 // One warp per window: resolve tiles whose predecessor did not converge, compute the frame
 // offsets of every tile and the window's optimal cost C[w1].
+template <int V>
 __global__ void k_dp_cascade(DPParams P)
 {
     extern __shared__ __align__(16) char smem[];
@@ -944,12 +1125,13 @@ __global__ void k_dp_cascade(DPParams P)
     for (uint32_t k = 1; k < K; ++k) {
         TileRec r = P.tiles[t0 + k];
         if (!tail_local) {
-            DpResult R = dp_run<true>(P, smem, 0, r.s, r.e, P.CFx, r.fix_end);
+            DpResult R = dp_run<true, V>(P, smem, 0, r.s, r.e, P.CFx, r.fix_end, true, entry_uniform(P, t0 + k, r.s));
             r.conv = R.conv; r.conv_pos = R.conv_pos; r.fix_end = max(R.fix_end, r.fix_end); r.delta = R.delta;
             if (lane == 0) {
                 atomicAdd(&P.diag->cascade_reruns, 1ull);
                 atomicAdd(&P.diag->fixup_positions, (unsigned long long)R.positions);
                 atomicAdd(&P.diag->dp_evals, (unsigned long long)R.evals);
+                if (R.filled) atomicAdd(&P.diag->dp_filled, (unsigned long long)R.filled);
             }
         }
         r.off_fix = tail_off;
@@ -974,34 +1156,48 @@ static uint32_t warps_per_cta(uint32_t per)
     return wpc;
 }
 
-cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void *const ev[3], int *launches)
+template <int V>
+static cudaError_t launch_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void *const ev[3], int *launches)
 {
-    *launches = 0;
-    if (P.n == 0 || ntiles == 0) return cudaSuccess;
     const uint32_t per = warp_smem_bytes(P);
     const uint32_t wpc = warps_per_cta(per);
     const size_t smem = (size_t)wpc * per;
     const size_t smem1 = (size_t)per;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_dp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_dp_cascade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1))) return e;
+    if ((e = cudaFuncSetAttribute(k_dp_tiles<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_dp_cascade<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1))) return e;
     int dev = 0, nsm = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dp_tiles, (int)(wpc * 32), smem))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dp_tiles<V>, (int)(wpc * 32), smem))) return e;
     if (per_sm < 1) per_sm = 1;
     const uint64_t want = ceil_div(ntiles, wpc);
     const uint64_t cap = (uint64_t)nsm * (uint64_t)per_sm;
     const unsigned blocks = (unsigned)(want < cap ? want : cap);
     if ((e = cudaMemsetAsync(P.tflags, 0, 4 * (ntiles + 2), st))) return e;
-    k_dp_tiles<<<blocks, wpc * 32, smem, st>>>(P, ntiles);
+    k_dp_tiles<V><<<blocks, wpc * 32, smem, st>>>(P, ntiles);
     ++*launches;
     if (ev[0]) cudaEventRecord((cudaEvent_t)ev[0], st);
     if (ev[1]) cudaEventRecord((cudaEvent_t)ev[1], st);
-    k_dp_cascade<<<P.nwin, 32, smem1, st>>>(P);
+    k_dp_cascade<V><<<P.nwin, 32, smem1, st>>>(P);
     ++*launches;
     if (ev[2]) cudaEventRecord((cudaEvent_t)ev[2], st);
     return cudaGetLastError();
+}
+
+cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void *const ev[3], int *launches)
+{
+    *launches = 0;
+    if (P.n == 0 || ntiles == 0) return cudaSuccess;
+    switch (dp_variant(P)) {
+    case 0: return launch_segdp<0>(P, ntiles, st, ev, launches);
+    case 1: return launch_segdp<1>(P, ntiles, st, ev, launches);
+    case 2: return launch_segdp<2>(P, ntiles, st, ev, launches);
+    case 3: return launch_segdp<3>(P, ntiles, st, ev, launches);
+    case 4: return launch_segdp<4>(P, ntiles, st, ev, launches);
+    case 5: return launch_segdp<5>(P, ntiles, st, ev, launches);
+    default: return launch_segdp<6>(P, ntiles, st, ev, launches);
+    }
 }
 
 }  // namespace uellm

@@ -105,7 +105,8 @@ class Diagnostics(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("tiles", "tile_len", "fixups_unconverged", "cascade_reruns",
                                           "fixup_positions", "trace_unmerged", "trace_rewalks",
                                           "sort_passes", "dp_cost", "dp_candidate_evals",
-                                          "sched_launches", "stats_launches", "sort_key_bits")]
+                                          "sched_launches", "stats_launches", "sort_key_bits",
+                                          "dp_filled_positions")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

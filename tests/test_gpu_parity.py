@@ -106,6 +106,48 @@ def test_identical_keys_tiles():
     assert_parity(inp, out, slo, cfg.replace(kv_cap_bytes=0, dp_tile=768))
 
 
+@pytest.mark.parametrize("case", ["cap42", "windows", "viol_mid", "all_viol", "w64_nocap", "tiny_tiles",
+                                  "split", "lam0", "w512"])
+def test_uniform_runs_periodic_fill(case):
+    """Runs of identical queries between other queries (c5-(i) embedded at an arbitrary DP phase):
+    the periodic fill of uniform stretches (DESIGN.md SEG-DP step 8) must reproduce the oracle
+    exactly -- local runs, parallel fix-ups (args by direct scan) and cascade re-runs (trusted
+    source args), the list re-built after a stretch, every cost regime of the run's batches."""
+    kw = {}
+    runs = ((3_000, 128, 257), (20_000, 64, 513), (1_500, 7, 33))
+    cfg_kw = {}
+    if case == "windows":
+        kw["window"] = 50_000
+    if case == "viol_mid":
+        kw["slo_s"] = 0.8              # est(b) > 0.8 s from b = 25 on: batches of 24 avoid the penalty
+    if case == "all_viol":
+        kw["slo_s"] = 0.3              # every batch of the 513-output run violates
+    if case == "w64_nocap":
+        kw["W"] = 64
+        kw["cap_tokens"] = 0
+    if case == "tiny_tiles":
+        cfg_kw["dp_tile"] = 512        # 2 W: fix-up look-back at its lower limit, many cascade re-runs
+    if case == "split":
+        cfg_kw["split_on_slo_change"] = 1
+    if case == "lam0":
+        kw["lam"] = 0
+    if case == "w512":
+        kw["W"] = 512
+        kw["cap_tokens"] = 1_000_000
+        runs = ((9_000, 128, 257), (4_000, 3, 5))
+    inp, out, slo, cfg = W.uniform_runs(31, n=150_000, runs=runs, **kw)
+    if case == "w64_nocap":
+        cfg = cfg.replace(kv_cap_bytes=0)
+    r = assert_parity(inp, out, slo, cfg.replace(**cfg_kw))
+    assert r["diag"]["dp_filled_positions"] > 0
+
+
+def test_uniform_runs_generic_path_exact():
+    """The generic 64-bit path has no periodic fill (slow but exact): same schedule."""
+    inp, out, slo, cfg = W.uniform_runs(32, n=40_000, runs=((6_000, 128, 257),))
+    assert_parity(inp, out, slo, cfg.replace(flags=1))
+
+
 def test_all_violating_and_over_cap():
     inp, out, slo, cfg = W.c5(2, n=40_000, window=10_000)
     r = assert_parity(inp, out, slo, cfg)
@@ -230,18 +272,26 @@ def test_repeat_schedule_same_profile():
 def _window_sample_parity(inp, out, slo, cfg, r, windows):
     """Windows are independent (O1): the oracle recomputes sampled windows one by one and
     they must match the GPU's full-size run bit for bit."""
+    import concurrent.futures as cf
+    import os
     wl = cfg.window
     offs = r["offsets"].astype(np.int64)
+    c = cfg.replace(window=0)
+
+    def orc(w):                  # (ctypes releases the GIL: windows run on all host cores)
+        a, z = w * wl, min(len(inp), (w + 1) * wl)
+        o = oracle.schedule(inp[a:z], out[a:z], slo[a:z], c)
+        return o, oracle.stats(inp[a:z], out[a:z], slo[a:z], c, o[0], o[1])
+    with cf.ThreadPoolExecutor(max_workers=min(len(windows), os.cpu_count() or 1)) as ex:
+        res = dict(zip(windows, ex.map(orc, windows)))
     for w in windows:
         a, z = w * wl, min(len(inp), (w + 1) * wl)
-        c = cfg.replace(window=0)
-        o_order, o_offs, o_m, o_cost = oracle.schedule(inp[a:z], out[a:z], slo[a:z], c)
+        (o_order, o_offs, o_m, o_cost), (o_pb, o_tot) = res[w]
         assert np.array_equal(r["order"][a:z], o_order + a), w
         sel = offs[(offs >= a) & (offs <= z)]
         assert np.array_equal(sel, o_offs.astype(np.int64) + a), w
         pb = r["per_batch"]
         mine = pb[(pb["start"] >= a) & (pb["start"] < z)]
-        o_pb, o_tot = oracle.stats(inp[a:z], out[a:z], slo[a:z], c, o_order, o_offs)
         # every per-batch record element by element; the window-local oracle run differs only in
         # the position base (start + a) and the window index (+ w); completion_us restarts at
         # every window in both (R17)
@@ -279,15 +329,19 @@ def test_c4_full_size_sampled():
     inp, out, slo, cfg = W.c4(0)
     r = gpu_run(inp, out, slo, cfg)
     _global_properties(len(inp), cfg, r)
-    _window_sample_parity(inp, out, slo, cfg, r, [0, 57, 99])
+    _window_sample_parity(inp, out, slo, cfg, r, [0, 13, 26, 41, 57, 70, 88, 99])
 
 
 @pytest.mark.slow
-def test_c5_full_size_sampled():
+def test_c5_full_size_all_windows():
+    """BJ configs[4] at full size (10^7 adversarial queries): every one of the 10 windows is
+    oracle-identical, per-batch record by record (the identical-key windows go through the
+    periodic fill)."""
     inp, out, slo, cfg = W.c5(0)
     r = gpu_run(inp, out, slo, cfg)
     _global_properties(len(inp), cfg, r)
-    _window_sample_parity(inp, out, slo, cfg, r, [1, 3, 6, 9])
+    _window_sample_parity(inp, out, slo, cfg, r, list(range(10)))
+    assert r["diag"]["dp_filled_positions"] > 0
 
 
 @pytest.mark.parametrize("gen", [lambda: W.c2(3, n=20_000), lambda: W.c3(6, n=150_000)])

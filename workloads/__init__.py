@@ -185,6 +185,30 @@ def c5(seed: int, n: int = 10_000_000, window: int = 1_000_000, lam: int = 10**9
     return inp, out, slo, cfg
 
 
+def uniform_runs(seed: int, n: int = 200_000, runs=((3_000, 128, 257), (20_000, 64, 513)), slo_s: float = 30.0,
+                 window: int = 0, W: int = 256, cap_tokens: int = 16_384, lam: int = 10**9):
+    """c3-shaped background plus maximal runs of identical queries (in, out, slo) -- the shape of
+    c5-(i) (identical keys) embedded between other queries, so the run starts at an arbitrary
+    phase of the DP and is followed by more work.  All queries share one SLO; each run uses an
+    output length no background query has (odd values; the background is a multiple of 16), so
+    after the (slo, out, idx) sort every run is contiguous and preceded and followed by other
+    queries.  runs: (length, input, output) triples."""
+    rng = _rng(seed, 61)
+    m = n - sum(r[0] for r in runs)
+    inp, out, _ = long_tail(m, seed, stream=62)
+    parts_in, parts_out = [inp], [out]
+    for length, ri, ro in runs:
+        assert ro % 2 == 1, "run outputs must be odd (unique against the 16-bucketed background)"
+        parts_in.append(np.full(length, ri, np.uint32))
+        parts_out.append(np.full(length, ro, np.uint32))
+    inp = np.concatenate(parts_in); out = np.concatenate(parts_out)
+    perm = rng.permutation(n)
+    inp, out = inp[perm], out[perm]
+    slo = np.full(n, slo_s, np.float32)
+    cfg = SchedConfig(window=window, max_batch=W, kv_cap_bytes=cap_tokens * 524_288, lambda_us=lam)
+    return inp, out, slo, cfg
+
+
 # Mean inter-arrival gaps (us) for the simulator (NEXT f2): about one query's share of the
 # makespan the R7 service model gives the SEG-DP schedules of these shapes (c2 ~10 ms/query,
 # c3/c4 ~21.6 ms/query), i.e. a replica loaded close to saturation.
