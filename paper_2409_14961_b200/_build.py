@@ -13,6 +13,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-diag-suppress", "177", f"-I{os.path.join(ROOT, 'include')}"]
+# tuning builds only (tools/variant_build.sh): extra -D knobs, e.g. "-DUELLM_HULL_MIN=12"
+FLAGS += os.environ.get("UELLM_NVCC_DEFS", "").split()
 
 
 def sources():

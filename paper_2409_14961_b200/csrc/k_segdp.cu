@@ -285,7 +285,17 @@ __device__ DpResult dp_warp(const DPParams &P, const WarpSlots &S, uint32_t s, u
 struct NarrowSlots {
     longlong2 *sl;              // .x = C, .y = i | mo << 32 | mi << 48
     uint32_t *tri;              // per-block triangular max table M[q][k], q < k < 32 (496 words)
+    uint2 *hl;                  // per-block lower-hull subset of the lean external candidates
 };
+// Capacity of the hull subset (larger subsets fall back to the whole list).
+constexpr uint32_t kHullCap = 64;
+#ifndef UELLM_HULL_MIN
+#define UELLM_HULL_MIN 12
+#endif
+constexpr uint32_t kHullMin = UELLM_HULL_MIN;
+#ifndef UELLM_DP_PREFETCH
+#define UELLM_DP_PREFETCH 1
+#endif   // shorter lean ranges are evaluated whole
 // offset of row q of the triangular table (row q holds k = q+1 .. 31)
 __host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
 
@@ -587,12 +597,25 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     uint32_t kin = 0, kout = 0, kslo = 0;
     bool tile_uni = !FIX;
     if (!FIX) { kin = __ldg(rin + s); kout = __ldg(rout + s); kslo = prev_slo; }
+    // records of the next block, loaded one block ahead (the block's own loads were the largest
+    // single source of long-scoreboard stalls)
+    uint32_t pf_j0 = s, pf_in = 0, pf_out = 0, pf_slo = 0;
+    auto prefetch = [&](uint32_t jb) {
+        const uint32_t p = jb + lane;
+        const bool v = p < e;
+        pf_j0 = jb;
+        pf_in = v ? __ldg(rin + p) : 0u;
+        pf_out = v ? __ldg(rout + p) : 0u;
+        pf_slo = v ? __ldg(rslo + p) : 0u;
+    };
+    prefetch(s);
     for (uint32_t j0 = s; j0 < e && !stop; j0 += 32) {
         const uint32_t B = min(32u, e - j0);
         const bool vl = lane < B;
         const uint32_t x = j0 + lane, jl = x + 1;
-        const uint32_t in_l = vl ? __ldg(rin + x) : 0, out_l = vl ? __ldg(rout + x) : 0;
-        const uint32_t slo_l = vl ? __ldg(rslo + x) : 0;
+        if (!UELLM_DP_PREFETCH || pf_j0 != j0) prefetch(j0);   // (after a periodic fill moved j0)
+        const uint32_t in_l = pf_in, out_l = pf_out, slo_l = pf_slo;
+        if (UELLM_DP_PREFETCH && j0 + 32 < e) prefetch(j0 + 32);
         if (!FIX && tile_uni) {
             tile_uni = __all_sync(0xffffffffu, !vl || (in_l == kin && out_l == kout && slo_l == kslo));
             if (tile_uni && B == 32 && j0 >= next_try) {
@@ -764,14 +787,71 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             if (Vs > Pd) ext_lean(Pd, Vs);             // may violate: 64-bit with the penalty
             const uint32_t base_lo = (uint32_t)base;
             uint32_t r32 = 0xffffffffu, ri = 0xffffffffu;
+            // Lower-hull subset of the lean candidates [Vs, L) (exact).  Inside one SLO run every
+            // candidate of a group with one stored MI (the maxima up to the block start) has the
+            // same MI = max(mi, pmi) and MO = pmo at every boundary of the block, so its cost is
+            // (C_i - i*K) + const with one slope K per (group, lane): the minimum over the group is
+            // attained on the lower convex hull of its points (i, C_i).  A candidate k lying on or
+            // above the chord of two other members a < k < c is never the SMALLEST minimiser (if it
+            // minimised, equality would make a minimise too), so dropping every such k keeps the
+            // minimum and the smallest minimising i (R9); the chord of the list neighbours
+            // removes almost all non-vertices in one pass.  C offsets from base fit 32 bits
+            // (checked above) and |dC| * di < 2^45.
+            uint32_t H = 0xffffffffu;
+            if (L - Vs >= kHullMin) {
+                H = 0;
+                for (uint32_t r0 = Vs; r0 < L; r0 += 32) {
+                    const uint32_t k = r0 + lane;
+                    bool keep = false;
+                    uint2 ent = make_uint2(0u, 0u);
+                    if (k < L) {
+                        const longlong2 sv = S.sl[k];
+                        const uint32_t ck = (uint32_t)sv.x - base_lo, ik = (uint32_t)sv.y;
+                        const uint32_t mk = (uint32_t)((unsigned long long)sv.y >> 48);
+                        keep = true;
+                        if (k > Vs && k + 1 < L) {
+                            const longlong2 sa = S.sl[k - 1], sc = S.sl[k + 1];
+                            if ((uint32_t)((unsigned long long)sa.y >> 48) == mk &&
+                                (uint32_t)((unsigned long long)sc.y >> 48) == mk) {
+                                const long long ca = (long long)((uint32_t)sa.x - base_lo);
+                                const long long cc = (long long)((uint32_t)sc.x - base_lo);
+                                const uint32_t ia = (uint32_t)sa.y, ic = (uint32_t)sc.y;
+                                keep = ((long long)ck - ca) * (long long)(ic - ia) < (cc - ca) * (long long)(ik - ia);
+                            }
+                        }
+                        ent = make_uint2(ck, (j0 - ik) | (mk << 16));
+                    }
+                    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                    const uint32_t pos = H + __popc(bal & lt);
+                    if (keep && pos < kHullCap) S.hl[pos] = ent;
+                    H += __popc(bal);
+                }
+                __syncwarp();
+                if (H > kHullCap) H = 0xffffffffu;
+            }
+            if (H != 0xffffffffu) {
+                const uint32_t lp1 = lane + 1;           // b = jl - i = lane + 1 + (j0 - i)
+                uint32_t rd = 0;
+                evals -= (L - Vs - H) * B;           // evaluations actually run
 #pragma unroll (kExtUnroll)
-            for (uint32_t c = Vs; c < L; ++c) {
-                const longlong2 sv = S.sl[c];
-                const uint32_t ci = (uint32_t)sv.y;
-                const uint32_t b = jl - ci;
-                const uint32_t mi = max((uint32_t)((unsigned long long)sv.y >> 48), pmi);
-                const uint32_t tot = ((uint32_t)sv.x - base_lo) + A_l + b * (T_l + t_pre * mi);
-                if (tot < r32) { r32 = tot; ri = ci; }
+                for (uint32_t c = 0; c < H; ++c) {
+                    const uint2 he = S.hl[c];
+                    const uint32_t b = lp1 + (he.y & 0xffffu);
+                    const uint32_t mi = max(he.y >> 16, pmi);
+                    const uint32_t tot = he.x + A_l + b * (T_l + t_pre * mi);
+                    if (tot < r32) { r32 = tot; rd = he.y; }
+                }
+                if (r32 != 0xffffffffu) ri = j0 - (rd & 0xffffu);
+            } else {
+#pragma unroll (kExtUnroll)
+                for (uint32_t c = Vs; c < L; ++c) {
+                    const longlong2 sv = S.sl[c];
+                    const uint32_t ci = (uint32_t)sv.y;
+                    const uint32_t b = jl - ci;
+                    const uint32_t mi = max((uint32_t)((unsigned long long)sv.y >> 48), pmi);
+                    const uint32_t tot = ((uint32_t)sv.x - base_lo) + A_l + b * (T_l + t_pre * mi);
+                    if (tot < r32) { r32 = tot; ri = ci; }
+                }
             }
             // the older candidates (win ties) were evaluated in 64 bits: lb >= C(jl) >= base
             if (lb <= (unsigned long long)base + r32) { r32 = (uint32_t)(lb - (unsigned long long)base); ri = lbi; }
@@ -953,7 +1033,7 @@ __device__ __forceinline__ void tile_bounds(const DPParams &P, uint64_t t, uint3
 constexpr uint32_t kRmqBytes = 500 * 4;            // 1 pad word + 496 + 3, keeps 16-byte alignment
 static __host__ __device__ __forceinline__ uint32_t warp_smem_bytes(const DPParams &P)
 {
-    return P.narrow ? P.cap_slots * 16 + kRmqBytes : P.cap_slots * 20;
+    return P.narrow ? P.cap_slots * 16 + kRmqBytes + kHullCap * 8 : P.cap_slots * 20;
 }
 
 // Variant V of the SEG-DP kernels, fixed on the host (one instantiation per kernel keeps the code
@@ -975,6 +1055,7 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
         NarrowSlots S;
         S.sl = (longlong2 *)p;
         S.tri = (uint32_t *)(p + (size_t)P.cap_slots * 16);
+        S.hl = (uint2 *)(p + (size_t)P.cap_slots * 16 + kRmqBytes);
         return dp_warp_blocked<FIX, LK, SPLIT>(P, S, s, e, src, stop_min, src_args_ok, entry_uni);
     }
 }
