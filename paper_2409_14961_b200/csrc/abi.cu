@@ -71,6 +71,8 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.order = take(4 * N); L.offsets = take(4 * (N + 1));
     L.argx = take(2 * N);
     L.tiles = take(sizeof(TileRec) * (L.ntiles ? L.ntiles : 1));
+    L.tmaps = take(2 * L.W * (L.ntiles ? L.ntiles : 1));
+    L.twflag = take(4 * (L.nwin ? L.nwin : 1));
     L.tflags = take(4 * (L.ntiles + 2));
     L.bitmap = take(4 * L.nwords); L.wscan = take(4 * L.nwords);
     const uint64_t nblk = ceil_div(L.nwords, kScanBlock) + ceil_div(N, kScanBlock) + 2;
@@ -438,8 +440,9 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         int dl = 0;
         CU(run_segdp(P, L.ntiles, st, ev, &dl));
         launches += dl;
-        CU(run_traceback(P, bm, L.ntiles, st));
-        launches += 3;
+        int tl = 0;
+        CU(run_traceback(P, bm, L.ntiles, at<uint16_t>(w, L.tmaps), at<uint32_t>(w, L.twflag), st, &tl));
+        launches += tl;
     } else if (cfg->mode == UELLM_MODE_SLO_ODBS) {
         Alg1Params A;
         std::memset(&A, 0, sizeof A);

@@ -72,6 +72,10 @@ struct TileRec {
     uint32_t exitA, exitB;   // traceback: exit of the walk from e / from the true entry
     uint32_t merged;
     uint32_t uni;            // local run: every record of the tile is the same (periodic fill)
+    uint32_t fill_s, fill_P; // cascade: fix frame deferred to k_dp_fill, periodic with period fill_P
+    int64_t fill_F;          //   from the reference boundaries (fill_s - fill_P, fill_s]: C += fill_F per period
+    uint32_t remark;         // traceback: 1 + the true entry when the tile must be re-marked, else 0
+    uint32_t pad_;
 };
 
 struct Diag {                // device counters, see uellm_diagnostics
@@ -133,6 +137,7 @@ struct WsLayout {
     uint64_t order, offsets;                      // internal copies of the schedule
     uint64_t argx;                                // u16 per position
     uint64_t tiles;                               // TileRec[ntiles]
+    uint64_t tmaps, twflag;                       // traceback exit maps (u16[ntiles][W]), window flags
     uint64_t tflags;                              // u32[ntiles + 2]: local-done flags + 2 work counters
     uint64_t bitmap, wscan, blocksum, blockagg;   // boundary bitmap + scan scratch
     uint64_t st_so, st_pin, st_pout;              // per-batch stats scratch (u64 each)
@@ -236,8 +241,9 @@ struct DPParams {
 // ev[0..2]: events recorded after the local, fix-up and cascade kernels (NULL = none).
 cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void *const ev[3], int *launches);
 
-// Traceback of SEG-DP args into the boundary bitmap.
-cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, cudaStream_t st);
+// Traceback of SEG-DP args into the boundary bitmap (maps: u16[ntiles][W] scratch, wflag: u32[nwin]).
+cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, uint16_t *maps, uint32_t *wflag,
+                          cudaStream_t st, int *launches);
 
 // Bitmaps of the other modes.
 cudaError_t launch_mark_fifo(uint32_t *bitmap, uint64_t n, uint64_t window, uint32_t W, int sort_only,

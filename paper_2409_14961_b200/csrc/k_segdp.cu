@@ -563,12 +563,14 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             bool dominated = false;
             if (!dead) {
 // successors tested besides the next one (tools/variant_run.sh on c4, DP ms: {8, 32}: 6.74,
-// {32}: 6.57, {16}: 6.59, {64}: 6.67, {8}: 6.69, {}: 6.82, {4, 16}: 6.84, {16, 64}: 6.68)
+// {32}: 6.57, {16}: 6.59, {64}: 6.67, {8}: 6.69, {}: 6.82, {4, 16}: 6.84, {16, 64}: 6.68; with the
+// hull subset of the fast block the list length matters less: {}: 5.93, {32}: 6.06, {64}: 6.10,
+// {8}: 6.38)
 #ifndef UELLM_D1_D2
 #define UELLM_D1_D2 0
 #endif
 #ifndef UELLM_D1_D3
-#define UELLM_D1_D3 32
+#define UELLM_D1_D3 0
 #endif
                 if (k + 1 < Lt) dominated = dominated_by(k + 1);
                 if (UELLM_D1_D2 && !dominated && k + UELLM_D1_D2 < Lt) dominated = dominated_by(k + UELLM_D1_D2);
@@ -1151,6 +1153,47 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_tiles
     if (lane == 0 && evals) atomicAdd(&P.diag->dp_evals, evals);
 }
 
+// Periodic reference of the fix frame CFx at boundary s (the start of a tile inside a uniform
+// stretch whose predecessor starts at s_prev): Pp = s - arg[s] (the last batch) when
+// C[i] - C[i-Pp] = F on the W boundaries (s-W, s] and every boundary read lies in (s_prev, s]
+// (the predecessor's fix frame, true args); 0 if the check fails.  Warp-collective.
+__device__ uint32_t periodic_ref(const DPParams &P, uint32_t s, uint32_t s_prev, long long &F)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t W = P.W;
+    const uint32_t Pp = (uint32_t)__ldcg(reinterpret_cast<const unsigned short *>(P.argx) + s - 1);
+    if (Pp < 1 || Pp > W || s < s_prev + W + Pp) return 0;
+    F = __ldcg(P.CFx + s - 1) - __ldcg(P.CFx + s - Pp - 1);
+    bool ok = true;
+    for (uint32_t i = s + 1 - W + lane; i <= s; i += 32)
+        ok &= (__ldcg(P.CFx + i - 1) - __ldcg(P.CFx + i - Pp - 1)) == F;
+    return __all_sync(0xffffffffu, ok) ? Pp : 0u;
+}
+
+// Writes boundaries j in (a, b] of the fix frame from the periodic reference (ref_s - Pp, ref_s]:
+// j - m*Pp lands in the reference for m = ceil((j - ref_s) / Pp).
+__device__ __forceinline__ void fill_from_ref(const DPParams &P, uint32_t a, uint32_t b, uint32_t ref_s, uint32_t Pp,
+                                              long long F, uint32_t tid, uint32_t nthr)
+{
+    for (uint32_t j = a + 1 + tid; j <= b; j += nthr) {
+        const uint32_t m = (j - ref_s + Pp - 1) / Pp;
+        const uint32_t src = j - m * Pp;
+        P.CFx[j - 1] = __ldcg(P.CFx + src - 1) + (long long)m * F;
+        P.argx[j - 1] = __ldcg(reinterpret_cast<const unsigned short *>(P.argx) + src - 1);
+    }
+}
+
+// The tiles the cascade deferred (fill_P != 0), written in parallel: one CTA per tile.
+__global__ void __launch_bounds__(256) k_dp_fill(DPParams P, uint64_t ntiles)
+{
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileRec &r = P.tiles[t];
+        if (!r.valid || r.fill_P == 0) continue;
+        fill_from_ref(P, r.s, r.e, r.fill_s, r.fill_P, r.fill_F, threadIdx.x, blockDim.x);
+        if (threadIdx.x == 0) atomicAdd(&P.diag->dp_filled, (unsigned long long)(r.e - r.s));
+    }
+}
+
 // One warp per window: resolve tiles whose predecessor did not converge, compute the frame
 // offsets of every tile and the window's optimal cost C[w1].
 template <int V>
@@ -1202,24 +1245,62 @@ __global__ void k_dp_cascade(DPParams P)
     // tile 0 is exact in its local frame
     long long tail_off = 0;          // offset of the frame holding tile (k-1)'s tail values
     bool tail_local = true;          // tail in Cx (local frame) vs CFx (fix-up frame)
+    // Deferred periodic fill of uniform stretches (DESIGN.md "SEG-DP" step 8): once tile k-1's
+    // fix frame is periodic at the start of tile k (C[i] = C[i-Pp] + F on the W boundaries up to
+    // s_k, uniform elements behind them), every later boundary of the same uniform stretch is
+    // C[j] = C[j - m*Pp] + m*F, arg[j] = arg[j - m*Pp] + m*Pp (periodic_fill's induction), so the
+    // tiles of the stretch only record that reference here and k_dp_fill writes them in
+    // parallel afterwards; a re-run that leaves the stretch first gets its predecessor's tail.
+    uint32_t ref_s = 0, ref_P = 0;   // active reference: boundaries (ref_s - ref_P, ref_s] of CFx
+    long long ref_F = 0;
     if (lane == 0) { P.tiles[t0].off_local = 0; P.tiles[t0].off_fix = 0; }
     for (uint32_t k = 1; k < K; ++k) {
         TileRec r = P.tiles[t0 + k];
+        r.fill_s = 0; r.fill_P = 0; r.fill_F = 0;
         if (!tail_local) {
-            DpResult R = dp_run<true, V>(P, smem, 0, r.s, r.e, P.CFx, r.fix_end, true, entry_uniform(P, t0 + k, r.s));
-            r.conv = R.conv; r.conv_pos = R.conv_pos; r.fix_end = max(R.fix_end, r.fix_end); r.delta = R.delta;
-            if (lane == 0) {
-                atomicAdd(&P.diag->cascade_reruns, 1ull);
-                atomicAdd(&P.diag->fixup_positions, (unsigned long long)R.positions);
-                atomicAdd(&P.diag->dp_evals, (unsigned long long)R.evals);
-                if (R.filled) atomicAdd(&P.diag->dp_filled, (unsigned long long)R.filled);
+            const bool eu = entry_uniform(P, t0 + k, r.s);
+            bool deferred = false;
+            if (V != 0 && eu) {
+                if (ref_P == 0) {
+                    ref_P = periodic_ref(P, r.s, P.tiles[t0 + k - 1].s, ref_F);
+                    ref_s = r.s;
+                }
+                deferred = ref_P != 0;
+            } else if (ref_P) {
+                // leaving the stretch: materialise the last 2W boundaries of the deferred predecessor
+                const TileRec &q = P.tiles[t0 + k - 1];
+                fill_from_ref(P, max(q.s, q.e > 2 * P.W ? q.e - 2 * P.W : 0u), q.e, ref_s, ref_P, ref_F, lane, 32);
+                __syncwarp();
+                __threadfence_block();
+                ref_P = 0; ref_s = 0;
             }
+            if (deferred) {
+                r.fill_s = ref_s; r.fill_P = ref_P; r.fill_F = ref_F;
+                r.conv = 0; r.fix_end = r.e;
+            } else {
+                DpResult R = dp_run<true, V>(P, smem, 0, r.s, r.e, P.CFx, r.fix_end, true, eu);
+                r.conv = R.conv; r.conv_pos = R.conv_pos; r.fix_end = max(R.fix_end, r.fix_end); r.delta = R.delta;
+                if (lane == 0) {
+                    atomicAdd(&P.diag->cascade_reruns, 1ull);
+                    atomicAdd(&P.diag->fixup_positions, (unsigned long long)R.positions);
+                    atomicAdd(&P.diag->dp_evals, (unsigned long long)R.evals);
+                    if (R.filled) atomicAdd(&P.diag->dp_filled, (unsigned long long)R.filled);
+                }
+            }
+        } else {
+            ref_P = 0; ref_s = 0;
         }
         r.off_fix = tail_off;
         if (r.conv) { r.off_local = tail_off + r.delta; tail_off = r.off_local; tail_local = true; }
         else { r.off_local = 0; tail_local = false; }
         if (lane == 0) P.tiles[t0 + k] = r;
         __syncwarp();
+    }
+    if (ref_P) {            // the window ends inside a deferred stretch: its last value is needed now
+        const TileRec &q = P.tiles[t0 + K - 1];
+        fill_from_ref(P, q.e - 1, q.e, ref_s, ref_P, ref_F, lane, 32);
+        __syncwarp();
+        __threadfence_block();
     }
     if (lane == 0) {
         const TileRec &r = P.tiles[t0 + K - 1];
@@ -1262,6 +1343,10 @@ static cudaError_t launch_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t
     if (ev[1]) cudaEventRecord((cudaEvent_t)ev[1], st);
     k_dp_cascade<V><<<P.nwin, 32, smem1, st>>>(P);
     ++*launches;
+    if (V != 0) {           // deferred uniform tiles (none: every CTA exits after reading the records)
+        k_dp_fill<<<(unsigned)(ntiles < (uint64_t)nsm * 8 ? ntiles : (uint64_t)nsm * 8), 256, 0, st>>>(P, ntiles);
+        ++*launches;
+    }
     if (ev[2]) cudaEventRecord((cudaEvent_t)ev[2], st);
     return cudaGetLastError();
 }

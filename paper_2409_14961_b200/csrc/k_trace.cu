@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(1024) k_trace_a_smem(const uint16_t *__restric
 }
 
 __global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t ntiles, uint64_t tpw,
-                          uint32_t *bm, Diag *diag)
+                          uint32_t *bm, Diag *diag, uint32_t *wflag)
 {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles) return;
@@ -92,19 +92,62 @@ __global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uin
                 if (i <= r.s) { exitB = i; merged = (i == r.exitA); break; }
                 j = i;
             }
-            if (!merged) atomicAdd(&diag->trace_unmerged, 1ull);
+            if (!merged) { atomicAdd(&diag->trace_unmerged, 1ull); wflag[t / tpw] = 1u; }
         }
     }
     tiles[t].exitB = exitB;
     tiles[t].merged = merged;
 }
 
-__global__ void k_trace_c(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t tpw, uint64_t nwin,
-                          uint64_t window, uint32_t *bm, Diag *diag)
+// Tile args staged in shared memory (up to kTraceStage positions; longer tiles read global memory).
+constexpr uint32_t kTraceStage = 16384;
+struct TileArgs {
+    const uint16_t *g, *sm;
+    uint32_t s;
+    __device__ __forceinline__ uint32_t arg(uint32_t j) const
+    {
+        const uint32_t k = j - 1 - s;
+        return j - (uint32_t)(sm && k < kTraceStage ? sm[k] : g[j - 1]);
+    }
+};
+__device__ __forceinline__ TileArgs stage_args(const uint16_t *argx, const TileRec &r, uint16_t *sa)
 {
-    // one warp per window: count the valid tiles (a prefix) and check 32 tiles at a time whether
-    // every B-walk merged (exitB == exitA for tiles 1 .. K-1) -- then every tile's entry was right
-    // and nothing needs re-walking; otherwise lane 0 walks the tiles in order (rare)
+    const uint32_t len = r.e - r.s;
+    for (uint32_t k = threadIdx.x; k < len && k < kTraceStage; k += blockDim.x) sa[k] = argx[r.s + k];
+    __syncthreads();
+    return TileArgs{argx, sa, r.s};
+}
+
+// T2b (windows with an unmerged B-walk only): exit maps.  For every possible entry q into tile t
+// -- q in [e - W + 1, e], where the walk from the next tile lands -- the first node <= s of the
+// walk from q, stored as s - exit (< W).  One CTA per tile, one thread per entry.
+__global__ void __launch_bounds__(256) k_trace_maps(const uint16_t *__restrict__ argx, const TileRec *tiles,
+                                                    uint64_t ntiles, uint64_t tpw, const uint32_t *wflag, uint32_t W,
+                                                    uint16_t *maps)
+{
+    extern __shared__ uint16_t sa[];
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (!wflag[t / tpw]) continue;
+        const TileRec r = tiles[t];
+        if (!r.valid) continue;
+        const TileArgs A = stage_args(argx, r, sa);
+        for (uint32_t qo = threadIdx.x; qo < W; qo += blockDim.x) {
+            uint32_t j = r.e - qo, i = j;                // entry e - qo (a node <= s exits at once)
+            while (i > r.s) { j = i; i = A.arg(j); }
+            maps[t * W + qo] = (uint16_t)(r.s - i);
+        }
+        __syncthreads();
+    }
+}
+
+// T3: one warp per window.  Counts the valid tiles (a prefix) and checks 32 tiles at a time whether
+// every B-walk merged (exitB == exitA for tiles 1 .. K-1) -- then every tile's entry was right and
+// nothing needs re-walking.  Otherwise lane 0 follows the true path through the tiles from the
+// window end: a tile entered where its B-walk started keeps its marks and exit; any other tile
+// takes its exit from the exit map and is queued for re-marking (k_trace_remark, in parallel).
+__global__ void k_trace_c(const uint16_t *__restrict__ maps, TileRec *tiles, uint64_t tpw, uint64_t nwin,
+                          uint64_t window, uint32_t W, uint32_t *bm, Diag *diag)
+{
     const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     if (w >= nwin) return;
@@ -124,48 +167,80 @@ __global__ void k_trace_c(const uint16_t *__restrict__ argx, TileRec *tiles, uin
     bm_set(bm, (uint32_t)(w * window));                 // every window starts a batch
     if (allm) return;
     uint32_t exit_true = tiles[t0 + K - 1].exitB;
+    uint32_t rewalks = 0;
     for (int k = (int)K - 2; k >= 0; --k) {
-        const TileRec r = tiles[t0 + k];
+        const TileRec &r = tiles[t0 + k];
         if (exit_true == tiles[t0 + k + 1].exitA) {
             exit_true = r.exitB;
             continue;
         }
-        // the walk into this tile enters elsewhere: re-walk it in full
-        atomicAdd(&diag->trace_rewalks, 1ull);
-        bm_clear(bm, r.s + 1, r.e);
-        uint32_t j = exit_true, i;
-        for (;;) {
-            bm_set(bm, j);
-            i = arg_of(argx, j);
-            if (i <= r.s) break;
-            j = i;
+        ++rewalks;
+        tiles[t0 + k].remark = exit_true + 1u;
+        exit_true = r.s - (uint32_t)maps[(t0 + k) * W + (r.e - exit_true)];
+        tiles[t0 + k].exitB = exit_true;
+    }
+    if (rewalks) atomicAdd(&diag->trace_rewalks, (unsigned long long)rewalks);
+}
+
+// T4: tiles entered elsewhere than their B-walk assumed are re-marked from the true entry (one CTA
+// per tile, the walk over the staged args).
+__global__ void __launch_bounds__(128) k_trace_remark(const uint16_t *__restrict__ argx, const TileRec *tiles,
+                                                      uint64_t ntiles, uint64_t tpw, const uint32_t *wflag,
+                                                      uint32_t *bm)
+{
+    extern __shared__ uint16_t sa[];
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (!wflag[t / tpw]) continue;
+        const TileRec r = tiles[t];
+        if (!r.valid || !r.remark) continue;
+        const TileArgs A = stage_args(argx, r, sa);
+        if (threadIdx.x == 0) {
+            bm_clear(bm, r.s + 1, r.e);
+            uint32_t j = r.remark - 1u;
+            for (;;) {
+                bm_set(bm, j);
+                const uint32_t i = A.arg(j);
+                if (i <= r.s) break;
+                j = i;
+            }
         }
-        tiles[t0 + k].exitB = i;
-        exit_true = i;
+        __syncthreads();
     }
 }
 
-cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, cudaStream_t st)
+cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, uint16_t *maps, uint32_t *wflag,
+                          cudaStream_t st, int *launches)
 {
+    *launches = 0;
     if (P.n == 0) return cudaSuccess;
     const unsigned tb = 128;
-    const size_t stage = (size_t)P.tile_len * sizeof(uint16_t);
+    const size_t stage = (size_t)(P.tile_len < kTraceStage ? P.tile_len : kTraceStage) * sizeof(uint16_t);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)(ntiles < (uint64_t)nsm * 8 ? ntiles : (uint64_t)nsm * 8);
+    cudaError_t e = cudaMemsetAsync(wflag, 0, 4 * P.nwin, st);
+    if (e != cudaSuccess) return e;
 // walk A: thread per tile through L1/L2 (0) or one CTA per tile with the tile's args staged in
 // shared memory (threads per CTA).  Measured on c4 (traceback ms): 0: 0.292, 256: 0.316,
 // 64: 0.374, 32: 0.475 -- with 21,800 tiles every walk runs at once and hides its own latency.
 #ifndef UELLM_TRACE_A
 #define UELLM_TRACE_A 0
 #endif
-    if (UELLM_TRACE_A && stage <= 160 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_trace_a_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+    if (UELLM_TRACE_A && P.tile_len * sizeof(uint16_t) <= 160 * 1024) {
+        e = cudaFuncSetAttribute(k_trace_a_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(P.tile_len * sizeof(uint16_t)));
         if (e != cudaSuccess) return e;
-        k_trace_a_smem<<<(unsigned)ntiles, UELLM_TRACE_A, stage, st>>>(P.argx, P.tiles, bitmap);
+        k_trace_a_smem<<<(unsigned)ntiles, UELLM_TRACE_A, P.tile_len * sizeof(uint16_t), st>>>(P.argx, P.tiles, bitmap);
     } else {
         k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
     }
-    k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag);
-    k_trace_c<<<(unsigned)ceil_div(P.nwin * 32, 128), 128, 0, st>>>(P.argx, P.tiles, P.tpw, P.nwin, P.window, bitmap,
-                                                           P.diag);
+    k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag, wflag);
+    k_trace_maps<<<grid, 256, stage, st>>>(P.argx, P.tiles, ntiles, P.tpw, wflag, P.W, maps);
+    k_trace_c<<<(unsigned)ceil_div(P.nwin * 32, 128), 128, 0, st>>>(maps, P.tiles, P.tpw, P.nwin, P.window, P.W,
+                                                                   bitmap, P.diag);
+    k_trace_remark<<<grid, 128, stage, st>>>(P.argx, P.tiles, ntiles, P.tpw, wflag, bitmap);
+    *launches = 5;
     return cudaGetLastError();
 }
 

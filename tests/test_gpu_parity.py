@@ -142,6 +142,32 @@ def test_uniform_runs_periodic_fill(case):
     assert r["diag"]["dp_filled_positions"] > 0
 
 
+@pytest.mark.parametrize("case", ["many_tiles", "windows", "tile_1000", "w64", "no_cap"])
+def test_uniform_long_runs_deferred(case):
+    """Uniform stretches spanning many DP tiles: the cascade defers every tile past the first periodic
+    one to k_dp_fill (reference frame, parallel fill), materialises the tail where a re-run leaves
+    the stretch or the window ends inside it; the traceback's B-walks never merge there, so the exit
+    maps + parallel re-marking carry the true path through (DESIGN.md SEG-DP step 8, a7)."""
+    kw = {}
+    cfg_kw = {"dp_tile": 4096}
+    runs = ((70_000, 128, 257), (45_000, 64, 513), (9_000, 7, 33))
+    if case == "windows":
+        kw["window"] = 90_000          # window ends cut the runs (stretch tails at window ends)
+    if case == "tile_1000":
+        cfg_kw["dp_tile"] = 1000       # tile length not a multiple of the period
+    if case == "w64":
+        kw["W"] = 64
+    if case == "no_cap":
+        kw["cap_tokens"] = 0           # period W (batches of W) instead of the cap's 42
+    inp, out, slo, cfg = W.uniform_runs(33, n=260_000, runs=runs, **kw)
+    if case == "no_cap":
+        cfg = cfg.replace(kv_cap_bytes=0)
+    r = assert_parity(inp, out, slo, cfg.replace(**cfg_kw))
+    d = r["diag"]
+    assert d["dp_filled_positions"] > 100_000, d
+    assert d["cascade_reruns"] < d["tiles"] // 4, d
+
+
 def test_uniform_runs_generic_path_exact():
     """The generic 64-bit path has no periodic fill (slow but exact): same schedule."""
     inp, out, slo, cfg = W.uniform_runs(32, n=40_000, runs=((6_000, 128, 257),))
