@@ -67,7 +67,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.vals0 = take(4 * N); L.vals1 = take(4 * N); L.vals2 = take(4 * N);
     L.rin = take(4 * N); L.rout = take(4 * N); L.rslo = take(4 * N);
     L.keysc = take(4 * N);
-    L.slo_set = take(4 * kSloSetSize); L.slo_rank = take(4 * kSloSetSize); L.slo_table = take(4 * kSloRankMax);
+    L.slo_set = take(4 * kSloSetSize); L.slo_ctab = take(8 * kSloSetSize); L.slo_table = take(4 * kSloRankMax);
     L.order = take(4 * N); L.offsets = take(4 * (N + 1));
     L.argx = take(2 * N);
     L.tiles = take(sizeof(TileRec) * (L.ntiles ? L.ntiles : 1));
@@ -80,7 +80,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.blockagg = take(8 * nblk);
     L.st_so = take(8 * N); L.st_pin = take(8 * N); L.st_pout = take(8 * N);
     L.a1tiles = take(alg1_scratch_bytes(L.window, L.nwin, (uint32_t)L.W));
-    L.hist = take(4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));
+    L.hist = take(2 * 4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));   // two histogram buffers (passes alternate)
     L.meta = take(sizeof(LoadMeta)); L.diag = take(sizeof(Diag)); L.acc = take(sizeof(StatAcc));
     L.nb = take(8); L.totals = take(sizeof(uellm_totals));
     L.wincost = take(8 * (L.nwin ? L.nwin : 1));
@@ -336,13 +336,23 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
                             v.slo_distinct <= kSloRankMax && rb + ob <= 32;
     DecodeArgs D;
     D.in = v.d_in; D.table = at<uint32_t>(w, L.slo_table); D.ob = ob;
+    D.nslo = v.slo_distinct < kSloRankMax ? v.slo_distinct : kSloRankMax;
+    D.packin = 0; D.wb = 0;
     D.rin = rin; D.rout = rout; D.rslo = rslo; D.order = d_order;
     if (compressed) {
         // rank table, then keys rank << ob | out packed straight from the caller arrays together
         // with the digit-0 histogram; the last pass writes the records (fused decode)
         uint32_t *kc = at<uint32_t>(w, L.keysc);
         uint32_t *vals0 = at<uint32_t>(w, L.vals0);
-        CU(launch_slo_table(at<uint32_t>(w, L.slo_set), at<uint32_t>(w, L.slo_table), at<uint32_t>(w, L.slo_rank), st));
+        int cbits = 4;                                         // compact hash: >= 2 slots per value
+        while ((1u << cbits) < 2 * v.slo_distinct && cbits < (int)kSloSetBits) ++cbits;
+        CU(launch_slo_table(at<uint32_t>(w, L.slo_set), at<uint32_t>(w, L.slo_table),
+                            at<unsigned long long>(w, L.slo_ctab), cbits, st));
+        // window-local index and input length packed into the payload when they fit 32 bits
+        int wbits = 0, ibits = 0;
+        while (wbits < 32 && ((L.window - 1) >> wbits)) ++wbits;
+        while (ibits < 32 && ((uint64_t)(v.max_in - 1) >> ibits)) ++ibits;
+        if (wbits + ibits <= 32 && wbits < 32) { D.packin = 1; D.wb = wbits; }
         launches += 1;
         uint32_t mask = 0;
         for (int d = 0; d < 4; ++d) if (8 * d < rb + ob) mask |= 1u << d;
@@ -352,16 +362,17 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         const uint32_t *k32 = kc;
         for (uint64_t w0 = 0; w0 < L.nwin; w0 += gw) {
             const uint64_t wn = L.nwin - w0 < gw ? L.nwin - w0 : gw;
-            CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, w0, wn, at<uint32_t>(w, L.slo_set),
-                                  at<uint32_t>(w, L.slo_rank), ob, kc, vals0, at<uint32_t>(w, L.hist), st));
+            CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, w0, wn, at<unsigned long long>(w, L.slo_ctab),
+                                  cbits, ob, kc, vals0, at<uint32_t>(w, L.hist), st));
             launches += 1;
             k32 = kc;
             const uint32_t *vals = nullptr;            // identity payload (arrival index = position)
             CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                     (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                                    at<uint32_t>(w, L.hist), n, L.window, w0, wn, mask, &passes, st,
+                                    at<uint32_t>(w, L.hist), at<uint32_t>(w, L.hist) + 256 * L.sort_tiles, n,
+                                    L.window, w0, wn, mask, &passes, st,
                                     (mask & 1u) != 0, &D));
-            launches += 3 * passes - ((mask & 1u) && passes ? 1 : 0);
+            launches += 2 * passes + ((mask & 1u) || !passes ? 0 : 1);   // scan + scatter per pass, one histogram
             if (passes == 0) {
                 CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
                 launches += 1;                         // (mask == 0: one group covers every window)
@@ -387,8 +398,9 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
                 vals = v0;
                 CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                       at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
-                                      at<uint32_t>(w, L.hist), n, L.window, w0, wn, mask, &passes, st, &D));
-                launches += 3 * passes;
+                                      at<uint32_t>(w, L.hist), at<uint32_t>(w, L.hist) + 256 * L.sort_tiles, n,
+                                    L.window, w0, wn, mask, &passes, st, &D));
+                launches += 2 * passes + (passes ? 1 : 0);
                 if (passes == 0) break;
             }
         }

@@ -133,7 +133,7 @@ struct WsLayout {
     uint64_t vals0, vals1, vals2;                 // keys1/keys2 re-used as Cx/CFx, est/completion
     uint64_t rin, rout, rslo;                     // scheduled-order records
     uint64_t keysc;                               // rank-compressed u32 keys
-    uint64_t slo_set, slo_rank, slo_table;        // distinct-SLO hash set, slot ranks, sorted values
+    uint64_t slo_set, slo_ctab, slo_table;        // distinct-SLO hash set, compact (value, rank) hash, sorted values
     uint64_t order, offsets;                      // internal copies of the schedule
     uint64_t argx;                                // u16 per position
     uint64_t tiles;                               // TileRec[ntiles]
@@ -191,17 +191,23 @@ struct DecodeArgs {
     const uint32_t *in;        // caller input lengths (gathered by arrival index)
     const uint32_t *table;     // compressed keys: rank -> slo_us (kSloRankMax entries)
     int ob;                    // compressed keys: bits of max_out
+    uint32_t nslo;             // compressed keys: ranks in use (table entries the decode stages)
+    uint32_t packin;           // payload = (idx - window start) | (in - 1) << wb (no gather in the decode)
+    int wb;
     uint32_t *rin, *rout, *rslo, *order;
 };
-// compressed path: rank table, then pack key32 = rank << ob | out with the digit-0 histogram
-cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, uint32_t *rank_of_slot, cudaStream_t st);
+// compressed path: rank table + compact (value, rank) hash of 2^cbits slots (ctab), then pack
+// key32 = rank << ob | out with the digit-0 histogram
+cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, unsigned long long *ctab, int cbits,
+                             cudaStream_t st);
 // [w_first, w_first + nwin): the windows processed by this call (window groups keep a group's
 // intermediate arrays resident in L2 across the passes)
 cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t w_first,
-                               uint64_t nwin, const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob,
-                               uint32_t *keys32, uint32_t *vals, uint32_t *hist0, cudaStream_t st);
+                               uint64_t nwin, const unsigned long long *ctab, int cbits, int ob, uint32_t *keys32,
+                               uint32_t *vals, uint32_t *hist0, cudaStream_t st);
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
-                                 uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
+                                 uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
+                                 uint64_t n,
                                  uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
                                  cudaStream_t st, bool hist0_ready = false, const DecodeArgs *dec = nullptr);
 // windows per sort group: about kSortGroupQueries queries (env UELLM_SORT_GROUP_Q overrides, tuning)
@@ -216,7 +222,7 @@ cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const ui
 // the sorted result (the input itself when no digit varies).  *passes = passes run.
 cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
                                unsigned long long *keys_a, uint32_t *vals_a,
-                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
+                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
                                int *passes, cudaStream_t st, const struct DecodeArgs *dec = nullptr);
 

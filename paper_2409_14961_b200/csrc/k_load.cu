@@ -181,14 +181,17 @@ cudaError_t launch_pack64(const uint32_t *out, const float *slo, uint64_t n, uns
 }
 
 // ---------------------------------------------------------------------------------------
-// Rank table of the distinct SLO values (one CTA): table[r] = r-th smallest value,
-// rank_of_slot[h] = rank of the value stored in global-set slot h.
+// Rank table of the distinct SLO values (one CTA): table[r] = r-th smallest value, and a compact
+// open-addressing hash ctab (2^cbits slots >= 2 x the distinct values) of (value << 32 | rank) for
+// the key packer -- a few hundred bytes to stage per CTA instead of the 4096-slot set.
 __global__ void __launch_bounds__(1024) k_slo_table(const uint32_t *__restrict__ slo_set, uint32_t *__restrict__ table,
-                                                    uint32_t *__restrict__ rank_of_slot)
+                                                    unsigned long long *__restrict__ ctab, int cbits)
 {
     __shared__ uint32_t vals[kSloRankMax];
     __shared__ uint32_t cnt;
+    const uint32_t C = 1u << cbits;
     if (threadIdx.x == 0) cnt = 0;
+    for (uint32_t h = threadIdx.x; h < C; h += blockDim.x) ctab[h] = 0ull;
     __syncthreads();
     for (uint32_t h = threadIdx.x; h < kSloSetSize; h += blockDim.x) {
         const uint32_t v = slo_set[h];
@@ -197,19 +200,21 @@ __global__ void __launch_bounds__(1024) k_slo_table(const uint32_t *__restrict__
     __syncthreads();
     const uint32_t K = min(cnt, kSloRankMax);
     for (uint32_t r = K + threadIdx.x; r < kSloRankMax; r += blockDim.x) table[r] = 0;   // unused ranks
-    for (uint32_t h = threadIdx.x; h < kSloSetSize; h += blockDim.x) {
-        const uint32_t v = slo_set[h];
-        if (!v) { rank_of_slot[h] = 0; continue; }     // empty slots are copied too (initcheck-clean)
+    for (uint32_t f = threadIdx.x; f < K; f += blockDim.x) {
+        const uint32_t v = vals[f];
         uint32_t r = 0;
-        for (uint32_t f = 0; f < K; ++f) r += vals[f] < v;
-        rank_of_slot[h] = r;
+        for (uint32_t g = 0; g < K; ++g) r += vals[g] < v;
         table[r] = v;
+        const unsigned long long e = ((unsigned long long)v << 32) | r;
+        uint32_t h = slo_hash(v, (uint32_t)cbits);
+        while (atomicCAS(ctab + h, 0ull, e) != 0ull) h = (h + 1) & (C - 1);    // values are distinct
     }
 }
 
-cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, uint32_t *rank_of_slot, cudaStream_t st)
+cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, unsigned long long *ctab, int cbits,
+                             cudaStream_t st)
 {
-    k_slo_table<<<1, 1024, 0, st>>>(slo_set, table, rank_of_slot);
+    k_slo_table<<<1, 1024, 0, st>>>(slo_set, table, ctab, cbits);
     return cudaGetLastError();
 }
 

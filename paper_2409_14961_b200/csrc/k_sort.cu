@@ -8,9 +8,10 @@
 //        of slo_us among the distinct values preserves the order exactly; 2 passes for c3/c4)
 //
 // Per pass (reduce-then-scan):
-//   k_sort_up    per 4096-key tile (tiles never cross a window): digit histogram, warp-
+//   k_sort_up    per 2048-key tile (tiles never cross a window): digit histogram, warp-
 //                aggregated with match.any (skewed class-valued SLO digits would otherwise
-//                serialise on a few shared-memory bins).
+//                serialise on a few shared-memory bins).  Only for the first pass without a
+//                fused histogram: every scatter counts the next pass's digit per destination tile.
 //   k_sort_scan  per window: exclusive offsets of (tile, digit) in window-major order.
 //   k_sort_down  per tile: stable rank of every key (match.any peers + per-warp running
 //                counts), then scatter.  Stability: tile order, warp order, iteration order,
@@ -117,120 +118,276 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__res
     for (; k < k1; ++k) { const uint32_t v = col[(uint64_t)k * 256]; col[(uint64_t)k * 256] = run; run += v; }
 }
 
+#ifndef UELLM_SORT_PIPE
+#define UELLM_SORT_PIPE 1
+#endif
 #ifndef UELLM_SORT_DOWN_MINB
 #define UELLM_SORT_DOWN_MINB 5
 #endif
-template <class K, bool DECODE>
-__global__ void __launch_bounds__(kSortThreads, UELLM_SORT_DOWN_MINB) k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
-                                                            K *__restrict__ kout, uint32_t *__restrict__ vout,
-                                                            const uint32_t *__restrict__ hist, uint64_t n,
-                                                            uint64_t window, uint64_t tpw, int shift, DecodeArgs D,
-                                                            uint64_t t0)
+
+// ---- TMA bulk copies (cp.async.bulk) into shared memory, completion on an mbarrier -------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred P1;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@!P1 bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Scatter pass of one digit.  Per 2048-key tile (tiles never cross a window): stable rank of
+// every key (match.any peers + per-warp running counts), per-digit exclusive offsets, the tile
+// staged in shared memory in (digit, rank) order, then every digit bucket written as one
+// contiguous run.  Stability: tile order x warp order x iteration order x lane order = input order.
+// PIPE: persistent CTAs; tile i+1's keys, payloads and histogram row are brought into shared
+// memory by TMA bulk copies (cp.async.bulk, mbarrier completion) while tile i is ranked and
+// written -- the load latency no longer sits between the CTA's phases.
+// NEXT: also count the next pass's digit (shift_next) per destination tile into hist_next (the
+// next pass then needs no histogram kernel of its own); a warp's (tile, digit) pairs are
+// aggregated with match.any first.
+// DECODE (last pass): a4 fused -- records written straight at the scheduled position.
+template <class K, bool DECODE, bool NEXT, bool PIPE>
+__global__ void __launch_bounds__(kSortThreads, PIPE ? 1 : UELLM_SORT_DOWN_MINB)
+k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+            uint32_t *__restrict__ vout, const uint32_t *__restrict__ hist, uint64_t n, uint64_t window,
+            uint64_t tpw, int shift, DecodeArgs D, uint64_t t0, uint64_t ntiles, uint32_t *__restrict__ hist_next,
+            int shift_next)
 {
     constexpr int kWarps = kSortThreads / 32;
-    constexpr int kPerWarpIters = kSortTile / kWarps / 32;     // 16
+    constexpr int kPerWarpIters = kSortTile / kWarps / 32;
+    constexpr uint32_t kStageBytes = kSortTile * (sizeof(K) + 4) + 1024;   // keys, payloads, hist row
     __shared__ uint32_t whist[kWarps][256];
-    __shared__ uint32_t tbase[256], dstart[256];
+    __shared__ uint32_t dstart[256], wsum[kWarps];
+    __shared__ uint32_t tbase_s[PIPE ? 1 : 256];
     __shared__ uint32_t stab[DECODE && sizeof(K) == 4 ? kSloRankMax : 1];
-    extern __shared__ __align__(16) unsigned char dyn[];      // staging: K[kSortTile] + u32[kSortTile]
-    uint64_t start, end;
-    const uint64_t tile = t0 + blockIdx.x;
-    tile_range(tile, n, window, tpw, start, end);
-    if (start >= end) return;
+    __shared__ __align__(8) uint64_t mbar[2];
+    extern __shared__ __align__(16) unsigned char dyn[];      // staging K[tile] + u32[tile] (+ 2 stages)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < kWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
-    if (tid < 256) tbase[tid] = hist[tile * 256 + tid];
-    if (DECODE && sizeof(K) == 4)
-        for (int i = tid; i < (int)kSloRankMax; i += kSortThreads) stab[i] = D.table[i];
-    __syncthreads();
-
-    K kr[kPerWarpIters];
-    uint32_t vr[kPerWarpIters], rank[kPerWarpIters];
-    const uint64_t base = start + (uint64_t)warp * (kPerWarpIters * 32);
-#pragma unroll
-    for (int r = 0; r < kPerWarpIters; ++r) {
-        uint64_t p = base + r * 32 + lane;
-        bool valid = p < end;
-        kr[r] = valid ? kin[p] : (K)0;
-        vr[r] = valid ? (vin ? vin[p] : (uint32_t)p) : 0u;     // vin == NULL: identity payload
-    }
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int r = 0; r < kPerWarpIters; ++r) {
-        uint64_t p = base + r * 32 + lane;
-        bool valid = p < end;
-        uint32_t act = __ballot_sync(0xffffffffu, valid);
-        uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
-        uint32_t peers = 0;
-        if (valid) {
-            peers = __match_any_sync(act, d);
-            rank[r] = whist[warp][d] + __popc(peers & lt);
-        }
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) whist[warp][d] += __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    if (tid < 256) {   // exclusive scan over warps, per digit; dstart = tile total of the digit
-        uint32_t run = 0;
-#pragma unroll
-        for (int wv = 0; wv < kWarps; ++wv) {
-            uint32_t c = whist[wv][tid];
-            whist[wv][tid] = run;
-            run += c;
-        }
-        dstart[tid] = run;
-    }
-    __syncthreads();
-    for (int off = 1; off < 256; off <<= 1) {   // inclusive scan of the digit totals
-        uint32_t v = (tid < 256 && tid >= off) ? dstart[tid - off] : 0u;
-        __syncthreads();
-        if (tid < 256) dstart[tid] += v;
-        __syncthreads();
-    }
-    // stage the tile in shared memory in (digit, rank) order, then write every digit bucket as
-    // one contiguous run: consecutive threads store consecutive addresses
     K *sk = reinterpret_cast<K *>(dyn);
     uint32_t *sv = reinterpret_cast<uint32_t *>(dyn + kSortTile * sizeof(K));
-#pragma unroll
-    for (int r = 0; r < kPerWarpIters; ++r) {
-        uint64_t p = base + r * 32 + lane;
-        if (p < end) {
-            const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
-            const uint32_t loc = (d ? dstart[d - 1] : 0u) + whist[warp][d] + rank[r];
-            sk[loc] = kr[r];
-            sv[loc] = vr[r];
+    unsigned char *stg = dyn + kSortTile * (sizeof(K) + 4);
+    // payload source of the tile: vin, or (first pass, packin) the caller's input lengths
+    const bool vsrc = vin != nullptr || D.packin;
+    const uint32_t *vptr = vin ? vin : D.in;
+    auto issue = [&](uint64_t tile, int s) {                  // one thread: stage s <- tile
+        uint64_t st_, en_;
+        tile_range(tile, n, window, tpw, st_, en_);
+        const uint32_t cnt = (uint32_t)(en_ - st_);
+        const uint32_t bk = (cnt * (uint32_t)sizeof(K)) & ~15u, bv = vsrc ? (cnt * 4u) & ~15u : 0u;
+        unsigned char *b = stg + s * kStageBytes;
+        mbar_expect_tx(&mbar[s], bk + bv + 1024u);
+        bulk_g2s(b + kSortTile * (sizeof(K) + 4), hist + tile * 256, 1024u, &mbar[s]);
+        if (bk) bulk_g2s(b, kin + st_, bk, &mbar[s]);
+        if (bv) bulk_g2s(b + kSortTile * sizeof(K), vptr + st_, bv, &mbar[s]);
+    };
+    if (DECODE && sizeof(K) == 4)
+        for (uint32_t i = tid; i < D.nslo; i += kSortThreads) stab[i] = D.table[i];
+    if (PIPE) {
+        if (tid == 0) {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            if (blockIdx.x < ntiles) issue(t0 + blockIdx.x, 0);
         }
+        __syncthreads();
     }
-    __syncthreads();
-    const uint32_t cnt = (uint32_t)(end - start);
-    for (uint32_t i = tid; i < cnt; i += kSortThreads) {
-        const K key = sk[i];
-        const uint32_t d = (uint32_t)(key >> shift) & 0xffu;
-        const uint32_t pos = tbase[d] + i - (d ? dstart[d - 1] : 0u);
-        const uint32_t idx = sv[i];
-        if (DECODE) {           // a4 fused: records at the final scheduled position
-            if (sizeof(K) == 8) {
-                D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
-                D.rout[pos] = (uint32_t)key;
-            } else {
-                const uint32_t k32 = (uint32_t)key;
-                D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
-                D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
-            }
-            D.order[pos] = idx;
-            D.rin[pos] = __ldg(D.in + idx);
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t it = 0;; ++it) {
+        const uint64_t tl = (uint64_t)blockIdx.x + (PIPE ? (uint64_t)it * gridDim.x : 0ull);
+        if (tl >= ntiles || (!PIPE && it > 0)) break;
+        const uint64_t tile = t0 + tl;
+        const int s = (int)(it & 1u);
+        if (PIPE && tid == 0 && tl + gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);   // stage s^1: read last round
+        uint64_t start, end;
+        tile_range(tile, n, window, tpw, start, end);
+        const uint32_t cnt = (uint32_t)(end - start);
+        const uint64_t wt0 = (tile / tpw) * tpw;                 // first tile of this window
+        const uint64_t wp0 = (tile / tpw) * window;              // first position of this window
+        const K *bkp = reinterpret_cast<const K *>(stg + s * kStageBytes);
+        const uint32_t *bvp = reinterpret_cast<const uint32_t *>(stg + s * kStageBytes + kSortTile * sizeof(K));
+        const uint32_t *tbase = PIPE ? reinterpret_cast<const uint32_t *>(stg + s * kStageBytes + kSortTile * (sizeof(K) + 4))
+                                     : tbase_s;
+        for (int i = tid; i < kWarps * 256; i += kSortThreads) (&whist[0][0])[i] = 0;
+        if (!PIPE) {
+            if (start >= end) return;
+            if (tid < 256) tbase_s[tid] = hist[tile * 256 + tid];
         } else {
-            kout[pos] = key;
-            vout[pos] = idx;
+            mbar_wait(&mbar[s], (it >> 1) & 1u);
+            // the bulk copies moved whole 16-byte granules: the last few keys / payloads directly
+            K *bk_w = const_cast<K *>(bkp);
+            uint32_t *bv_w = const_cast<uint32_t *>(bvp);
+            const uint32_t ck = ((cnt * (uint32_t)sizeof(K)) & ~15u) / (uint32_t)sizeof(K);
+            const uint32_t cv = vsrc ? ((cnt * 4u) & ~15u) / 4u : cnt;
+            for (uint32_t i = ck + tid; i < cnt; i += kSortThreads) bk_w[i] = kin[start + i];
+            for (uint32_t i = cv + tid; i < cnt; i += kSortThreads) bv_w[i] = vptr[start + i];
         }
+        __syncthreads();
+
+        K kr[kPerWarpIters];
+        uint32_t vr[kPerWarpIters], rank[kPerWarpIters];
+        const uint32_t base = (uint32_t)warp * (kPerWarpIters * 32);   // offset in the tile
+#pragma unroll
+        for (int r = 0; r < kPerWarpIters; ++r) {
+            const uint32_t o = base + r * 32 + lane;
+            const bool valid = o < cnt;
+            const uint64_t p = start + o;
+            uint32_t v = 0;
+            if (PIPE) {
+                kr[r] = valid ? bkp[o] : (K)0;
+                if (valid) v = vsrc ? bvp[o] : (uint32_t)p;
+            } else {
+                kr[r] = valid ? kin[p] : (K)0;
+                if (valid) v = vin ? vin[p] : D.packin ? __ldg(D.in + p) : (uint32_t)p;
+            }
+            // first pass with packin: window-local index and input length (no gather at decode)
+            if (!vin && D.packin) v = (uint32_t)(p - wp0) | ((v - 1u) << D.wb);
+            vr[r] = v;
+        }
+#pragma unroll
+        for (int r = 0; r < kPerWarpIters; ++r) {
+            const bool valid = base + r * 32 + lane < cnt;
+            const uint32_t act = __ballot_sync(0xffffffffu, valid);
+            const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
+            uint32_t peers = 0;
+            if (valid) {
+                peers = __match_any_sync(act, d);
+                rank[r] = whist[warp][d] + __popc(peers & lt);
+            }
+            __syncwarp();
+            if (valid && lane == __ffs(peers) - 1) whist[warp][d] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        {   // exclusive scan over warps, per digit; dstart = tile total of the digit
+            uint32_t run = 0;
+#pragma unroll
+            for (int wv = 0; wv < kWarps; ++wv) {
+                const uint32_t c = whist[wv][tid];
+                whist[wv][tid] = run;
+                run += c;
+            }
+            // inclusive scan of the 256 digit totals: warp shuffles, then the 8 warp sums
+            static_assert(kSortThreads == 256, "one thread per digit");
+            uint32_t v = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            if (lane == 31) wsum[warp] = v;
+            __syncthreads();
+            uint32_t add = 0;
+            for (int q = 0; q < warp; ++q) add += wsum[q];
+            dstart[tid] = v + add;
+            __syncthreads();
+        }
+        // stage the tile in shared memory in (digit, rank) order
+#pragma unroll
+        for (int r = 0; r < kPerWarpIters; ++r) {
+            if (base + r * 32 + lane < cnt) {
+                const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
+                const uint32_t loc = (d ? dstart[d - 1] : 0u) + whist[warp][d] + rank[r];
+                sk[loc] = kr[r];
+                sv[loc] = vr[r];
+            }
+        }
+        __syncthreads();
+        // every digit bucket as one contiguous run: consecutive threads store consecutive addresses
+        for (uint32_t i0 = tid - lane; i0 < cnt; i0 += kSortThreads) {   // whole warps iterate together
+            const uint32_t i = i0 + lane;
+            const bool valid = i < cnt;
+            K key = 0;
+            uint32_t pos = 0;
+            if (valid) {
+                key = sk[i];
+                const uint32_t d = (uint32_t)(key >> shift) & 0xffu;
+                pos = tbase[d] + i - (d ? dstart[d - 1] : 0u);
+            }
+            if (NEXT) {
+                const uint32_t act = __ballot_sync(0xffffffffu, valid);
+                if (valid) {
+                    const uint32_t slot = (uint32_t)(wt0 + ((pos - wp0) / kSortTile)) * 256u +
+                                          ((uint32_t)(key >> shift_next) & 0xffu);
+                    const uint32_t peers = __match_any_sync(act, slot);
+                    if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(hist_next + slot, (uint32_t)__popc(peers));
+                }
+            }
+            if (!valid) continue;
+            const uint32_t idx = sv[i];
+            if (DECODE) {
+                if (sizeof(K) == 8) {
+                    D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
+                    D.rout[pos] = (uint32_t)key;
+                } else {
+                    const uint32_t k32 = (uint32_t)key;
+                    D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
+                    D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
+                }
+                if (D.packin) {
+                    D.order[pos] = (uint32_t)wp0 + (idx & ((1u << D.wb) - 1u));
+                    D.rin[pos] = (idx >> D.wb) + 1u;
+                } else {
+                    D.order[pos] = idx;
+                    D.rin[pos] = __ldg(D.in + idx);
+                }
+            } else {
+                kout[pos] = key;
+                vout[pos] = idx;
+            }
+        }
+        // staging and stage s are free for the next round; the generic-proxy accesses of this round
+        // are ordered before the next round's bulk copies (async proxy) into the same buffer
+        if (PIPE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
     }
+}
+
+// launches one scatter pass (pipelined persistent kernel when the TMA copies are 16-byte aligned)
+template <class K, bool DECODE, bool NEXT>
+static cudaError_t launch_down(bool pipe, const K *kin, const uint32_t *vin, K *kout, uint32_t *vout,
+                               const uint32_t *hist, uint64_t n, uint64_t window, uint64_t tpw, int shift,
+                               const DecodeArgs &D, uint64_t t0, uint64_t tiles, uint32_t *hist_next, int shift_next,
+                               cudaStream_t st)
+{
+    const size_t stage = kSortTile * (sizeof(K) + sizeof(uint32_t));
+    if (!pipe) {
+        cudaFuncSetAttribute(k_sort_down<K, DECODE, NEXT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
+        k_sort_down<K, DECODE, NEXT, false><<<(unsigned)tiles, kSortThreads, stage, st>>>(
+            kin, vin, kout, vout, hist, n, window, tpw, shift, D, t0, tiles, hist_next, shift_next);
+        return cudaGetLastError();
+    }
+    const size_t smem = stage + 2 * (stage + 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_sort_down<K, DECODE, NEXT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sort_down<K, DECODE, NEXT, true>, kSortThreads, smem);
+    if (per < 1) per = 1;
+    const uint64_t grid = tiles < (uint64_t)nsm * per ? tiles : (uint64_t)nsm * per;
+    k_sort_down<K, DECODE, NEXT, true><<<(unsigned)grid, kSortThreads, smem, st>>>(
+        kin, vin, kout, vout, hist, n, window, tpw, shift, D, t0, tiles, hist_next, shift_next);
+    return cudaGetLastError();
 }
 
 template <class K>
 static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, K *keys_a, uint32_t *vals_a,
-                                   K *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n, uint64_t window,
-                                   uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
+                                   K *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2, uint64_t n,
+                                   uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
                                    cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
 {
     *passes = 0;
@@ -239,31 +396,45 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
     const uint64_t tiles = tpw * nwin, t0 = tpw * w_first;
     const K *kin = *keys_io;
     const uint32_t *vin = *vals_io;
-    int last = -1;
-    for (int d = 0; d < (int)sizeof(K); ++d) if (digit_mask >> d & 1u) last = d;
     const DecodeArgs D0 = dec ? *dec : DecodeArgs{};
+    uint32_t *hcur = hist, *hnext = hist2;
+    bool ready = hist0_ready;                  // hcur already holds this pass's per-tile counts
     for (int d = 0; d < (int)sizeof(K); ++d) {
         if (!(digit_mask >> d & 1u)) continue;
+        int dn = -1;                           // the next pass's digit
+        for (int q = d + 1; q < (int)sizeof(K); ++q) if (digit_mask >> q & 1u) { dn = q; break; }
         K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
-        if (!(hist0_ready && *passes == 0))
-            k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hist, n, window, tpw, 8 * d, t0);
-        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hist, n, window, tpw, w_first);
-        const size_t stage = kSortTile * (sizeof(K) + sizeof(uint32_t));
-        if (dec && d == last) {
-            cudaFuncSetAttribute(k_sort_down<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
-            k_sort_down<K, true><<<(unsigned)tiles, kSortThreads, stage, st>>>(kin, vin, kout, vout, hist, n, window,
-                                                                              tpw, 8 * d, D0, t0);
+        if (!ready)
+            k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hcur, n, window, tpw, 8 * d, t0);
+        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hcur, n, window, tpw, w_first);
+        // TMA bulk copies need 16-byte aligned tile starts: every tile of a window starts at a
+        // multiple of kSortTile, so window starts (and the base pointers) must be aligned
+        const bool vals_ok = vin ? ((uintptr_t)vin & 15u) == 0 : (!D0.packin || ((uintptr_t)D0.in & 15u) == 0);
+        // (u64 keys: 83 KB per pipelined CTA leaves 2 CTAs per SM -- measured slower than the
+        // one-tile kernel on c5, 0.94 vs 0.73 ms)
+        const bool pipe = UELLM_SORT_PIPE && sizeof(K) == 4 && ((uintptr_t)kin & 15u) == 0 && vals_ok &&
+                          (nwin + w_first == 1 || (window * sizeof(K)) % 16 == 0) && (window * 4) % 16 == 0;
+        cudaError_t e;
+        if (dn >= 0) {
+            if ((e = cudaMemsetAsync(hnext + t0 * 256, 0, tiles * 256 * sizeof(uint32_t), st))) return e;
+            e = launch_down<K, false, true>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
+                                            hnext, 8 * dn, st);
+        } else if (dec) {
+            e = launch_down<K, true, false>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
+                                            nullptr, 0, st);
         } else {
-            cudaFuncSetAttribute(k_sort_down<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage);
-            k_sort_down<K, false><<<(unsigned)tiles, kSortThreads, stage, st>>>(kin, vin, kout, vout, hist, n, window,
-                                                                               tpw, 8 * d, D0, t0);
+            e = launch_down<K, false, false>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
+                                             nullptr, 0, st);
         }
-        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         kin = kout;
         vin = vout;
         ++*passes;
+        uint32_t *tmp = hcur; hcur = hnext; hnext = tmp;
+        ready = true;
     }
     *keys_io = kin;
     *vals_io = vin;
@@ -272,37 +443,38 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
 
 cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_t **vals_io,
                                unsigned long long *keys_a, uint32_t *vals_a,
-                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist,
+                               unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
                                int *passes, cudaStream_t st, const DecodeArgs *dec)
 {
-    return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window,
-                                               w_first, nwin, digit_mask, passes, st, false, dec);
+    return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, hist2, n,
+                                               window, w_first, nwin, digit_mask, passes, st, false, dec);
 }
 
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
-                                 uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint64_t n,
-                                 uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
-                                 cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
+                                 uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
+                                 uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
+                                 int *passes, cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
 {
-    return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, n, window, w_first,
-                                     nwin, digit_mask, passes, st, hist0_ready, dec);
+    return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, hist2, n, window,
+                                     w_first, nwin, digit_mask, passes, st, hist0_ready, dec);
 }
 
 // a2 (compressed key) fused with the digit-0 histogram of the first radix pass:
-// key32 = rank(slo_us) << ob | out per 4096-query tile, payload = arrival index.
+// key32 = rank(slo_us) << ob | out per 2048-query tile, payload = arrival index (implicit).
+// The rank comes from the compact (value, rank) hash of k_slo_table (2^cbits slots).
 __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__restrict__ out,
                                                               const float *__restrict__ slo, uint64_t n,
                                                               uint64_t window, uint64_t tpw,
-                                                              const uint32_t *__restrict__ slo_set,
-                                                              const uint32_t *__restrict__ rank_of_slot, int ob,
-                                                              uint32_t *__restrict__ keys32, uint32_t *__restrict__ vals,
+                                                              const unsigned long long *__restrict__ ctab, int cbits,
+                                                              int ob, uint32_t *__restrict__ keys32,
                                                               uint32_t *__restrict__ hist, uint64_t t0)
 {
-    __shared__ uint32_t sset[kSloSetSize], srank[kSloSetSize];
+    extern __shared__ unsigned long long sct[];
     __shared__ uint32_t h[256];
     const int tid = threadIdx.x;
-    for (uint32_t i = tid; i < kSloSetSize; i += kSortThreads) { sset[i] = slo_set[i]; srank[i] = rank_of_slot[i]; }
+    const uint32_t C = 1u << cbits;
+    for (uint32_t i = tid; i < C; i += kSortThreads) sct[i] = ctab[i];
     if (tid < 256) h[tid] = 0;
     __syncthreads();
     uint64_t start, end;
@@ -325,9 +497,10 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
         if (valid) {
             bool ok;
             const uint32_t su = slo_to_us(fr[i], ok);
-            uint32_t hh = slo_hash(su, kSloSetBits);
-            while (sset[hh] != su) hh = (hh + 1) & (kSloSetSize - 1);
-            const uint32_t key = (srank[hh] << ob) | orr[i];
+            uint32_t hh = slo_hash(su, (uint32_t)cbits);
+            unsigned long long e = sct[hh];
+            while ((uint32_t)(e >> 32) != su) { hh = (hh + 1) & (C - 1); e = sct[hh]; }
+            const uint32_t key = ((uint32_t)e << ob) | orr[i];
             keys32[p] = key;                       // payload = arrival index p: implicit (NULL vals)
             const uint32_t d = key & 0xffu;
             const uint32_t peers = __match_any_sync(act, d);
@@ -339,13 +512,14 @@ __global__ void __launch_bounds__(kSortThreads) k_pack32_hist(const uint32_t *__
 }
 
 cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t w_first,
-                               uint64_t nwin, const uint32_t *slo_set, const uint32_t *rank_of_slot, int ob,
-                               uint32_t *keys32, uint32_t *vals, uint32_t *hist0, cudaStream_t st)
+                               uint64_t nwin, const unsigned long long *ctab, int cbits, int ob, uint32_t *keys32,
+                               uint32_t *vals, uint32_t *hist0, cudaStream_t st)
 {
+    (void)vals;
     if (n == 0) return cudaSuccess;
     const uint64_t tpw = ceil_div(window, kSortTile);
-    k_pack32_hist<<<(unsigned)(tpw * nwin), kSortThreads, 0, st>>>(out, slo, n, window, tpw, slo_set, rank_of_slot,
-                                                                  ob, keys32, vals, hist0, tpw * w_first);
+    k_pack32_hist<<<(unsigned)(tpw * nwin), kSortThreads, sizeof(unsigned long long) << cbits, st>>>(
+        out, slo, n, window, tpw, ctab, cbits, ob, keys32, hist0, tpw * w_first);
     return cudaGetLastError();
 }
 
