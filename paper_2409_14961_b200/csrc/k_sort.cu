@@ -121,6 +121,9 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__res
 #ifndef UELLM_SORT_PIPE
 #define UELLM_SORT_PIPE 1
 #endif
+#ifndef UELLM_SORT_NEXT
+#define UELLM_SORT_NEXT 1            // the scatter counts the next pass's digits (no k_sort_up)
+#endif
 #ifndef UELLM_SORT_DOWN_MINB
 #define UELLM_SORT_DOWN_MINB 5
 #endif
@@ -159,8 +162,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // next pass then needs no histogram kernel of its own); a warp's (tile, digit) pairs are
 // aggregated with match.any first.
 // DECODE (last pass): a4 fused -- records written straight at the scheduled position.
+#ifndef UELLM_SORT_PIPE_MINB
+#define UELLM_SORT_PIPE_MINB 4
+#endif
 template <class K, bool DECODE, bool NEXT, bool PIPE>
-__global__ void __launch_bounds__(kSortThreads, PIPE ? 1 : UELLM_SORT_DOWN_MINB)
+__global__ void __launch_bounds__(kSortThreads, PIPE ? UELLM_SORT_PIPE_MINB : UELLM_SORT_DOWN_MINB)
 k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
             uint32_t *__restrict__ vout, const uint32_t *__restrict__ hist, uint64_t n, uint64_t window,
             uint64_t tpw, int shift, DecodeArgs D, uint64_t t0, uint64_t ntiles, uint32_t *__restrict__ hist_next,
@@ -174,11 +180,12 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
     __shared__ uint32_t tbase_s[PIPE ? 1 : 256];
     __shared__ uint32_t stab[DECODE && sizeof(K) == 4 ? kSloRankMax : 1];
     __shared__ __align__(8) uint64_t mbar[2];
-    extern __shared__ __align__(16) unsigned char dyn[];      // staging K[tile] + u32[tile] (+ 2 stages)
+    // dynamic smem: PIPE: 2 stages {keys, payloads, hist row}; a stage's keys / payloads are in
+    // registers after the first phase, so its buffer doubles as the (digit, rank) staging area.
+    // !PIPE: the staging area only.
+    extern __shared__ __align__(16) unsigned char dyn[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    K *sk = reinterpret_cast<K *>(dyn);
-    uint32_t *sv = reinterpret_cast<uint32_t *>(dyn + kSortTile * sizeof(K));
-    unsigned char *stg = dyn + kSortTile * (sizeof(K) + 4);
+    unsigned char *stg = dyn;
     // payload source of the tile: vin, or (first pass, packin) the caller's input lengths
     const bool vsrc = vin != nullptr || D.packin;
     const uint32_t *vptr = vin ? vin : D.in;
@@ -216,6 +223,8 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
         const uint32_t cnt = (uint32_t)(end - start);
         const uint64_t wt0 = (tile / tpw) * tpw;                 // first tile of this window
         const uint64_t wp0 = (tile / tpw) * window;              // first position of this window
+        K *sk = reinterpret_cast<K *>(stg + (PIPE ? s * kStageBytes : 0));
+        uint32_t *sv = reinterpret_cast<uint32_t *>(stg + (PIPE ? s * kStageBytes : 0) + kSortTile * sizeof(K));
         const K *bkp = reinterpret_cast<const K *>(stg + s * kStageBytes);
         const uint32_t *bvp = reinterpret_cast<const uint32_t *>(stg + s * kStageBytes + kSortTile * sizeof(K));
         const uint32_t *tbase = PIPE ? reinterpret_cast<const uint32_t *>(stg + s * kStageBytes + kSortTile * (sizeof(K) + 4))
@@ -294,7 +303,8 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
             dstart[tid] = v + add;
             __syncthreads();
         }
-        // stage the tile in shared memory in (digit, rank) order
+        // stage the tile in shared memory in (digit, rank) order (PIPE: over the stage buffer, whose
+        // reads all precede the __syncthreads of the scan above)
 #pragma unroll
         for (int r = 0; r < kPerWarpIters; ++r) {
             if (base + r * 32 + lane < cnt) {
@@ -306,8 +316,10 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
         }
         __syncthreads();
         // every digit bucket as one contiguous run: consecutive threads store consecutive addresses
-        for (uint32_t i0 = tid - lane; i0 < cnt; i0 += kSortThreads) {   // whole warps iterate together
-            const uint32_t i = i0 + lane;
+#pragma unroll 4
+        for (uint32_t r = 0; r < kSortItems; ++r) {                      // whole warps iterate together
+            const uint32_t i = r * kSortThreads + tid;
+            if (r * kSortThreads + (uint32_t)(tid - lane) >= cnt) break;
             const bool valid = i < cnt;
             K key = 0;
             uint32_t pos = 0;
@@ -369,7 +381,7 @@ static cudaError_t launch_down(bool pipe, const K *kin, const uint32_t *vin, K *
             kin, vin, kout, vout, hist, n, window, tpw, shift, D, t0, tiles, hist_next, shift_next);
         return cudaGetLastError();
     }
-    const size_t smem = stage + 2 * (stage + 1024);
+    const size_t smem = 2 * (stage + 1024);
     cudaError_t e = cudaFuncSetAttribute(k_sort_down<K, DECODE, NEXT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -403,6 +415,7 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         if (!(digit_mask >> d & 1u)) continue;
         int dn = -1;                           // the next pass's digit
         for (int q = d + 1; q < (int)sizeof(K); ++q) if (digit_mask >> q & 1u) { dn = q; break; }
+        const bool fuse_next = UELLM_SORT_NEXT && dn >= 0;
         K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
         if (!ready)
@@ -416,16 +429,16 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         const bool pipe = UELLM_SORT_PIPE && sizeof(K) == 4 && ((uintptr_t)kin & 15u) == 0 && vals_ok &&
                           (nwin + w_first == 1 || (window * sizeof(K)) % 16 == 0) && (window * 4) % 16 == 0;
         cudaError_t e;
-        if (dn >= 0) {
+        if (fuse_next) {
             if ((e = cudaMemsetAsync(hnext + t0 * 256, 0, tiles * 256 * sizeof(uint32_t), st))) return e;
             e = launch_down<K, false, true>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
                                             hnext, 8 * dn, st);
-        } else if (dec) {
-            e = launch_down<K, true, false>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
-                                            nullptr, 0, st);
-        } else {
+        } else if (dn >= 0 || !dec) {
             e = launch_down<K, false, false>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
                                              nullptr, 0, st);
+        } else {
+            e = launch_down<K, true, false>(pipe, kin, vin, kout, vout, hcur, n, window, tpw, 8 * d, D0, t0, tiles,
+                                            nullptr, 0, st);
         }
         if (e != cudaSuccess) return e;
         e = cudaGetLastError();
@@ -434,7 +447,7 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         vin = vout;
         ++*passes;
         uint32_t *tmp = hcur; hcur = hnext; hnext = tmp;
-        ready = true;
+        ready = fuse_next;
     }
     *keys_io = kin;
     *vals_io = vin;
