@@ -280,6 +280,7 @@ def main():
                     help="process-group backend for N > 1 (gloo only for multi-rank tests on one GPU)")
     ap.add_argument("--e2e-groups", type=int, default=0, help="window groups of the pipelined e2e call (0 = 12)")
     ap.add_argument("--dp-tile", type=int, default=0, help="SEG-DP tile length override (tuning only)")
+    ap.add_argument("--no-graph", action="store_true", help="time the eager step instead of its CUDA graph")
     ap.add_argument("--mode", default="seg_dp", choices=["seg_dp", "slo_odbs", "fifo", "sort_only"],
                     help="segmentation mode (default: the SEG-DP hot path)")
     args = ap.parse_args()
@@ -338,13 +339,18 @@ def main():
             for e in row:
                 e.record(stream)          # materialise the cudaEvent_t handles
 
-    def step(k=None):
+    def step(k=None, sync_load=False):
         if k is not None:
             ld[k][0].record(stream)
-        g.load(d_in, d_out, d_slo, stream)
+        if sync_load or g.profile is None:
+            g.load(d_in, d_out, d_slo, stream)        # validates on the host, fixes the profile's decisions
+        else:
+            g.reload(d_in, d_out, d_slo, stream)      # same validation on the device, no host sync
         if k is not None:
             ld[k][1].record(stream)
             U.set_stage_events(g.profile, ev[k])
+        elif g.profile is not None:
+            U.set_stage_events(g.profile, [])
         g.schedule(stream)
         g.stats(stream)
         if X is not None:   # a9: pack -> ONE allgather -> every rank rebuilds the job
@@ -357,18 +363,47 @@ def main():
             if k is not None:
                 xe[k][1].record(stream)
 
-    for _ in range(Wm):
+    step(sync_load=True)
+    for _ in range(Wm - 1):
         step()
     torch.cuda.synchronize(dev)
+    # the whole step (reload -> schedule -> stats [-> a9 pack / NCCL allgather / combine]) captured
+    # once as a CUDA graph and replayed: one launch per step, no host synchronisation inside it
+    graph, graph_err = None, None
+    if not args.no_graph and (world == 1 or args.dist_backend == "nccl"):
+        try:
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=stream, capture_error_mode="thread_local"):
+                step()
+            graph = cg
+            for _ in range(2):
+                with torch.cuda.stream(stream):
+                    graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as ex:      # (recorded in the JSON line; the eager step is timed instead)
+            graph, graph_err = None, f"{type(ex).__name__}: {ex}"[:300]
+            torch.cuda.synchronize(dev)
+
+    def timed_step(k=None):
+        if graph is not None:
+            with torch.cuda.stream(stream):
+                graph.replay()
+        else:
+            step()
     clocks = ClockSampler(local)
     time.sleep(0.3)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    ms_step = time_steps(step, K, stream, dev)
+    ms_step = time_steps(timed_step, K, stream, dev)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    status = int(g.status_word().item())
+    if status != 0:
+        raise SystemExit(f"device status word {status} after the timed steps")
+    # per-stage device times: the same step run eagerly with the library's stage events
+    ms_eager = time_steps(step, K, stream, dev)
     t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -522,6 +557,10 @@ def main():
                        "l2": "inputs 1.2 GB >> 126 MB L2; no flush needed",
                        "parallelism": f"{world} rank(s), contiguous window blocks of one job; a9: one allgather "
                                       f"of [totals | boundary bitmap] records, job rebuilt on every rank"},
+            "step_launch": {"cuda_graph": graph is not None, "graph_error": graph_err,
+                            "eager_ms_per_step": ms_eager,
+                            "load": "uellm_profile_reload (device-side validation, no host sync); "
+                                    "one synchronising uellm_profile_load before the timed region"},
             "roofline": roof, "step_hbm_roofline": step_hbm,
             "stage_hbm": stage_hbm(st_ms, n, m, diag["sort_passes"], hbm_gbs), "stage_ms": st_ms,
             # our kernels launched inside the timed region: K steps x (load + schedule + stats [+ a9])

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define UELLM_ABI_VERSION 2u
+#define UELLM_ABI_VERSION 3u
 
 typedef int32_t uellm_status;
 enum {
@@ -60,7 +60,10 @@ enum {
     UELLM_ERR_CONFIG = 3,       /* config invariant violated                       */
     UELLM_ERR_OVERFLOW = 4,     /* a KV-byte or cost bound could overflow 64 bits          */
     UELLM_ERR_CUDA = 5,         /* a CUDA runtime call or kernel launch failed                     */
-    UELLM_ERR_UNSUPPORTED = 6   /* valid, but outside this build's limits (e.g. max_batch > 4096)  */
+    UELLM_ERR_UNSUPPORTED = 6,  /* valid, but outside this build's limits (e.g. max_batch > 4096)  */
+    UELLM_ERR_STALE = 7         /* uellm_profile_reload: the new queries need other decisions than
+                                   the profile holds (larger maxima, other SLO set size, new
+                                   varying key bits): load them with uellm_profile_load          */
 };
 
 /* Segmentation of the sorted stream (uellm_config.mode). */
@@ -222,6 +225,26 @@ size_t uellm_workspace_bytes(uint64_t n, const uellm_config *cfg);
  * does not fit 64 bits.  Synchronises `stream` once (64-byte validation record). */
 uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg, void *ws,
                                 size_t ws_bytes, void *stream, uellm_profile *out);
+
+/* Load the next n profiled queries into an existing profile WITHOUT a host synchronisation, so
+ * that reload -> schedule -> stats can be enqueued (or captured in one CUDA graph) per step.
+ *   p          [host] profile from uellm_profile_load with the same n and cfg; updated in place.
+ *   q          [host] query SoA whose arrays are [device] (UELLM_ERR_ARG otherwise; same contract
+ *              as uellm_profile_load: unchanged until the last call on the profile).
+ * The validation of uellm_profile_load runs on the device and its verdict goes to the profile's
+ * device status word (uellm_profile_status): UELLM_OK; UELLM_ERR_CONTRACT for an invalid query;
+ * UELLM_ERR_STALE when the new queries exceed the decisions the profile was loaded with
+ * (max_in or max_out larger, another number of distinct SLO values or a distinct-set overflow,
+ * key bits varying that were constant).  Every decision the later calls take from the profile
+ * stays valid for queries inside those limits (the cost and KV overflow bounds, the 32-bit DP
+ * path and the packed sort payload only need maxima not above the recorded ones; the radix
+ * passes cover every digit that varied before).  The schedule / stats of a step whose status
+ * word is not UELLM_OK are undefined: read the word (asynchronously) before using them. */
+uellm_status uellm_profile_reload(uellm_profile *p, const uellm_queries *q, const uellm_config *cfg,
+                                  void *stream);
+
+/* Device address of the profile's status word (uint32_t, written by uellm_profile_reload). [host] */
+uellm_status uellm_profile_status(const uellm_profile *p, uint32_t **device_word);
 
 /* Sort and segment the loaded queries (Alg. 1 stages 1-3; SEG-DP, R14).
  *   p              [host] profile from uellm_profile_load (same cfg).

@@ -208,6 +208,7 @@ const char *uellm_status_string(uellm_status s)
     case UELLM_ERR_OVERFLOW: return "UELLM_ERR_OVERFLOW";
     case UELLM_ERR_CUDA: return "UELLM_ERR_CUDA";
     case UELLM_ERR_UNSUPPORTED: return "UELLM_ERR_UNSUPPORTED";
+    case UELLM_ERR_STALE: return "UELLM_ERR_STALE";
     default: return "UELLM_ERR_UNKNOWN";
     }
 }
@@ -240,6 +241,7 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     v.cfg_hash = layout_key(cfg);
     v.diag_off = L.diag;
     v.wincost_off = L.wincost;
+    v.meta_off = L.meta;
     if (n == 0) {
         std::memcpy(out, &v, sizeof v);
         return UELLM_OK;
@@ -281,6 +283,42 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     v.key_or = hm.key_or; v.key_and = hm.key_and;
     v.slo_distinct = hm.slo_distinct; v.slo_overflow = hm.slo_overflow;
     std::memcpy(out, &v, sizeof v);
+    return UELLM_OK;
+}
+
+uellm_status uellm_profile_reload(uellm_profile *p, const uellm_queries *q, const uellm_config *cfg, void *stream)
+{
+    if (!p || !q || !cfg) return UELLM_ERR_ARG;
+    ProfileView v;
+    std::memcpy(&v, p, sizeof v);
+    if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg) || q->n != v.n) return UELLM_ERR_ARG;
+    const uint64_t n = v.n;
+    if (n == 0) return UELLM_OK;
+    if (!is_device_ptr(q->input_len) || !is_device_ptr(q->pred_out_len) || !is_device_ptr(q->slo_s))
+        return UELLM_ERR_ARG;
+    const WsLayout L = make_layout(n, *cfg);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = v.ws;
+    LoadMeta *meta = at<LoadMeta>(w, L.meta);
+    CU(cudaMemsetAsync(meta, 0, sizeof(LoadMeta), st));
+    CU(cudaMemsetAsync(&meta->key_and, 0xff, sizeof(unsigned long long), st));
+    CU(cudaMemsetAsync(at<uint32_t>(w, L.slo_set), 0, 4 * kSloSetSize, st));
+    CU(launch_load(q->input_len, q->pred_out_len, q->slo_s, n, meta, at<uint32_t>(w, L.slo_set), st));
+    ReloadRef ref;
+    ref.max_in = v.max_in; ref.max_out = v.max_out; ref.slo_distinct = v.slo_distinct;
+    ref.slo_overflow = v.slo_overflow; ref.key_or = v.key_or; ref.key_and = v.key_and;
+    CU(launch_reload_check(meta, ref, st));
+    v.d_in = q->input_len; v.d_out = q->pred_out_len; v.d_slo = q->slo_s;
+    std::memcpy(p, &v, sizeof v);
+    return UELLM_OK;
+}
+
+uellm_status uellm_profile_status(const uellm_profile *p, uint32_t **device_word)
+{
+    if (!p || !device_word) return UELLM_ERR_ARG;
+    const ProfileView &v = *view_of(p);
+    if (v.magic != kProfileMagic) return UELLM_ERR_ARG;
+    *device_word = &reinterpret_cast<LoadMeta *>(v.ws + v.meta_off)->status;
     return UELLM_OK;
 }
 
@@ -770,8 +808,16 @@ uellm_status uellm_exchange_combine(const void *gathered, uint32_t world, uint64
     uint8_t *w = (uint8_t *)ws;
     const bool dev_tot = is_device_ptr(totals);
     uellm_totals *d_tot = dev_tot ? totals : at<uellm_totals>(w, X.totals);
-    // (a pageable host->device copy returns once the source has been staged)
-    CU(cudaMemcpyAsync(at<unsigned long long>(w, X.qb), query_begin, 8ull * (world + 1), cudaMemcpyHostToDevice, st));
+    // query_begin goes down as kernel parameters (a pageable host->device copy would synchronise
+    // the stream first, and cannot be captured in a CUDA graph)
+    unsigned long long *dqb = at<unsigned long long>(w, X.qb);
+    for (uint32_t r0 = 0; r0 <= world; r0 += 4) {
+        const uint32_t c = world + 1 - r0 < 4 ? world + 1 - r0 : 4;
+        CU(launch_set_u64s(st, {{dqb + r0, query_begin[r0]},
+                                {dqb + r0 + (c > 1 ? 1 : 0), query_begin[r0 + (c > 1 ? 1 : 0)]},
+                                {dqb + r0 + (c > 2 ? 2 : 0), query_begin[r0 + (c > 2 ? 2 : 0)]},
+                                {dqb + r0 + (c > 3 ? 3 : 0), query_begin[r0 + (c > 3 ? 3 : 0)]}}));
+    }
     CU(run_exchange_combine((const uint8_t *)gathered, world, exchange_record_bytes(n_max),
                             at<unsigned long long>(w, X.qb), n_total, at<uint32_t>(w, X.bitmap),
                             at<uint32_t>(w, X.wscan), at<uint32_t>(w, X.blocksum), batch_offsets,

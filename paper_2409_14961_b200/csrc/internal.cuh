@@ -55,9 +55,16 @@ struct LoadMeta {
     uint32_t max_in, max_out, max_slo;
     unsigned long long key_or, key_and;
     uint32_t slo_distinct, slo_overflow;
-    uint32_t pad[6];
+    uint32_t status;         // uellm_profile_reload's verdict (device status word)
+    uint32_t pad[5];
 };
 static_assert(sizeof(LoadMeta) == 64, "LoadMeta is 64 bytes");
+// reload: compare the fresh LoadMeta with the decisions recorded in the profile
+struct ReloadRef {
+    uint32_t max_in, max_out, slo_distinct, slo_overflow;
+    unsigned long long key_or, key_and;
+};
+cudaError_t launch_reload_check(LoadMeta *meta, ReloadRef ref, cudaStream_t st);
 
 // Per-tile state of the SEG-DP and the traceback (one record per tile).
 struct TileRec {
@@ -163,7 +170,8 @@ struct ProfileView {
     void *events[UELLM_STAGE_COUNT];              // caller cudaEvent_t handles (stage timing)
     uint32_t slo_distinct, slo_overflow;
     const float *d_slo;                           // caller device SLO array or its staging copy
-    uint64_t pad[9];
+    uint64_t meta_off;                            // workspace offset of the LoadMeta (status word)
+    uint64_t pad[8];
 };
 static_assert(sizeof(ProfileView) <= sizeof(uellm_profile), "ProfileView fits uellm_profile");
 

@@ -142,6 +142,26 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
     }
 }
 
+// uellm_profile_reload: the verdict on the freshly loaded queries against the profile's decisions
+// (every decision of the schedule / stats calls is monotone in these limits, see uellm.h)
+__global__ void k_reload_check(LoadMeta *meta, ReloadRef ref)
+{
+    const LoadMeta m = *meta;
+    uint32_t st = UELLM_OK;
+    if (m.bad) st = UELLM_ERR_CONTRACT;
+    else if (m.max_in > ref.max_in || m.max_out > ref.max_out || m.slo_distinct != ref.slo_distinct ||
+             m.slo_overflow != ref.slo_overflow || (m.key_or & ~ref.key_or) != 0ull ||
+             (~m.key_and & ref.key_and) != 0ull)
+        st = UELLM_ERR_STALE;
+    meta->status = st;
+}
+
+cudaError_t launch_reload_check(LoadMeta *meta, ReloadRef ref, cudaStream_t st)
+{
+    k_reload_check<<<1, 1, 0, st>>>(meta, ref);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_load(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
                         LoadMeta *meta, uint32_t *slo_set, cudaStream_t st)
 {

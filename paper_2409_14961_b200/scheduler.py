@@ -38,6 +38,20 @@ class GpuScheduler:
                                       self.ws_bytes, stream)
         return self.profile
 
+    def reload(self, input_len, pred_out_len, slo_s, stream=None):
+        """Asynchronous load of the next n queries (device tensors) into the current profile; the
+        validation verdict lands in the device status word (status())."""
+        if self.profile is None:
+            raise RuntimeError("reload needs a profile from load()")
+        U.profile_reload(self.profile, input_len, pred_out_len, slo_s, self.cfg, stream)
+        return self.profile
+
+    def status_word(self):
+        """The profile's device status word as a 1-element int32 tensor view (no copy)."""
+        addr = U.profile_status(self.profile)
+        off = addr - self.ws.data_ptr()
+        return self.ws[off:off + 4].view(torch.int32)
+
     def schedule(self, stream=None):
         U.schedule_batches(self.profile, self.cfg, self.order, self.offsets, self.num_batches, stream)
 

@@ -15,7 +15,7 @@ import numpy as np
 
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libuellm.so")
 
-OK, ERR_ARG, ERR_CONTRACT, ERR_CONFIG, ERR_OVERFLOW, ERR_CUDA, ERR_UNSUPPORTED = range(7)
+OK, ERR_ARG, ERR_CONTRACT, ERR_CONFIG, ERR_OVERFLOW, ERR_CUDA, ERR_UNSUPPORTED, ERR_STALE = range(8)
 MODE_SEG_DP, MODE_SLO_ODBS, MODE_FIFO, MODE_SORT_ONLY = range(4)
 
 
@@ -101,6 +101,11 @@ class Profile(C.Structure):
     _fields_ = [("opaque", C.c_uint64 * 40)]
 
 
+def p_n(p: "Profile") -> int:
+    """Query count of a loaded profile (second word of the opaque view)."""
+    return int(p.opaque[1])
+
+
 class Diagnostics(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("tiles", "tile_len", "fixups_unconverged", "cascade_reruns",
                                           "fixup_positions", "trace_unmerged", "trace_rewalks",
@@ -133,6 +138,10 @@ _lib.uellm_workspace_bytes.argtypes = [C.c_uint64, C.POINTER(Config)]
 _lib.uellm_profile_load.restype = C.c_int32
 _lib.uellm_profile_load.argtypes = [C.POINTER(Queries), C.POINTER(Config), C.c_void_p, C.c_size_t,
                                     C.c_void_p, C.POINTER(Profile)]
+_lib.uellm_profile_reload.restype = C.c_int32
+_lib.uellm_profile_reload.argtypes = [C.POINTER(Profile), C.POINTER(Queries), C.POINTER(Config), C.c_void_p]
+_lib.uellm_profile_status.restype = C.c_int32
+_lib.uellm_profile_status.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p)]
 _lib.uellm_schedule_batches.restype = C.c_int32
 _lib.uellm_schedule_batches.argtypes = [C.POINTER(Profile), C.POINTER(Config), C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_void_p]
@@ -177,7 +186,7 @@ _lib.uellm_set_stage_events.argtypes = [C.POINTER(Profile), C.POINTER(C.c_void_p
 _lib.uellm_get_diagnostics.restype = C.c_int32
 _lib.uellm_get_diagnostics.argtypes = [C.POINTER(Profile), C.POINTER(Diagnostics), C.c_void_p]
 
-assert _lib.uellm_abi_version() == 2
+assert _lib.uellm_abi_version() == 3
 assert _lib.uellm_sizeof(0) == C.sizeof(Config)
 assert _lib.uellm_sizeof(1) == BATCH_STAT_DTYPE.itemsize == 80
 assert _lib.uellm_sizeof(2) == C.sizeof(Totals)
@@ -245,6 +254,22 @@ def profile_load(n: int, input_len, pred_out_len, slo_s, cfg: Config, ws, ws_byt
     _check(_lib.uellm_profile_load(C.byref(q), C.byref(cfg), _ptr(ws), ws_bytes,
                                    _stream_handle(stream), C.byref(p)), "uellm_profile_load")
     return p
+
+
+def profile_reload(p: Profile, input_len, pred_out_len, slo_s, cfg: Config, stream=None) -> Profile:
+    """Asynchronous re-load of the next queries (device arrays) into `p` (updated in place); the
+    verdict goes to the device status word (profile_status)."""
+    q = Queries(p_n(p), _ptr(input_len), _ptr(pred_out_len), _ptr(slo_s))
+    _check(_lib.uellm_profile_reload(C.byref(p), C.byref(q), C.byref(cfg), _stream_handle(stream)),
+           "uellm_profile_reload")
+    return p
+
+
+def profile_status(p: Profile) -> int:
+    """Device address of the profile's u32 status word."""
+    w = C.c_void_p()
+    _check(_lib.uellm_profile_status(C.byref(p), C.byref(w)), "uellm_profile_status")
+    return w.value
 
 
 def schedule_batches(p: Profile, cfg: Config, order, batch_offsets, num_batches, stream=None):

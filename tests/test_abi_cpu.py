@@ -42,7 +42,7 @@ def test_sm100a_cubin(lib):
 
 
 def test_host_only_calls(lib):
-    assert lib._lib.uellm_abi_version() == 2
+    assert lib._lib.uellm_abi_version() == 3
     assert lib.exchange_bytes(0) == 144 and lib.exchange_bytes(32) == 144 and lib.exchange_bytes(95) == 144
     assert lib.exchange_workspace_bytes(1000, 0) == 0 and lib.exchange_workspace_bytes(1000, 4) > 0
     assert lib.status_string(0) == "UELLM_OK" and lib.status_string(2) == "UELLM_ERR_CONTRACT"

@@ -584,3 +584,73 @@ def test_compute_sanitizer(tool):
     out = r.stdout + r.stderr
     assert "ERROR SUMMARY: 0 errors" in out or "(0 errors, 0 warnings)" in out, tail
 
+
+
+# ------------------------------------------------------------------ asynchronous reload + CUDA graph
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32 if a.dtype != np.float32 else np.float32)).cuda()
+
+
+def test_profile_reload_statuses_and_parity():
+    """uellm_profile_reload: device-side validation against the profile's decisions (uellm.h)."""
+    from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    inp, out, slo, cfg = W.c3(5, n=120_000)
+    cfg = cfg.replace(window=30_000)
+    g = GpuScheduler(len(inp), cfg, device="cuda:0")
+    g.load(_dev(inp), _dev(out), _dev(slo))
+    # a permutation of the same queries: same maxima, SLO set and key bits -> OK, oracle parity
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(len(inp))
+    p_in, p_out, p_slo = inp[perm], out[perm], slo[perm]
+    g.reload(_dev(p_in), _dev(p_out), _dev(p_slo))
+    g.schedule()
+    g.stats()
+    assert int(g.status_word().item()) == U.OK
+    r = g.results()
+    o_order, o_offs, o_m, o_cost = oracle.schedule(p_in, p_out, p_slo, cfg, nthreads=8)
+    assert np.array_equal(r["order"], o_order) and np.array_equal(r["offsets"], o_offs)
+    assert r["totals"]["dp_cost"] == o_cost
+    # a larger input length than the profile recorded -> STALE
+    b_in = p_in.copy(); b_in[7] = inp.max() + 1
+    g.reload(_dev(b_in), _dev(p_out), _dev(p_slo))
+    assert int(g.status_word().item()) == U.ERR_STALE
+    # an invalid query -> CONTRACT
+    z_in = p_in.copy(); z_in[11] = 0
+    g.reload(_dev(z_in), _dev(p_out), _dev(p_slo))
+    assert int(g.status_word().item()) == U.ERR_CONTRACT
+    # another SLO set size -> STALE
+    s2 = p_slo.copy(); s2[5] = 123.0
+    g.reload(_dev(p_in), _dev(p_out), _dev(s2))
+    assert int(g.status_word().item()) == U.ERR_STALE
+
+
+def test_cuda_graph_step_equals_eager():
+    """reload -> schedule -> stats captured once in a CUDA graph and replayed on new queries gives the
+    eager results (every decision lives in the profile; no host synchronisation inside the step)."""
+    from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    inp, out, slo, cfg = W.c3(6, n=200_000)
+    cfg = cfg.replace(window=50_000)
+    n = len(inp)
+    st = torch.cuda.Stream()
+    d_in, d_out, d_slo = _dev(inp), _dev(out), _dev(slo)
+    g = GpuScheduler(n, cfg, device="cuda:0")
+    g.load(d_in, d_out, d_slo, st)
+    torch.cuda.synchronize()
+    cg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(cg, stream=st, capture_error_mode="thread_local"):
+        g.reload(d_in, d_out, d_slo, st)
+        g.schedule(st)
+        g.stats(st)
+    rng = np.random.default_rng(9)
+    for it in range(3):
+        perm = rng.permutation(n)
+        d_in.copy_(_dev(inp[perm])); d_out.copy_(_dev(out[perm])); d_slo.copy_(_dev(slo[perm]))
+        cg.replay()
+        torch.cuda.synchronize()
+        assert int(g.status_word().item()) == U.OK
+        r = g.results()
+        o_order, o_offs, o_m, o_cost = oracle.schedule(inp[perm], out[perm], slo[perm], cfg, nthreads=8)
+        assert np.array_equal(r["order"], o_order) and np.array_equal(r["offsets"], o_offs), it
+        assert r["totals"]["dp_cost"] == o_cost
