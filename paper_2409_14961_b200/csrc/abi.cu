@@ -222,6 +222,7 @@ size_t uellm_workspace_bytes(uint64_t n, const uellm_config *cfg)
 uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg, void *ws, size_t ws_bytes,
                                 void *stream, uellm_profile *out)
 {
+    uellm::NvtxRange nvtx_("uellm_profile_load");
     if (!q || !cfg || !out) return UELLM_ERR_ARG;
     const uint64_t n = q->n;
     if (n >= 0xffffffffull) return UELLM_ERR_ARG;
@@ -288,6 +289,7 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
 
 uellm_status uellm_profile_reload(uellm_profile *p, const uellm_queries *q, const uellm_config *cfg, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_profile_reload");
     if (!p || !q || !cfg) return UELLM_ERR_ARG;
     ProfileView v;
     std::memcpy(&v, p, sizeof v);
@@ -325,6 +327,7 @@ uellm_status uellm_profile_status(const uellm_profile *p, uint32_t **device_word
 uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *cfg, uint32_t *order,
                                     uint32_t *batch_offsets, uint64_t *num_batches, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_schedule_batches");
     if (!p || !cfg || !num_batches) return UELLM_ERR_ARG;
     const ProfileView &v = *view_of(p);
     if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
@@ -535,6 +538,7 @@ uellm_status uellm_batch_stats(const uellm_profile *p, const uellm_config *cfg, 
                                const uint64_t *num_batches, uellm_batch_stat *per_batch, uellm_totals *totals,
                                void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_batch_stats");
     if (!p || !cfg || !totals || !batch_offsets || !num_batches) return UELLM_ERR_ARG;
     const ProfileView &v = *view_of(p);
     if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
@@ -585,6 +589,7 @@ uellm_status uellm_simulate(const uellm_profile *p, const uellm_config *cfg, con
                             const uint32_t *order, const uint32_t *batch_offsets, const uint64_t *num_batches,
                             uint64_t *batch_end_us, uint64_t *latency_us, uellm_sim_totals *totals, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_simulate");
     if (!p || !cfg || !totals || !batch_offsets || !num_batches) return UELLM_ERR_ARG;
     const ProfileView &v = *view_of(p);
     if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
@@ -672,6 +677,7 @@ uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, con
                                    uellm_monitor_state *state, uint32_t *pred_out_len, double *window_factors,
                                    void *ws, size_t ws_bytes, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_predict_lengths");
     if (!pc || !state || !is_device_ptr(state)) return UELLM_ERR_ARG;
     if (n >= 0xffffffffull) return UELLM_ERR_ARG;
     if (n > 0 && (!true_out_len || !pred_out_len || !is_device_ptr(true_out_len) || !is_device_ptr(pred_out_len)))
@@ -707,6 +713,7 @@ uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, con
 
 uellm_status uellm_boundary_bitmap(const uellm_profile *p, const uellm_config *cfg, uint32_t *words, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_boundary_bitmap");
     if (!p || !cfg || !words) return UELLM_ERR_ARG;
     const ProfileView &v = *view_of(p);
     if (v.magic != kProfileMagic || v.cfg_hash != layout_key(cfg)) return UELLM_ERR_ARG;
@@ -770,6 +777,7 @@ XcLayout xc_layout(uint64_t n_total, uint32_t world)
 uellm_status uellm_totals_combine(const void *parts, uint32_t count, uint64_t stride_bytes, uellm_totals *out,
                                   void *ws, size_t ws_bytes, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_totals_combine");
     if (!parts || count < 1 || stride_bytes < sizeof(uellm_totals) || (stride_bytes & 7) || !out) return UELLM_ERR_ARG;
     if (!is_device_ptr(parts)) return UELLM_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
@@ -795,6 +803,7 @@ uellm_status uellm_exchange_combine(const void *gathered, uint32_t world, uint64
                                     void *ws, size_t ws_bytes, uint32_t *batch_offsets, uint64_t *num_batches,
                                     uellm_totals *totals, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_exchange_combine");
     if (!gathered || world < 1 || !query_begin || !batch_offsets || !num_batches || !totals) return UELLM_ERR_ARG;
     if (query_begin[0] != 0) return UELLM_ERR_ARG;
     for (uint32_t r = 0; r < world; ++r)
@@ -897,11 +906,13 @@ static uellm_status deploy_plan(const uellm_topology *t, void *ws, size_t ws_byt
 
 uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_helr_plan");
     return deploy_plan(t, ws, ws_bytes, out, stream, false);
 }
 
 uellm_status uellm_bgs_plan(const uellm_topology *t, void *ws, size_t ws_bytes, uellm_device_map *out, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_bgs_plan");
     return deploy_plan(t, ws, ws_bytes, out, stream, true);
 }
 
@@ -917,6 +928,7 @@ uellm_status uellm_set_stage_events(uellm_profile *p, void *const *events, uint3
 
 uellm_status uellm_get_diagnostics(const uellm_profile *p, uellm_diagnostics *out, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_get_diagnostics");
     if (!p || !out) return UELLM_ERR_ARG;
     const ProfileView &v = *view_of(p);
     if (v.magic != kProfileMagic) return UELLM_ERR_ARG;

@@ -5,10 +5,20 @@
 #include <cstdint>
 #include <initializer_list>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>        // header-only NVTX v3 (CUDA toolkit): host ranges for nsys / ncu
 
 #include "../../include/uellm.h"
 
 namespace uellm {
+
+// NVTX range over a scope: every ABI entry point and the stages of uellm_schedule_batches show up
+// by name on an nsys timeline (ncu --nvtx filters by them too).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 constexpr uint32_t kMaxBatchLimit = 4096;      // W limit of this build (UELLM_ERR_UNSUPPORTED)
 // radix-sort CTA shape (tools/variant_run.sh on c4, sort ms: 2048 x 256: 2.51, 4096 x 512: 2.54,

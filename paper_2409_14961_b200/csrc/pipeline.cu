@@ -104,6 +104,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
                                       size_t ws_bytes, uint32_t *order, uint32_t *batch_offsets,
                                       uint64_t *num_batches, uellm_totals *totals, void *stream)
 {
+    uellm::NvtxRange nvtx_("uellm_schedule_pipelined");
     if (!q || !cfg || !order || !batch_offsets || !num_batches || !totals) return UELLM_ERR_ARG;
     const uint64_t n = q->n;
     if (n >= 0xffffffffull) return UELLM_ERR_ARG;
