@@ -29,9 +29,11 @@ def main():
     ap.add_argument("--launches", required=True)
     ap.add_argument("--bench", required=True)
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--steps", type=int, default=2, help="c4 steps in the launch list")
     a = ap.parse_args()
     bench = json.loads(open(a.bench).read().strip().splitlines()[-1])
     evals = bench["diagnostics"]["dp_candidate_evals"]
+    steps_in_launch_list = a.steps
 
     # launch shares
     rows = list(csv.reader(open(a.launches)))
@@ -45,8 +47,9 @@ def main():
         agg[kname(d["Kernel Name"])] += float(d["Metric Value"])
         cnt[kname(d["Kernel Name"])] += 1
     tot = sum(agg.values())
-    lines = [f"# {a.tag} launch list (ncu --metrics gpu__time_duration.sum --clock-control none), 2 steps of "
-             "bench.py c4 (warmup + timed); cold-cache, serialised: compare shares, not absolutes",
+    lines = [f"# {a.tag} launch list (ncu --metrics gpu__time_duration.sum --clock-control none) of "
+             "`bench.py --steps 1 --warmup 1 --no-configs` (c4 steps + NEXT rows); cold-cache, serialised: "
+             "compare shares, not absolutes",
              "kernel,launches,total_ns,share_pct"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1]):
         lines.append(f"{k},{cnt[k]},{v:.0f},{100 * v / tot:.2f}")
@@ -79,10 +82,11 @@ def main():
                   "issue_active_pct": float(r[ix["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
                   "warps_active_pct": float(r[ix["sm__warps_active.avg.pct_of_peak_sustained_active"]]),
                   "registers": int(float(r[ix["launch__registers_per_thread"]]))}
+    dp = next(v for k, v in K.items() if k.startswith("k_dp_tiles"))
     summ = {"round": a.tag, "source": f"ncu --set full --clock-control none; {os.path.basename(a.rep or a.raw)}; "
                                      "bench.py c4 (1e8 queries, seed 0), one step",
             "dp_candidate_evals_c4_seed0": evals,
-            "dp_warp_inst_per_eval": K["k_dp_tiles"]["inst_executed"] / evals, "kernels": K}
+            "dp_warp_inst_per_eval": dp["inst_executed"] / evals, "kernels": K}
     json.dump(summ, open(os.path.join(HERE, "ncu_summary.json"), "w"), indent=1)
     md = [f"# {a.tag} ncu summary (B200, c4 = 10^8 queries, one step)", "",
           f"Bench line of the same code: {bench['value']:.3e} q/s, {bench['ms_per_step']:.2f} ms/step "
@@ -94,7 +98,7 @@ def main():
                   f"{v['dram_write_bytes'] / 1e9:.3f} | {v['dram_gbs']:.0f} | {v['l2_bytes'] / v['duration_ms'] / 1e6:.0f} | "
                   f"{v['issue_active_pct']:.1f} | "
                   f"{v['warps_active_pct']:.1f} | {v['registers']} |")
-    md += ["", f"SEG-DP: {K['k_dp_tiles']['inst_executed'] / 1e8:.1f} warp instructions per query, "
+    md += ["", f"SEG-DP: {dp['inst_executed'] / 1e8:.1f} warp instructions per query, "
                f"{summ['dp_warp_inst_per_eval']:.3f} per candidate evaluation ({evals / 1e8:.1f} evaluations per query)."]
     open(os.path.join(HERE, f"{a.tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md))

@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round evidence in one gpurun call: bench line, launch list, one ncu --set full capture of the first
+# step's kernels, the PCIe floor.  usage: gpurun --timeout 2400 -- 'bash tools/gpu_evidence.sh r02'
+TAG=${1:-r02}
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -2 gpurun_out/bench_$TAG.err
+timeout 300 python tools/pcie_floor.py > gpurun_out/pcie_$TAG.json 2>&1; cat gpurun_out/pcie_$TAG.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
+   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-configs > /dev/null 2>&1
+# the first step's kernels (sync load -> schedule -> stats): about 30 launches
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_' -c 32 -o gpurun_out/prof_full_$TAG \
+   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-sim --no-configs > gpurun_out/ncu_full_$TAG.log 2>&1
+tail -2 gpurun_out/ncu_full_$TAG.log
+ncu -i gpurun_out/prof_full_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_raw_$TAG.csv
+ls -la gpurun_out | grep $TAG
