@@ -1,5 +1,7 @@
 #!/bin/bash
-for t in 0 3584 5632 6144 7168; do
-  timeout 300 python bench.py --dp-tile $t --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-sim > /tmp/b.json 2>/dev/null
-  python -c "import json; d=json.load(open('/tmp/b.json')); print($t, round(d['ms_per_step'],3), round(d['stage_ms']['dp_local'],3), d['diagnostics']['tiles'], d['diagnostics']['fixup_positions'], d['diagnostics']['cascade_reruns'])"
+# DP tile length sweep: bash tools/sweep_tile.sh CONFIG TILE...   (0 = automatic)
+CFG=${1:-c4}; shift
+for t in "$@"; do
+  timeout 300 python bench.py --config $CFG --dp-tile $t --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-sim --no-configs > /tmp/b.json 2>/dev/null
+  python -c "import json; d=json.load(open('/tmp/b.json')); s=d['stage_ms']; print('$CFG', $t, round(d['ms_per_step'],3), 'dp', round(s['dp_local'],3), 'casc', round(s['dp_cascade'],3), 'trace', round(s['traceback'],3), d['diagnostics']['tiles'], d['diagnostics']['fixup_positions'], d['diagnostics']['cascade_reruns'])"
 done
