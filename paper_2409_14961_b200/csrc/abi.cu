@@ -1,6 +1,7 @@
 // abi.cu -- the C ABI of include/uellm.h: argument/config validation, workspace carving and
 // stream-ordered orchestration of the kernels (host code only; no allocation, no globals).
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 
 #include "internal.cuh"
@@ -697,6 +698,9 @@ uellm_status uellm_predict_lengths(uint64_t n, const uint32_t *true_out_len, con
     P.nwin = n ? ceil_div(n, window) : 0;
     P.variant = pc->variant; P.bucket_width = pc->bucket_width; P.constant_tokens = pc->constant_tokens;
     P.monitor = pc->monitor; P.error_rate = pc->error_rate; P.gamma = pc->gamma; P.cap = pc->cap;
+    // the noisy draw u = (z >> 11) * 2^-53 is exact, so u < e  <=>  (z >> 11) < ceil(e * 2^53)
+    // (e * 2^53 is exact; 0 <= e <= 1 checked above): one integer compare instead of FP64 work
+    P.err_thresh = (unsigned long long)std::ceil(pc->error_rate * 9007199254740992.0);
     P.seed = pc->seed;
     uint64_t nwin_l = 0;
     const uint64_t need = predict_ws_bytes(n, pc, &nwin_l);

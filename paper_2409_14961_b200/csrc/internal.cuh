@@ -352,6 +352,7 @@ struct PredictParams {
     uint64_t nwin;
     uint32_t variant, bucket_width, constant_tokens, monitor;
     double error_rate, gamma, cap;
+    unsigned long long err_thresh;              // ceil(error_rate * 2^53): u < e  <=>  (z >> 11) < err_thresh
     unsigned long long seed;
 };
 cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cudaStream_t st, int *launches);

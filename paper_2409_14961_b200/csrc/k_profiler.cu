@@ -37,19 +37,22 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long seed, uns
     return z ^ (z >> 31);
 }
 
-// the variant's prediction before the inflation factor (R20)
+// the variant's prediction before the inflation factor (R20); VAR >= 0 fixes the
+// variant at compile time (the level-path kernels are instantiated per variant), -1 reads P.variant
+template <int VAR = -1>
 __device__ __forceinline__ unsigned long long base_of(const PredictParams &P, unsigned long long index, uint32_t t)
 {
-    if (P.variant == UELLM_PREDICT_ORACLE) return t;
-    if (P.variant == UELLM_PREDICT_CONSTANT) return P.constant_tokens;
+    const uint32_t var = VAR >= 0 ? (uint32_t)VAR : P.variant;
+    if (var == UELLM_PREDICT_ORACLE) return t;
+    if (var == UELLM_PREDICT_CONSTANT) return P.constant_tokens;
     const uint32_t w = P.bucket_width;
-    const uint32_t q = t / w;                                 // ceil(t / w) in 32-bit arithmetic
+    // ceil(t / w) in 32-bit arithmetic (power-of-two widths by a shift: the 16-token buckets)
+    const uint32_t q = (w & (w - 1)) == 0 ? t >> (__ffs(w) - 1) : t / w;
     unsigned long long k = q + (q * w != t ? 1u : 0u);
     k = k < 1 ? 1 : k;
-    if (P.variant == UELLM_PREDICT_NOISY) {
+    if (var == UELLM_PREDICT_NOISY) {
         const unsigned long long z = mix64(P.seed, index);
-        const double u = (double)(z >> 11) * 0x1.0p-53;
-        if (u < P.error_rate) {
+        if ((z >> 11) < P.err_thresh) {                     // u = (z >> 11) * 2^-53 < error_rate
             if (z & 1ull) k += 1;
             else if (k > 1) k -= 1;
         }
@@ -60,14 +63,16 @@ __device__ __forceinline__ unsigned long long base_of(const PredictParams &P, un
 // "multiplied by monitor.inflation_factor and rounded up", saturating (R20)
 __device__ __forceinline__ uint32_t inflate(unsigned long long base, double factor)
 {
-    const double x = ceil(__dmul_rn((double)base, factor));
+    const double b = base <= 0xffffffffull ? (double)(uint32_t)base : (double)base;   // (exact either way)
+    const double x = ceil(__dmul_rn(b, factor));
     return x >= 4294967295.0 ? 4294967295u : (uint32_t)x;
 }
 
+template <int VAR = -1>
 __device__ __forceinline__ uint32_t predict_one(const PredictParams &P, unsigned long long index, uint32_t t,
                                                 double factor)
 {
-    return inflate(base_of(P, index, t), factor);
+    return inflate(base_of<VAR>(P, index, t), factor);
 }
 
 }  // namespace
@@ -140,34 +145,51 @@ __global__ void k_pred_levels(PredictParams P)
     *P.nlevels = K;
 }
 
+// Per query, the levels at which it is under-predicted form a PREFIX of the chain (the factors
+// ascend and ceil(RN(base * v)) is monotone in v), and a base >= the true length is never under-
+// predicted (every factor >= 1): the common warp has no work beyond the draw.  Four consecutive
+// queries per thread (one 16-byte load when aligned); window indices from one division.
+template <int VAR>
 __global__ void __launch_bounds__(256) k_pred_count(PredictParams P, uint64_t n, uint64_t window)
 {
     __shared__ double V[kPredMaxLevels];
     const uint32_t K = *P.nlevels;
     if (threadIdx.x <= K) V[threadIdx.x] = P.levels[threadIdx.x];
     __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nq = ceil_div(n, 4);
     const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t n_pad = ceil_div(n, 32) * 32;             // whole warps stay in the loop
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_pad; k += nt) {
-        uint32_t under = 0;
-        uint32_t w = 0xffffffffu;
-        if (k < n) {
-            const uint32_t t = __ldg(P.true_len + k);
-            w = (uint32_t)k / (uint32_t)window;             // 32-bit: n < 2^32 (a 64-bit divide is ~10x)
-            const unsigned long long base = base_of(P, k, t);
-            // every level factor is >= 1, so inflate(base, v) >= base: only a base below the true
-            // length can be an under-prediction at some level (the noisy variant's downward moves,
-            // a small constant) -- the common case needs no double arithmetic
-            if (base < t)
-                for (uint32_t i = 0; i <= K; ++i) under |= (uint32_t)(t > inflate(base, V[i])) << i;
+    const bool vec = ((uintptr_t)P.true_len & 15u) == 0;
+    for (uint64_t g0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; g0 < nq; g0 += nt) {
+        const uint64_t g = g0 + lane;
+        const uint64_t k0 = 4 * g;
+        uint32_t t[4] = {0, 0, 0, 0};
+        if (g < nq) {
+            if (vec && k0 + 4 <= n) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.true_len) + g);
+                t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+            } else {
+                for (int i = 0; i < 4; ++i) t[i] = k0 + i < n ? __ldg(P.true_len + k0 + i) : 0u;
+            }
         }
-        const uint32_t grp = __match_any_sync(0xffffffffu, w);
-        const uint32_t lane = threadIdx.x & 31;
-        const bool leader = (__ffs(grp) - 1) == (int)lane;
-        for (uint32_t i = 0; i <= K; ++i) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (under >> i) & 1u) & grp;
-            if (leader && b && w != 0xffffffffu)
-                atomicAdd(P.hist + (uint64_t)w * kPredMaxLevels + i, (unsigned long long)__popc(b));
+        unsigned long long base[4];
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            base[i] = k0 + i < n ? base_of<VAR>(P, k0 + i, t[i]) : ~0ull;
+            any |= base[i] < t[i];
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;            // warp-uniform: nothing under-predicted
+        const uint32_t w0 = g < nq ? (uint32_t)k0 / (uint32_t)window : 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint32_t c = 0;                                     // levels under-predicted: 0 .. K+1
+            if (base[i] < t[i])
+                while (c <= K && t[i] > inflate(base[i], V[c])) ++c;
+            const uint32_t w = (k0 + i) < n ? w0 + ((uint32_t)(k0 + i) >= (w0 + 1) * (uint32_t)window ? 1u : 0u)
+                                            : 0xffffffffu;
+            if (c && w != 0xffffffffu)
+                for (uint32_t l = 0; l < c; ++l) atomicAdd(P.hist + (uint64_t)w * kPredMaxLevels + l, 1ull);
         }
     }
 }
@@ -193,13 +215,38 @@ __global__ void k_pred_chain(PredictParams P, uint64_t nwin)
     }
 }
 
+template <int VAR>
 __global__ void __launch_bounds__(256) k_pred_write(PredictParams P, uint64_t n, uint64_t window)
 {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nq = ceil_div(n, 4);
     const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += nt) {
-        const uint32_t t = __ldg(P.true_len + k);
-        P.pred[k] = predict_one(P, k, t, P.levels[P.wlevel[(uint32_t)k / (uint32_t)window]]);
+    const bool vec = (((uintptr_t)P.true_len | (uintptr_t)P.pred) & 15u) == 0;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nq; g += nt) {
+        const uint64_t k0 = 4 * g;
+        uint32_t t[4] = {0, 0, 0, 0}, p[4];
+        const bool full = vec && k0 + 4 <= n;
+        if (full) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.true_len) + g);
+            t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+        } else {
+            for (int i = 0; i < 4; ++i) t[i] = k0 + i < n ? __ldg(P.true_len + k0 + i) : 0u;
+        }
+        const uint32_t w0 = (uint32_t)k0 / (uint32_t)window;
+        const double f0 = P.levels[P.wlevel[w0]];
+        const uint32_t wend = (w0 + 1) * (uint32_t)window;      // first query of the next window
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double f = (k0 + i >= n || (uint32_t)(k0 + i) < wend) ? f0 : P.levels[P.wlevel[w0 + 1]];
+            p[i] = predict_one<VAR>(P, k0 + i, t[i], f);
+        }
+        if (full) {
+            reinterpret_cast<uint4 *>(P.pred)[g] = make_uint4(p[0], p[1], p[2], p[3]);
+        } else {
+            for (int i = 0; i < 4; ++i) if (k0 + i < n) P.pred[k0 + i] = p[i];
+        }
     }
+    (void)lane;
 }
 
 __global__ void k_predict_empty(PredictParams P)
@@ -218,11 +265,21 @@ cudaError_t run_predict(const PredictParams &P, uint64_t n, uint64_t window, cud
         cudaError_t e;
         if ((e = cudaMemsetAsync(P.hist, 0, 8 * kPredMaxLevels * nwin, st))) return e;
         k_pred_levels<<<1, 32, 0, st>>>(P);
-        const uint64_t nb = ceil_div(n, 256 * 4);
+        const uint64_t nb = ceil_div(n, 256 * 4 * 4);
         const unsigned blocks = (unsigned)(nb < 148 * 8 ? nb : 148 * 8);
-        k_pred_count<<<blocks, 256, 0, st>>>(P, n, window);
+        switch (P.variant) {
+        case UELLM_PREDICT_ORACLE: k_pred_count<UELLM_PREDICT_ORACLE><<<blocks, 256, 0, st>>>(P, n, window); break;
+        case UELLM_PREDICT_BUCKETED: k_pred_count<UELLM_PREDICT_BUCKETED><<<blocks, 256, 0, st>>>(P, n, window); break;
+        case UELLM_PREDICT_NOISY: k_pred_count<UELLM_PREDICT_NOISY><<<blocks, 256, 0, st>>>(P, n, window); break;
+        default: k_pred_count<UELLM_PREDICT_CONSTANT><<<blocks, 256, 0, st>>>(P, n, window); break;
+        }
         k_pred_chain<<<1, 32, 0, st>>>(P, nwin);
-        k_pred_write<<<blocks, 256, 0, st>>>(P, n, window);
+        switch (P.variant) {
+        case UELLM_PREDICT_ORACLE: k_pred_write<UELLM_PREDICT_ORACLE><<<blocks, 256, 0, st>>>(P, n, window); break;
+        case UELLM_PREDICT_BUCKETED: k_pred_write<UELLM_PREDICT_BUCKETED><<<blocks, 256, 0, st>>>(P, n, window); break;
+        case UELLM_PREDICT_NOISY: k_pred_write<UELLM_PREDICT_NOISY><<<blocks, 256, 0, st>>>(P, n, window); break;
+        default: k_pred_write<UELLM_PREDICT_CONSTANT><<<blocks, 256, 0, st>>>(P, n, window); break;
+        }
         l = 4;
     } else {
         for (uint64_t w = 0, a = 0; a < n; a += window, ++w) {
