@@ -652,8 +652,19 @@ def run_next_rows(args, g, cfg, n, d_in, d_out, d_slo, m, stream, dev, hbm_gbs, 
             f1_step()
         f1_ms = time_steps(f1_step, K, stream, dev)
         r1 = g1.results()
+        nk = ncu_summary().get("next_kernels", {})
+        a1 = nk.get("k_alg1_next")
+        f1_roof = None
+        if a1:
+            peak = SMS * ISSUE_PER_SM * peaks()[1] * 1e6 / 1e12
+            ach = a1["inst_executed"] / (a1["duration_ms"] / 1e3) / 1e12
+            f1_roof = {"bound": "alu", "kernel": "k_alg1_next (one thread per position simulates Alg. 1 from a "
+                                                  "fresh batch: FP64 expression trees)",
+                       "achieved": ach, "peak": peak, "unit": "T warp-instr/s", "frac": ach / peak,
+                       "source": "ncu inst_executed / duration of the kernel (profiles/ncu_summary.json next_kernels)",
+                       "share_of_f1_ms": a1["duration_ms"] / f1_ms}
         next_rows["f1_slo_odbs"] = {
-            "ms": f1_ms, "queries_per_s": n / (f1_ms / 1e3),
+            "ms": f1_ms, "queries_per_s": n / (f1_ms / 1e3), "roofline": f1_roof,
             "algorithm": "Alg. 1 literal (w1=1, w2=0.02, threshold=900), load + schedule + stats",
             "batches": r1["m"], "dp_objective_of_its_schedule": r1["totals"]["dp_cost"]}
         del g1
@@ -677,8 +688,13 @@ def run_next_rows(args, g, cfg, n, d_in, d_out, d_slo, m, stream, dev, hbm_gbs, 
     next_rows["f3_helr"] = {
         "ms": hms, "devices": 20, "dp_states": (1 << 20) * 20, "relaxations": relax,
         "relaxations_per_s": relax / (hms / 1e3),
-        "roofline": {"bound": "latency", "note": "20 dependent popcount levels; the DP table "
-                     "(168 MB) streams once per level", "dram_table_bytes": (1 << 20) * 20 * 9},
+        # compulsory traffic: every DP entry (8 B value + 1 B argument) written once and read back
+        # by its successors at the next level at least once
+        "roofline": {"bound": "latency", "note": "20 dependent popcount levels, one launch each; the DP "
+                     "table (2^20 x 20 x 9 B) is written once and read once at least",
+                     "dram_table_bytes": (1 << 20) * 20 * 9,
+                     "achieved_gbs": 2 * (1 << 20) * 20 * 9 / (hms / 1e3) / 1e9, "peak_gbs": hbm_gbs,
+                     "frac": 2 * (1 << 20) * 20 * 9 / (hms / 1e3) / 1e9 / hbm_gbs},
         "device_map": {"devices": dm["devices"], "layer_count": dm["layer_count"],
                        "latency_s": dm["latency_s"], "objective": dm["objective"]},
         "bgs_baseline": {"devices": bg["devices"], "latency_s": bg["latency_s"], "objective": bg["objective"]}}

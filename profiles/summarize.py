@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--bench", required=True)
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--steps", type=int, default=2, help="c4 steps in the launch list")
+    ap.add_argument("--next-raw", default=None, help="raw csv of an ncu capture of the NEXT-row kernels")
     a = ap.parse_args()
     bench = json.loads(open(a.bench).read().strip().splitlines()[-1])
     evals = bench["diagnostics"]["dp_candidate_evals"]
@@ -87,6 +88,21 @@ def main():
                                      "bench.py c4 (1e8 queries, seed 0), one step",
             "dp_candidate_evals_c4_seed0": evals,
             "dp_warp_inst_per_eval": dp["inst_executed"] / evals, "kernels": K}
+    if a.next_raw:
+        nr = list(csv.reader(open(a.next_raw)))
+        nh, nu, nb = nr[0], nr[1], nr[2:]
+        nix = {n_: nh.index(n_) for n_ in nh}
+        NK = {}
+        for r in nb:
+            nm = kname(r[nix["Kernel Name"]]).split("<")[0]
+            if nm in NK:
+                continue                       # first launch of each kernel
+            u = nu[nix["gpu__time_duration.sum"]]
+            dur = float(r[nix["gpu__time_duration.sum"]]) * {"ms": 1.0, "us": 1e-3, "ns": 1e-6}.get(u, 1.0)
+            NK[nm] = {"duration_ms": dur, "inst_executed": float(r[nix["smsp__inst_executed.sum"]]),
+                      "issue_active_pct": float(r[nix["smsp__issue_active.avg.pct_of_peak_sustained_active"]]),
+                      "dram_bytes_per_launch": float(r[nix["dram__bytes_read.sum"]]) + float(r[nix["dram__bytes_write.sum"]])}
+        summ["next_kernels"] = NK
     json.dump(summ, open(os.path.join(HERE, "ncu_summary.json"), "w"), indent=1)
     md = [f"# {a.tag} ncu summary (B200, c4 = 10^8 queries, one step)", "",
           f"Bench line of the same code: {bench['value']:.3e} q/s, {bench['ms_per_step']:.2f} ms/step "

@@ -14,3 +14,7 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_
 tail -2 gpurun_out/ncu_full_$TAG.log
 ncu -i gpurun_out/prof_full_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_raw_$TAG.csv
 ls -la gpurun_out | grep $TAG
+# NEXT-row kernels (f1 Alg. 1, f2 simulator, f3 HELR, f4 predictor): first launch of each
+timeout 900 ncu --set full --clock-control none -k regex:'k_alg1_next|k_a1_|k_helr_level|k_sim_|k_pred_' -c 40 -o gpurun_out/prof_next_$TAG \
+   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-configs > gpurun_out/ncu_next_$TAG.log 2>&1
+ncu -i gpurun_out/prof_next_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_raw_next_$TAG.csv
