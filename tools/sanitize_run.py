@@ -1,7 +1,8 @@
 """Small end-to-end run of every entry point, for compute-sanitizer (T6 in SURVEY.md section 4):
   compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize_run.py
-c1 / c2 shapes, forced small DP tiles (fix-up + cascade), Alg. 1, FIFO, simulator, profiler
-stand-ins (both paths) and HELR.  Prints SANITIZE_RUN_OK at the end."""
+c1 / c2 shapes, forced small DP tiles (fix-up + cascade), uniform stretches (deferred fills,
+traceback exit maps), reload, Alg. 1, FIFO, simulator, profiler stand-ins (both paths), HELR and the
+pipelined host-buffer call.  Prints SANITIZE_RUN_OK at the end."""
 import ctypes
 import os
 import sys
@@ -43,6 +44,20 @@ for levels in (True, False):
     wsb = U.predict_workspace_bytes(20_000, pc) if levels else 0
     ws = torch.zeros(max(wsb, 1), dtype=torch.uint8, device=dev)
     U.predict_lengths(20_000, t, pc, s, p, None, None, ws if wsb else None, wsb)
+# uniform stretches over many tiles: deferred periodic fills (k_dp_fill), traceback exit maps and
+# parallel re-marking (k_trace_maps / k_trace_remark)
+inp, out, slo, cfg = W.uniform_runs(5, n=60_000, runs=((14_000, 128, 257), (9_000, 64, 513)))
+run(inp, out, slo, cfg.replace(dp_tile=1024))
+# asynchronous reload into the same profile (device-side validation, status word)
+inp, out, slo, cfg = W.c2(3, n=4000)
+g = run(inp, out, slo, cfg.replace(window=1000))
+perm = np.random.default_rng(1).permutation(4000)
+g.reload(torch.from_numpy(inp[perm].view(np.int32)).to(dev), torch.from_numpy(out[perm].view(np.int32)).to(dev),
+         torch.from_numpy(slo[perm]).to(dev))
+g.schedule()
+g.stats()
+torch.cuda.synchronize()
+assert int(g.status_word().item()) == 0
 topo = W.random_topology(3, 6)
 wsb = U.helr_workspace_bytes(6)
 U.helr_plan(topo, torch.zeros(wsb, dtype=torch.uint8, device=dev), wsb)
