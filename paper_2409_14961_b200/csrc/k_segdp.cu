@@ -1254,11 +1254,34 @@ __global__ void k_dp_cascade(DPParams P)
     uint32_t ref_s = 0, ref_P = 0;   // active reference: boundaries (ref_s - ref_P, ref_s] of CFx
     long long ref_F = 0;
     if (lane == 0) { P.tiles[t0].off_local = 0; P.tiles[t0].off_fix = 0; }
+    uint32_t eu_mask = 0;            // entry_uniform of tiles (k & ~31) + lane, 32 at a time
     for (uint32_t k = 1; k < K; ++k) {
+        if (k == 1 || (k & 31u) == 0) {
+            const uint32_t kk = (k & ~31u) + lane;
+            bool e = false;
+            if (kk >= 1 && kk < K) {
+                uint32_t ts, te, tk, tw; bool tv;
+                tile_bounds(P, t0 + kk, ts, te, tk, tw, tv);
+                e = tv && entry_uniform(P, t0 + kk, ts);
+            }
+            eu_mask = __ballot_sync(0xffffffffu, e);
+        }
+        const bool eu = (eu_mask >> (k & 31u)) & 1u;
+        if (V != 0 && !tail_local && eu && ref_P != 0) {
+            // a further tile of the deferred stretch: only the record fields change (no reads)
+            if (lane == 0) {
+                uint32_t ts, te, tk, tw; bool tv;
+                tile_bounds(P, t0 + k, ts, te, tk, tw, tv);
+                TileRec &q = P.tiles[t0 + k];
+                q.fill_s = ref_s; q.fill_P = ref_P; q.fill_F = ref_F;
+                q.conv = 0; q.fix_end = te; q.off_fix = tail_off; q.off_local = 0;
+            }
+            __syncwarp();
+            continue;
+        }
         TileRec r = P.tiles[t0 + k];
         r.fill_s = 0; r.fill_P = 0; r.fill_F = 0;
         if (!tail_local) {
-            const bool eu = entry_uniform(P, t0 + k, r.s);
             bool deferred = false;
             if (V != 0 && eu) {
                 if (ref_P == 0) {
