@@ -221,13 +221,17 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
     const unsigned grid = (unsigned)(ntiles < (uint64_t)nsm * 8 ? ntiles : (uint64_t)nsm * 8);
     cudaError_t e = cudaMemsetAsync(wflag, 0, 4 * P.nwin, st);
     if (e != cudaSuccess) return e;
-// walk A: thread per tile through L1/L2 (0) or one CTA per tile with the tile's args staged in
-// shared memory (threads per CTA).  Measured on c4 (traceback ms): 0: 0.292, 256: 0.316,
-// 64: 0.374, 32: 0.475 -- with 21,800 tiles every walk runs at once and hides its own latency.
+// walk A: thread per tile through L1/L2, or one CTA of kTraceAThreads per tile with the tile's
+// args staged in shared memory.  Measured (traceback ms, thread / CTA of 128 / CTA of 256):
+// c4 (21,800 tiles): 0.321 / 0.329 / 0.333 -- every walk runs at once and hides its own latency;
+// c5 (2,450 tiles of 4096): 0.772 / 0.390 / 0.392 -- too few walks in flight, each hop an L2
+// round trip.  So the thread walk only for jobs with many tiles.
 #ifndef UELLM_TRACE_A
-#define UELLM_TRACE_A 0
+#define UELLM_TRACE_A 128
 #endif
-    if (UELLM_TRACE_A && P.tile_len * sizeof(uint16_t) <= 160 * 1024) {
+    const bool stage_walk = UELLM_TRACE_A && ntiles < (uint64_t)nsm * 64 &&
+                            P.tile_len * sizeof(uint16_t) <= 160 * 1024;
+    if (stage_walk) {
         e = cudaFuncSetAttribute(k_trace_a_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(P.tile_len * sizeof(uint16_t)));
         if (e != cudaSuccess) return e;
