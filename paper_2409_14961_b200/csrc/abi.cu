@@ -484,6 +484,7 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
             const u128 E = (u128)cfg->t_batch_us + (u128)cfg->t_iter_us * v.max_out +
                            ((u128)cfg->t_tok_us * v.max_out + (u128)cfg->t_prefill_us * v.max_in) * cfg->max_batch;
             P.narrow = (v.max_in < 65536u && v.max_out < 65536u && E < ((u128)1 << 32) && !(cfg->flags & 1u)) ? 1u : 0u;
+            P.many_runs = (v.slo_overflow || v.slo_distinct > kSloRankMax) ? 1u : 0u;
         }
         // candidate slots per warp: the blocked path holds at most W live + 32 new candidates; the
         // generic path at most W + 1 and reads one slot ahead

@@ -259,6 +259,7 @@ struct DPParams {
     unsigned long long *wincost;
     uint32_t n, window, nwin, tile_len, tpw, W, cap_slots, split;
     uint32_t narrow;                             // 32-bit fast path valid (see k_segdp.cu)
+    uint32_t many_runs;                          // more distinct SLO values than the compressed sort key holds
     unsigned long long cap_tok;                  // ~0ull = no cap
     unsigned long long t_batch, t_iter, t_tok, t_pre, lambda;
 };

@@ -295,6 +295,9 @@ constexpr uint32_t kHullCap = 64;
 constexpr uint32_t kHullMin = UELLM_HULL_MIN;
 #ifndef UELLM_DP_PREFETCH
 #define UELLM_DP_PREFETCH 1
+#endif
+#ifndef UELLM_DP_VFREE
+#define UELLM_DP_VFREE 1
 #endif   // shorter lean ranges are evaluated whole
 // offset of row q of the triangular table (row q holds k = q+1 .. 31)
 __host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
@@ -430,7 +433,7 @@ __device__ __forceinline__ uint32_t periodic_fill(const DPParams &P, const Narro
 //  3. once per block the list is extended by the 32 new candidates and pruned at the block-end
 //     state (dead prefix + D1), which is valid for every later boundary.
 // LAMK: 0 = no SLO penalty, 1 = lambda < 2^32 (32x32 -> 64-bit product), 2 = 64-bit lambda.
-template <bool FIX, int LAMK, bool SPLIT>
+template <bool FIX, int LAMK, bool SPLIT, bool VFREE = false>
 __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uint32_t s, uint32_t e,
                                     const long long *__restrict__ src, uint32_t stop_min, bool src_args_ok,
                                     bool entry_uni)
@@ -902,7 +905,24 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             lb = (unsigned long long)base + r32;
             lbi = ri;
         } else {
-                    if (ext_slow) {
+            // Violation-free block (only computed here, off the fast block's path): records ascend in
+            // slo_us inside a window, so the smallest SLO of any interval this block evaluates is that
+            // of the oldest live candidate i0, and est is largest for [i0, block end); when even that
+            // SLO is not below that est, nothing violates for any lane and the one-comparison
+            // violation test (0 here) replaces the binary-search count.
+            bool vfree = false;
+            if (VFREE && (ext_slow || intra_slow)) {
+                const unsigned long long cp0 = (unsigned long long)S.sl[0].y;
+                const uint32_t i0 = (uint32_t)cp0;
+                const uint32_t bmo_ = __shfl_sync(0xffffffffu, pmo, B - 1), bmi_ = __shfl_sync(0xffffffffu, pmi, B - 1);
+                const unsigned long long mo = max((uint32_t)(cp0 >> 32) & 0xffffu, bmo_);
+                const unsigned long long mi = max((uint32_t)(cp0 >> 48), bmi_);
+                const unsigned long long emax = (unsigned long long)t_b + (unsigned long long)t_it * mo +
+                                                (unsigned long long)(j0 + B - i0) *
+                                                    ((unsigned long long)t_tok * mo + (unsigned long long)t_pre * mi);
+                vfree = (unsigned long long)__ldg(rslo + i0) >= emax;
+            }
+            if (ext_slow && !vfree) {
                 if (single_ok) ext_pass(T1{}, T1{}, F0{}, 0, L); else ext_pass(T1{}, F0{}, F0{}, 0, L);
             } else if (one_run_ext) {
                 if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd);
@@ -948,7 +968,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 }
             };
             const uint32_t QB = B - 1;                   // intra candidates q = 0 .. B-2
-            if (intra_slow) {
+            if (intra_slow && !vfree) {
                 if (single_ok) intra_pass(T1{}, T1{}, F0{}, T1{}, 0, QB); else intra_pass(T1{}, F0{}, F0{}, T1{}, 0, QB);
             } else if (one_run_intra) {
                 // deaths inside one run are monotone (b > W, KV cap): candidates dead at the block end
@@ -1051,21 +1071,29 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
         R.filled = 0; R.uni = 0;
         return R;
     } else {
-        constexpr int LK = (V - 1) % 3;
-        constexpr bool SPLIT = (V - 1) / 3 != 0;
+        // V = 1 + LK + 3 * SPLIT (1 .. 6); V = 6 + LK (7, 8): lambda > 0, no split, many SLO runs
+        constexpr int LK = V >= 7 ? V - 6 : (V - 1) % 3;
+        constexpr bool SPLIT = V >= 7 ? false : (V - 1) / 3 != 0;
+        constexpr bool VF = V >= 7;
         char *p = smem + (size_t)warp * warp_smem_bytes(P);
         NarrowSlots S;
         S.sl = (longlong2 *)p;
         S.tri = (uint32_t *)(p + (size_t)P.cap_slots * 16);
         S.hl = (uint2 *)(p + (size_t)P.cap_slots * 16 + kRmqBytes);
-        return dp_warp_blocked<FIX, LK, SPLIT>(P, S, s, e, src, stop_min, src_args_ok, entry_uni);
+        return dp_warp_blocked<FIX, LK, SPLIT, VF>(P, S, s, e, src, stop_min, src_args_ok, entry_uni);
     }
 }
 
+// Variants 7 / 8 add the violation-free block test for inputs with many SLO runs (more distinct
+// SLO values than the rank-compressed sort key takes, e.g. BJ c5's anti-sorted segment): there
+// most blocks span several runs and would count violations by binary search.  A separate
+// instantiation, because the extra code in the same kernel cost the one-run fast block of c4
+// 0.11 ms (register allocation / instruction footprint), while c5 gains 0.39 ms.
 static int dp_variant(const DPParams &P)
 {
     if (!P.narrow) return 0;
     const int lk = P.lambda == 0 ? 0 : (P.lambda < (1ull << 32) ? 1 : 2);
+    if (lk && !P.split && P.many_runs && UELLM_DP_VFREE) return 6 + lk;
     return 1 + lk + 3 * (P.split ? 1 : 0);
 }
 
@@ -1385,7 +1413,9 @@ cudaError_t run_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t st, void 
     case 3: return launch_segdp<3>(P, ntiles, st, ev, launches);
     case 4: return launch_segdp<4>(P, ntiles, st, ev, launches);
     case 5: return launch_segdp<5>(P, ntiles, st, ev, launches);
-    default: return launch_segdp<6>(P, ntiles, st, ev, launches);
+    case 6: return launch_segdp<6>(P, ntiles, st, ev, launches);
+    case 7: return launch_segdp<7>(P, ntiles, st, ev, launches);
+    default: return launch_segdp<8>(P, ntiles, st, ev, launches);
     }
 }
 
