@@ -6,6 +6,10 @@
 
 #include "internal.cuh"
 
+#ifndef UELLM_DP_PRUNE_EVERY
+#define UELLM_DP_PRUNE_EVERY 1
+#endif
+
 using namespace uellm;
 
 namespace uellm {
@@ -486,9 +490,10 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
             P.narrow = (v.max_in < 65536u && v.max_out < 65536u && E < ((u128)1 << 32) && !(cfg->flags & 1u)) ? 1u : 0u;
             P.many_runs = (v.slo_overflow || v.slo_distinct > kSloRankMax) ? 1u : 0u;
         }
-        // candidate slots per warp: the blocked path holds at most W live + 32 new candidates; the
+        // candidate slots per warp: the blocked path holds at most W + 1 candidates after a prune
+        // (b = 0 .. W at the block end) + 32 new ones (+ 32 more when a block only folds); the
         // generic path at most W + 1 and reads one slot ahead
-        P.cap_slots = (uint32_t)align_up(cfg->max_batch + (P.narrow ? 32 : 33), 32);
+        P.cap_slots = (uint32_t)align_up(cfg->max_batch + (P.narrow ? 33 + (UELLM_DP_PRUNE_EVERY > 1 ? 32 : 0) : 33), 32);
         void *ev[3] = {nullptr, nullptr, nullptr};
         for (int k = 0; k < 3; ++k)
             if ((uint64_t)(UELLM_STAGE_DP_LOCAL_END + k) < v.n_events) ev[k] = v.events[UELLM_STAGE_DP_LOCAL_END + k];

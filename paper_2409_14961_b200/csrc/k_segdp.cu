@@ -298,6 +298,9 @@ constexpr uint32_t kHullMin = UELLM_HULL_MIN;
 #endif
 #ifndef UELLM_DP_VFREE
 #define UELLM_DP_VFREE 1
+#endif
+#ifndef UELLM_DP_PRUNE_EVERY
+#define UELLM_DP_PRUNE_EVERY 1
 #endif   // shorter lean ranges are evaluated whole
 // offset of row q of the triangular table (row q holds k = q+1 .. 31)
 __host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
@@ -594,6 +597,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
     if (FIX) prune(L, L, 0, 0, s, false, 0u);   // the W fix-up candidates, pruned before the first block
 
     uint32_t evals = 0;
+    uint32_t nblk = 0;
     bool stop = false;
     uint32_t done = s;
     uint64_t filled = 0;
@@ -1028,7 +1032,20 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         if (vl) SW.put(S, L + lane, iC, j0 + 1 + lane, imo, imi);
         evals += B * (B - 1) / 2;
         __syncwarp();
-        prune(L + B, L, bmo, bmi, jend, one_run_ext && one_run_intra, prev_slo);
+        // Pruning is optional (any subset of what D1 allows is exact); folding the block maxima into
+        // the older slots is not.  With UELLM_DP_PRUNE_EVERY = 2 every other block only folds and
+        // appends (the list then holds at most W + 1 + 2 * 32 candidates, see cap_slots).
+        if (UELLM_DP_PRUNE_EVERY == 1 || (++nblk % UELLM_DP_PRUNE_EVERY) == 0 || L + 2 * B > P.cap_slots) {
+            prune(L + B, L, bmo, bmi, jend, one_run_ext && one_run_intra, prev_slo);
+        } else {
+            for (uint32_t k = lane; k < L; k += 32) {
+                const unsigned long long cp = (unsigned long long)S.sl[k].y;
+                const uint32_t mo = max((uint32_t)(cp >> 32) & 0xffffu, bmo), mi = max((uint32_t)(cp >> 48), bmi);
+                S.sl[k].y = (long long)pack_slot((uint32_t)cp, mo, mi);
+            }
+            L += B;
+            __syncwarp();
+        }
     }
     R.positions = done - s;
     R.evals = evals;

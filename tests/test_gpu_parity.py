@@ -168,6 +168,18 @@ def test_uniform_long_runs_deferred(case):
     assert d["cascade_reruns"] < d["tiles"] // 4, d
 
 
+@pytest.mark.parametrize("W_", [16, 64, 256])
+def test_zero_cost_full_candidate_list(W_):
+    """Every service-time term and the penalty zero: every batch costs 0, no candidate dominates
+    another, so after each block's prune all W + 1 candidates (b = 0 .. W) are alive and the block
+    appends 32 more -- the candidate list at its largest (slot capacity W + 33).  The tie rule
+    (smallest minimising i) then picks batches of W from the window start."""
+    inp, out, slo, cfg = W.c3(8, n=30_000)
+    cfg = cfg.replace(max_batch=W_, kv_cap_bytes=0, lambda_us=0, t_batch_us=0, t_iter_us=0, t_tok_us=0,
+                      t_prefill_us=0, window=10_000)
+    assert_parity(inp, out, slo, cfg)
+
+
 def test_uniform_runs_generic_path_exact():
     """The generic 64-bit path has no periodic fill (slow but exact): same schedule."""
     inp, out, slo, cfg = W.uniform_runs(32, n=40_000, runs=((6_000, 128, 257),))
