@@ -86,12 +86,20 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
         const uint64_t n4 = n / 4;
         const uint4 *in4 = reinterpret_cast<const uint4 *>(in), *out4 = reinterpret_cast<const uint4 *>(out);
         const float4 *slo4 = reinterpret_cast<const float4 *>(slo);
+        // the next iteration's three 16-byte loads are issued before this one is consumed (twice
+        // the bytes in flight per warp: the consume loop is long enough to hide them)
+        uint4 na = make_uint4(0, 0, 0, 0), no = make_uint4(0, 0, 0, 0);
+        float4 nf = make_float4(0.f, 0.f, 0.f, 0.f);
+        auto fetch = [&](uint64_t g) {
+            if (g < n4) { na = __ldg(in4 + g); no = __ldg(out4 + g); nf = __ldg(slo4 + g); }
+        };
+        fetch(tid);
         for (uint64_t g0 = tid - lane; g0 < n4; g0 += stride) {    // whole warps iterate together
             const uint64_t g = g0 + lane;
             const bool v = g < n4;
-            uint4 a = make_uint4(0, 0, 0, 0), o = make_uint4(0, 0, 0, 0);
-            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (v) { a = __ldg(in4 + g); o = __ldg(out4 + g); f = __ldg(slo4 + g); }
+            const uint4 a = na, o = no;
+            const float4 f = nf;
+            fetch(g + stride);
             const bool cv = cover_now();
             consume(a.x, o.x, f.x, v, cv);
             consume(a.y, o.y, f.y, v, cv);

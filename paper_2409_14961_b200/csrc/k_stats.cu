@@ -75,7 +75,17 @@ __device__ __forceinline__ void stats_est_body(const StatsParams &S, uint64_t m)
         const uint32_t a = S.offsets[t], z = S.offsets[t + 1];
         uint32_t s = 0, O = 0;
         unsigned long long si64 = 0, so64 = 0;
-        for (uint32_t k = a + sub; k < z; k += G) {
+        // four member loads per array in flight per lane (the batch's loads are independent; a
+        // rolled loop waited for each before issuing the next)
+        uint32_t k = a + sub;
+        for (; k + 3 * G < z; k += 4 * G) {
+            uint32_t vi[4], vo[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { vi[u] = __ldg(S.rin + k + u * G); vo[u] = __ldg(S.rout + k + u * G); }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { s = max(s, vi[u]); O = max(O, vo[u]); si64 += vi[u]; so64 += vo[u]; }
+        }
+        for (; k < z; k += G) {
             const uint32_t vi = __ldg(S.rin + k), vo = __ldg(S.rout + k);
             s = max(s, vi); O = max(O, vo);
             si64 += vi; so64 += vo;
