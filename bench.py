@@ -357,39 +357,50 @@ def main():
             if k is not None:
                 xe[k][0].record(stream)
             X.pack(g.profile, g.cfg, g.totals, stream)
-            with torch.cuda.stream(stream):
-                X.all_gather(backend=args.dist_backend)
-            X.combine(stream)
-            if k is not None:
-                xe[k][1].record(stream)
+            if not local_only:
+                exchange(k)
 
+    def exchange(k=None):
+        with torch.cuda.stream(stream):
+            X.all_gather(backend=args.dist_backend)
+        X.combine(stream)
+        if k is not None:
+            xe[k][1].record(stream)
+
+    local_only = False
     step(sync_load=True)
     for _ in range(Wm - 1):
         step()
     torch.cuda.synchronize(dev)
-    # the whole step (reload -> schedule -> stats [-> a9 pack / NCCL allgather / combine]) captured
-    # once as a CUDA graph and replayed: one launch per step, no host synchronisation inside it
+    # the rank's local step (reload -> schedule -> stats [-> a9 pack]) captured once as a CUDA graph
+    # and replayed: one launch, no host synchronisation inside it.  At N > 1 the collective and the
+    # combine stay eager on the same stream (every rank issues exactly one allgather per step
+    # whether or not its own capture succeeded, so a rank falling back cannot desynchronise them)
     graph, graph_err = None, None
-    if not args.no_graph and (world == 1 or args.dist_backend == "nccl"):
+    if not args.no_graph:
         try:
+            local_only = True
             cg = torch.cuda.CUDAGraph()
             with torch.cuda.graph(cg, stream=stream, capture_error_mode="thread_local"):
                 step()
             graph = cg
-            for _ in range(2):
-                with torch.cuda.stream(stream):
-                    graph.replay()
             torch.cuda.synchronize(dev)
         except Exception as ex:      # (recorded in the JSON line; the eager step is timed instead)
             graph, graph_err = None, f"{type(ex).__name__}: {ex}"[:300]
             torch.cuda.synchronize(dev)
+        local_only = False
 
     def timed_step(k=None):
         if graph is not None:
             with torch.cuda.stream(stream):
                 graph.replay()
+            if X is not None:
+                exchange()
         else:
             step()
+    for _ in range(2):                   # warm replays (every rank: one allgather each)
+        timed_step()
+    torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
     time.sleep(0.3)
     if world > 1:
