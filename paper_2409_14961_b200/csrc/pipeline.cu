@@ -32,10 +32,13 @@ static cudaError_t add_base(uint32_t *a, uint64_t n, uint32_t base, cudaStream_t
     return cudaGetLastError();
 }
 
+constexpr uint64_t kPipeMaxGroups = 64;
+
 struct PipeLayout {
     uint64_t group_q;                 // queries of the largest group (whole windows)
     uint64_t groups;
-    uint64_t wl, nwin, tail, per, rem; // group g = windows [gwin(g), gwin(g+1)) (see gwin)
+    uint64_t wl, nwin, tail;          // group g = windows [start[g], start[g+1])
+    uint64_t start[kPipeMaxGroups + 1];
     uint64_t ws[2], ws_bytes;         // scheduling workspaces of the two compute lanes
     uint64_t in[3], out[3], slo[3];   // input staging slots (g % 3)
     uint64_t order[3], offs[3];       // output staging slots (g % 3)
@@ -50,16 +53,36 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     const uint64_t wl = cfg.window ? (cfg.window < n ? cfg.window : n) : n;
     const uint64_t nwin = n ? ceil_div(n, wl ? wl : 1) : 0;
     uint64_t G = groups ? groups : 12;
+    if (G > kPipeMaxGroups) G = kPipeMaxGroups;
     if (G > nwin) G = nwin ? nwin : 1;
-    // The pipeline is bound by the host->device copies; once the last group's copy lands, its
-    // load / schedule / stats and device->host copy are exposed.  So the last group is small
-    // (about 1/4 of an even share, at least one window) and the rest split evenly.
+    // The pipeline is bound by the host->device copies; once the last copy lands, the groups still
+    // computing (two compute lanes) and the last device->host copy are exposed.  So the last groups
+    // taper -- about 1/2, 1/4, 1/8 of an even share (at least one window each) -- and the rest
+    // split evenly: little GPU work is left when the copies end.
     P.wl = wl; P.nwin = nwin;
-    P.tail = G > 1 ? (nwin / (4 * G) > 1 ? nwin / (4 * G) : 1) : nwin;
-    const uint64_t body = nwin - P.tail;
-    P.per = G > 1 ? body / (G - 1) : 0;
-    P.rem = G > 1 ? body % (G - 1) : 0;
-    const uint64_t maxw = G > 1 ? (P.per + (P.rem ? 1 : 0) > P.tail ? P.per + (P.rem ? 1 : 0) : P.tail) : nwin;
+    const uint64_t share = G ? nwin / G : 0;
+    uint64_t K = G > 1 ? (G - 1 < 3 ? G - 1 : 3) : 0;
+    uint64_t tsz[3] = {0, 0, 0}, tail = 0;
+    for (uint64_t k = 0; k < K; ++k) {
+        tsz[k] = share >> (k + 1);
+        if (tsz[k] < 1) tsz[k] = 1;
+        tail += tsz[k];
+    }
+    if (tail + (G - K) > nwin) { K = 0; tail = 0; }   // too few windows to taper
+    P.tail = tail;
+    const uint64_t body = nwin - tail, nb = G - K;
+    uint64_t w = 0;
+    for (uint64_t g = 0; g < nb; ++g) {
+        P.start[g] = w;
+        w += body / nb + (g < body % nb ? 1 : 0);
+    }
+    for (uint64_t k = 0; k < K; ++k) {
+        P.start[nb + k] = w;
+        w += tsz[k];
+    }
+    P.start[G] = nwin;
+    uint64_t maxw = 0;
+    for (uint64_t g = 0; g < G; ++g) maxw = P.start[g + 1] - P.start[g] > maxw ? P.start[g + 1] - P.start[g] : maxw;
     P.group_q = n ? maxw * wl : 0;
     if (P.group_q > n) P.group_q = n;
     P.groups = n ? G : 0;
@@ -83,9 +106,7 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
 static uint64_t gwin(const PipeLayout &P, uint64_t g)
 {
     if (P.groups <= 1) return g ? P.nwin : 0;
-    if (g >= P.groups) return P.nwin;
-    const uint64_t gg = g < P.groups - 1 ? g : P.groups - 1;
-    return gg * P.per + (gg < P.rem ? gg : P.rem);
+    return g >= P.groups ? P.nwin : P.start[g];
 }
 
 }  // namespace uellm

@@ -56,7 +56,7 @@ def d2h():
 
 
 print("h2d_ms", round(timed(h2d), 3), "d2h_ms", round(timed(d2h), 3))
-for groups in (6, 8, 10, 12, 16):
+for groups in (10, 12, 16, 20, 24):
     wsb = U.pipeline_workspace_bytes(n, c, groups)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     ms = timed(lambda: U.schedule_pipelined(n, p_in, p_out, p_slo, c, groups, ws, wsb, h_order, h_offs, nb,
