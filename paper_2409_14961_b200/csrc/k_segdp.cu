@@ -1252,17 +1252,22 @@ __global__ void k_dp_cascade(DPParams P)
     // whether every fix-up converged (the common case: then the frame offsets are a prefix sum
     // of the deltas, computed warp-parallel instead of walking the tiles one by one)
     uint32_t K = 0;
-    bool allconv = true;
     for (uint32_t k0 = 0; k0 < P.tpw; k0 += 32) {
         const uint32_t k = k0 + lane;
         const bool v = k < P.tpw && P.tiles[t0 + k].valid;
         const uint32_t bv = __ballot_sync(0xffffffffu, v);
         K += __popc(bv);
-        const bool nc = v && k >= 1 && !P.tiles[t0 + k].conv;
-        if (__any_sync(0xffffffffu, nc)) allconv = false;
         if (bv != 0xffffffffu) break;
     }
     if (K == 0) return;
+    // every fix-up converged except possibly the window's LAST tile's (it has no successor to meet:
+    // its fix-up runs to the window end in the exact frame of its predecessor) -- the common case
+    bool allconv = true;
+    for (uint32_t k0 = 0; k0 + 1 < K; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool nc = k >= 1 && k + 1 < K && !P.tiles[t0 + k].conv;
+        if (__any_sync(0xffffffffu, nc)) { allconv = false; break; }
+    }
     if (allconv) {
         long long carry = 0;                                    // off_local of the previous tile
         for (uint32_t k0 = 0; k0 < K; k0 += 32) {
@@ -1275,15 +1280,20 @@ __global__ void k_dp_cascade(DPParams P)
                 if ((int)lane >= o) inc += y;
             }
             if (k < K) {
+                // (an unconverged last tile has delta 0: off_fix = its predecessor's off_local)
+                const bool lc = k == 0 || P.tiles[t0 + k].conv;
                 P.tiles[t0 + k].off_fix = k ? carry + inc - d : 0ll;
-                P.tiles[t0 + k].off_local = k ? carry + inc : 0ll;
+                P.tiles[t0 + k].off_local = (k && lc) ? carry + inc : 0ll;
             }
             carry += __shfl_sync(0xffffffffu, inc, 31);
         }
         __syncwarp();
         if (lane == 0) {
             const TileRec &r = P.tiles[t0 + K - 1];
-            P.wincost[w] = (unsigned long long)(P.Cx[r.e - 1] + (K == 1 ? 0ll : r.off_local));
+            long long c;
+            if (K == 1) c = P.Cx[r.e - 1];
+            else c = r.conv ? P.Cx[r.e - 1] + r.off_local : P.CFx[r.e - 1] + r.off_fix;
+            P.wincost[w] = (unsigned long long)c;
         }
         return;
     }
