@@ -473,6 +473,8 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         P.rin = rin; P.rout = rout; P.rslo = rslo;
         P.Cx = at<long long>(w, L.keys1); P.CFx = at<long long>(w, L.keys2);
         P.argx = at<uint16_t>(w, L.argx);
+        P.Crf = at<long long>(w, L.st_so);             // the stats' scratch is free during the schedule
+        P.Arf = at<uint16_t>(w, L.st_pin);
         P.tiles = at<TileRec>(w, L.tiles);
         P.tflags = at<uint32_t>(w, L.tflags);
         P.diag = diag;

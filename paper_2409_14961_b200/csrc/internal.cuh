@@ -92,7 +92,9 @@ struct TileRec {
     uint32_t fill_s, fill_P; // cascade: fix frame deferred to k_dp_fill, periodic with period fill_P
     int64_t fill_F;          //   from the reference boundaries (fill_s - fill_P, fill_s]: C += fill_F per period
     uint32_t remark;         // traceback: 1 + the true entry when the tile must be re-marked, else 0
-    uint32_t pad_;
+    uint32_t refixed;        // k_dp_refix re-ran the fix-up from the predecessor's fix frame into the
+    uint32_t rf_conv, rf_conv_pos, rf_fix_end;   //   side arrays; its results (the cascade may adopt them)
+    int64_t rf_delta;
 };
 
 struct Diag {                // device counters, see uellm_diagnostics
@@ -253,6 +255,8 @@ struct DPParams {
     const uint32_t *rin, *rout, *rslo;
     long long *Cx, *CFx;
     uint16_t *argx;
+    long long *Crf;                              // k_dp_refix outputs (scratch free during the schedule)
+    uint16_t *Arf;
     TileRec *tiles;
     uint32_t *tflags;                            // [ntiles] local-done flags, then the local / fix-up work counters
     Diag *diag;

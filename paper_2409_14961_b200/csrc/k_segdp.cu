@@ -301,6 +301,9 @@ constexpr uint32_t kHullMin = UELLM_HULL_MIN;
 #endif
 #ifndef UELLM_DP_PRUNE_EVERY
 #define UELLM_DP_PRUNE_EVERY 1
+#endif
+#ifndef UELLM_DP_REFIX
+#define UELLM_DP_REFIX 1
 #endif   // shorter lean ranges are evaluated whole
 // offset of row q of the triangular table (row q holds k = q+1 .. 31)
 __host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
@@ -1241,6 +1244,46 @@ __global__ void __launch_bounds__(256) k_dp_fill(DPParams P, uint64_t ntiles)
 
 // One warp per window: resolve tiles whose predecessor did not converge, compute the frame
 // offsets of every tile and the window's optimal cost C[w1].
+// Second fix-up round, in parallel (speculative).  A tile whose predecessor's fix-up did not
+// converge has a fix-up computed from the wrong (local) frame; the cascade would re-run it from the
+// predecessor's fix frame, one tile after another.  Here every such tile whose pre-predecessor
+// converged in round 1 is re-run from the predecessor's round-1 fix frame in parallel, into side
+// arrays (round 1's values stay intact).  The cascade adopts a re-run (copies it in) only when it
+// did not touch the predecessor itself -- then the frame the re-run read is the one the cascade
+// would read.  Eligibility reads round-1 states only, and an eligible tile's predecessor is never
+// eligible, so no re-run reads what another writes.  Uniform stretches stay with the cascade.
+template <int V>
+__global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_refix(DPParams P, uint64_t ntiles)
+{
+    extern __shared__ __align__(16) char smem[];
+    const uint32_t lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < ntiles; t += nw) {
+        uint32_t s, e, k, w; bool valid;
+        tile_bounds(P, t, s, e, k, w, valid);
+        if (!valid || k < 2) continue;
+        const TileRec &a = P.tiles[t - 2], &b = P.tiles[t - 1];
+        if (b.conv || !a.conv || !b.valid) continue;
+        if (entry_uniform(P, t, s)) continue;                  // uniform stretches: the cascade's deferral
+        TileRec r = P.tiles[t];
+        DPParams Q = P;                   // outputs to the side arrays: round 1's values stay intact
+        Q.CFx = P.Crf;
+        Q.argx = P.Arf;
+        DpResult R = dp_run<true, V>(Q, smem, warp, r.s, r.e, P.CFx, r.fix_end, true, false);
+        if (lane == 0) {
+            TileRec &q = P.tiles[t];
+            q.rf_conv = R.conv; q.rf_conv_pos = R.conv_pos; q.rf_fix_end = max(R.fix_end, r.fix_end);
+            q.rf_delta = R.delta;
+            q.refixed = 1;
+            atomicAdd(&P.diag->fixup_positions, (unsigned long long)R.positions);
+            atomicAdd(&P.diag->dp_evals, (unsigned long long)R.evals);
+            if (R.filled) atomicAdd(&P.diag->dp_filled, (unsigned long long)R.filled);
+        }
+        __syncwarp();
+    }
+}
+
 template <int V>
 __global__ void k_dp_cascade(DPParams P)
 {
@@ -1310,7 +1353,9 @@ __global__ void k_dp_cascade(DPParams P)
     long long ref_F = 0;
     if (lane == 0) { P.tiles[t0].off_local = 0; P.tiles[t0].off_fix = 0; }
     uint32_t eu_mask = 0;            // entry_uniform of tiles (k & ~31) + lane, 32 at a time
+    bool prev_touched = false;       // the cascade changed tile k-1's fix frame (re-run / adopted / deferred)
     for (uint32_t k = 1; k < K; ++k) {
+        bool touched = false;
         if (k == 1 || (k & 31u) == 0) {
             const uint32_t kk = (k & ~31u) + lane;
             bool e = false;
@@ -1332,6 +1377,7 @@ __global__ void k_dp_cascade(DPParams P)
                 q.conv = 0; q.fix_end = te; q.off_fix = tail_off; q.off_local = 0;
             }
             __syncwarp();
+            prev_touched = true;
             continue;
         }
         TileRec r = P.tiles[t0 + k];
@@ -1355,9 +1401,22 @@ __global__ void k_dp_cascade(DPParams P)
             if (deferred) {
                 r.fill_s = ref_s; r.fill_P = ref_P; r.fill_F = ref_F;
                 r.conv = 0; r.fix_end = r.e;
+                touched = true;
+            } else if (r.refixed && !prev_touched) {
+                // k_dp_refix already re-ran it from the predecessor's round-1 fix frame, which the
+                // cascade left untouched: adopt the side arrays' values and results
+                for (uint32_t j = r.s + 1 + lane; j <= r.rf_fix_end; j += 32) {
+                    P.CFx[j - 1] = __ldcg(P.Crf + j - 1);
+                    P.argx[j - 1] = __ldcg(reinterpret_cast<const unsigned short *>(P.Arf) + j - 1);
+                }
+                __syncwarp();
+                r.conv = r.rf_conv; r.conv_pos = r.rf_conv_pos; r.fix_end = max(r.rf_fix_end, r.fix_end);
+                r.delta = r.rf_delta;
+                touched = true;
             } else {
                 DpResult R = dp_run<true, V>(P, smem, 0, r.s, r.e, P.CFx, r.fix_end, true, eu);
                 r.conv = R.conv; r.conv_pos = R.conv_pos; r.fix_end = max(R.fix_end, r.fix_end); r.delta = R.delta;
+                touched = true;
                 if (lane == 0) {
                     atomicAdd(&P.diag->cascade_reruns, 1ull);
                     atomicAdd(&P.diag->fixup_positions, (unsigned long long)R.positions);
@@ -1373,6 +1432,7 @@ __global__ void k_dp_cascade(DPParams P)
         else { r.off_local = 0; tail_local = false; }
         if (lane == 0) P.tiles[t0 + k] = r;
         __syncwarp();
+        prev_touched = touched;
     }
     if (ref_P) {            // the window ends inside a deferred stretch: its last value is needed now
         const TileRec &q = P.tiles[t0 + K - 1];
@@ -1418,6 +1478,11 @@ static cudaError_t launch_segdp(const DPParams &P, uint64_t ntiles, cudaStream_t
     k_dp_tiles<V><<<blocks, wpc * 32, smem, st>>>(P, ntiles);
     ++*launches;
     if (ev[0]) cudaEventRecord((cudaEvent_t)ev[0], st);
+    if (UELLM_DP_REFIX && V != 0) {
+        if ((e = cudaFuncSetAttribute(k_dp_refix<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+        k_dp_refix<V><<<blocks, wpc * 32, smem, st>>>(P, ntiles);
+        ++*launches;
+    }
     if (ev[1]) cudaEventRecord((cudaEvent_t)ev[1], st);
     k_dp_cascade<V><<<P.nwin, 32, smem1, st>>>(P);
     ++*launches;
