@@ -141,6 +141,11 @@ __global__ void __launch_bounds__(256) k_load(const uint32_t *__restrict__ in, c
         if (!su) continue;
         uint32_t h = slo_hash(su, kSloSetBits);
         for (uint32_t probe = 0; probe < kSloSetSize; ++probe) {
+            // a plain read first: after the first CTAs, every class value is already in the set, and
+            // thousands of CTAs CAS-ing the same few slots serialised the kernel's tail
+            const uint32_t cur = *(volatile uint32_t *)&slo_set[h];
+            if (cur == su) break;
+            if (cur != 0u) { h = (h + 1) & (kSloSetSize - 1); continue; }
             if (*(volatile uint32_t *)&meta->slo_distinct > kSloRankMax) { atomicExch(&meta->slo_overflow, 1u); break; }
             const uint32_t old = atomicCAS(&slo_set[h], 0u, su);
             if (old == 0u) { atomicAdd(&meta->slo_distinct, 1u); break; }
