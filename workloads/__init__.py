@@ -352,3 +352,67 @@ def random_small(seed: int, n: int, pattern: str = "rand"):
     if cfg.t_batch_us == 0 and cfg.t_iter_us == 0 and rng.random() < 0.5:
         cfg.t_batch_us = 1
     return inp, out, slo, cfg
+
+
+def random_medium(seed: int):
+    """Randomised medium-size instances for the GPU parity fuzz test: every SEG-DP kernel variant
+    (lambda 0 / < 2^32 / >= 2^32, SLO split, many SLO runs), both sort key layouts (class-valued
+    SLOs vs more than 1024 distinct values), windows of any length (16-byte aligned or not), forced
+    DP tile lengths, the generic 64-bit path, KV caps that bind or not, zero service-time terms,
+    uniform stretches.  Returns (inp, out, slo, cfg)."""
+    rng = _rng(seed, 71)
+    n = int(rng.choice([1, 2, 31, 33, 1000, 4097, 20_000, 60_000]))
+    shape = str(rng.choice(["longtail", "alpaca", "runs", "identical", "distinct", "tiny"]))
+    if shape == "longtail":
+        inp, out, slo = long_tail(n, seed, stream=72)
+    elif shape == "alpaca":
+        inp = _lognormal_int(rng, 24, 0.6, 1, 512, n)
+        out = _bucket_up(_lognormal_int(rng, 64, 0.9, 1, 1024, n), 32, 1024)
+        slo = SLO_CLASSES_3[rng.integers(0, 3, size=n)]
+    elif shape == "runs":
+        inp, out, slo = long_tail(n, seed, stream=73)
+        k = int(rng.integers(1, 4))
+        for _ in range(k):                       # a few long stretches of one identical query
+            a = int(rng.integers(0, max(1, n)))
+            z = min(n, a + int(rng.integers(1, max(2, n // 2))))
+            inp[a:z] = int(rng.integers(1, 300)); out[a:z] = 2 * int(rng.integers(1, 200)) + 1
+            slo[a:z] = slo[a]
+    elif shape == "identical":
+        inp = np.full(n, int(rng.integers(1, 500)), np.uint32)
+        out = np.full(n, int(rng.integers(1, 2000)), np.uint32)
+        slo = np.full(n, np.float32(rng.uniform(0.5, 100.0)), np.float32)
+    elif shape == "distinct":                   # > 1024 distinct SLOs: the u64 key path, many runs
+        inp = _lognormal_int(rng, 128, 1.0, 1, 4096, n)
+        out = rng.integers(1, 4097, size=n).astype(np.uint32)
+        slo = rng.uniform(0.5, 350.0, size=n).astype(np.float32)
+    else:
+        inp = rng.integers(1, 40, size=n).astype(np.uint32)
+        out = rng.integers(1, 40, size=n).astype(np.uint32)
+        slo = rng.uniform(0.001, 0.05, size=n).astype(np.float32)
+    W = int(rng.choice([1, 2, 8, 16, 64, 256, 512]))
+    lam = int(rng.choice([0, 1000, 10**9, 10**10]))
+    window = int(rng.choice([0, 0, 1000, 4097, 25_000, 30_000]))
+    cap_tok = int(rng.choice([0, 2000, 16_384, 317_617]))
+    t = [int(rng.choice(v)) for v in ([0, 1000, 1000], [0, 2000, 2000], [0, 40, 40], [0, 10, 10])]
+    if t[0] == 0 and t[1] == 0 and rng.random() < 0.5:
+        t[0] = 1000
+    tile = 0
+    if rng.random() < 0.3:
+        tile = W * int(rng.choice([2, 3, 4, 8, 16]))
+    cfg = SchedConfig(window=window, max_batch=W, split_on_slo_change=int(rng.integers(0, 2)),
+                      kv_cap_bytes=cap_tok * 524_288, t_batch_us=t[0], t_iter_us=t[1], t_tok_us=t[2],
+                      t_prefill_us=t[3], lambda_us=lam, dp_tile=tile,
+                      flags=1 if rng.random() < 0.1 else 0)
+    u = rng.random()
+    if u < 0.15:                                # the paper's Alg. 1 (random weights / threshold)
+        cfg = cfg.replace(mode=MODE_SLO_ODBS, w1=float(rng.choice([0.0, 0.3, 1.0])),
+                          w2=float(rng.choice([0.02, 0.5, 1.0])), threshold=float(rng.choice([50.0, 900.0, 5000.0])),
+                          l1=float(rng.choice([1.0, 2.0])), l2=float(rng.choice([1.0, 0.5])),
+                          eq2_additive=int(rng.integers(0, 2)))
+        if cfg.w1 + cfg.w2 == 0.0:
+            cfg = cfg.replace(w2=1.0)
+    elif u < 0.2:
+        cfg = cfg.replace(mode=MODE_FIFO)
+    elif u < 0.25:
+        cfg = cfg.replace(mode=MODE_SORT_ONLY)
+    return inp, out, slo, cfg
