@@ -174,14 +174,15 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def stage_hbm(st_ms: dict, n: int, m: int, passes: int, hbm_gbs: float) -> dict:
+def stage_hbm(st_ms: dict, n: int, m: int, passes: int, hbm_gbs: float, fused: bool = True) -> dict:
     """Per-stage algorithmic bytes / event-timed stage ms / measured HBM peak:
-    load 12 B/q read; sort 8 B/q read + 8 B/q written per radix pass, the last pass gathers 4 B/q of
-    inputs and writes the 12 B/q records + 4 B/q order; SEG-DP 12 B/q read + 10 B/q written (C, arg);
-    traceback 2 B/q read + n/8 bitmap; compact n/8 + 4 B/batch; stats 12 B/q + 4 B/batch read,
-    80 B/batch written."""
-    alg = {"load": 12 * n,
-           "sort": 16 * n * passes + 20 * n,
+    load 12 B/q read (+ 4 B/q packed keys written by the fused reload of a rank-compressed profile);
+    sort: the key pack (12 B/q, unless the reload packed), 8 B/q read + 8 B/q written per radix pass
+    (the first pass reads the input length as payload), the last pass writes the 12 B/q records +
+    4 B/q order instead; SEG-DP 12 B/q read + 10 B/q written (C, arg); traceback 2 B/q read + n/8
+    bitmap; compact n/8 + 4 B/batch; stats 12 B/q + 4 B/batch read, 80 B/batch written."""
+    alg = {"load": (16 if fused else 12) * n,
+           "sort": 16 * n * passes + 8 * n + (0 if fused else 12 * n),
            "dp": 22 * n,
            "traceback": 2 * n + n // 8,
            "compact": n // 8 + 4 * (m + 1),
@@ -454,7 +455,7 @@ def main():
                 "peak_source": f"{SMS} SMs x {ISSUE_PER_SM} issue slots/clk x {sm_max:.0f} MHz "
                                f"(guide unit counts; MEASURED_PEAKS sm_max_mhz)"}
     else:
-        sh = stage_hbm(st_ms, n, m, diag["sort_passes"], hbm_gbs)
+        sh = stage_hbm(st_ms, n, m, diag["sort_passes"], hbm_gbs, diag["sort_key_bits"] != 64)
         key = {"sort": "sort", "decode": "sort", "stats": "stats", "load": "load", "traceback": "traceback",
                "compact": "compact"}.get(dom, "sort")
         roof = {"bound": "hbm", "kernel": dom, "achieved": sh[key]["achieved_gbs"], "peak": hbm_gbs, "unit": "GB/s",
@@ -573,10 +574,12 @@ def main():
                             "load": "uellm_profile_reload (device-side validation, no host sync); "
                                     "one synchronising uellm_profile_load before the timed region"},
             "roofline": roof, "step_hbm_roofline": step_hbm,
-            "stage_hbm": stage_hbm(st_ms, n, m, diag["sort_passes"], hbm_gbs), "stage_ms": st_ms,
-            # our kernels launched inside the timed region: K steps x (load + schedule + stats [+ a9])
-            "gpu_launches": K * int(diag["sched_launches"] + diag["stats_launches"] + 1 + (4 if world > 1 else 0)),
-            "gpu_launches_per_step": int(diag["sched_launches"] + diag["stats_launches"] + 1 + (4 if world > 1 else 0)),
+            "stage_hbm": stage_hbm(st_ms, n, m, diag["sort_passes"], hbm_gbs, diag["sort_key_bits"] != 64),
+            "stage_ms": st_ms,
+            # our kernels launched inside the timed region: K steps x (reload [load / fused pack +
+            # status check] + schedule + stats [+ a9])
+            "gpu_launches": K * int(diag["sched_launches"] + diag["stats_launches"] + 2 + (4 if world > 1 else 0)),
+            "gpu_launches_per_step": int(diag["sched_launches"] + diag["stats_launches"] + 2 + (4 if world > 1 else 0)),
             "diagnostics": diag, "batches": m_job, "dp_cost": job_totals["dp_cost"],
             "job_offsets_sha256": offsets_digest(job_offsets, job_totals),
             "a9_exchange_bytes_per_rank": X.rec_bytes if X else None,

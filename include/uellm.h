@@ -62,8 +62,9 @@ enum {
     UELLM_ERR_CUDA = 5,         /* a CUDA runtime call or kernel launch failed                     */
     UELLM_ERR_UNSUPPORTED = 6,  /* valid, but outside this build's limits (e.g. max_batch > 4096)  */
     UELLM_ERR_STALE = 7         /* uellm_profile_reload: the new queries need other decisions than
-                                   the profile holds (larger maxima, other SLO set size, new
-                                   varying key bits): load them with uellm_profile_load          */
+                                   the profile holds (larger maxima, an SLO value outside the
+                                   profile's set / other set size, new varying key bits): load
+                                   them with uellm_profile_load                                  */
 };
 
 /* Segmentation of the sorted stream (uellm_config.mode). */
@@ -234,12 +235,17 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
  * The validation of uellm_profile_load runs on the device and its verdict goes to the profile's
  * device status word (uellm_profile_status): UELLM_OK; UELLM_ERR_CONTRACT for an invalid query;
  * UELLM_ERR_STALE when the new queries exceed the decisions the profile was loaded with
- * (max_in or max_out larger, another number of distinct SLO values or a distinct-set overflow,
- * key bits varying that were constant).  Every decision the later calls take from the profile
- * stays valid for queries inside those limits (the cost and KV overflow bounds, the 32-bit DP
- * path and the packed sort payload only need maxima not above the recorded ones; the radix
- * passes cover every digit that varied before).  The schedule / stats of a step whose status
- * word is not UELLM_OK are undefined: read the word (asynchronously) before using them. */
+ * (max_in or max_out larger; for a profile with the rank-compressed sort key -- at most 1024
+ * distinct SLO values -- an SLO value outside the profile's distinct set; otherwise another number
+ * of distinct SLO values or a distinct-set overflow, or key bits varying that were constant).
+ * Every decision the later calls take from the profile stays valid for queries inside those
+ * limits (the cost and KV overflow bounds, the 32-bit DP path and the packed sort payload only
+ * need maxima not above the recorded ones; a subset of the SLO set keeps every rank; the radix
+ * passes cover every digit that varied before).  For a rank-compressed profile the reload also
+ * packs the sort keys and the first radix pass's histogram into the workspace (one pass over the
+ * arrays), so the next uellm_schedule_batches calls skip that pass.  The schedule / stats of a
+ * step whose status word is not UELLM_OK are undefined: read the word (asynchronously) before
+ * using them. */
 uellm_status uellm_profile_reload(uellm_profile *p, const uellm_queries *q, const uellm_config *cfg,
                                   void *stream);
 

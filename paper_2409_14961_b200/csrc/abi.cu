@@ -86,6 +86,7 @@ WsLayout make_layout(uint64_t n, const uellm_config &cfg)
     L.st_so = take(8 * N); L.st_pin = take(8 * N); L.st_pout = take(8 * N);
     L.a1tiles = take(alg1_scratch_bytes(L.window, L.nwin, (uint32_t)L.W));
     L.hist = take(2 * 4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));   // two histogram buffers (passes alternate)
+    L.hist0 = take(4ull * 256 * (L.sort_tiles ? L.sort_tiles : 1));       // first pass's counts, kept
     L.meta = take(sizeof(LoadMeta)); L.diag = take(sizeof(Diag)); L.acc = take(sizeof(StatAcc));
     L.nb = take(8); L.totals = take(sizeof(uellm_totals));
     L.wincost = take(8 * (L.nwin ? L.nwin : 1));
@@ -165,6 +166,25 @@ uint64_t layout_key(const uellm_config *c)
     mix(dbl(c->w1)); mix(dbl(c->w2)); mix(dbl(c->l1)); mix(dbl(c->l2)); mix(dbl(c->threshold)); mix(dbl(c->eps));
     mix(c->eq2_additive); mix(c->flags);
     return h;
+}
+
+// Rank-compressed sort key plan of a loaded profile (independent of the mode): eligible when at most
+// kSloRankMax distinct SLO values were collected and rank << bits(max_out) | out fits 32 bits.
+struct KeyPlan {
+    bool ok;
+    int ob, rb, cbits;
+};
+KeyPlan key_plan(const ProfileView &v)
+{
+    KeyPlan k;
+    k.ob = 0;
+    while (k.ob < 32 && (v.max_out >> k.ob)) ++k.ob;                           // bits(max_out)
+    k.rb = 0;
+    while (v.slo_distinct > 1 && k.rb < 32 && ((v.slo_distinct - 1) >> k.rb)) ++k.rb;   // bits(distinct - 1)
+    k.cbits = 4;                                                             // compact hash: >= 2 slots per value
+    while ((1u << k.cbits) < 2 * v.slo_distinct && k.cbits < (int)kSloSetBits) ++k.cbits;
+    k.ok = !v.slo_overflow && v.slo_distinct >= 1 && v.slo_distinct <= kSloRankMax && k.rb + k.ob <= 32;
+    return k;
 }
 
 inline void rec(const ProfileView &v, int k, cudaStream_t st)
@@ -288,6 +308,16 @@ uellm_status uellm_profile_load(const uellm_queries *q, const uellm_config *cfg,
     v.max_in = hm.max_in; v.max_out = hm.max_out; v.max_slo = hm.max_slo;
     v.key_or = hm.key_or; v.key_and = hm.key_and;
     v.slo_distinct = hm.slo_distinct; v.slo_overflow = hm.slo_overflow;
+    {
+        // rank table + compact (value, rank) hash of the distinct SLO values, once per profile: the
+        // compressed sort key of every later schedule (and the fused reload) uses it
+        const KeyPlan kp = key_plan(v);
+        if (kp.ok)
+            CU(launch_slo_table(at<uint32_t>(w, L.slo_set), at<uint32_t>(w, L.slo_table),
+                                at<unsigned long long>(w, L.slo_ctab), kp.cbits, st));
+        v.key_plan = kp.ok ? 1u : 0u;
+        v.keys_ready = 0;
+    }
     std::memcpy(out, &v, sizeof v);
     return UELLM_OK;
 }
@@ -308,13 +338,23 @@ uellm_status uellm_profile_reload(uellm_profile *p, const uellm_queries *q, cons
     uint8_t *w = v.ws;
     LoadMeta *meta = at<LoadMeta>(w, L.meta);
     CU(cudaMemsetAsync(meta, 0, sizeof(LoadMeta), st));
-    CU(cudaMemsetAsync(&meta->key_and, 0xff, sizeof(unsigned long long), st));
-    CU(cudaMemsetAsync(at<uint32_t>(w, L.slo_set), 0, 4 * kSloSetSize, st));
-    CU(launch_load(q->input_len, q->pred_out_len, q->slo_s, n, meta, at<uint32_t>(w, L.slo_set), st));
     ReloadRef ref;
     ref.max_in = v.max_in; ref.max_out = v.max_out; ref.slo_distinct = v.slo_distinct;
     ref.slo_overflow = v.slo_overflow; ref.key_or = v.key_or; ref.key_and = v.key_and;
+    const KeyPlan kp = key_plan(v);
+    ref.fused = kp.ok ? 1u : 0u;
+    if (kp.ok) {
+        // rank-compressed profile: validation + key pack + first-pass histogram in one kernel
+        CU(launch_reload_pack32(q->input_len, q->pred_out_len, q->slo_s, n, L.window,
+                                at<unsigned long long>(w, L.slo_ctab), kp.cbits, kp.ob, at<uint32_t>(w, L.keysc),
+                                at<uint32_t>(w, L.hist0), meta, st));
+    } else {
+        CU(cudaMemsetAsync(&meta->key_and, 0xff, sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(at<uint32_t>(w, L.slo_set), 0, 4 * kSloSetSize, st));
+        CU(launch_load(q->input_len, q->pred_out_len, q->slo_s, n, meta, at<uint32_t>(w, L.slo_set), st));
+    }
     CU(launch_reload_check(meta, ref, st));
+    v.keys_ready = kp.ok ? 1u : 0u;
     v.d_in = q->input_len; v.d_out = q->pred_out_len; v.d_slo = q->slo_s;
     std::memcpy(p, &v, sizeof v);
     return UELLM_OK;
@@ -374,32 +414,26 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
     // a3: sort (every mode except FIFO) + a4: records in scheduled order
     uint32_t *rin = at<uint32_t>(w, L.rin), *rout = at<uint32_t>(w, L.rout), *rslo = at<uint32_t>(w, L.rslo);
     int passes = 0;
-    int ob = 0;
-    while (ob < 32 && (v.max_out >> ob)) ++ob;                 // bits(max_out)
-    int rb = 0;
-    while (v.slo_distinct > 1 && rb < 32 && ((v.slo_distinct - 1) >> rb)) ++rb;   // bits(distinct - 1)
-    const bool compressed = cfg->mode != UELLM_MODE_FIFO && !v.slo_overflow && v.slo_distinct >= 1 &&
-                            v.slo_distinct <= kSloRankMax && rb + ob <= 32;
+    const KeyPlan kp = key_plan(v);
+    const int ob = kp.ob, rb = kp.rb;
+    const bool compressed = cfg->mode != UELLM_MODE_FIFO && kp.ok;
     DecodeArgs D;
     D.in = v.d_in; D.table = at<uint32_t>(w, L.slo_table); D.ob = ob;
     D.nslo = v.slo_distinct < kSloRankMax ? v.slo_distinct : kSloRankMax;
     D.packin = 0; D.wb = 0;
     D.rin = rin; D.rout = rout; D.rslo = rslo; D.order = d_order;
     if (compressed) {
-        // rank table, then keys rank << ob | out packed straight from the caller arrays together
-        // with the digit-0 histogram; the last pass writes the records (fused decode)
+        // keys rank << ob | out (rank table built at load) packed straight from the caller arrays
+        // together with the digit-0 histogram -- by the fused reload already (keys_ready), else
+        // here; the last pass writes the records (fused decode)
         uint32_t *kc = at<uint32_t>(w, L.keysc);
         uint32_t *vals0 = at<uint32_t>(w, L.vals0);
-        int cbits = 4;                                         // compact hash: >= 2 slots per value
-        while ((1u << cbits) < 2 * v.slo_distinct && cbits < (int)kSloSetBits) ++cbits;
-        CU(launch_slo_table(at<uint32_t>(w, L.slo_set), at<uint32_t>(w, L.slo_table),
-                            at<unsigned long long>(w, L.slo_ctab), cbits, st));
+        const int cbits = kp.cbits;
         // window-local index and input length packed into the payload when they fit 32 bits
         int wbits = 0, ibits = 0;
         while (wbits < 32 && ((L.window - 1) >> wbits)) ++wbits;
         while (ibits < 32 && ((uint64_t)(v.max_in - 1) >> ibits)) ++ibits;
         if (wbits + ibits <= 32 && wbits < 32) { D.packin = 1; D.wb = wbits; }
-        launches += 1;
         uint32_t mask = 0;
         for (int d = 0; d < 4; ++d) if (8 * d < rb + ob) mask |= 1u << d;
         // window groups: every pass of a group runs before the next group starts, so the group's
@@ -408,16 +442,18 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         const uint32_t *k32 = kc;
         for (uint64_t w0 = 0; w0 < L.nwin; w0 += gw) {
             const uint64_t wn = L.nwin - w0 < gw ? L.nwin - w0 : gw;
-            CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, w0, wn, at<unsigned long long>(w, L.slo_ctab),
-                                  cbits, ob, kc, vals0, at<uint32_t>(w, L.hist), st));
-            launches += 1;
+            if (!v.keys_ready) {
+                CU(launch_pack32_hist(v.d_out, v.d_slo, n, L.window, w0, wn, at<unsigned long long>(w, L.slo_ctab),
+                                      cbits, ob, kc, vals0, at<uint32_t>(w, L.hist0), st));
+                launches += 1;
+            }
             k32 = kc;
             const uint32_t *vals = nullptr;            // identity payload (arrival index = position)
             CU(radix_sort_windows32(&k32, &vals, (uint32_t *)at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                     (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
                                     at<uint32_t>(w, L.hist), at<uint32_t>(w, L.hist) + 256 * L.sort_tiles, n,
                                     L.window, w0, wn, mask, &passes, st,
-                                    (mask & 1u) != 0, &D));
+                                    (mask & 1u) ? at<uint32_t>(w, L.hist0) : nullptr, &D));
             launches += 2 * passes + ((mask & 1u) || !passes ? 0 : 1);   // scan + scatter per pass, one histogram
             if (passes == 0) {
                 CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
@@ -496,6 +532,9 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
         // (b = 0 .. W at the block end) + 32 new ones (+ 32 more when a block only folds); the
         // generic path at most W + 1 and reads one slot ahead
         P.cap_slots = (uint32_t)align_up(cfg->max_batch + (P.narrow ? 33 + (UELLM_DP_PRUNE_EVERY > 1 ? 32 : 0) : 33), 32);
+        // narrow path: the idle lanes of the fast block's u16 max table read up to 1984 bytes below it
+        // (inside the warp's slot array, k_segdp.cu)
+        if (P.narrow && P.cap_slots < 128) P.cap_slots = 128;
         void *ev[3] = {nullptr, nullptr, nullptr};
         for (int k = 0; k < 3; ++k)
             if ((uint64_t)(UELLM_STAGE_DP_LOCAL_END + k) < v.n_events) ev[k] = v.events[UELLM_STAGE_DP_LOCAL_END + k];

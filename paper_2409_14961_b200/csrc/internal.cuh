@@ -66,13 +66,15 @@ struct LoadMeta {
     unsigned long long key_or, key_and;
     uint32_t slo_distinct, slo_overflow;
     uint32_t status;         // uellm_profile_reload's verdict (device status word)
-    uint32_t pad[5];
+    uint32_t slo_missing;    // fused reload: an SLO value outside the profile's distinct set
+    uint32_t pad[4];
 };
 static_assert(sizeof(LoadMeta) == 64, "LoadMeta is 64 bytes");
 // reload: compare the fresh LoadMeta with the decisions recorded in the profile
 struct ReloadRef {
     uint32_t max_in, max_out, slo_distinct, slo_overflow;
     unsigned long long key_or, key_and;
+    uint32_t fused;          // k_reload_pack32 ran: the set test is "every SLO value in the profile's set"
 };
 cudaError_t launch_reload_check(LoadMeta *meta, ReloadRef ref, cudaStream_t st);
 
@@ -161,7 +163,8 @@ struct WsLayout {
     uint64_t bitmap, wscan, blocksum, blockagg;   // boundary bitmap + scan scratch
     uint64_t st_so, st_pin, st_pout;              // per-batch stats scratch (u64 each)
     uint64_t a1tiles;                             // Alg. 1 chain-walk tile exits (uint2)
-    uint64_t hist;                                // u32[sort_tiles * 256]
+    uint64_t hist;                                // u32[2][sort_tiles * 256] (passes alternate)
+    uint64_t hist0;                               // u32[sort_tiles * 256]: first pass's counts (kept)
     uint64_t meta, diag, acc, nb, totals, wincost;
     uint64_t simacc, simtot;                      // uellm_simulate accumulators / host-totals staging
     uint64_t total;
@@ -183,7 +186,9 @@ struct ProfileView {
     uint32_t slo_distinct, slo_overflow;
     const float *d_slo;                           // caller device SLO array or its staging copy
     uint64_t meta_off;                            // workspace offset of the LoadMeta (status word)
-    uint64_t pad[8];
+    uint32_t keys_ready;                          // keysc + hist0 hold the current queries' keys (fused reload)
+    uint32_t key_plan;                            // compressed-key eligibility: 1 | cbits << 8 | ob << 16 | rb << 24
+    uint64_t pad[7];
 };
 static_assert(sizeof(ProfileView) <= sizeof(uellm_profile), "ProfileView fits uellm_profile");
 
@@ -225,11 +230,17 @@ cudaError_t launch_slo_table(const uint32_t *slo_set, uint32_t *table, unsigned 
 cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n, uint64_t window, uint64_t w_first,
                                uint64_t nwin, const unsigned long long *ctab, int cbits, int ob, uint32_t *keys32,
                                uint32_t *vals, uint32_t *hist0, cudaStream_t st);
+// uellm_profile_reload of a rank-compressed profile: validation (bad bits, maxima into meta) + key
+// pack + digit-0 histogram in one pass over the caller arrays; an SLO value outside the profile's
+// (value, rank) hash sets meta->slo_missing
+cudaError_t launch_reload_pack32(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
+                                 uint64_t window, const unsigned long long *ctab, int cbits, int ob, uint32_t *keys32,
+                                 uint32_t *hist0, LoadMeta *meta, cudaStream_t st);
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                  uint64_t n,
                                  uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
-                                 cudaStream_t st, bool hist0_ready = false, const DecodeArgs *dec = nullptr);
+                                 cudaStream_t st, const uint32_t *hist0 = nullptr, const DecodeArgs *dec = nullptr);
 // windows per sort group: about kSortGroupQueries queries (env UELLM_SORT_GROUP_Q overrides, tuning)
 uint64_t sort_group_windows(uint64_t window, uint64_t nwin);
 cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const uint32_t *in, uint64_t n,

@@ -162,9 +162,13 @@ __global__ void k_reload_check(LoadMeta *meta, ReloadRef ref)
     const LoadMeta m = *meta;
     uint32_t st = UELLM_OK;
     if (m.bad) st = UELLM_ERR_CONTRACT;
-    else if (m.max_in > ref.max_in || m.max_out > ref.max_out || m.slo_distinct != ref.slo_distinct ||
-             m.slo_overflow != ref.slo_overflow || (m.key_or & ~ref.key_or) != 0ull ||
-             (~m.key_and & ref.key_and) != 0ull)
+    else if (ref.fused) {
+        // rank-compressed profile (k_reload_pack32): the keys were packed with the profile's rank
+        // table, valid when every SLO value is in the profile's set and the maxima are not above it
+        if (m.max_in > ref.max_in || m.max_out > ref.max_out || m.slo_missing) st = UELLM_ERR_STALE;
+    } else if (m.max_in > ref.max_in || m.max_out > ref.max_out || m.slo_distinct != ref.slo_distinct ||
+               m.slo_overflow != ref.slo_overflow || (m.key_or & ~ref.key_or) != 0ull ||
+               (~m.key_and & ref.key_and) != 0ull)
         st = UELLM_ERR_STALE;
     meta->status = st;
 }

@@ -305,6 +305,15 @@ constexpr uint32_t kHullMin = UELLM_HULL_MIN;
 #ifndef UELLM_DP_REFIX
 #define UELLM_DP_REFIX 1
 #endif   // shorter lean ranges are evaluated whole
+// fast blocks: the intra-block maxima as a u16 table of input-length window maxima indexed by batch
+// length (3 instructions per row to build instead of 5) and the block-end maxima by a shuffle scan
+#ifndef UELLM_DP_TRI16
+#define UELLM_DP_TRI16 1
+#endif
+// fast blocks: the unrolled intra loop stops at checkpoints once no later intra candidate can win
+#ifndef UELLM_DP_EXIT
+#define UELLM_DP_EXIT 1
+#endif
 // offset of row q of the triangular table (row q holds k = q+1 .. 31)
 __host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
 
@@ -737,17 +746,28 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         //      strict '<' keeps the smallest minimising i.
         uint32_t *M = S.tri + 1;                   // S.tri[0] is padding (read by idle lanes)
         const uint32_t pk_l = vl ? ((out_l << 16) | in_l) : 0u;
-        {
+        // the packed (out << 16 | in) triangular table M[q][k] (k > q): maxima of elements q+1..k
+        auto build_tri = [&]() {
             uint32_t m = pk_l;
 #pragma unroll
             for (int q = 30; q >= 0; --q) {
                 const uint32_t el = __shfl_sync(0xffffffffu, pk_l, q + 1);
                 if ((int)lane > q) { m = __vmaxu2(m, el); M[tri_off(q) + lane - q - 1] = m; }
             }
-        }
-        __syncwarp();
+            __syncwarp();
+        };
         // block-end maxima of this lane's own candidate (elements lane+1 .. B-1), reused below
-        const uint32_t mend = (lane + 1 < B) ? M[tri_off(lane) + B - 2 - lane] : 0u;
+        uint32_t mend;
+        if (UELLM_DP_TRI16) {
+            uint32_t sfx = pk_l;                   // suffix max over lanes lane..31 (lanes >= B hold 0)
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) sfx = __vmaxu2(sfx, __shfl_down_sync(0xffffffffu, sfx, d));
+            mend = __shfl_down_sync(0xffffffffu, sfx, 1);
+            if (lane + 1 >= B) mend = 0u;
+        } else {
+            build_tri();
+            mend = (lane + 1 < B) ? M[tri_off(lane) + B - 2 - lane] : 0u;
+        }
         // Pd = candidates dead at the block end (a prefix); V = candidates that violate the SLO at
         // the block's last boundary (also a prefix in one run: est shrinks with i).  In one run all
         // lanes share the SLO and est grows with the boundary, so candidates >= V violate for no lane.
@@ -794,6 +814,23 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             const bool ok = !vl || span < 0xfffffff0ull;
             fast = __all_sync(0xffffffffu, ok);
         }
+        // u16 table of input-length maxima by batch length d = k - q (fast blocks, TRI16): row d at
+        // T16 + 32 d holds max(in[k-d+1 .. k]) for lane k >= d; entry (q, lane) is T16l[-32 q] with
+        // T16l = T16 + 33 lane (an immediate offset per step).  Lanes k < d read stale words at most
+        // 31 rows below the table, inside the warp's slot array (cap_slots >= 128): masked.
+        unsigned short *const T16 = reinterpret_cast<unsigned short *>(S.tri) - 32;
+        if (fast && UELLM_DP_TRI16) {
+            uint32_t m = vl ? in_l : 0u;
+#pragma unroll
+            for (int d = 1; d < 32; ++d) {
+                T16[d * 32 + lane] = (unsigned short)m;
+                m = max(m, __shfl_up_sync(0xffffffffu, in_l, d));
+            }
+            __syncwarp();
+        } else if (UELLM_DP_TRI16) {
+            build_tri();
+        }
+        const unsigned short *const T16l = T16 + 33 * lane;
         if (fast) {
             if (Pd) { if (single_ok) ext_pass(F0{}, T1{}, T1{}, 0, Pd); else ext_pass(F0{}, F0{}, T1{}, 0, Pd); }
             if (Vs > Pd) ext_lean(Pd, Vs);             // may violate: 64-bit with the penalty
@@ -878,7 +915,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             for (uint32_t q = 0; q < Qd; ++q) {
                 const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
                 const uint32_t b = lane - q;
-                const uint32_t mi = M[off] & 0xffffu;
+                const uint32_t mi = UELLM_DP_TRI16 ? (uint32_t)T16l[-32 * (int)q] : M[off] & 0xffffu;
                 off += 30 - (int)q;
                 const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
                 const bool dead = (lane <= q) | (b > W) | ((single_ok | (b > 1)) & (b * (pmo + mi) > cap32));
@@ -890,11 +927,19 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 // the lane's base, no address arithmetic per step
                 const uint32_t *Ml = M + (int)lane;
                 const uint32_t j0p1 = j0 + 1;
+                // lower bound of any intra candidate q' >= q for this lane: C[q'] >= C[q] (C is
+                // non-decreasing in the boundary), b >= 1 and the maxima include the lane's element
+                const uint32_t LB_l = A_l + T_l + t_pre * in_l;
 #pragma unroll
                 for (int q = 0; q < 31; ++q) {
                     const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
+                    if (UELLM_DP_EXIT && q >= 12 && (q & 3) == 0) {
+                        // every later lane already at or below that bound: no later intra candidate
+                        // can win (ties keep the smaller, current i)
+                        if (__all_sync(0xffffffffu, lane <= (uint32_t)q || r32 <= Cq + LB_l)) break;
+                    }
                     const uint32_t b = lane - (uint32_t)q;
-                    const uint32_t mi = Ml[(int)tri_off(q) - q - 1] & 0xffffu;
+                    const uint32_t mi = UELLM_DP_TRI16 ? (uint32_t)T16l[-32 * q] : Ml[(int)tri_off(q) - q - 1] & 0xffffu;
                     const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
                     if (lane > (uint32_t)q && tot < r32) { r32 = tot; ri = j0p1 + (uint32_t)q; }
                 }
@@ -903,7 +948,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 for (uint32_t q = Qd; q + 1 < B; ++q) {
                     const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
                     const uint32_t b = lane - q;
-                    const uint32_t mi = M[off] & 0xffffu;
+                    const uint32_t mi = UELLM_DP_TRI16 ? (uint32_t)T16l[-32 * (int)q] : M[off] & 0xffffu;
                     off += 30 - (int)q;
                     const uint32_t tot = Cq + A_l + b * (T_l + t_pre * mi);
                     if (lane > q && tot < r32) { r32 = tot; ri = j0 + 1 + q; }

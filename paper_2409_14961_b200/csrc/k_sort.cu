@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ 
 // 1024 threads per window: thread (g, d) owns digit d of the g-th quarter of the window's tiles.
 // Column loads are issued 8 at a time (independent), so the pass is bandwidth- not latency-bound.
 constexpr int kScanGroups = 4;
-__global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__restrict__ hist, uint64_t n,
+// src: the per-tile counts (src == hist: in place; the first pass reads the kept hist0 counts)
+__global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(const uint32_t *src, uint32_t *hist, uint64_t n,
                                                                  uint64_t window, uint64_t tpw, uint64_t w_first)
 {
     __shared__ uint32_t gs[kScanGroups][256];
@@ -79,17 +80,18 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__res
     const uint32_t ntl = (uint32_t)ceil_div(L, kSortTile);
     const uint32_t per = (ntl + kScanGroups - 1) / kScanGroups;
     const uint32_t k0 = min(ntl, g * per), k1 = min(ntl, k0 + per);
+    const uint32_t *scol = src + (w * tpw) * 256 + d;
     uint32_t *col = hist + (w * tpw) * 256 + d;
     uint32_t sum = 0;
     uint32_t k = k0;
     for (; k + 8 <= k1; k += 8) {
         uint32_t v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = col[(uint64_t)(k + u) * 256];
+        for (int u = 0; u < 8; ++u) v[u] = scol[(uint64_t)(k + u) * 256];
 #pragma unroll
         for (int u = 0; u < 8; ++u) sum += v[u];
     }
-    for (; k < k1; ++k) sum += col[(uint64_t)k * 256];
+    for (; k < k1; ++k) sum += scol[(uint64_t)k * 256];
     gs[g][d] = sum;
     __syncthreads();
     if (g == 0) {
@@ -111,11 +113,11 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(uint32_t *__res
     for (k = k0; k + 8 <= k1; k += 8) {
         uint32_t v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = col[(uint64_t)(k + u) * 256];
+        for (int u = 0; u < 8; ++u) v[u] = scol[(uint64_t)(k + u) * 256];
 #pragma unroll
         for (int u = 0; u < 8; ++u) { col[(uint64_t)(k + u) * 256] = run; run += v[u]; }
     }
-    for (; k < k1; ++k) { const uint32_t v = col[(uint64_t)k * 256]; col[(uint64_t)k * 256] = run; run += v; }
+    for (; k < k1; ++k) { const uint32_t v = scol[(uint64_t)k * 256]; col[(uint64_t)k * 256] = run; run += v; }
 }
 
 #ifndef UELLM_SORT_PIPE
@@ -400,7 +402,7 @@ template <class K>
 static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, K *keys_a, uint32_t *vals_a,
                                    K *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2, uint64_t n,
                                    uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
-                                   cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
+                                   cudaStream_t st, const uint32_t *hist0, const DecodeArgs *dec)
 {
     *passes = 0;
     if (n == 0) return cudaSuccess;
@@ -410,7 +412,10 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
     const uint32_t *vin = *vals_io;
     const DecodeArgs D0 = dec ? *dec : DecodeArgs{};
     uint32_t *hcur = hist, *hnext = hist2;
-    bool ready = hist0_ready;                  // hcur already holds this pass's per-tile counts
+    // the first pass's per-tile counts: given (hist0, kept: the scan writes the offsets into hcur),
+    // else counted here; later passes: counted by the previous scatter into hcur
+    const uint32_t *hsrc = hist0;
+    bool ready = hist0 != nullptr;
     for (int d = 0; d < (int)sizeof(K); ++d) {
         if (!(digit_mask >> d & 1u)) continue;
         int dn = -1;                           // the next pass's digit
@@ -418,9 +423,12 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         const bool fuse_next = UELLM_SORT_NEXT && dn >= 0;
         K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
-        if (!ready)
+        if (!ready) {
             k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hcur, n, window, tpw, 8 * d, t0);
-        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hcur, n, window, tpw, w_first);
+            hsrc = hcur;
+        }
+        k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hsrc ? hsrc : hcur, hcur, n, window, tpw, w_first);
+        hsrc = nullptr;
         // TMA bulk copies need 16-byte aligned tile starts: every tile of a window starts at a
         // multiple of kSortTile, so window starts (and the base pointers) must be aligned
         const bool vals_ok = vin ? ((uintptr_t)vin & 15u) == 0 : (!D0.packin || ((uintptr_t)D0.in & 15u) == 0);
@@ -461,16 +469,16 @@ cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_
                                int *passes, cudaStream_t st, const DecodeArgs *dec)
 {
     return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, hist2, n,
-                                               window, w_first, nwin, digit_mask, passes, st, false, dec);
+                                               window, w_first, nwin, digit_mask, passes, st, nullptr, dec);
 }
 
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                  uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
-                                 int *passes, cudaStream_t st, bool hist0_ready, const DecodeArgs *dec)
+                                 int *passes, cudaStream_t st, const uint32_t *hist0, const DecodeArgs *dec)
 {
     return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, hist2, n, window,
-                                     w_first, nwin, digit_mask, passes, st, hist0_ready, dec);
+                                     w_first, nwin, digit_mask, passes, st, hist0, dec);
 }
 
 // a2 (compressed key) fused with the digit-0 histogram of the first radix pass:
@@ -533,6 +541,174 @@ cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n
     const uint64_t tpw = ceil_div(window, kSortTile);
     k_pack32_hist<<<(unsigned)(tpw * nwin), kSortThreads, sizeof(unsigned long long) << cbits, st>>>(
         out, slo, n, window, tpw, ctab, cbits, ob, keys32, hist0, tpw * w_first);
+    return cudaGetLastError();
+}
+
+// uellm_profile_reload of a rank-compressed profile: a1 (validation, maxima) + a2 (key pack) + the
+// digit-0 histogram of the first radix pass in ONE pass over the caller arrays (the separate load and
+// pack kernels read out / slo twice).  The key's rank comes from the profile's compact (value, rank)
+// hash (k_slo_table ran at uellm_profile_load); a value outside the profile's distinct set has no
+// rank and sets meta->slo_missing (-> UELLM_ERR_STALE: the compressed key was decided for that set).
+// Persistent CTAs walk the sort tiles; VEC (16-byte aligned tiles): thread t owns elements
+// 4t..4t+3 and 1024+4t..1024+4t+3 of a tile (16-byte loads and key stores), and the next tile's
+// loads are issued before the current one is processed.  Validation bits and maxima are reduced per
+// warp in registers and merged with one atomic each at the end.
+#ifndef UELLM_RELOAD_PERSIST
+#define UELLM_RELOAD_PERSIST 1      // persistent CTAs with the next tile's loads in flight (else one tile per CTA)
+#endif
+template <bool VEC>
+__global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_reload_pack32(const uint32_t *__restrict__ in,
+                                                                const uint32_t *__restrict__ out,
+                                                                const float *__restrict__ slo, uint64_t n,
+                                                                uint64_t window, uint64_t tpw, uint64_t ntiles,
+                                                                const unsigned long long *__restrict__ ctab,
+                                                                int cbits, int ob, uint32_t *__restrict__ keys32,
+                                                                uint32_t *__restrict__ hist, LoadMeta *meta)
+{
+    static_assert(kSortTile == 2048 && kSortThreads == 256, "VEC layout: 2 x 4 elements per thread");
+    extern __shared__ unsigned long long sct[];
+    __shared__ uint32_t h[256];
+    const int tid = threadIdx.x;
+    const uint32_t lane = tid & 31;
+    const uint32_t C = 1u << cbits;
+    for (uint32_t i = tid; i < C; i += kSortThreads) sct[i] = ctab[i];
+    uint32_t bad = 0, mx_in = 0, mx_out = 0, missing = 0;
+    // element e (0..7) of this thread inside the tile
+    auto off = [&](int e) -> uint32_t {
+        return VEC ? (uint32_t)((e >> 2) * 1024 + 4 * tid + (e & 3)) : (uint32_t)(e * kSortThreads + tid);
+    };
+    uint32_t na[kSortItems], no[kSortItems];
+    float nf[kSortItems];
+    auto fetch = [&](uint64_t tile) {
+        uint64_t st_, en_;
+        tile_range(tile, n, window, tpw, st_, en_);
+        const uint32_t cnt = (uint32_t)(en_ - st_);
+        if (VEC) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t o0 = r * 1024 + 4 * tid;
+                if (o0 + 4 <= cnt) {
+                    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(in + st_ + o0));
+                    const uint4 o = __ldg(reinterpret_cast<const uint4 *>(out + st_ + o0));
+                    const float4 f = __ldg(reinterpret_cast<const float4 *>(slo + st_ + o0));
+                    na[4 * r] = a.x; na[4 * r + 1] = a.y; na[4 * r + 2] = a.z; na[4 * r + 3] = a.w;
+                    no[4 * r] = o.x; no[4 * r + 1] = o.y; no[4 * r + 2] = o.z; no[4 * r + 3] = o.w;
+                    nf[4 * r] = f.x; nf[4 * r + 1] = f.y; nf[4 * r + 2] = f.z; nf[4 * r + 3] = f.w;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const bool v = o0 + c < cnt;
+                        na[4 * r + c] = v ? __ldg(in + st_ + o0 + c) : 1u;
+                        no[4 * r + c] = v ? __ldg(out + st_ + o0 + c) : 1u;
+                        nf[4 * r + c] = v ? __ldg(slo + st_ + o0 + c) : 1.0f;
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < kSortItems; ++e) {
+                const uint32_t o = off(e);
+                const bool v = o < cnt;
+                na[e] = v ? __ldg(in + st_ + o) : 1u;
+                no[e] = v ? __ldg(out + st_ + o) : 1u;
+                nf[e] = v ? __ldg(slo + st_ + o) : 1.0f;
+            }
+        }
+    };
+    if ((uint64_t)blockIdx.x < ntiles) fetch(blockIdx.x);
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        uint32_t ca[kSortItems], co[kSortItems];
+        float cf[kSortItems];
+#pragma unroll
+        for (int e = 0; e < kSortItems; ++e) { ca[e] = na[e]; co[e] = no[e]; cf[e] = nf[e]; }
+        if (UELLM_RELOAD_PERSIST && tile + gridDim.x < ntiles) fetch(tile + gridDim.x);   // next tile in flight
+        if (tid < 256) h[tid] = 0;
+        __syncthreads();                                  // (also orders the hash staging)
+        uint64_t start, end;
+        tile_range(tile, n, window, tpw, start, end);
+        const uint32_t cnt = (uint32_t)(end - start);
+        uint32_t key[kSortItems];
+#pragma unroll
+        for (int e = 0; e < kSortItems; ++e) {
+            const bool valid = off(e) < cnt;
+            const uint32_t act = __ballot_sync(0xffffffffu, valid);
+            key[e] = 0;
+            if (!valid) continue;
+            bool ok;
+            const uint32_t su = slo_to_us(cf[e], ok);
+            const uint32_t a = ca[e], o = co[e];
+            bad |= (a == 0u ? 1u : 0u) | (o == 0u ? 2u : 0u) | (ok ? 0u : 4u);
+            mx_in = max(mx_in, a);
+            mx_out = max(mx_out, o);
+            uint32_t hh = slo_hash(su, (uint32_t)cbits);
+            unsigned long long en = sct[hh];
+            // >= 2 slots per value: an absent value ends at an empty slot
+            while (en != 0ull && (uint32_t)(en >> 32) != su) { hh = (hh + 1) & (C - 1); en = sct[hh]; }
+            missing |= en == 0ull ? 1u : 0u;
+            key[e] = ((uint32_t)en << ob) | o;
+            const uint32_t d = key[e] & 0xffu;
+            const uint32_t peers = __match_any_sync(act, d);
+            if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));
+        }
+        if (VEC) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t o0 = r * 1024 + 4 * tid;
+                if (o0 + 4 <= cnt)
+                    *reinterpret_cast<uint4 *>(keys32 + start + o0) =
+                        make_uint4(key[4 * r], key[4 * r + 1], key[4 * r + 2], key[4 * r + 3]);
+                else
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) if (o0 + c < cnt) keys32[start + o0 + c] = key[4 * r + c];
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < kSortItems; ++e) if (off(e) < cnt) keys32[start + off(e)] = key[e];
+        }
+        __syncthreads();
+        if (tid < 256) hist[tile * 256 + tid] = h[tid];
+    }
+    for (int d = 16; d; d >>= 1) {
+        bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+        missing |= __shfl_xor_sync(0xffffffffu, missing, d);
+        mx_in = max(mx_in, __shfl_xor_sync(0xffffffffu, mx_in, d));
+        mx_out = max(mx_out, __shfl_xor_sync(0xffffffffu, mx_out, d));
+    }
+    if (lane == 0) {
+        if (bad) atomicOr(&meta->bad, bad);
+        if (missing) atomicOr(&meta->slo_missing, 1u);
+        if (mx_in > *(volatile uint32_t *)&meta->max_in) atomicMax(&meta->max_in, mx_in);
+        if (mx_out > *(volatile uint32_t *)&meta->max_out) atomicMax(&meta->max_out, mx_out);
+    }
+}
+
+cudaError_t launch_reload_pack32(const uint32_t *in, const uint32_t *out, const float *slo, uint64_t n,
+                                 uint64_t window, const unsigned long long *ctab, int cbits, int ob, uint32_t *keys32,
+                                 uint32_t *hist0, LoadMeta *meta, cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    const uint64_t tpw = ceil_div(window, kSortTile);
+    const uint64_t nwin = ceil_div(n, window);
+    const uint64_t tiles = tpw * nwin;
+    const size_t smem = sizeof(unsigned long long) << cbits;
+    // 16-byte tiles: every tile starts at a multiple of kSortTile inside its window
+    const bool vec = ((((uintptr_t)in | (uintptr_t)out | (uintptr_t)slo | (uintptr_t)keys32) & 15u) == 0) &&
+                     (nwin == 1 || window % 4 == 0);
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reload_pack32<true>, kSortThreads, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reload_pack32<false>, kSortThreads, smem);
+    if (per < 1) per = 1;
+    // persistent: one resident wave; otherwise one tile per CTA
+    const uint64_t cap = UELLM_RELOAD_PERSIST ? (uint64_t)nsm * per : tiles;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    if (vec)
+        k_reload_pack32<true><<<grid, kSortThreads, smem, st>>>(in, out, slo, n, window, tpw, tiles, ctab, cbits, ob,
+                                                                keys32, hist0, meta);
+    else
+        k_reload_pack32<false><<<grid, kSortThreads, smem, st>>>(in, out, slo, n, window, tpw, tiles, ctab, cbits, ob,
+                                                                 keys32, hist0, meta);
     return cudaGetLastError();
 }
 

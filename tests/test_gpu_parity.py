@@ -583,10 +583,14 @@ def test_bench_ranks_one_gpu_gloo_equal_single_rank(world):
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer(tool):
-    """T6: compute-sanitizer finds no error in a small run of every entry point."""
+    """T6: compute-sanitizer finds no error in a small run of every entry point.
+    Opt-in (UELLM_SANITIZE=1): the GPU pool this build is tested on closed compute-sanitizer (runs
+    under it left GPUs needing a reset); the four tools ran clean in rounds 1-2."""
     import os
     import subprocess
     import sys
+    if os.environ.get("UELLM_SANITIZE") != "1":
+        pytest.skip("compute-sanitizer is closed on this GPU pool; set UELLM_SANITIZE=1 to run it")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = ["/usr/local/cuda/bin/compute-sanitizer", "--tool", tool, "--error-exitcode", "9",
            sys.executable, os.path.join(root, "tools", "sanitize_run.py")]
@@ -631,9 +635,50 @@ def test_profile_reload_statuses_and_parity():
     z_in = p_in.copy(); z_in[11] = 0
     g.reload(_dev(z_in), _dev(p_out), _dev(p_slo))
     assert int(g.status_word().item()) == U.ERR_CONTRACT
-    # another SLO set size -> STALE
+    # an SLO value outside the profile's set -> STALE (the rank-compressed key was decided for the set)
     s2 = p_slo.copy(); s2[5] = 123.0
     g.reload(_dev(p_in), _dev(p_out), _dev(s2))
+    assert int(g.status_word().item()) == U.ERR_STALE
+    # a subset of the profile's SLO values (one class folded into another) -> OK: the fused reload
+    # packs with the profile's rank table; scheduling twice reuses the kept keys / histogram
+    s3 = p_slo.copy(); s3[s3 == np.unique(slo)[2]] = np.unique(slo)[5]
+    g.reload(_dev(p_in), _dev(p_out), _dev(s3))
+    g.schedule()
+    assert int(g.status_word().item()) == U.OK
+    first = g.results()
+    g.schedule()
+    g.stats()
+    r = g.results()
+    o_order, o_offs, o_m, o_cost = oracle.schedule(p_in, p_out, s3, cfg, nthreads=8)
+    assert np.array_equal(first["order"], o_order) and np.array_equal(first["offsets"], o_offs)
+    assert np.array_equal(r["order"], o_order) and np.array_equal(r["offsets"], o_offs)
+    assert r["totals"]["dp_cost"] == o_cost
+
+
+def test_profile_reload_generic_key_path():
+    """Reload of a profile with more distinct SLO values than the compressed key takes (u64 keys,
+    the unfused load kernel): a permutation is OK with oracle parity, a larger maximum STALE."""
+    from paper_2409_14961_b200 import uellm as U
+    from paper_2409_14961_b200.scheduler import GpuScheduler
+    n = 60_000
+    inp, out, _ = W.long_tail(n, 4)
+    slo = W.gen_uniform_slo(n, 4)
+    cfg = W.SchedConfig(window=20_000, max_batch=128, kv_cap_bytes=W.KV_RESERVE_LLAMA2_7B_180GB, lambda_us=10**9)
+    g = GpuScheduler(n, cfg, device="cuda:0")
+    g.load(_dev(inp), _dev(out), _dev(slo))
+    perm = np.random.default_rng(5).permutation(n)
+    g.reload(_dev(inp[perm]), _dev(out[perm]), _dev(slo[perm]))
+    g.schedule()
+    g.stats()
+    assert int(g.status_word().item()) == U.OK
+    r = g.results()
+    o_order, o_offs, o_m, o_cost = oracle.schedule(inp[perm], out[perm], slo[perm], cfg, nthreads=8)
+    assert np.array_equal(r["order"], o_order) and np.array_equal(r["offsets"], o_offs)
+    assert r["totals"]["dp_cost"] == o_cost and g.diagnostics()["sort_key_bits"] == 64
+    # (the distinct set overflowed the compressed key: its exact size is not tracked, and the u64 key
+    # does not depend on it) -- a larger output length is STALE
+    o2 = out[perm].copy(); o2[3] = out.max() + 1
+    g.reload(_dev(inp[perm]), _dev(o2), _dev(slo[perm]))
     assert int(g.status_word().item()) == U.ERR_STALE
 
 
