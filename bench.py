@@ -54,6 +54,9 @@ def workload(name: str, rank: int, n_override: int | None):
         inp, out, slo, cfg = W.c4(seed=rank, n=n)
         return "c4: 1e8 queries, 1e6-query windows, 8 SLO classes, long-tail outputs <=4096, " \
                "LLaMA-2-7B KV cap, W=256, lambda=1e9 us", inp, out, slo, cfg
+    if name == "c2":
+        inp, out, slo, cfg = W.c2(seed=rank, n=n_override or 10_000)
+        return "c2: 1e4 queries, one window", inp, out, slo, cfg
     if name == "c3":
         inp, out, slo, cfg = W.c3(seed=rank, n=n_override or 1_000_000)
         return "c3: 1e6 queries, one window", inp, out, slo, cfg

@@ -39,14 +39,31 @@ uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_ti
         // The 16 W floor stays for small jobs too: one-wave tiles of 4 W .. 16 W were measured
         // slower on 6-7 M-query window groups (3.5-7 ms against 2.7 ms per group: more fix-ups
         // and cascade re-runs than the extra parallelism gains).
+        // A job with fewer 16 W tiles than one wave of resident DP warps (148 SMs x 24) is bound by
+        // its tiles' sequential walks, not by the total work: 8 W tiles there (measured: c3 1e6
+        // queries 0.95 -> 0.69 ms, c5 1e7 3.42 -> 3.00 ms; 4 W: c5 3.90 ms, the fix-ups and cascade
+        // grow faster than the walks shrink)  Throughput-bound callers (the pipelined host call,
+        // whose window groups share the GPU) pass dp_tile = tile_len_throughput() instead.
         const uint64_t target_tiles = 148ull * 148;
         T = ceil_div(n ? n : 1, target_tiles);
-        T = T < 16ull * W ? 16ull * W : T;
+        const uint64_t floor16 = 16ull * W;
+        T = T < floor16 ? floor16 : T;
+        // (at least one 16 W tile per SM: a job of a handful of tiles -- c2: 10 -- is bound by its
+        // per-window cascade and launches instead, 0.75 vs 1.09 ms with 8 W tiles)
+        const uint64_t t16 = ceil_div(n ? n : 1, floor16);
+        if (T == floor16 && t16 >= 148 && t16 < 148ull * 24) T = 8ull * W;
         T = align_up(T, W);
     }
     if (T < 2ull * W) T = 2ull * W;
     if (T > window) T = align_up(window, W);   // one tile per window
     return T;
+}
+
+uint32_t tile_len_throughput(uint64_t n, uint32_t W)
+{
+    uint64_t T = ceil_div(n ? n : 1, 148ull * 148);
+    if (T < 16ull * W) T = 16ull * W;
+    return (uint32_t)align_up(T, W);
 }
 
 WsLayout make_layout(uint64_t n, const uellm_config &cfg)

@@ -203,6 +203,8 @@ struct U64Store {
 };
 cudaError_t launch_set_u64s(cudaStream_t st, std::initializer_list<U64Store> stores, bool zero_diag = false);
 uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_tile);
+// the SEG-DP tile length of a throughput-bound job of n queries (the 16 W floor, no one-wave rule)
+uint32_t tile_len_throughput(uint64_t n, uint32_t W);
 
 // --------------------------------------------------------------------------------------
 // Kernel launchers (each returns cudaGetLastError()).

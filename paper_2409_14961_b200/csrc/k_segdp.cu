@@ -310,6 +310,11 @@ constexpr uint32_t kHullMin = UELLM_HULL_MIN;
 #ifndef UELLM_DP_TRI16
 #define UELLM_DP_TRI16 1
 #endif
+// fast blocks: merged MI groups and the predecessor test in the hull subset (see the chord filter).
+// Off: c4 evaluations 34.7 -> 31.8 per query, but the filter's extra work costs more (DP 5.76 -> 5.94 ms)
+#ifndef UELLM_DP_HULL2
+#define UELLM_DP_HULL2 0
+#endif
 // fast blocks: the unrolled intra loop stops at checkpoints once no later intra candidate can win
 #ifndef UELLM_DP_EXIT
 #define UELLM_DP_EXIT 1
@@ -849,6 +854,15 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
             uint32_t H = 0xffffffffu;
             if (L - Vs >= kHullMin) {
                 H = 0;
+                // HULL2: (i) candidates whose stored MI is at most the block's first element's prefix
+                // maximum pmi0 have MI = pmi_l at every lane: one group (key max(mi, pmi0));
+                // (ii) a candidate whose list predecessor (same group, lean) is strictly cheaper at the
+                // block's largest slope Kmax = t_tok*bmo + t_pre*max(g, bmi) is strictly worse for every
+                // lane (K_l <= Kmax and cost_a - cost_k = C_a - C_k + (k - a) K_l): dropped for this
+                // block.  The smallest minimiser of any lane is a hull vertex not beaten by its
+                // predecessor, so it survives both tests.
+                const uint32_t pmi0 = UELLM_DP_HULL2 ? __shfl_sync(0xffffffffu, pmi, 0) : 0u;
+                const uint32_t hbmo = __shfl_sync(0xffffffffu, pmo, B - 1), hbmi = __shfl_sync(0xffffffffu, pmi, B - 1);
                 for (uint32_t r0 = Vs; r0 < L; r0 += 32) {
                     const uint32_t k = r0 + lane;
                     bool keep = false;
@@ -857,15 +871,25 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                         const longlong2 sv = S.sl[k];
                         const uint32_t ck = (uint32_t)sv.x - base_lo, ik = (uint32_t)sv.y;
                         const uint32_t mk = (uint32_t)((unsigned long long)sv.y >> 48);
+                        const uint32_t gk = max(mk, pmi0);
                         keep = true;
-                        if (k > Vs && k + 1 < L) {
-                            const longlong2 sa = S.sl[k - 1], sc = S.sl[k + 1];
-                            if ((uint32_t)((unsigned long long)sa.y >> 48) == mk &&
-                                (uint32_t)((unsigned long long)sc.y >> 48) == mk) {
-                                const long long ca = (long long)((uint32_t)sa.x - base_lo);
-                                const long long cc = (long long)((uint32_t)sc.x - base_lo);
-                                const uint32_t ia = (uint32_t)sa.y, ic = (uint32_t)sc.y;
-                                keep = ((long long)ck - ca) * (long long)(ic - ia) < (cc - ca) * (long long)(ik - ia);
+                        if (k > Vs) {
+                            const longlong2 sa = S.sl[k - 1];
+                            const uint32_t ga = max((uint32_t)((unsigned long long)sa.y >> 48), pmi0);
+                            const long long ca = (long long)((uint32_t)sa.x - base_lo);
+                            const uint32_t ia = (uint32_t)sa.y;
+                            if (UELLM_DP_HULL2 && ga == gk) {
+                                const unsigned long long Kmax = (unsigned long long)t_tok * hbmo +
+                                                                (unsigned long long)t_pre * max(gk, hbmi);
+                                if ((long long)ck - ca > (long long)((unsigned long long)(ik - ia) * Kmax)) keep = false;
+                            }
+                            if (keep && k + 1 < L) {
+                                const longlong2 sc = S.sl[k + 1];
+                                if (ga == gk && max((uint32_t)((unsigned long long)sc.y >> 48), pmi0) == gk) {
+                                    const long long cc = (long long)((uint32_t)sc.x - base_lo);
+                                    const uint32_t ic = (uint32_t)sc.y;
+                                    keep = ((long long)ck - ca) * (long long)(ic - ia) < (cc - ca) * (long long)(ik - ia);
+                                }
                             }
                         }
                         ent = make_uint2(ck, (j0 - ik) | (mk << 16));
@@ -930,13 +954,25 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 // lower bound of any intra candidate q' >= q for this lane: C[q'] >= C[q] (C is
                 // non-decreasing in the boundary), b >= 1 and the maxima include the lane's element
                 const uint32_t LB_l = A_l + T_l + t_pre * in_l;
+                // EXIT == 2: C also grows by at least t_tok*out[e] + t_pre*in[e] per element e
+                // between two boundaries (adding e to the last batch raises its est by at least that
+                // much and never lowers its violations), so C[q'] >= C[q] + (q' - q) * dblk with dblk
+                // the block's smallest such increment, and the bound of lane k over q' in [q, k)
+                // becomes C[q] + LB_k + (k - q - 1) * dblk.  (A 32-bit wrap of a bound only lowers
+                // it: the test stays conservative.)
+                const uint32_t dblk = UELLM_DP_EXIT == 2 ? __reduce_min_sync(0xffffffffu, t_tok * out_l + t_pre * in_l) : 0u;
 #pragma unroll
                 for (int q = 0; q < 31; ++q) {
                     const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
-                    if (UELLM_DP_EXIT && q >= 12 && (q & 3) == 0) {
+                    if (UELLM_DP_EXIT && q >= (UELLM_DP_EXIT == 2 ? 8 : 12) && (q & 3) == 0) {
                         // every later lane already at or below that bound: no later intra candidate
                         // can win (ties keep the smaller, current i)
-                        if (__all_sync(0xffffffffu, lane <= (uint32_t)q || r32 <= Cq + LB_l)) break;
+                        const uint32_t bnd = Cq + LB_l + (UELLM_DP_EXIT == 2 ? (lane - (uint32_t)q - 1u) * dblk : 0u);
+                        if (__all_sync(0xffffffffu, lane <= (uint32_t)q || r32 <= bnd)) {
+                            // (diagnostics: the pairs (q', k) with q' >= q were not evaluated)
+                            evals -= (uint32_t)((31 - q) * (32 - q) / 2);
+                            break;
+                        }
                     }
                     const uint32_t b = lane - (uint32_t)q;
                     const uint32_t mi = UELLM_DP_TRI16 ? (uint32_t)T16l[-32 * q] : Ml[(int)tri_off(q) - q - 1] & 0xffffu;

@@ -16,6 +16,8 @@
 //   k_sort_down  per tile: stable rank of every key (match.any peers + per-warp running
 //                counts), then scatter.  Stability: tile order, warp order, iteration order,
 //                lane order all follow input order.
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace uellm {
@@ -178,7 +180,7 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
     constexpr int kPerWarpIters = kSortTile / kWarps / 32;
     constexpr uint32_t kStageBytes = kSortTile * (sizeof(K) + 4) + 1024;   // keys, payloads, hist row
     __shared__ uint32_t whist[kWarps][256];
-    __shared__ uint32_t dstart[256], wsum[kWarps];
+    __shared__ uint32_t dofs[256], wsum[kWarps];
     __shared__ uint32_t tbase_s[PIPE ? 1 : 256];
     __shared__ uint32_t stab[DECODE && sizeof(K) == 4 ? kSloRankMax : 1];
     __shared__ __align__(8) uint64_t mbar[2];
@@ -250,49 +252,52 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
         K kr[kPerWarpIters];
         uint32_t vr[kPerWarpIters], rank[kPerWarpIters];
         const uint32_t base = (uint32_t)warp * (kPerWarpIters * 32);   // offset in the tile
+        // FULL (every tile but a window's last): no per-key bounds tests
+        const bool full = cnt == (uint32_t)kSortTile;
+        auto load_rank = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-        for (int r = 0; r < kPerWarpIters; ++r) {
-            const uint32_t o = base + r * 32 + lane;
-            const bool valid = o < cnt;
-            const uint64_t p = start + o;
-            uint32_t v = 0;
-            if (PIPE) {
-                kr[r] = valid ? bkp[o] : (K)0;
-                if (valid) v = vsrc ? bvp[o] : (uint32_t)p;
-            } else {
-                kr[r] = valid ? kin[p] : (K)0;
-                if (valid) v = vin ? vin[p] : D.packin ? __ldg(D.in + p) : (uint32_t)p;
+            for (int r = 0; r < kPerWarpIters; ++r) {
+                const uint32_t o = base + r * 32 + lane;
+                const bool valid = FULL || o < cnt;
+                const uint64_t p = start + o;
+                uint32_t v = 0;
+                if (PIPE) {
+                    kr[r] = valid ? bkp[o] : (K)0;
+                    if (valid) v = vsrc ? bvp[o] : (uint32_t)p;
+                } else {
+                    kr[r] = valid ? kin[p] : (K)0;
+                    if (valid) v = vin ? vin[p] : D.packin ? __ldg(D.in + p) : (uint32_t)p;
+                }
+                // first pass with packin: window-local index and input length (no gather at decode)
+                if (!vin && D.packin) v = (uint32_t)(p - wp0) | ((v - 1u) << D.wb);
+                vr[r] = v;
             }
-            // first pass with packin: window-local index and input length (no gather at decode)
-            if (!vin && D.packin) v = (uint32_t)(p - wp0) | ((v - 1u) << D.wb);
-            vr[r] = v;
-        }
 #pragma unroll
-        for (int r = 0; r < kPerWarpIters; ++r) {
-            const bool valid = base + r * 32 + lane < cnt;
-            const uint32_t act = __ballot_sync(0xffffffffu, valid);
-            const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
-            uint32_t peers = 0;
-            if (valid) {
-                peers = __match_any_sync(act, d);
-                rank[r] = whist[warp][d] + __popc(peers & lt);
+            for (int r = 0; r < kPerWarpIters; ++r) {
+                const bool valid = FULL || base + r * 32 + lane < cnt;
+                const uint32_t act = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+                const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
+                uint32_t peers = 0;
+                if (valid) {
+                    peers = __match_any_sync(act, d);
+                    rank[r] = whist[warp][d] + __popc(peers & lt);
+                }
+                __syncwarp();
+                if (valid && lane == __ffs(peers) - 1) whist[warp][d] += __popc(peers);
+                __syncwarp();
             }
-            __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) whist[warp][d] += __popc(peers);
-            __syncwarp();
-        }
+        };
+        if (full) load_rank(std::true_type{}); else load_rank(std::false_type{});
         __syncthreads();
-        {   // exclusive scan over warps, per digit; dstart = tile total of the digit
+        {   // per digit (thread tid): the 8 warps' counts -> each warp's first staging slot of the
+            // digit, and dofs[d] = global position of staging slot 0 of digit d's run
+            static_assert(kSortThreads == 256, "one thread per digit");
+            uint32_t c[kWarps];
             uint32_t run = 0;
 #pragma unroll
-            for (int wv = 0; wv < kWarps; ++wv) {
-                const uint32_t c = whist[wv][tid];
-                whist[wv][tid] = run;
-                run += c;
-            }
-            // inclusive scan of the 256 digit totals: warp shuffles, then the 8 warp sums
-            static_assert(kSortThreads == 256, "one thread per digit");
-            uint32_t v = run;
+            for (int wv = 0; wv < kWarps; ++wv) { c[wv] = whist[wv][tid]; run += c[wv]; }
+            uint32_t v = run;               // inclusive scan of the digit totals: shuffles + warp sums
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
@@ -302,66 +307,74 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
             __syncthreads();
             uint32_t add = 0;
             for (int q = 0; q < warp; ++q) add += wsum[q];
-            dstart[tid] = v + add;
+            const uint32_t excl = v + add - run;
+            uint32_t acc = excl;
+#pragma unroll
+            for (int wv = 0; wv < kWarps; ++wv) { whist[wv][tid] = acc; acc += c[wv]; }
+            dofs[tid] = tbase[tid] - excl;  // (mod 2^32)
             __syncthreads();
         }
         // stage the tile in shared memory in (digit, rank) order (PIPE: over the stage buffer, whose
         // reads all precede the __syncthreads of the scan above)
 #pragma unroll
         for (int r = 0; r < kPerWarpIters; ++r) {
-            if (base + r * 32 + lane < cnt) {
+            if (full || base + r * 32 + lane < cnt) {
                 const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
-                const uint32_t loc = (d ? dstart[d - 1] : 0u) + whist[warp][d] + rank[r];
+                const uint32_t loc = whist[warp][d] + rank[r];
                 sk[loc] = kr[r];
                 sv[loc] = vr[r];
             }
         }
         __syncthreads();
         // every digit bucket as one contiguous run: consecutive threads store consecutive addresses
-#pragma unroll 4
-        for (uint32_t r = 0; r < kSortItems; ++r) {                      // whole warps iterate together
-            const uint32_t i = r * kSortThreads + tid;
-            if (r * kSortThreads + (uint32_t)(tid - lane) >= cnt) break;
-            const bool valid = i < cnt;
-            K key = 0;
-            uint32_t pos = 0;
-            if (valid) {
-                key = sk[i];
-                const uint32_t d = (uint32_t)(key >> shift) & 0xffu;
-                pos = tbase[d] + i - (d ? dstart[d - 1] : 0u);
-            }
-            if (NEXT) {
-                const uint32_t act = __ballot_sync(0xffffffffu, valid);
+        const uint32_t wt0_32 = (uint32_t)wt0, wp0_32 = (uint32_t)wp0;
+        auto write_out = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll(FULL ? kSortItems : 4)
+            for (uint32_t r = 0; r < kSortItems; ++r) {                  // whole warps iterate together
+                const uint32_t i = r * kSortThreads + tid;
+                if (!FULL && r * kSortThreads + (uint32_t)(tid - lane) >= cnt) break;
+                const bool valid = FULL || i < cnt;
+                K key = 0;
+                uint32_t pos = 0;
                 if (valid) {
-                    const uint32_t slot = (uint32_t)(wt0 + ((pos - wp0) / kSortTile)) * 256u +
-                                          ((uint32_t)(key >> shift_next) & 0xffu);
-                    const uint32_t peers = __match_any_sync(act, slot);
-                    if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(hist_next + slot, (uint32_t)__popc(peers));
+                    key = sk[i];
+                    pos = dofs[(uint32_t)(key >> shift) & 0xffu] + i;
+                }
+                if (NEXT) {
+                    const uint32_t act = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+                    if (valid) {
+                        const uint32_t slot = (wt0_32 + ((pos - wp0_32) / (uint32_t)kSortTile)) * 256u +
+                                              ((uint32_t)(key >> shift_next) & 0xffu);
+                        const uint32_t peers = __match_any_sync(act, slot);
+                        if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(hist_next + slot, (uint32_t)__popc(peers));
+                    }
+                }
+                if (!valid) continue;
+                const uint32_t idx = sv[i];
+                if (DECODE) {
+                    if (sizeof(K) == 8) {
+                        D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
+                        D.rout[pos] = (uint32_t)key;
+                    } else {
+                        const uint32_t k32 = (uint32_t)key;
+                        D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
+                        D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
+                    }
+                    if (D.packin) {
+                        D.order[pos] = wp0_32 + (idx & ((1u << D.wb) - 1u));
+                        D.rin[pos] = (idx >> D.wb) + 1u;
+                    } else {
+                        D.order[pos] = idx;
+                        D.rin[pos] = __ldg(D.in + idx);
+                    }
+                } else {
+                    kout[pos] = key;
+                    vout[pos] = idx;
                 }
             }
-            if (!valid) continue;
-            const uint32_t idx = sv[i];
-            if (DECODE) {
-                if (sizeof(K) == 8) {
-                    D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
-                    D.rout[pos] = (uint32_t)key;
-                } else {
-                    const uint32_t k32 = (uint32_t)key;
-                    D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
-                    D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
-                }
-                if (D.packin) {
-                    D.order[pos] = (uint32_t)wp0 + (idx & ((1u << D.wb) - 1u));
-                    D.rin[pos] = (idx >> D.wb) + 1u;
-                } else {
-                    D.order[pos] = idx;
-                    D.rin[pos] = __ldg(D.in + idx);
-                }
-            } else {
-                kout[pos] = key;
-                vout[pos] = idx;
-            }
-        }
+        };
+        if (full) write_out(std::true_type{}); else write_out(std::false_type{});
         // staging and stage s are free for the next round; the generic-proxy accesses of this round
         // are ordered before the next round's bulk copies (async proxy) into the same buffer
         if (PIPE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -567,11 +580,14 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
 {
     static_assert(kSortTile == 2048 && kSortThreads == 256, "VEC layout: 2 x 4 elements per thread");
     extern __shared__ unsigned long long sct[];
-    __shared__ uint32_t h[256];
+    // per-warp digit counts (no match.any: a lane's count is one shared RED, same-address lanes of a
+    // warp serialise in the shared-memory pipe instead of costing issue slots), summed per tile
+    __shared__ uint32_t hw[kSortThreads / 32][256];
     const int tid = threadIdx.x;
     const uint32_t lane = tid & 31;
     const uint32_t C = 1u << cbits;
     for (uint32_t i = tid; i < C; i += kSortThreads) sct[i] = ctab[i];
+    uint32_t *const myh = hw[tid >> 5];
     uint32_t bad = 0, mx_in = 0, mx_out = 0, missing = 0;
     // element e (0..7) of this thread inside the tile
     auto off = [&](int e) -> uint32_t {
@@ -622,16 +638,17 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
 #pragma unroll
         for (int e = 0; e < kSortItems; ++e) { ca[e] = na[e]; co[e] = no[e]; cf[e] = nf[e]; }
         if (UELLM_RELOAD_PERSIST && tile + gridDim.x < ntiles) fetch(tile + gridDim.x);   // next tile in flight
-        if (tid < 256) h[tid] = 0;
+#pragma unroll
+        for (int w = 0; w < kSortThreads / 32; ++w) hw[w][tid] = 0;
         __syncthreads();                                  // (also orders the hash staging)
         uint64_t start, end;
         tile_range(tile, n, window, tpw, start, end);
         const uint32_t cnt = (uint32_t)(end - start);
+        const bool full = cnt == kSortTile;
         uint32_t key[kSortItems];
 #pragma unroll
         for (int e = 0; e < kSortItems; ++e) {
-            const bool valid = off(e) < cnt;
-            const uint32_t act = __ballot_sync(0xffffffffu, valid);
+            const bool valid = full || off(e) < cnt;
             key[e] = 0;
             if (!valid) continue;
             bool ok;
@@ -646,9 +663,7 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
             while (en != 0ull && (uint32_t)(en >> 32) != su) { hh = (hh + 1) & (C - 1); en = sct[hh]; }
             missing |= en == 0ull ? 1u : 0u;
             key[e] = ((uint32_t)en << ob) | o;
-            const uint32_t d = key[e] & 0xffu;
-            const uint32_t peers = __match_any_sync(act, d);
-            if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));
+            atomicAdd(myh + (key[e] & 0xffu), 1u);
         }
         if (VEC) {
 #pragma unroll
@@ -666,7 +681,13 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
             for (int e = 0; e < kSortItems; ++e) if (off(e) < cnt) keys32[start + off(e)] = key[e];
         }
         __syncthreads();
-        if (tid < 256) hist[tile * 256 + tid] = h[tid];
+        {
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kSortThreads / 32; ++w) c += hw[w][tid];
+            hist[tile * 256 + tid] = c;
+        }
+        __syncthreads();                                  // hw is cleared for the next tile
     }
     for (int d = 16; d; d >>= 1) {
         bad |= __shfl_xor_sync(0xffffffffu, bad, d);

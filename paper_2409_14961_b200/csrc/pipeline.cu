@@ -90,6 +90,8 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
     uellm_config c = cfg;
     c.window = (uint32_t)wl;
+    // the groups share the GPU (throughput-bound): no one-wave short tiles
+    if (!c.dp_tile) c.dp_tile = tile_len_throughput(P.group_q, c.max_batch ? c.max_batch : 1);
     P.ws_bytes = make_layout(P.group_q, c).total;
     P.ws[0] = take(P.ws_bytes);
     P.ws[1] = take(P.ws_bytes);
@@ -145,6 +147,7 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     const uint64_t G = PL.groups;
     uellm_config gcfg = *cfg;
     gcfg.window = (uint32_t)(cfg->window ? (cfg->window < n ? cfg->window : n) : n);
+    if (!gcfg.dp_tile) gcfg.dp_tile = tile_len_throughput(PL.group_q, gcfg.max_batch ? gcfg.max_batch : 1);
     cudaStream_t H = nullptr, D = nullptr, C2 = nullptr;
     std::vector<cudaEvent_t> h2d(G, nullptr), done(G, nullptr), d2h(G, nullptr);
     std::vector<uint64_t> m(G, 0);
