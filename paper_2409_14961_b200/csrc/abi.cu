@@ -198,8 +198,10 @@ KeyPlan key_plan(const ProfileView &v)
     while (k.ob < 32 && (v.max_out >> k.ob)) ++k.ob;                           // bits(max_out)
     k.rb = 0;
     while (v.slo_distinct > 1 && k.rb < 32 && ((v.slo_distinct - 1) >> k.rb)) ++k.rb;   // bits(distinct - 1)
-    k.cbits = 4;                                                             // compact hash: >= 2 slots per value
-    while ((1u << k.cbits) < 2 * v.slo_distinct && k.cbits < (int)kSloSetBits) ++k.cbits;
+    // compact hash: >= 8 slots per value (>= 4 at the 1024-value maximum: 4096 slots), so a lookup
+    // almost never probes twice
+    k.cbits = 6;
+    while ((1u << k.cbits) < 8 * v.slo_distinct && k.cbits < (int)kSloSetBits) ++k.cbits;
     k.ok = !v.slo_overflow && v.slo_distinct >= 1 && v.slo_distinct <= kSloRankMax && k.rb + k.ob <= 32;
     return k;
 }

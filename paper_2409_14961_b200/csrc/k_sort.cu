@@ -328,6 +328,33 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
         __syncthreads();
         // every digit bucket as one contiguous run: consecutive threads store consecutive addresses
         const uint32_t wt0_32 = (uint32_t)wt0, wp0_32 = (uint32_t)wp0;
+        // one key's record stores (payload idx from the staging area)
+        auto store = [&](K key, uint32_t pos, uint32_t i) {
+            const uint32_t idx = sv[i];
+            if (DECODE) {
+                if (sizeof(K) == 8) {
+                    D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
+                    D.rout[pos] = (uint32_t)key;
+                } else {
+                    const uint32_t k32 = (uint32_t)key;
+                    D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
+                    D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
+                }
+                if (D.packin) {
+                    D.order[pos] = wp0_32 + (idx & ((1u << D.wb) - 1u));
+                    D.rin[pos] = (idx >> D.wb) + 1u;
+                } else {
+                    D.order[pos] = idx;
+                    D.rin[pos] = __ldg(D.in + idx);
+                }
+            } else {
+                kout[pos] = key;
+                vout[pos] = idx;
+            }
+        };
+        auto next_slot = [&](K key, uint32_t pos) -> uint32_t {
+            return (wt0_32 + ((pos - wp0_32) / (uint32_t)kSortTile)) * 256u + ((uint32_t)(key >> shift_next) & 0xffu);
+        };
         auto write_out = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll(FULL ? kSortItems : 4)
@@ -344,34 +371,12 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
                 if (NEXT) {
                     const uint32_t act = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
                     if (valid) {
-                        const uint32_t slot = (wt0_32 + ((pos - wp0_32) / (uint32_t)kSortTile)) * 256u +
-                                              ((uint32_t)(key >> shift_next) & 0xffu);
+                        const uint32_t slot = next_slot(key, pos);
                         const uint32_t peers = __match_any_sync(act, slot);
                         if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(hist_next + slot, (uint32_t)__popc(peers));
                     }
                 }
-                if (!valid) continue;
-                const uint32_t idx = sv[i];
-                if (DECODE) {
-                    if (sizeof(K) == 8) {
-                        D.rslo[pos] = (uint32_t)((unsigned long long)key >> 32);
-                        D.rout[pos] = (uint32_t)key;
-                    } else {
-                        const uint32_t k32 = (uint32_t)key;
-                        D.rslo[pos] = stab[D.ob >= 32 ? 0u : k32 >> D.ob];
-                        D.rout[pos] = D.ob >= 32 ? k32 : (k32 & ((1u << D.ob) - 1));
-                    }
-                    if (D.packin) {
-                        D.order[pos] = wp0_32 + (idx & ((1u << D.wb) - 1u));
-                        D.rin[pos] = (idx >> D.wb) + 1u;
-                    } else {
-                        D.order[pos] = idx;
-                        D.rin[pos] = __ldg(D.in + idx);
-                    }
-                } else {
-                    kout[pos] = key;
-                    vout[pos] = idx;
-                }
+                if (valid) store(key, pos, i);
             }
         };
         if (full) write_out(std::true_type{}); else write_out(std::false_type{});
@@ -588,7 +593,8 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
     const uint32_t C = 1u << cbits;
     for (uint32_t i = tid; i < C; i += kSortThreads) sct[i] = ctab[i];
     uint32_t *const myh = hw[tid >> 5];
-    uint32_t bad = 0, mx_in = 0, mx_out = 0, missing = 0;
+    uint32_t mx_in = 0, mx_out = 0, mn_in = 0xffffffffu, mn_out = 0xffffffffu, missing = 0;
+    bool okall = true;
     // element e (0..7) of this thread inside the tile
     auto off = [&](int e) -> uint32_t {
         return VEC ? (uint32_t)((e >> 2) * 1024 + 4 * tid + (e & 3)) : (uint32_t)(e * kSortThreads + tid);
@@ -654,14 +660,20 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
             bool ok;
             const uint32_t su = slo_to_us(cf[e], ok);
             const uint32_t a = ca[e], o = co[e];
-            bad |= (a == 0u ? 1u : 0u) | (o == 0u ? 2u : 0u) | (ok ? 0u : 4u);
+            // validation by minima (a zero length is the minimum 0) and one flag: no per-key branches
+            mn_in = min(mn_in, a);
+            mn_out = min(mn_out, o);
+            okall &= ok;
             mx_in = max(mx_in, a);
             mx_out = max(mx_out, o);
             uint32_t hh = slo_hash(su, (uint32_t)cbits);
             unsigned long long en = sct[hh];
-            // >= 2 slots per value: an absent value ends at an empty slot
-            while (en != 0ull && (uint32_t)(en >> 32) != su) { hh = (hh + 1) & (C - 1); en = sct[hh]; }
-            missing |= en == 0ull ? 1u : 0u;
+            // (>= 8 slots per value up to 4096 slots: the first probe almost always decides; an
+            // absent value ends at an empty slot)
+            if ((uint32_t)(en >> 32) != su) {
+                while (en != 0ull && (uint32_t)(en >> 32) != su) { hh = (hh + 1) & (C - 1); en = sct[hh]; }
+                missing |= en == 0ull ? 1u : 0u;
+            }
             key[e] = ((uint32_t)en << ob) | o;
             atomicAdd(myh + (key[e] & 0xffu), 1u);
         }
@@ -689,6 +701,7 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
         }
         __syncthreads();                                  // hw is cleared for the next tile
     }
+    uint32_t bad = (mn_in == 0u ? 1u : 0u) | (mn_out == 0u ? 2u : 0u) | (okall ? 0u : 4u);
     for (int d = 16; d; d >>= 1) {
         bad |= __shfl_xor_sync(0xffffffffu, bad, d);
         missing |= __shfl_xor_sync(0xffffffffu, missing, d);
