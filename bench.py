@@ -111,7 +111,9 @@ def ncu_summary() -> dict:
 
 def ncu_traffic(kernel: str):
     """dram bytes per launch of `kernel` from the committed ncu summary, if present."""
-    k = ncu_summary().get("kernels", {}).get(kernel)
+    ks = ncu_summary().get("kernels", {})
+    # exact name, else the first launch of its instantiation (e.g. k_dp_tiles -> k_dp_tiles<2>)
+    k = ks.get(kernel) or next((v for n, v in ks.items() if n.split("<")[0] == kernel and "#" not in n), None)
     return k.get("dram_bytes_per_launch") if k else None
 
 

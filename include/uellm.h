@@ -23,8 +23,8 @@
  *                           S:341-400)
  *
  * Citations: P:NNN = /root/reference/PAPER.md line; S:NNN = SPEC.md line; Rk = reading k in
- * DESIGN.md.  The C ABI is plain: no exceptions, no C++ or torch types, no global state, no
- * allocation.  All device work is stream-ordered on `stream` (a cudaStream_t passed as void*,
+ * DESIGN.md.  The C ABI is plain: no exceptions, no C++ or torch types, no device allocation,
+ * no global state except the pipelined call's reused streams / events.  All device work is stream-ordered on `stream` (a cudaStream_t passed as void*,
  * NULL = legacy default stream).
  *
  * Pointers: each pointer argument is marked [host], [device] or [host|device].  [host|device]
@@ -441,9 +441,10 @@ uellm_status uellm_helr_plan(const uellm_topology *t, void *ws, size_t ws_bytes,
  *   ws                      [device] >= uellm_pipeline_workspace_bytes(n, cfg, groups), 256-B aligned.
  *   order, batch_offsets    [host] n and n+1 x u32 (pinned for overlap), as uellm_schedule_batches.
  *   num_batches, totals     [host].
- * Creates and destroys two streams and 3 x groups events per call (no host or device
- * allocation); synchronises `stream` once per group (each group's load reads its validation
- * record) and at the end.  On an error the host outputs are unspecified. */
+ * Its three internal streams and the per-group events are created on the device's first call and
+ * reused by every later call (held for the process lifetime; calls on one device serialise on
+ * them); no device allocation.  Synchronises `stream` once per group (each group's load reads its
+ * validation record) and at the end.  On an error the host outputs are unspecified. */
 size_t uellm_pipeline_workspace_bytes(uint64_t n, const uellm_config *cfg, uint32_t groups);
 uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config *cfg, uint32_t groups, void *ws,
                                       size_t ws_bytes, uint32_t *order, uint32_t *batch_offsets,

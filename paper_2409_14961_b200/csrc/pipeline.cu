@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "internal.cuh"
@@ -43,8 +44,12 @@ struct PipeLayout {
     uint64_t in[3], out[3], slo[3];   // input staging slots (g % 3)
     uint64_t order[3], offs[3];       // output staging slots (g % 3)
     uint64_t tot, nb;                 // per-group totals / num_batches (device)
+    uint64_t tail_groups;             // the tapered last groups
     uint64_t total;
 };
+#ifndef UELLM_PIPE_TAIL_AUTO
+#define UELLM_PIPE_TAIL_AUTO 1        // tail groups: automatic (one-wave) DP tiles
+#endif
 
 static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t groups)
 {
@@ -90,9 +95,21 @@ static PipeLayout pipe_layout(uint64_t n, const uellm_config &cfg, uint32_t grou
     auto take = [&](uint64_t bytes) { uint64_t o = off; off = align_up(off + (bytes ? bytes : 1), 256); return o; };
     uellm_config c = cfg;
     c.window = (uint32_t)wl;
-    // the groups share the GPU (throughput-bound): no one-wave short tiles
-    if (!c.dp_tile) c.dp_tile = tile_len_throughput(P.group_q, c.max_batch ? c.max_batch : 1);
+    // the body groups share the GPU (throughput-bound): no one-wave short tiles; the tapered tail
+    // groups are exposed after the last copy (latency-bound): the automatic tile choice
+    const bool auto_tile = !c.dp_tile;
+    if (auto_tile) c.dp_tile = tile_len_throughput(P.group_q, c.max_batch ? c.max_batch : 1);
     P.ws_bytes = make_layout(P.group_q, c).total;
+    if (auto_tile && UELLM_PIPE_TAIL_AUTO) {
+        uellm_config ct = c;
+        ct.dp_tile = 0;
+        for (uint64_t g = G - K; g < G; ++g) {
+            const uint64_t q = (P.start[g + 1] - P.start[g]) * wl;
+            const uint64_t b = make_layout(q < n ? q : n, ct).total;
+            if (b > P.ws_bytes) P.ws_bytes = b;
+        }
+    }
+    P.tail_groups = K;
     P.ws[0] = take(P.ws_bytes);
     P.ws[1] = take(P.ws_bytes);
     const uint64_t q = P.group_q ? P.group_q : 1;
@@ -114,6 +131,42 @@ static uint64_t gwin(const PipeLayout &P, uint64_t g)
 }  // namespace uellm
 
 using namespace uellm;
+
+namespace {
+// Streams and events of uellm_schedule_pipelined, created on a device's first call and reused by
+// every later call on it (held for the process lifetime): the per-call creation and destruction of
+// 3 streams and 3 x groups events is gone from the call.  Calls on one device serialise on its
+// pool's mutex (they share the copy streams).
+struct PipePool {
+    std::mutex mu;
+    bool ready = false;
+    cudaStream_t H = nullptr, D = nullptr, C2 = nullptr;
+    cudaEvent_t start = nullptr;
+    cudaEvent_t ev[3][kPipeMaxGroups] = {};     // h2d, done, d2h per group
+    bool timing = false;
+    cudaError_t init(bool with_timing)
+    {
+        if (ready && timing == with_timing) return cudaSuccess;
+        cudaError_t e;
+        if (!ready) {
+            if ((e = cudaStreamCreateWithFlags(&H, cudaStreamNonBlocking))) return e;
+            if ((e = cudaStreamCreateWithFlags(&D, cudaStreamNonBlocking))) return e;
+            if ((e = cudaStreamCreateWithFlags(&C2, cudaStreamNonBlocking))) return e;
+        } else {
+                for (auto &row : ev) for (auto &x : row) cudaEventDestroy(x);
+        }
+        const unsigned fl = with_timing ? cudaEventDefault : cudaEventDisableTiming;
+        if ((e = cudaEventCreateWithFlags(&start, fl))) return e;
+        for (auto &row : ev)
+            for (auto &x : row) if ((e = cudaEventCreateWithFlags(&x, fl))) return e;
+        timing = with_timing;
+        ready = true;
+        return cudaSuccess;
+    }
+};
+constexpr int kPoolDevices = 64;
+PipePool g_pools[kPoolDevices];
+}  // namespace
 
 extern "C" {
 
@@ -147,9 +200,15 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
     const uint64_t G = PL.groups;
     uellm_config gcfg = *cfg;
     gcfg.window = (uint32_t)(cfg->window ? (cfg->window < n ? cfg->window : n) : n);
+    uellm_config tcfg = gcfg;                                  // the tapered tail groups' config
     if (!gcfg.dp_tile) gcfg.dp_tile = tile_len_throughput(PL.group_q, gcfg.max_batch ? gcfg.max_batch : 1);
+    if (!UELLM_PIPE_TAIL_AUTO || cfg->dp_tile) tcfg = gcfg;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kPoolDevices) return UELLM_ERR_CUDA;
+    PipePool &pool = g_pools[dev];
+    std::lock_guard<std::mutex> pool_lock(pool.mu);
     cudaStream_t H = nullptr, D = nullptr, C2 = nullptr;
-    std::vector<cudaEvent_t> h2d(G, nullptr), done(G, nullptr), d2h(G, nullptr);
+    cudaEvent_t *h2d = pool.ev[0], *done = pool.ev[1], *d2h = pool.ev[2];
     std::vector<uint64_t> m(G, 0);
     std::vector<uellm_totals> tot_host(G);
     uellm_status status = UELLM_OK;
@@ -169,20 +228,12 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
     };
   auto body = [&]() -> uellm_status {
-    PCU(cudaStreamCreateWithFlags(&H, cudaStreamNonBlocking));
-    PCU(cudaStreamCreateWithFlags(&D, cudaStreamNonBlocking));
-    PCU(cudaStreamCreateWithFlags(&C2, cudaStreamNonBlocking));
+    PCU(pool.init(trace));
+    H = pool.H; D = pool.D; C2 = pool.C2;
     cudaStream_t CS[2] = {C, C2};       // compute lanes: group g runs on lane g % 2
-    const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
-    for (uint64_t g = 0; g < G; ++g) {
-        PCU(cudaEventCreateWithFlags(&h2d[g], evflags));
-        PCU(cudaEventCreateWithFlags(&done[g], evflags));
-        PCU(cudaEventCreateWithFlags(&d2h[g], evflags));
-    }
-    cudaEvent_t start = nullptr;
+    cudaEvent_t start = pool.start;
     {
         // everything already queued on the caller's stream happens before our copies
-        PCU(cudaEventCreateWithFlags(&start, evflags));
         cudaEventRecord(start, C);
         cudaStreamWaitEvent(H, start, 0);
         cudaStreamWaitEvent(D, start, 0);
@@ -236,7 +287,8 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
                                  (const float *)(w + PL.slo[si])};
             uellm_profile prof;
             const double t0 = ms();
-            uellm_status st = uellm_profile_load(&gq_, &gcfg, w + PL.ws[s], PL.ws_bytes, L, &prof);
+            const uellm_config &ccfg = g >= G - PL.tail_groups ? tcfg : gcfg;
+            uellm_status st = uellm_profile_load(&gq_, &ccfg, w + PL.ws[s], PL.ws_bytes, L, &prof);
             if (st != UELLM_OK) return st;
             const double t1 = ms();
             if (g >= 2) PCU(flush_group(g - 2, L));
@@ -245,9 +297,9 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
             uint32_t *d_offs = (uint32_t *)(w + PL.offs[o]);
             uint64_t *d_nb = (uint64_t *)(w + PL.nb) + g;
             uellm_totals *d_tot = (uellm_totals *)(w + PL.tot) + g;
-            if ((st = uellm_schedule_batches(&prof, &gcfg, d_order, d_offs, d_nb, L)) != UELLM_OK) return st;
+            if ((st = uellm_schedule_batches(&prof, &ccfg, d_order, d_offs, d_nb, L)) != UELLM_OK) return st;
             const double t2 = ms();
-            if ((st = uellm_batch_stats(&prof, &gcfg, d_offs, d_nb, nullptr, d_tot, L)) != UELLM_OK) return st;
+            if ((st = uellm_batch_stats(&prof, &ccfg, d_offs, d_nb, nullptr, d_tot, L)) != UELLM_OK) return st;
             if (trace)
                 fprintf(stderr, "[pipe] g=%llu load_in %.3f load_out %.3f sched_out %.3f stats_out %.3f ms\n",
                         (unsigned long long)g, t0, t1, t2, ms());
@@ -271,7 +323,6 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
                         (unsigned long long)g, (unsigned long long)(qz(g) - qa(g)), a, b, c);
             }
         }
-        cudaEventDestroy(start);
         batch_offsets[moff] = (uint32_t)n;
         *num_batches = moff;
         // whole-job totals from the per-group integer totals (exact); the latency mean is
@@ -287,14 +338,10 @@ uellm_status uellm_schedule_pipelined(const uellm_queries *q, const uellm_config
   };
     status = body();
     if (status != UELLM_OK) { cudaStreamSynchronize(C); }
-    if (H) { cudaStreamSynchronize(H); cudaStreamDestroy(H); }
-    if (D) { cudaStreamSynchronize(D); cudaStreamDestroy(D); }
-    if (C2) { cudaStreamSynchronize(C2); cudaStreamDestroy(C2); }
-    for (uint64_t g = 0; g < G; ++g) {
-        if (h2d[g]) cudaEventDestroy(h2d[g]);
-        if (done[g]) cudaEventDestroy(done[g]);
-        if (d2h[g]) cudaEventDestroy(d2h[g]);
-    }
+    // (the pool's streams stay; an error leaves no copy of this call in flight on them)
+    if (H) cudaStreamSynchronize(H);
+    if (D) cudaStreamSynchronize(D);
+    if (C2) cudaStreamSynchronize(C2);
 #undef PCU
     return status;
 }
