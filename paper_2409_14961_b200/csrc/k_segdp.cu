@@ -286,7 +286,22 @@ struct NarrowSlots {
     longlong2 *sl;              // .x = C, .y = i | mo << 32 | mi << 48
     uint32_t *tri;              // per-block triangular max table M[q][k], q < k < 32 (496 words)
     uint2 *hl;                  // per-block lower-hull subset of the lean external candidates
+    uint32_t *ss;               // many-run variants: the block's SLO range staged for the violation counts
 };
+
+// #{k in [i, j) : slo[k] < est} on an ascending run staged in shared memory (ss[k - base]).
+__device__ __forceinline__ uint32_t viol_count_sm(const uint32_t *ss, uint32_t base, uint32_t i, uint32_t j,
+                                                  unsigned long long est, uint32_t slo_x)
+{
+    if ((unsigned long long)slo_x < est) return j - i;
+    if ((unsigned long long)ss[i - base] >= est) return 0;
+    uint32_t lo = i + 1, hi = j - 1;      // slo[i] < est <= slo[j-1]
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if ((unsigned long long)ss[mid - base] < est) lo = mid + 1; else hi = mid;
+    }
+    return lo - i;
+}
 // Capacity of the hull subset (larger subsets fall back to the whole list).
 constexpr uint32_t kHullCap = 64;
 #ifndef UELLM_HULL_MIN
@@ -318,6 +333,20 @@ constexpr uint32_t kHullMin = UELLM_HULL_MIN;
 // fast blocks: the unrolled intra loop stops at checkpoints once no later intra candidate can win
 #ifndef UELLM_DP_EXIT
 #define UELLM_DP_EXIT 1
+#endif
+#ifndef UELLM_DP_EXIT_MASK
+#define UELLM_DP_EXIT_MASK 0x2AA40000u    // q = 18, 21, 23, 25, 27, 29 (0x11111000u: 12, 16, 20, 24, 28)
+#endif
+// many-run variants: stage the slow block's SLO range in shared memory for the violation counts
+#ifndef UELLM_DP_SLO_STAGE
+#define UELLM_DP_SLO_STAGE 1
+#endif
+// block prefix maxima as one packed u16x2 scan; RSV_SKIP: the run-start scan only when needed
+#ifndef UELLM_DP_PACKSCAN
+#define UELLM_DP_PACKSCAN 1
+#endif
+#ifndef UELLM_DP_RSV_SKIP
+#define UELLM_DP_RSV_SKIP 0
 #endif
 // offset of row q of the triangular table (row q holds k = q+1 .. 31)
 __host__ __device__ constexpr uint32_t tri_off(int q) { return (uint32_t)(q * 31 - q * (q - 1) / 2); }
@@ -668,16 +697,35 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         long long cl_l = 0;
         if (FIX) cl_l = vl ? P.Cx[x] : 0;
         // block prefix maxima of the elements j0..j0+lane and run starts
-        uint32_t pmo = out_l, pmi = in_l;
         uint32_t sprev = __shfl_up_sync(0xffffffffu, slo_l, 1);
         if (lane == 0) sprev = prev_slo;
         uint32_t rsv = (vl && slo_l != sprev) ? x : 0u;
+#if UELLM_DP_PACKSCAN
+        // (out, in) as one u16x2 word (narrow path: both < 2^16; idle lanes hold 0): one shuffle and
+        // one paired max per step; the run-start scan only when a run starts in the block
+        uint32_t pk = (out_l << 16) | in_l;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, pk, d);
+            if ((int)lane >= d) pk = __vmaxu2(pk, a);
+        }
+        if (!UELLM_DP_RSV_SKIP || __any_sync(0xffffffffu, rsv != 0u)) {
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t c = __shfl_up_sync(0xffffffffu, rsv, d);
+                if ((int)lane >= d) rsv = max(rsv, c);
+            }
+        }
+        const uint32_t pmo = pk >> 16, pmi = pk & 0xffffu;
+#else
+        uint32_t pmo = out_l, pmi = in_l;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const uint32_t a = __shfl_up_sync(0xffffffffu, pmo, d), b = __shfl_up_sync(0xffffffffu, pmi, d);
             const uint32_t c = __shfl_up_sync(0xffffffffu, rsv, d);
             if ((int)lane >= d) { pmo = max(pmo, a); pmi = max(pmi, b); rsv = max(rsv, c); }
         }
+#endif
         const uint32_t rs_l = max(run_start, rsv);
         const uint32_t rs_last = __shfl_sync(0xffffffffu, rs_l, B - 1);
         // An interval [i, j) lies inside one SLO run iff i >= run start of element j-1; only then
@@ -697,6 +745,14 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
         // any interval ending at the lane's element is that element's own: MO = pmo for every
         // candidate and the lane-constant parts of est are computed once.
         const uint32_t A_l = t_b + t_it * pmo, T_l = t_tok * pmo;
+        // violation count of [ci, jl) for the binary-search (several-run) case: from the staged SLO
+        // range when this block staged it (many-run variants), else from global memory
+        bool staged = false;
+        uint32_t ss_base = 0;
+        auto vcount = [&](uint32_t ci, unsigned long long est) -> uint32_t {
+            return (VFREE && staged) ? viol_count_sm(S.ss, ss_base, ci, jl, est, slo_l)
+                                     : viol_count_slow(rslo, ci, jl, est, slo_l);
+        };
         auto ext_pass = [&](auto slow_tag, auto single_tag, auto onerun_tag, uint32_t c0, uint32_t c1) {
             constexpr bool SLOW = decltype(slow_tag)::value;
             constexpr bool SINGLE_OK = decltype(single_tag)::value;
@@ -718,7 +774,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                 if (LAM) {
                     uint32_t v;
                     if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
-                                               : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
+                                               : (dead ? 0u : vcount(ci, est));
                     else v = (slo_l < est) ? b : 0u;
                     tot += penalty(v);
                 }
@@ -965,7 +1021,9 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
 #pragma unroll
                 for (int q = 0; q < 31; ++q) {
                     const uint32_t Cq = __shfl_sync(0xffffffffu, r32, q);
-                    if (UELLM_DP_EXIT && q >= (UELLM_DP_EXIT == 2 ? 8 : 12) && (q & 3) == 0) {
+                    // checkpoints q = 18, 21, 23, 25, 27, 29: the cheapest set under the exit-step
+                    // distribution of a sequential C model on c3 data (mean first exact exit 21.5)
+                    if (UELLM_DP_EXIT && ((UELLM_DP_EXIT_MASK >> q) & 1u)) {
                         // every later lane already at or below that bound: no later intra candidate
                         // can win (ties keep the smaller, current i)
                         const uint32_t bnd = Cq + LB_l + (UELLM_DP_EXIT == 2 ? (lane - (uint32_t)q - 1u) * dblk : 0u);
@@ -1011,6 +1069,16 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                                                     ((unsigned long long)t_tok * mo + (unsigned long long)t_pre * mi);
                 vfree = (unsigned long long)__ldg(rslo + i0) >= emax;
             }
+            if (VFREE && S.ss && !vfree && (ext_slow || intra_slow)) {
+                // stage slo[oldest candidate .. block end) (b <= W after the last prune: <= W + 32)
+                const uint32_t lo = (uint32_t)S.sl[0].y, len = j0 + B - lo;
+                if (len <= (P.W + 64u + 31u & ~31u)) {
+                    for (uint32_t k = lane; k < len; k += 32) S.ss[k] = __ldg(rslo + lo + k);
+                    __syncwarp();
+                    staged = true;
+                    ss_base = lo;
+                }
+            }
             if (ext_slow && !vfree) {
                 if (single_ok) ext_pass(T1{}, T1{}, F0{}, 0, L); else ext_pass(T1{}, F0{}, F0{}, 0, L);
             } else if (one_run_ext) {
@@ -1049,7 +1117,7 @@ __device__ DpResult dp_warp_blocked(const DPParams &P, const NarrowSlots &S, uin
                     if (LAM) {
                         uint32_t v;
                         if (SLOW) v = (ci >= rs_l) ? ((slo_l < est) ? b : 0u)
-                                                   : (dead ? 0u : viol_count_slow(rslo, ci, jl, est, slo_l));
+                                                   : (dead ? 0u : vcount(ci, est));
                         else v = (slo_l < est) ? b : 0u;
                         tot += penalty(v);
                     }
@@ -1155,9 +1223,16 @@ __device__ __forceinline__ void tile_bounds(const DPParams &P, uint64_t t, uint3
 
 // shared memory per warp: narrow = 16 B slots + the 496-word triangular max table; wide = 20 B slots
 constexpr uint32_t kRmqBytes = 500 * 4;            // 1 pad word + 496 + 3, keeps 16-byte alignment
+// many-run variants (7, 8): the SLO values of a slow block's candidate range [oldest candidate,
+// block end) -- at most W + 32 positions -- staged per warp, so each violation count is a binary
+// search in shared memory instead of up to 9 dependent global loads (c5's anti-sorted segment)
+static __host__ __device__ __forceinline__ uint32_t slo_stage_cap(const DPParams &P)
+{
+    return (P.narrow && P.many_runs && P.W <= 480u && UELLM_DP_SLO_STAGE) ? ((P.W + 64u + 31u) & ~31u) : 0u;
+}
 static __host__ __device__ __forceinline__ uint32_t warp_smem_bytes(const DPParams &P)
 {
-    return P.narrow ? P.cap_slots * 16 + kRmqBytes + kHullCap * 8 : P.cap_slots * 20;
+    return P.narrow ? P.cap_slots * 16 + kRmqBytes + kHullCap * 8 + slo_stage_cap(P) * 4 : P.cap_slots * 20;
 }
 
 // Variant V of the SEG-DP kernels, fixed on the host (one instantiation per kernel keeps the code
@@ -1182,6 +1257,7 @@ __device__ DpResult dp_run(const DPParams &P, char *smem, int warp, uint32_t s, 
         S.sl = (longlong2 *)p;
         S.tri = (uint32_t *)(p + (size_t)P.cap_slots * 16);
         S.hl = (uint2 *)(p + (size_t)P.cap_slots * 16 + kRmqBytes);
+        S.ss = (VF && slo_stage_cap(P)) ? (uint32_t *)(p + (size_t)P.cap_slots * 16 + kRmqBytes + kHullCap * 8) : nullptr;
         return dp_warp_blocked<FIX, LK, SPLIT, VF>(P, S, s, e, src, stop_min, src_args_ok, entry_uni);
     }
 }
