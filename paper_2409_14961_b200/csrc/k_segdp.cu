@@ -1526,16 +1526,23 @@ __global__ void k_dp_cascade(DPParams P)
         }
         const bool eu = (eu_mask >> (k & 31u)) & 1u;
         if (V != 0 && !tail_local && eu && ref_P != 0) {
-            // a further tile of the deferred stretch: only the record fields change (no reads)
-            if (lane == 0) {
+            // further tiles of the deferred stretch: only the record fields change (no reads), and
+            // every tile of the run of entry-uniform tiles from k to the end of this 32-tile chunk
+            // takes the same fields -- one lane per tile
+            const uint32_t sh = k & 31u;
+            const uint32_t run = (uint32_t)__ffs(~(eu_mask >> sh)) - 1u;     // set bits from bit sh
+            uint32_t cnt = (run == 0xffffffffu || sh + run > 32u) ? 32u - sh : run;
+            if (k + cnt > K) cnt = K - k;
+            if (lane < cnt) {
                 uint32_t ts, te, tk, tw; bool tv;
-                tile_bounds(P, t0 + k, ts, te, tk, tw, tv);
-                TileRec &q = P.tiles[t0 + k];
+                tile_bounds(P, t0 + k + lane, ts, te, tk, tw, tv);
+                TileRec &q = P.tiles[t0 + k + lane];
                 q.fill_s = ref_s; q.fill_P = ref_P; q.fill_F = ref_F;
                 q.conv = 0; q.fix_end = te; q.off_fix = tail_off; q.off_local = 0;
             }
             __syncwarp();
             prev_touched = true;
+            k += cnt - 1;                                // (the loop adds 1)
             continue;
         }
         TileRec r = P.tiles[t0 + k];

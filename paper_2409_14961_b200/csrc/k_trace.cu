@@ -182,6 +182,74 @@ __global__ void k_trace_c(const uint16_t *__restrict__ maps, TileRec *tiles, uin
     if (rewalks) atomicAdd(&diag->trace_rewalks, (unsigned long long)rewalks);
 }
 
+// k_trace_c with the walk's data staged (one 32-thread CTA per window, W <= kTraceCStageW): for 32
+// tiles at a time the warp brings their exit maps (W u16 each, 16-byte loads) and the record fields
+// the walk reads into shared memory, then lane 0 follows the true path through them -- one
+// shared-memory hop per tile instead of a dependent global load (windows of one long uniform
+// stretch re-walk every tile: c5's identical-key segment).
+constexpr uint32_t kTraceCStageW = 384;
+__global__ void __launch_bounds__(32) k_trace_c_staged(const uint16_t *__restrict__ maps, TileRec *tiles, uint64_t tpw,
+                                                       uint64_t nwin, uint64_t window, uint32_t W, uint32_t *bm,
+                                                       Diag *diag)
+{
+    extern __shared__ __align__(16) uint16_t smap[];             // [32][W]
+    __shared__ uint32_t fs[32], fe[32], fa[33], fb[32];
+    const uint64_t w = blockIdx.x;
+    const uint32_t lane = threadIdx.x;
+    if (w >= nwin) return;
+    const uint64_t t0 = w * tpw;
+    uint32_t K = 0;
+    bool allm = true;
+    for (uint32_t k0 = 0; k0 < tpw; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool v = k < tpw && tiles[t0 + k].valid;
+        const uint32_t bv = __ballot_sync(0xffffffffu, v);
+        K += __popc(bv);
+        const bool bad = v && k >= 1 && tiles[t0 + k].exitB != tiles[t0 + k].exitA;
+        if (__any_sync(0xffffffffu, bad)) allm = false;
+        if (bv != 0xffffffffu) break;
+    }
+    if (K == 0) return;
+    if (lane == 0) bm_set(bm, (uint32_t)(w * window));          // every window starts a batch
+    if (allm) return;
+    uint32_t exit_true = tiles[t0 + K - 1].exitB;                 // (uniform across the warp)
+    uint32_t rewalks = 0;
+    const uint32_t vec = W / 8;                                  // 16-byte chunks per map row
+    for (int k_hi = (int)K - 2; k_hi >= 0; k_hi -= 32) {
+        const int k_lo = k_hi - 31 > 0 ? k_hi - 31 : 0;
+        const int rows = k_hi - k_lo + 1;
+        if ((int)lane < rows) {
+            const TileRec &r = tiles[t0 + k_lo + lane];
+            fs[lane] = r.s; fe[lane] = r.e; fa[lane] = r.exitA; fb[lane] = r.exitB;
+        }
+        if (lane == 0) fa[rows] = tiles[t0 + k_hi + 1].exitA;
+        if ((W & 7u) == 0) {
+            for (int row = 0; row < rows; ++row) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(maps + (t0 + k_lo + row) * W);
+                uint4 *dst = reinterpret_cast<uint4 *>(smap + (uint32_t)row * W);
+                for (uint32_t c = lane; c < vec; c += 32) dst[c] = __ldg(src + c);
+            }
+        } else {
+            for (int row = 0; row < rows; ++row)
+                for (uint32_t c = lane; c < W; c += 32) smap[(uint32_t)row * W + c] = maps[(t0 + k_lo + row) * W + c];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (int k = k_hi; k >= k_lo; --k) {
+                const int q = k - k_lo;
+                if (exit_true == fa[q + 1]) { exit_true = fb[q]; continue; }
+                ++rewalks;
+                tiles[t0 + k].remark = exit_true + 1u;
+                exit_true = fs[q] - (uint32_t)smap[(uint32_t)q * W + (fe[q] - exit_true)];
+                tiles[t0 + k].exitB = exit_true;
+            }
+        }
+        exit_true = __shfl_sync(0xffffffffu, exit_true, 0);
+        __syncwarp();
+    }
+    if (lane == 0 && rewalks) atomicAdd(&diag->trace_rewalks, (unsigned long long)rewalks);
+}
+
 // T4: tiles entered elsewhere than their B-walk assumed are re-marked from the true entry (one CTA
 // per tile, the walk over the staged args).
 __global__ void __launch_bounds__(128) k_trace_remark(const uint16_t *__restrict__ argx, const TileRec *tiles,
@@ -229,6 +297,9 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 #ifndef UELLM_TRACE_A
 #define UELLM_TRACE_A 128
 #endif
+#ifndef UELLM_TRACE_C_STAGED
+#define UELLM_TRACE_C_STAGED 1
+#endif
     const bool stage_walk = UELLM_TRACE_A && ntiles < (uint64_t)nsm * 64 &&
                             P.tile_len * sizeof(uint16_t) <= 160 * 1024;
     if (stage_walk) {
@@ -241,8 +312,17 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
     }
     k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag, wflag);
     k_trace_maps<<<grid, 256, stage, st>>>(P.argx, P.tiles, ntiles, P.tpw, wflag, P.W, maps);
-    k_trace_c<<<(unsigned)ceil_div(P.nwin * 32, 128), 128, 0, st>>>(maps, P.tiles, P.tpw, P.nwin, P.window, P.W,
-                                                                   bitmap, P.diag);
+    if (UELLM_TRACE_C_STAGED && P.W <= kTraceCStageW) {
+        const size_t sm = (size_t)32 * P.W * sizeof(uint16_t);
+        if (sm > 48 * 1024) {
+            e = cudaFuncSetAttribute(k_trace_c_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+        }
+        k_trace_c_staged<<<(unsigned)P.nwin, 32, sm, st>>>(maps, P.tiles, P.tpw, P.nwin, P.window, P.W, bitmap, P.diag);
+    } else {
+        k_trace_c<<<(unsigned)ceil_div(P.nwin * 32, 128), 128, 0, st>>>(maps, P.tiles, P.tpw, P.nwin, P.window, P.W,
+                                                                       bitmap, P.diag);
+    }
     k_trace_remark<<<grid, 128, stage, st>>>(P.argx, P.tiles, ntiles, P.tpw, wflag, bitmap);
     *launches = 5;
     return cudaGetLastError();
