@@ -70,6 +70,57 @@ __global__ void __launch_bounds__(1024) k_trace_a_smem(const uint16_t *__restric
     tiles[t].exitA = i;
 }
 
+// Walk A, one warp per tile (kTraceWarps tiles per CTA): the warp stages the tile's args in shared
+// memory (16-byte loads when aligned), lane 0 walks them and sets the path's bits in a shared copy
+// of the tile's bitmap words, and the warp ORs the words into the global bitmap -- neither the walk's
+// hops nor its bit sets wait on global memory (the thread walk's hops each waited for a DRAM read).
+constexpr uint32_t kTraceWarps = 4;
+__host__ __device__ constexpr uint32_t trace_warp_smem(uint32_t tile_len)
+{
+    return ((tile_len * 2 + 15) & ~15u) + (((tile_len / 32 + 3) * 4 + 15) & ~15u);   // 16-byte aligned per warp
+}
+__global__ void __launch_bounds__(32 * kTraceWarps) k_trace_a_warp(const uint16_t *__restrict__ argx, TileRec *tiles,
+                                                                   uint64_t ntiles, uint32_t *bm, uint32_t tile_len)
+{
+    extern __shared__ __align__(16) unsigned char tsm[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t t = (uint64_t)blockIdx.x * kTraceWarps + warp;
+    if (t >= ntiles) return;
+    const TileRec r = tiles[t];
+    if (!r.valid) return;
+    unsigned char *base = tsm + (size_t)warp * trace_warp_smem(tile_len);
+    uint16_t *sa = reinterpret_cast<uint16_t *>(base);
+    uint32_t *sw = reinterpret_cast<uint32_t *>(base + ((tile_len * 2 + 15) & ~15u));
+    const uint32_t len = r.e - r.s;                               // sa[k] = delta of boundary s+1+k
+    if ((r.s & 7u) == 0 && (len & 7u) == 0) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(argx + r.s);
+        uint4 *dst = reinterpret_cast<uint4 *>(sa);
+        for (uint32_t k = lane; k < len / 8; k += 32) dst[k] = __ldg(src + k);
+    } else {
+        for (uint32_t k = lane; k < len; k += 32) sa[k] = argx[r.s + k];
+    }
+    // bitmap words w0 .. w1 cover the positions (s, e] the walk marks
+    const uint32_t w0 = (r.s + 1) >> 5, w1 = r.e >> 5, nw = w1 - w0 + 1;
+    for (uint32_t k = lane; k < nw; k += 32) sw[k] = 0u;
+    __syncwarp();
+    if (lane == 0) {
+        uint32_t j = r.e, i;
+        sw[(j >> 5) - w0] |= 1u << (j & 31);
+        for (;;) {
+            i = j - (uint32_t)sa[j - 1 - r.s];
+            if (i <= r.s) break;
+            sw[(i >> 5) - w0] |= 1u << (i & 31);
+            j = i;
+        }
+        tiles[t].exitA = i;
+    }
+    __syncwarp();
+    for (uint32_t k = lane; k < nw; k += 32) {
+        const uint32_t v = sw[k];
+        if (v) atomicOr(bm + w0 + k, v);
+    }
+}
+
 __global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uint64_t ntiles, uint64_t tpw,
                           uint32_t *bm, Diag *diag, uint32_t *wflag)
 {
@@ -300,9 +351,20 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 #ifndef UELLM_TRACE_C_STAGED
 #define UELLM_TRACE_C_STAGED 1
 #endif
+#ifndef UELLM_TRACE_A_WARP
+#define UELLM_TRACE_A_WARP 1
+#endif
     const bool stage_walk = UELLM_TRACE_A && ntiles < (uint64_t)nsm * 64 &&
                             P.tile_len * sizeof(uint16_t) <= 160 * 1024;
-    if (stage_walk) {
+    if (UELLM_TRACE_A_WARP && P.tile_len <= 8192) {
+        const size_t sm = (size_t)kTraceWarps * trace_warp_smem(P.tile_len);
+        if (sm > 48 * 1024) {
+            e = cudaFuncSetAttribute(k_trace_a_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+        }
+        k_trace_a_warp<<<(unsigned)ceil_div(ntiles, kTraceWarps), 32 * kTraceWarps, sm, st>>>(P.argx, P.tiles, ntiles,
+                                                                                            bitmap, P.tile_len);
+    } else if (stage_walk) {
         e = cudaFuncSetAttribute(k_trace_a_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(P.tile_len * sizeof(uint16_t)));
         if (e != cudaSuccess) return e;
