@@ -432,7 +432,7 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
     }
     // a3: sort (every mode except FIFO) + a4: records in scheduled order
     uint32_t *rin = at<uint32_t>(w, L.rin), *rout = at<uint32_t>(w, L.rout), *rslo = at<uint32_t>(w, L.rslo);
-    int passes = 0;
+    int passes = 0, sk = 0;
     const KeyPlan kp = key_plan(v);
     const int ob = kp.ob, rb = kp.rb;
     const bool compressed = cfg->mode != UELLM_MODE_FIFO && kp.ok;
@@ -472,8 +472,8 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
                                     (uint32_t *)at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
                                     at<uint32_t>(w, L.hist), at<uint32_t>(w, L.hist) + 256 * L.sort_tiles, n,
                                     L.window, w0, wn, mask, &passes, st,
-                                    (mask & 1u) ? at<uint32_t>(w, L.hist0) : nullptr, &D));
-            launches += 2 * passes + ((mask & 1u) || !passes ? 0 : 1);   // scan + scatter per pass, one histogram
+                                    (mask & 1u) ? at<uint32_t>(w, L.hist0) : nullptr, &D, &sk));
+            launches += sk;                            // scan + scatter per pass, histogram kernels
             if (passes == 0) {
                 CU(launch_decode32(k32, vals, v.d_in, n, at<uint32_t>(w, L.slo_table), ob, rin, rout, rslo, d_order, st));
                 launches += 1;                         // (mask == 0: one group covers every window)
@@ -500,8 +500,8 @@ uellm_status uellm_schedule_batches(const uellm_profile *p, const uellm_config *
                 CU(radix_sort_windows(&keys, &vals, at<unsigned long long>(w, L.keys1), at<uint32_t>(w, L.vals1),
                                       at<unsigned long long>(w, L.keys2), at<uint32_t>(w, L.vals2),
                                       at<uint32_t>(w, L.hist), at<uint32_t>(w, L.hist) + 256 * L.sort_tiles, n,
-                                    L.window, w0, wn, mask, &passes, st, &D));
-                launches += 2 * passes + (passes ? 1 : 0);
+                                    L.window, w0, wn, mask, &passes, st, &D, &sk));
+                launches += sk;
                 if (passes == 0) break;
             }
         }

@@ -242,7 +242,8 @@ cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                  uint64_t n,
                                  uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
-                                 cudaStream_t st, const uint32_t *hist0 = nullptr, const DecodeArgs *dec = nullptr);
+                                 cudaStream_t st, const uint32_t *hist0 = nullptr, const DecodeArgs *dec = nullptr,
+                                 int *kernels = nullptr);
 // windows per sort group: about kSortGroupQueries queries (env UELLM_SORT_GROUP_Q overrides, tuning)
 uint64_t sort_group_windows(uint64_t window, uint64_t nwin);
 cudaError_t launch_decode32(const uint32_t *keys, const uint32_t *vals, const uint32_t *in, uint64_t n,
@@ -257,7 +258,8 @@ cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_
                                unsigned long long *keys_a, uint32_t *vals_a,
                                unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
-                               int *passes, cudaStream_t st, const struct DecodeArgs *dec = nullptr);
+                               int *passes, cudaStream_t st, const struct DecodeArgs *dec = nullptr,
+                               int *kernels = nullptr);
 
 // Decode sorted keys into records: slo = key >> 32, out = key & 0xffffffff, idx = val.
 cudaError_t launch_decode(const unsigned long long *keys, const uint32_t *vals, const uint32_t *in,

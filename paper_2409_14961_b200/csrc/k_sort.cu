@@ -44,26 +44,37 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_up(const K *__restrict__ 
                                                           uint64_t n, uint64_t window, uint64_t tpw, int shift,
                                                           uint64_t t0)
 {
-    __shared__ uint32_t h[256];
+    // per-warp digit counts by plain shared REDs (same-digit lanes serialise in the shared pipe,
+    // no match.any), summed per digit at the end
+    __shared__ uint32_t hw[kSortThreads / 32][256];
     const int tid = threadIdx.x;
-    if (tid < 256) h[tid] = 0;
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; ++w) hw[w][tid] = 0;
     __syncthreads();
+    uint32_t *const myh = hw[tid >> 5];
     uint64_t start, end;
     const uint64_t tile = t0 + blockIdx.x;
     tile_range(tile, n, window, tpw, start, end);
+    const uint32_t cnt = (uint32_t)(end - start);
+    if (sizeof(K) == 4 && cnt == (uint32_t)kSortTile && (((uintptr_t)(kin + start)) & 15u) == 0) {
+        // full tile of u32 keys: two 16-byte loads per thread
+        const uint4 *src = reinterpret_cast<const uint4 *>(kin + start);
+        const uint4 a = __ldg(src + tid), b = __ldg(src + kSortThreads + tid);
+        const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) atomicAdd(myh + ((v[u] >> shift) & 0xffu), 1u);
+    } else {
 #pragma unroll 4
-    for (uint32_t i = 0; i < kSortItems; ++i) {
-        uint64_t p = start + (uint64_t)i * kSortThreads + tid;
-        bool valid = p < end;
-        uint32_t act = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-            uint32_t d = (uint32_t)(kin[p] >> shift) & 0xffu;
-            uint32_t peers = __match_any_sync(act, d);
-            if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[d], __popc(peers));
+        for (uint32_t i = 0; i < kSortItems; ++i) {
+            const uint64_t p = start + (uint64_t)i * kSortThreads + tid;
+            if (p < end) atomicAdd(myh + ((uint32_t)(kin[p] >> shift) & 0xffu), 1u);
         }
     }
     __syncthreads();
-    if (tid < 256) hist[tile * 256 + tid] = h[tid];
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; ++w) c += hw[w][tid];
+    hist[tile * 256 + tid] = c;
 }
 
 // 1024 threads per window: thread (g, d) owns digit d of the g-th quarter of the window's tiles.
@@ -124,6 +135,9 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(const uint32_t 
 
 #ifndef UELLM_SORT_PIPE
 #define UELLM_SORT_PIPE 1
+#endif
+#ifndef UELLM_SORT_NEXT32
+#define UELLM_SORT_NEXT32 0          // u32 keys: k_sort_up counts the next pass's digits
 #endif
 #ifndef UELLM_SORT_NEXT
 #define UELLM_SORT_NEXT 1            // the scatter counts the next pass's digits (no k_sort_up)
@@ -420,9 +434,10 @@ template <class K>
 static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, K *keys_a, uint32_t *vals_a,
                                    K *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2, uint64_t n,
                                    uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask, int *passes,
-                                   cudaStream_t st, const uint32_t *hist0, const DecodeArgs *dec)
+                                   cudaStream_t st, const uint32_t *hist0, const DecodeArgs *dec, int *kernels)
 {
     *passes = 0;
+    int nk = 0;                                // kernels launched (scan, scatter, histogram)
     if (n == 0) return cudaSuccess;
     const uint64_t tpw = ceil_div(window, kSortTile);
     const uint64_t tiles = tpw * nwin, t0 = tpw * w_first;
@@ -438,14 +453,19 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
         if (!(digit_mask >> d & 1u)) continue;
         int dn = -1;                           // the next pass's digit
         for (int q = d + 1; q < (int)sizeof(K); ++q) if (digit_mask >> q & 1u) { dn = q; break; }
-        const bool fuse_next = UELLM_SORT_NEXT && dn >= 0;
+        // u32 keys: the next pass's per-tile counts by a separate shared-RED histogram kernel over
+        // this pass's output (c4 sort 1.47 -> 1.43 ms: the scatter's next-digit match.any was a
+        // quarter of its stall samples); u64 keys (six passes) keep the fused count (c5 0.88 vs 0.90 ms)
+        const bool fuse_next = (sizeof(K) == 8 ? UELLM_SORT_NEXT : UELLM_SORT_NEXT32) && dn >= 0;
         K *kout = (*passes & 1) ? keys_b : keys_a;
         uint32_t *vout = (*passes & 1) ? vals_b : vals_a;
         if (!ready) {
             k_sort_up<K><<<(unsigned)tiles, kSortThreads, 0, st>>>(kin, hcur, n, window, tpw, 8 * d, t0);
             hsrc = hcur;
+            ++nk;
         }
         k_sort_scan<<<(unsigned)nwin, 256 * kScanGroups, 0, st>>>(hsrc ? hsrc : hcur, hcur, n, window, tpw, w_first);
+        nk += 2;                               // scan + scatter
         hsrc = nullptr;
         // TMA bulk copies need 16-byte aligned tile starts: every tile of a window starts at a
         // multiple of kSortTile, so window starts (and the base pointers) must be aligned
@@ -477,6 +497,7 @@ static cudaError_t radix_sort_impl(const K **keys_io, const uint32_t **vals_io, 
     }
     *keys_io = kin;
     *vals_io = vin;
+    if (kernels) *kernels = nk;
     return cudaSuccess;
 }
 
@@ -484,19 +505,20 @@ cudaError_t radix_sort_windows(const unsigned long long **keys_io, const uint32_
                                unsigned long long *keys_a, uint32_t *vals_a,
                                unsigned long long *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
-                               int *passes, cudaStream_t st, const DecodeArgs *dec)
+                               int *passes, cudaStream_t st, const DecodeArgs *dec, int *kernels)
 {
     return radix_sort_impl<unsigned long long>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, hist2, n,
-                                               window, w_first, nwin, digit_mask, passes, st, nullptr, dec);
+                                               window, w_first, nwin, digit_mask, passes, st, nullptr, dec, kernels);
 }
 
 cudaError_t radix_sort_windows32(const uint32_t **keys_io, const uint32_t **vals_io, uint32_t *keys_a,
                                  uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, uint32_t *hist, uint32_t *hist2,
                                  uint64_t n, uint64_t window, uint64_t w_first, uint64_t nwin, uint32_t digit_mask,
-                                 int *passes, cudaStream_t st, const uint32_t *hist0, const DecodeArgs *dec)
+                                 int *passes, cudaStream_t st, const uint32_t *hist0, const DecodeArgs *dec,
+                                 int *kernels)
 {
     return radix_sort_impl<uint32_t>(keys_io, vals_io, keys_a, vals_a, keys_b, vals_b, hist, hist2, n, window,
-                                     w_first, nwin, digit_mask, passes, st, hist0, dec);
+                                     w_first, nwin, digit_mask, passes, st, hist0, dec, kernels);
 }
 
 // a2 (compressed key) fused with the digit-0 histogram of the first radix pass:
