@@ -49,9 +49,12 @@ uint64_t choose_tile_len(uint64_t n, uint64_t window, uint32_t W, uint32_t dp_ti
         const uint64_t floor16 = 16ull * W;
         T = T < floor16 ? floor16 : T;
         // (at least one 16 W tile per SM: a job of a handful of tiles -- c2: 10 -- is bound by its
-        // per-window cascade and launches instead, 0.75 vs 1.09 ms with 8 W tiles)
-        const uint64_t t16 = ceil_div(n ? n : 1, floor16);
-        if (T == floor16 && t16 >= 148 && t16 < 148ull * 24) T = 8ull * W;
+        // per-window cascade and launches instead, 0.75 vs 1.09 ms with 8 W tiles; and at most 1.5
+        // waves of 8 W tiles: a 12.5 M-query c4-shaped job -- one rank of an 8-GPU run, 1.7 waves --
+        // took 2.45 ms with 8 W tiles against 2.13 ms with 16 W, its fix-ups and cascade re-runs
+        // outgrowing the shorter walks)
+        const uint64_t t16 = ceil_div(n ? n : 1, floor16), t8 = ceil_div(n ? n : 1, 8ull * W);
+        if (T == floor16 && t16 >= 148 && 2 * t8 <= 3ull * 148 * 24) T = 8ull * W;
         T = align_up(T, W);
     }
     if (T < 2ull * W) T = 2ull * W;
