@@ -136,6 +136,14 @@ __global__ void __launch_bounds__(256 * kScanGroups) k_sort_scan(const uint32_t 
 #ifndef UELLM_SORT_PIPE
 #define UELLM_SORT_PIPE 1
 #endif
+// scatter rank phase: ballot multisplit instead of match.any -- kept for the one-tile u64 kernel
+// (c5 sort 0.876 -> 0.831 ms), not for the pipelined u32 kernel (c4 sort 1.44 -> 1.64 ms)
+#ifndef UELLM_SORT_RANK_BALLOT
+#define UELLM_SORT_RANK_BALLOT 0
+#endif
+#ifndef UELLM_SORT_RANK_BALLOT64
+#define UELLM_SORT_RANK_BALLOT64 1
+#endif
 #ifndef UELLM_SORT_NEXT32
 #define UELLM_SORT_NEXT32 0          // u32 keys: k_sort_up counts the next pass's digits
 #endif
@@ -293,7 +301,18 @@ k_sort_down(const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__re
                 const uint32_t act = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
                 const uint32_t d = (uint32_t)(kr[r] >> shift) & 0xffu;
                 uint32_t peers = 0;
-                if (valid) {
+                if (sizeof(K) == 8 ? UELLM_SORT_RANK_BALLOT64 : UELLM_SORT_RANK_BALLOT) {
+                    // peers by a ballot per digit bit (multisplit): eight short-latency votes in
+                    // place of one match.any whose result the rank chain waits for
+                    peers = act;
+#pragma unroll
+                    for (int bb = 0; bb < 8; ++bb) {
+                        const bool bit = (d >> bb) & 1u;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                        peers &= bit ? bal : ~bal;
+                    }
+                    if (valid) rank[r] = whist[warp][d] + __popc(peers & lt);
+                } else if (valid) {
                     peers = __match_any_sync(act, d);
                     rank[r] = whist[warp][d] + __popc(peers & lt);
                 }
