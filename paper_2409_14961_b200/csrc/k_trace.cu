@@ -239,12 +239,37 @@ __global__ void k_trace_c(const uint16_t *__restrict__ maps, TileRec *tiles, uin
 // shared-memory hop per tile instead of a dependent global load (windows of one long uniform
 // stretch re-walk every tile: c5's identical-key segment).
 constexpr uint32_t kTraceCStageW = 384;
+__device__ __forceinline__ uint32_t tr_smem(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tr_mbar_init(uint64_t *bar)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(tr_smem(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tr_mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred P1;\n"
+                 "TRW_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@!P1 bra TRW_%=;\n}" :: "r"(tr_smem(bar)), "r"(parity) : "memory");
+}
+// one TMA bulk copy global -> shared of `bytes` (a multiple of 16) completing on `bar`
+__device__ __forceinline__ void tr_bulk(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(tr_smem(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(tr_smem(dst)), "l"(src), "r"(bytes), "r"(tr_smem(bar)) : "memory");
+}
+
+// The maps of the chunk's (up to) 32 consecutive tiles are one contiguous range: one TMA bulk copy
+// per chunk, double buffered (the next chunk's copy and record loads are in flight while lane 0
+// walks the current one).  W % 8 == 0 (16-byte rows).
 __global__ void __launch_bounds__(32) k_trace_c_staged(const uint16_t *__restrict__ maps, TileRec *tiles, uint64_t tpw,
                                                        uint64_t nwin, uint64_t window, uint32_t W, uint32_t *bm,
                                                        Diag *diag)
 {
-    extern __shared__ __align__(16) uint16_t smap[];             // [32][W]
-    __shared__ uint32_t fs[32], fe[32], fa[33], fb[32];
+    extern __shared__ __align__(16) uint16_t smap[];             // [2][32][W]
+    __shared__ uint32_t fs[2][32], fe[2][32], fa[2][33], fb[2][32];
+    __shared__ __align__(8) uint64_t bar[2];
     const uint64_t w = blockIdx.x;
     const uint32_t lane = threadIdx.x;
     if (w >= nwin) return;
@@ -263,39 +288,49 @@ __global__ void __launch_bounds__(32) k_trace_c_staged(const uint16_t *__restric
     if (K == 0) return;
     if (lane == 0) bm_set(bm, (uint32_t)(w * window));          // every window starts a batch
     if (allm) return;
+    if (lane == 0) { tr_mbar_init(&bar[0]); tr_mbar_init(&bar[1]); }
+    __syncwarp();
     uint32_t exit_true = tiles[t0 + K - 1].exitB;                 // (uniform across the warp)
     uint32_t rewalks = 0;
-    const uint32_t vec = W / 8;                                  // 16-byte chunks per map row
-    for (int k_hi = (int)K - 2; k_hi >= 0; k_hi -= 32) {
+    // chunk c covers tiles [k_lo, k_hi] with k_hi = K - 2 - 32 c
+    uint32_t rs = 0, re = 0, ra = 0, rb = 0, rtop = 0;             // the next chunk's record fields
+    auto issue = [&](int k_hi, int b) {
         const int k_lo = k_hi - 31 > 0 ? k_hi - 31 : 0;
         const int rows = k_hi - k_lo + 1;
+        if (lane == 0)
+            tr_bulk(smap + (size_t)b * 32 * W, maps + (t0 + (uint64_t)k_lo) * W, (uint32_t)rows * W * 2u, &bar[b]);
         if ((int)lane < rows) {
             const TileRec &r = tiles[t0 + k_lo + lane];
-            fs[lane] = r.s; fe[lane] = r.e; fa[lane] = r.exitA; fb[lane] = r.exitB;
+            rs = r.s; re = r.e; ra = r.exitA; rb = r.exitB;
         }
-        if (lane == 0) fa[rows] = tiles[t0 + k_hi + 1].exitA;
-        if ((W & 7u) == 0) {
-            for (int row = 0; row < rows; ++row) {
-                const uint4 *src = reinterpret_cast<const uint4 *>(maps + (t0 + k_lo + row) * W);
-                uint4 *dst = reinterpret_cast<uint4 *>(smap + (uint32_t)row * W);
-                for (uint32_t c = lane; c < vec; c += 32) dst[c] = __ldg(src + c);
-            }
-        } else {
-            for (int row = 0; row < rows; ++row)
-                for (uint32_t c = lane; c < W; c += 32) smap[(uint32_t)row * W + c] = maps[(t0 + k_lo + row) * W + c];
-        }
+        if (lane == 0) rtop = tiles[t0 + k_hi + 1].exitA;
+    };
+    issue((int)K - 2, 0);
+    uint32_t use[2] = {0u, 0u};
+    int b = 0;
+    for (int k_hi = (int)K - 2; k_hi >= 0; k_hi -= 32, b ^= 1) {
+        const int k_lo = k_hi - 31 > 0 ? k_hi - 31 : 0;
+        const int rows = k_hi - k_lo + 1;
+        if ((int)lane < rows) { fs[b][lane] = rs; fe[b][lane] = re; fa[b][lane] = ra; fb[b][lane] = rb; }
+        if (lane == 0) fa[b][rows] = rtop;
+        if (k_hi - 32 >= 0) issue(k_hi - 32, b ^ 1);            // buffer b^1 was consumed last round
+        tr_mbar_wait(&bar[b], use[b] & 1u);
+        ++use[b];
         __syncwarp();
         if (lane == 0) {
+            const uint16_t *sm = smap + (size_t)b * 32 * W;
             for (int k = k_hi; k >= k_lo; --k) {
                 const int q = k - k_lo;
-                if (exit_true == fa[q + 1]) { exit_true = fb[q]; continue; }
+                if (exit_true == fa[b][q + 1]) { exit_true = fb[b][q]; continue; }
                 ++rewalks;
                 tiles[t0 + k].remark = exit_true + 1u;
-                exit_true = fs[q] - (uint32_t)smap[(uint32_t)q * W + (fe[q] - exit_true)];
+                exit_true = fs[b][q] - (uint32_t)sm[(uint32_t)q * W + (fe[b][q] - exit_true)];
                 tiles[t0 + k].exitB = exit_true;
             }
         }
         exit_true = __shfl_sync(0xffffffffu, exit_true, 0);
+        // this buffer's generic reads precede the next bulk copy into it (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
     }
     if (lane == 0 && rewalks) atomicAdd(&diag->trace_rewalks, (unsigned long long)rewalks);
@@ -374,8 +409,8 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
     }
     k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag, wflag);
     k_trace_maps<<<grid, 256, stage, st>>>(P.argx, P.tiles, ntiles, P.tpw, wflag, P.W, maps);
-    if (UELLM_TRACE_C_STAGED && P.W <= kTraceCStageW) {
-        const size_t sm = (size_t)32 * P.W * sizeof(uint16_t);
+    if (UELLM_TRACE_C_STAGED && P.W <= kTraceCStageW && (P.W & 7u) == 0) {
+        const size_t sm = (size_t)2 * 32 * P.W * sizeof(uint16_t);
         if (sm > 48 * 1024) {
             e = cudaFuncSetAttribute(k_trace_c_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             if (e != cudaSuccess) return e;
