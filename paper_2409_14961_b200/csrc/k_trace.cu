@@ -150,6 +150,84 @@ __global__ void k_trace_b(const uint16_t *__restrict__ argx, TileRec *tiles, uin
     tiles[t].merged = merged;
 }
 
+// Walk B, one warp per tile (as walk A): the tile's args and its bitmap words are staged in shared
+// memory, lane 0 walks, clears and marks there, and the warp writes back only the changed bits of
+// each word (atomicOr / atomicAnd: a neighbouring tile's walk owns the other bits of a shared word).
+__device__ __forceinline__ void sbm_clear(uint32_t *sw, uint32_t w0, uint32_t a, uint32_t z)
+{
+    if (a > z) return;
+    const uint32_t wa = a >> 5, wz = z >> 5;
+    for (uint32_t w = wa; w <= wz; ++w) {
+        const uint32_t lo = (w == wa) ? (a & 31) : 0;
+        const uint32_t hi = (w == wz) ? (z & 31) : 31;
+        const uint32_t m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1)) & ~((1u << lo) - 1);
+        sw[w - w0] &= ~m;
+    }
+}
+__global__ void __launch_bounds__(32 * kTraceWarps) k_trace_b_warp(const uint16_t *__restrict__ argx, TileRec *tiles,
+                                                                   uint64_t ntiles, uint64_t tpw, uint32_t *bm,
+                                                                   Diag *diag, uint32_t *wflag, uint32_t tile_len)
+{
+    extern __shared__ __align__(16) unsigned char tsm[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t t = (uint64_t)blockIdx.x * kTraceWarps + warp;
+    if (t >= ntiles) return;
+    const TileRec r = tiles[t];
+    if (!r.valid) return;
+    const bool last = ((t + 1) % tpw == 0) || !tiles[t + 1].valid;
+    uint32_t exitB = r.exitA, merged = 1;
+    const uint32_t q = last ? r.e : tiles[t + 1].exitA;          // entry into this tile if tile t+1 is right
+    if (!last && q != r.e) {
+        unsigned char *base = tsm + (size_t)warp * trace_warp_smem(tile_len);
+        uint16_t *sa = reinterpret_cast<uint16_t *>(base);
+        uint32_t *sw = reinterpret_cast<uint32_t *>(base + ((tile_len * 2 + 15) & ~15u));
+        const uint32_t len = r.e - r.s;
+        if ((r.s & 7u) == 0 && (len & 7u) == 0) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(argx + r.s);
+            uint4 *dst = reinterpret_cast<uint4 *>(sa);
+            for (uint32_t k = lane; k < len / 8; k += 32) dst[k] = __ldg(src + k);
+        } else {
+            for (uint32_t k = lane; k < len; k += 32) sa[k] = argx[r.s + k];
+        }
+        const uint32_t w0 = (r.s + 1) >> 5, w1 = r.e >> 5, nw = w1 - w0 + 1;
+        for (uint32_t k = lane; k < nw; k += 32) sw[k] = __ldcg(bm + w0 + k);
+        __syncwarp();
+        uint32_t orig[9];                                          // lane's words before the walk (nw <= 258)
+#pragma unroll
+        for (int u = 0; u < 9; ++u) orig[u] = (lane + 32u * u < nw) ? sw[lane + 32u * u] : 0u;
+        __syncwarp();
+        if (lane == 0) {
+            sbm_clear(sw, w0, q + 1, r.e);
+            uint32_t j = q;
+            for (;;) {
+                if ((sw[(j >> 5) - w0] >> (j & 31)) & 1u) break;       // met the A-walk: identical below
+                sw[(j >> 5) - w0] |= 1u << (j & 31);
+                const uint32_t i = j - (uint32_t)sa[j - 1 - r.s];
+                sbm_clear(sw, w0, max(i, r.s) + 1, j - 1);
+                if (i <= r.s) { exitB = i; merged = (i == r.exitA); break; }
+                j = i;
+            }
+            if (!merged) { atomicAdd(&diag->trace_unmerged, 1ull); wflag[t / tpw] = 1u; }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 9; ++u) {
+            const uint32_t k = lane + 32u * u;
+            if (k < nw) {
+                const uint32_t nv = sw[k], ov = orig[u];
+                if (nv & ~ov) atomicOr(bm + w0 + k, nv & ~ov);
+                if (ov & ~nv) atomicAnd(bm + w0 + k, ~(ov & ~nv));
+            }
+        }
+        exitB = __shfl_sync(0xffffffffu, exitB, 0);
+        merged = __shfl_sync(0xffffffffu, merged, 0);
+    }
+    if (lane == 0) {
+        tiles[t].exitB = exitB;
+        tiles[t].merged = merged;
+    }
+}
+
 // Tile args staged in shared memory (up to kTraceStage positions; longer tiles read global memory).
 constexpr uint32_t kTraceStage = 16384;
 struct TileArgs {
@@ -389,6 +467,9 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
 #ifndef UELLM_TRACE_A_WARP
 #define UELLM_TRACE_A_WARP 1
 #endif
+#ifndef UELLM_TRACE_B_WARP
+#define UELLM_TRACE_B_WARP 1
+#endif
     const bool stage_walk = UELLM_TRACE_A && ntiles < (uint64_t)nsm * 64 &&
                             P.tile_len * sizeof(uint16_t) <= 160 * 1024;
     if (UELLM_TRACE_A_WARP && P.tile_len <= 8192) {
@@ -407,7 +488,17 @@ cudaError_t run_traceback(const DPParams &P, uint32_t *bitmap, uint64_t ntiles, 
     } else {
         k_trace_a<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, bitmap);
     }
-    k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag, wflag);
+    if (UELLM_TRACE_B_WARP && P.tile_len <= 8192) {
+        const size_t sm = (size_t)kTraceWarps * trace_warp_smem(P.tile_len);
+        if (sm > 48 * 1024) {
+            e = cudaFuncSetAttribute(k_trace_b_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+        }
+        k_trace_b_warp<<<(unsigned)ceil_div(ntiles, kTraceWarps), 32 * kTraceWarps, sm, st>>>(
+            P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag, wflag, P.tile_len);
+    } else {
+        k_trace_b<<<(unsigned)ceil_div(ntiles, tb), tb, 0, st>>>(P.argx, P.tiles, ntiles, P.tpw, bitmap, P.diag, wflag);
+    }
     k_trace_maps<<<grid, 256, stage, st>>>(P.argx, P.tiles, ntiles, P.tpw, wflag, P.W, maps);
     if (UELLM_TRACE_C_STAGED && P.W <= kTraceCStageW && (P.W & 7u) == 0) {
         const size_t sm = (size_t)2 * 32 * P.W * sizeof(uint16_t);
