@@ -1442,10 +1442,14 @@ __global__ void __launch_bounds__(kDpWarpsPerCta * 32, UELLM_DP_MINB) k_dp_refix
     }
 }
 
+#ifndef UELLM_CASCADE_STAGE
+#define UELLM_CASCADE_STAGE 1
+#endif
 template <int V>
 __global__ void k_dp_cascade(DPParams P)
 {
     extern __shared__ __align__(16) char smem[];
+    __shared__ TileRec srec[32];
     const uint32_t w = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t t0 = (uint64_t)w * P.tpw;
@@ -1521,8 +1525,13 @@ __global__ void k_dp_cascade(DPParams P)
                 uint32_t ts, te, tk, tw; bool tv;
                 tile_bounds(P, t0 + kk, ts, te, tk, tw, tv);
                 e = tv && entry_uniform(P, t0 + kk, ts);
+                // the chunk's records, one per lane: the walk below reads tile k's record from shared
+                // memory instead of a dependent global load per tile (only the walk writes them, tile
+                // k at step k, so the staged copy of a later tile is current when the walk reaches it)
+                if (UELLM_CASCADE_STAGE) srec[lane] = P.tiles[t0 + kk];
             }
             eu_mask = __ballot_sync(0xffffffffu, e);
+            __syncwarp();
         }
         const bool eu = (eu_mask >> (k & 31u)) & 1u;
         if (V != 0 && !tail_local && eu && ref_P != 0) {
@@ -1545,7 +1554,7 @@ __global__ void k_dp_cascade(DPParams P)
             k += cnt - 1;                                // (the loop adds 1)
             continue;
         }
-        TileRec r = P.tiles[t0 + k];
+        TileRec r = UELLM_CASCADE_STAGE ? srec[k & 31u] : P.tiles[t0 + k];
         r.fill_s = 0; r.fill_P = 0; r.fill_F = 0;
         if (!tail_local) {
             bool deferred = false;
