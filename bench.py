@@ -226,8 +226,8 @@ def time_steps(step, K, stream, dev):
 
 
 def sub_config(name, K, Wm, stream, dev, hbm_gbs):
-    """Another BJ config as a timed sub-record of the same line (N = 1): same step (load +
-    schedule + stats), inputs resident in HBM, CUDA events on the launching stream."""
+    """Another BJ config as a timed sub-record of the same line (N = 1): same step (reload +
+    schedule + stats, eager), inputs resident in HBM, CUDA events on the launching stream."""
     import torch
     from paper_2409_14961_b200.scheduler import GpuScheduler
     import workloads as W
@@ -246,15 +246,20 @@ def sub_config(name, K, Wm, stream, dev, hbm_gbs):
     d_out = torch.from_numpy(out.view(np.int32)).to(dev)
     d_slo = torch.from_numpy(slo).to(dev)
     g = GpuScheduler(n, cfg, device=dev)
+    # the same step as the c4 line: one synchronising load first, then reload (device-side
+    # validation, no host sync) -> schedule -> stats per step, launched eagerly
+    g.load(d_in, d_out, d_slo, stream)
 
     def step(k=None):
-        g.load(d_in, d_out, d_slo, stream)
+        g.reload(d_in, d_out, d_slo, stream)
         g.schedule(stream)
         g.stats(stream)
     for _ in range(Wm):
         step()
     torch.cuda.synchronize(dev)
     ms = time_steps(step, K, stream, dev)
+    if int(g.status_word().item()) != 0:
+        raise SystemExit(f"{name}: device status word {int(g.status_word().item())} after the timed steps")
     diag = g.diagnostics(stream)
     res = g.results()
     comp = compulsory_bytes(n, res["m"])
