@@ -612,6 +612,9 @@ cudaError_t launch_pack32_hist(const uint32_t *out, const float *slo, uint64_t n
 // 4t..4t+3 and 1024+4t..1024+4t+3 of a tile (16-byte loads and key stores), and the next tile's
 // loads are issued before the current one is processed.  Validation bits and maxima are reduced per
 // warp in registers and merged with one atomic each at the end.
+#ifndef UELLM_RELOAD_FCACHE
+#define UELLM_RELOAD_FCACHE 1
+#endif
 #ifndef UELLM_RELOAD_PERSIST
 #define UELLM_RELOAD_PERSIST 1      // persistent CTAs with the next tile's loads in flight (else one tile per CTA)
 #endif
@@ -636,6 +639,11 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
     uint32_t *const myh = hw[tid >> 5];
     uint32_t mx_in = 0, mx_out = 0, mn_in = 0xffffffffu, mn_out = 0xffffffffu, missing = 0;
     bool okall = true;
+    // per-CTA cache float bits -> rank of the SLO values already validated and ranked (class-valued
+    // SLOs hit it almost always: no double conversion, no rank-hash probe); one 64-bit entry per
+    // slot, written whole, so a reader sees an old or a new entry, never a mix
+    __shared__ unsigned long long fcache[64];
+    if (UELLM_RELOAD_FCACHE && tid < 64) fcache[tid] = 0ull;
     // element e (0..7) of this thread inside the tile
     auto off = [&](int e) -> uint32_t {
         return VEC ? (uint32_t)((e >> 2) * 1024 + 4 * tid + (e & 3)) : (uint32_t)(e * kSortThreads + tid);
@@ -698,24 +706,34 @@ __global__ void __launch_bounds__(kSortThreads, UELLM_RELOAD_PERSIST ? 4 : 6) k_
             const bool valid = full || off(e) < cnt;
             key[e] = 0;
             if (!valid) continue;
-            bool ok;
-            const uint32_t su = slo_to_us(cf[e], ok);
             const uint32_t a = ca[e], o = co[e];
             // validation by minima (a zero length is the minimum 0) and one flag: no per-key branches
             mn_in = min(mn_in, a);
             mn_out = min(mn_out, o);
-            okall &= ok;
             mx_in = max(mx_in, a);
             mx_out = max(mx_out, o);
-            uint32_t hh = slo_hash(su, (uint32_t)cbits);
-            unsigned long long en = sct[hh];
-            // (>= 8 slots per value up to 4096 slots: the first probe almost always decides; an
-            // absent value ends at an empty slot)
-            if ((uint32_t)(en >> 32) != su) {
-                while (en != 0ull && (uint32_t)(en >> 32) != su) { hh = (hh + 1) & (C - 1); en = sct[hh]; }
-                missing |= en == 0ull ? 1u : 0u;
+            uint32_t rank;
+            const uint32_t fb = __float_as_uint(cf[e]);
+            const unsigned long long ce = UELLM_RELOAD_FCACHE ? fcache[(fb * 0x9E3779B1u) >> 26] : 0ull;
+            if (UELLM_RELOAD_FCACHE && fb != 0u && (uint32_t)(ce >> 32) == fb) {
+                rank = (uint32_t)ce;                       // this float was validated and ranked before
+            } else {
+                bool ok;
+                const uint32_t su = slo_to_us(cf[e], ok);
+                okall &= ok;
+                uint32_t hh = slo_hash(su, (uint32_t)cbits);
+                unsigned long long en = sct[hh];
+                // (>= 8 slots per value up to 4096 slots: the first probe almost always decides; an
+                // absent value ends at an empty slot)
+                if ((uint32_t)(en >> 32) != su) {
+                    while (en != 0ull && (uint32_t)(en >> 32) != su) { hh = (hh + 1) & (C - 1); en = sct[hh]; }
+                    missing |= en == 0ull ? 1u : 0u;
+                }
+                rank = (uint32_t)en;
+                if (UELLM_RELOAD_FCACHE && ok && en != 0ull)
+                    fcache[(fb * 0x9E3779B1u) >> 26] = ((unsigned long long)fb << 32) | rank;
             }
-            key[e] = ((uint32_t)en << ob) | o;
+            key[e] = (rank << ob) | o;
             atomicAdd(myh + (key[e] & 0xffu), 1u);
         }
         if (VEC) {
